@@ -1,0 +1,147 @@
+/*
+ * dg.h -- C-ABI of libdgsip.so, the B200-native (sm_100a) implicit-stage hot path of
+ * arXiv 2112.04167 (Guesmi, Grotteschi, Stiller, "Assessment of high-order IMEX methods
+ * for incompressible flow").  Citations "P:L" are lines of the paper text
+ * (/root/reference/PAPER.md); readings A1..A21 are SURVEY.md §8(c), listed in DESIGN.md.
+ *
+ * What is computed.  Each IMEX-RK stage (Alg. 3) solves
+ *   line 5:  a periodic pressure Poisson problem  -lap psi = rhs  (lam = 0)
+ *   line 9:  per velocity component  v - dt a_ii div(nu grad v) = g,
+ *                        i.e.  lam v - div(nu grad v) = f  with lam = 1/(dt a_ii), f = lam g
+ * discretised by the symmetric interior-penalty DG method on tensor-product
+ * GLL elements of degree P, plus the explicit DG convective term
+ * F_c = -div(v v) with local Lax-Friedrichs fluxes.
+ *
+ * Mesh and data layout (all calls).  Periodic box [0,L0]x[0,L1](x[0,L2]) with N[d]
+ * uniform elements per direction.  Global element index e = ex + N0*(ey + N1*ez);
+ * node index i + n*(j + n*k), n = P+1.  Every field is a caller-owned DEVICE array of
+ * double, [local_elements][n^dim], holding the contiguous slab of elements owned by this
+ * rank: ranks split the slowest direction (z in 3-D, y in 2-D) into equal slabs, rank r
+ * owning global elements [r*E, (r+1)*E), E = N_el / nranks.
+ *
+ * Operator (dg_helmholtz_apply, weak form, reading A5):
+ *   (A u)_I = sum_K sum_{q in GLL^d} W_q [lam phi_I u + nu grad phi_I . grad u](x_q)
+ *           + sum_F sum_{q in GLL^{d-1}} W^F_q [-{nu d_n u}[phi_I] - {nu d_n phi_I}[u]
+ *                                              + sigma [u][phi_I]],
+ *   W_q = prod_d w_{q_d} h_d/2 (GLL collocation, reading A2), sigma = tau (nu^- + nu^+)/2,
+ *   tau = (P+1)^2 / h_d  (readings A1, A3).  A is symmetric; PSD with null space {1} at
+ *   lam = 0, SPD for lam > 0.
+ *
+ * Streams.  Every call is enqueued on the mesh's stream (set at create or by
+ * dg_mesh_set_stream; NULL = legacy default stream).  apply/diag/convect are
+ * asynchronous; dg_pcg_solve returns after convergence (it synchronises with the host
+ * every few iterations to test convergence).
+ *
+ * Errors.  No exception crosses the ABI.  Every call returns a dg_status; the message of
+ * the last failing call on this thread is dg_last_error().  Invalid arguments
+ * (null pointers, P outside [1,10], N[d] < 1, slab split not exact, lam < 0, nu_const <= 0
+ * when nu == NULL, tol <= 0, maxit < 1) return DG_EINVAL before anything is enqueued.
+ * A nu field is not scanned for positivity on the hot path (it is the caller's
+ * precondition, "nu_field > 0"); dg_check_field() does that on request.
+ */
+#ifndef DG_H
+#define DG_H
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct dg_mesh dg_mesh; /* opaque; owns all workspace, NCCL comm and halo buffers */
+
+typedef enum {
+    DG_OK = 0,
+    DG_EINVAL = 1,       /* invalid argument                                   */
+    DG_ECUDA = 2,        /* CUDA runtime error (message has cudaGetErrorString) */
+    DG_ENCCL = 3,        /* NCCL error                                          */
+    DG_ENOMEM = 4,       /* device allocation failed                            */
+    DG_ENOTCONV = 5,     /* maxit reached; info holds the final residual        */
+    DG_EBREAKDOWN = 6,   /* CG breakdown: p^T A p <= 0 or a non-finite scalar  */
+    DG_EUNSUPPORTED = 7  /* configuration not compiled (e.g. P > 10)            */
+} dg_status;
+
+typedef struct {
+    int iters;           /* CG iterations performed                             */
+    double rel_res;      /* ||M^-1 r||_2 / ||f||_2 at exit (RMS residual at the
+                            collocation points; reading A7)             */
+    double removed_mean; /* lam == 0: mass-weighted mean removed from f (A8)    */
+    double f_norm;       /* ||f||_2 after the lam == 0 projection               */
+    double kappa_est;    /* Lanczos estimate of cond(D^-1 A) from CG alpha/beta */
+} dg_solve_info;
+
+/* NCCL unique id for multi-rank meshes (call on rank 0, broadcast the 128 bytes with
+ * torch.distributed, pass to dg_mesh_create on every rank). */
+dg_status dg_nccl_unique_id(unsigned char out[128]);
+
+/* Create a mesh: GLL tables for degree P, periodic
+ * structured connectivity, the slab of rank `rank` out of `nranks`, and all workspace.
+ * dim in {2,3}; N[d] >= 1; L[d] > 0; 1 <= P <= 10; N[dim-1] % nranks == 0.
+ * nccl_uid: NULL when nranks == 1.  cuda_stream: a cudaStream_t (may be NULL).
+ * The caller must have selected the device (cudaSetDevice) before the call.  */
+dg_status dg_mesh_create(int dim, const int N[3], const double L[3], int P, int rank, int nranks,
+                         const unsigned char *nccl_uid, void *cuda_stream, dg_mesh **out);
+void dg_mesh_destroy(dg_mesh *m);
+dg_status dg_mesh_set_stream(dg_mesh *m, void *cuda_stream);
+
+long long dg_mesh_local_ndof(const dg_mesh *m);      /* local_elements * (P+1)^dim    */
+long long dg_mesh_local_elements(const dg_mesh *m);
+long long dg_mesh_element_offset(const dg_mesh *m);  /* first global element owned   */
+
+/* Node coordinates of the local slab: xyz is a DEVICE array [dim][local_ndof]. */
+dg_status dg_mesh_node_coords(const dg_mesh *m, double *xyz);
+
+/* GLL lumped mass m_I = prod_d w h_d/2 of the local slab, DEVICE [local_ndof]. */
+dg_status dg_mesh_mass(const dg_mesh *m, double *mass);
+
+/* out = A u (weak form, see above).  nu: DEVICE nodal viscosity [local_ndof] or NULL for
+ * the constant nu_const.  u and out must not alias.  lam >= 0.  Multi-rank: collective
+ * (face halos are exchanged with NCCL over NVLink). */
+dg_status dg_helmholtz_apply(dg_mesh *m, double lam, const double *nu, double nu_const,
+                             const double *u, double *out);
+
+/* diag = diag(A) (the Jacobi preconditioner of the north star). */
+dg_status dg_helmholtz_diag(dg_mesh *m, double lam, const double *nu, double nu_const, double *diag);
+
+/* Solve A u = M f (M = GLL-lumped mass, reading A6) by Jacobi-preconditioned CG.
+ * f: DEVICE nodal rhs.  u: DEVICE, initial guess on entry, solution on exit.
+ * Stops when ||M^-1 r||_2 <= tol ||f||_2 (reading A7) -> DG_OK, or after maxit
+ * iterations -> DG_ENOTCONV (u and info hold the last iterate).  lam == 0 (pressure
+ * Poisson, Alg. 3 line 5): f is projected to zero mass-weighted mean (info.removed_mean),
+ * the residual is kept orthogonal to constants, u is returned with zero mass-weighted
+ * mean (reading A8).  info may be NULL.  Collective for multi-rank meshes. */
+dg_status dg_pcg_solve(dg_mesh *m, double lam, const double *nu, double nu_const, const double *f,
+                       double tol, int maxit, double *u, dg_solve_info *info);
+
+/* Explicit convective tendency F_c = -div(v v) with LLF fluxes, nodal (M^-1 applied,
+ * GLL-lumped), Gauss quadrature with Q = floor(3P/2)+1 points per direction
+ * (readings A12-A14).  v[c], out[c]: DEVICE [local_ndof], c < dim.
+ * out must not alias v. */
+dg_status dg_convect_rhs(dg_mesh *m, const double *const v[3], double *const out[3]);
+
+/* Host-buffer variants: same operations on HOST arrays; H2D and D2H copies through
+ * mesh-owned device staging buffers are part of the call (allocated on first use). */
+dg_status dg_helmholtz_apply_host(dg_mesh *m, double lam, const double *nu_host, double nu_const,
+                                  const double *u_host, double *out_host);
+dg_status dg_pcg_solve_host(dg_mesh *m, double lam, const double *nu_host, double nu_const,
+                            const double *f_host, double tol, int maxit, double *u_host,
+                            dg_solve_info *info);
+
+/* Validate a nodal field (finite and, if positive != 0, > 0).  Synchronous. */
+dg_status dg_check_field(dg_mesh *m, const double *x, int positive);
+
+/* The product path's 1-D tables for degree P (host arrays): GLL nodes xi[P+1], weights
+ * w[P+1] and the differentiation matrix D[(P+1)*(P+1)] (row-major, D[i][j] = l_j'(xi_i)).
+ * Introspection only (tests pin them against closed forms); no CUDA call. */
+dg_status dg_gll_tables(int P, double *xi, double *w, double *D);
+
+/* Number of kernel launches this mesh enqueued since creation (evidence for bench.py). */
+long long dg_mesh_launch_count(const dg_mesh *m);
+
+/* Message for the last failing call on this thread ("" if none). */
+const char *dg_last_error(void);
+
+/* Library version string. */
+const char *dg_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,268 @@
+"""ctypes binding for libdgsip.so -- same names as include/dg.h, marshalling only.
+
+Field arguments are torch tensors (CUDA, float64, contiguous) passed by ``data_ptr()``,
+or raw integer device pointers.  Host variants take numpy float64 arrays.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIBPATH = os.environ.get("DG_LIBRARY", os.path.join(_HERE, "libdgsip.so"))
+
+DG_OK, DG_EINVAL, DG_ECUDA, DG_ENCCL, DG_ENOMEM, DG_ENOTCONV, DG_EBREAKDOWN, DG_EUNSUPPORTED = range(8)
+_NAMES = {0: "DG_OK", 1: "DG_EINVAL", 2: "DG_ECUDA", 3: "DG_ENCCL", 4: "DG_ENOMEM", 5: "DG_ENOTCONV",
+          6: "DG_EBREAKDOWN", 7: "DG_EUNSUPPORTED"}
+
+if not os.path.exists(_LIBPATH):
+    raise ImportError(
+        "libdgsip.so not found at %s -- build it with `python paper_2112_04167_b200/build.py` "
+        "(there is no CPU fallback)" % _LIBPATH)
+
+_lib = ctypes.CDLL(_LIBPATH)
+_vp = ctypes.c_void_p
+_d = ctypes.c_double
+_i = ctypes.c_int
+_ll = ctypes.c_longlong
+
+
+class SolveInfo(ctypes.Structure):
+    _fields_ = [("iters", _i), ("rel_res", _d), ("removed_mean", _d), ("f_norm", _d), ("kappa_est", _d)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+def _sig(name, res, args):
+    f = getattr(_lib, name)
+    f.restype = res
+    f.argtypes = args
+    return f
+
+
+_c = {
+    "dg_nccl_unique_id": _sig("dg_nccl_unique_id", _i, [ctypes.c_char_p]),
+    "dg_mesh_create": _sig("dg_mesh_create", _i, [_i, ctypes.POINTER(_i), ctypes.POINTER(_d), _i, _i, _i,
+                                                  ctypes.c_char_p, _vp, ctypes.POINTER(_vp)]),
+    "dg_mesh_destroy": _sig("dg_mesh_destroy", None, [_vp]),
+    "dg_mesh_set_stream": _sig("dg_mesh_set_stream", _i, [_vp, _vp]),
+    "dg_mesh_local_ndof": _sig("dg_mesh_local_ndof", _ll, [_vp]),
+    "dg_mesh_local_elements": _sig("dg_mesh_local_elements", _ll, [_vp]),
+    "dg_mesh_element_offset": _sig("dg_mesh_element_offset", _ll, [_vp]),
+    "dg_mesh_launch_count": _sig("dg_mesh_launch_count", _ll, [_vp]),
+    "dg_mesh_node_coords": _sig("dg_mesh_node_coords", _i, [_vp, _vp]),
+    "dg_mesh_mass": _sig("dg_mesh_mass", _i, [_vp, _vp]),
+    "dg_helmholtz_apply": _sig("dg_helmholtz_apply", _i, [_vp, _d, _vp, _d, _vp, _vp]),
+    "dg_helmholtz_diag": _sig("dg_helmholtz_diag", _i, [_vp, _d, _vp, _d, _vp]),
+    "dg_pcg_solve": _sig("dg_pcg_solve", _i, [_vp, _d, _vp, _d, _vp, _d, _i, _vp, ctypes.POINTER(SolveInfo)]),
+    "dg_convect_rhs": _sig("dg_convect_rhs", _i, [_vp, ctypes.POINTER(_vp), ctypes.POINTER(_vp)]),
+    "dg_helmholtz_apply_host": _sig("dg_helmholtz_apply_host", _i, [_vp, _d, _vp, _d, _vp, _vp]),
+    "dg_pcg_solve_host": _sig("dg_pcg_solve_host", _i, [_vp, _d, _vp, _d, _vp, _d, _i, _vp,
+                                                        ctypes.POINTER(SolveInfo)]),
+    "dg_gll_tables": _sig("dg_gll_tables", _i, [_i, _vp, _vp, _vp]),
+    "dg_check_field": _sig("dg_check_field", _i, [_vp, _vp, _i]),
+    "dg_last_error": _sig("dg_last_error", ctypes.c_char_p, []),
+    "dg_version": _sig("dg_version", ctypes.c_char_p, []),
+}
+
+EXPORTED = sorted(_c)
+
+
+def library_path() -> str:
+    return _LIBPATH
+
+
+class DGError(RuntimeError):
+    def __init__(self, status, msg, info=None):
+        super().__init__("%s: %s" % (_NAMES.get(status, status), msg))
+        self.status = status
+        self.info = info
+
+
+def dg_last_error() -> str:
+    return _c["dg_last_error"]().decode()
+
+
+def dg_version() -> str:
+    return _c["dg_version"]().decode()
+
+
+def _check(st, info=None, allow=()):
+    if st != DG_OK and st not in allow:
+        raise DGError(st, dg_last_error(), info)
+    return st
+
+
+def _ptr(x):
+    """Device pointer of a torch tensor (checked) / int / None."""
+    if x is None:
+        return None
+    if isinstance(x, int):
+        return x
+    import torch
+
+    if not isinstance(x, torch.Tensor):
+        raise TypeError("expected a torch tensor")
+    if not x.is_cuda or x.dtype != torch.float64 or not x.is_contiguous():
+        raise TypeError("fields must be contiguous CUDA float64 tensors")
+    return x.data_ptr()
+
+
+def _hptr(a):
+    if a is None:
+        return None
+    if not (isinstance(a, np.ndarray) and a.dtype == np.float64 and a.flags.c_contiguous):
+        raise TypeError("host fields must be C-contiguous float64 numpy arrays")
+    return a.ctypes.data
+
+
+def _stream_ptr(stream):
+    if stream is None:
+        return None
+    if isinstance(stream, int):
+        return stream
+    return stream.cuda_stream
+
+
+class Mesh:
+    """Owning handle of a ``dg_mesh*``."""
+
+    def __init__(self, handle, dim, N, L, P, rank, nranks):
+        self._h = handle
+        self.dim, self.N, self.L, self.P, self.rank, self.nranks = dim, tuple(N), tuple(L), P, rank, nranks
+
+    @property
+    def handle(self):
+        if not self._h:
+            raise DGError(DG_EINVAL, "mesh destroyed")
+        return self._h
+
+    @property
+    def n(self):
+        return self.P + 1
+
+    @property
+    def npe(self):
+        return self.n ** self.dim
+
+    @property
+    def ndof(self):
+        return dg_mesh_local_ndof(self)
+
+    @property
+    def n_el(self):
+        return dg_mesh_local_elements(self)
+
+    @property
+    def element_offset(self):
+        return dg_mesh_element_offset(self)
+
+    def close(self):
+        if self._h:
+            dg_mesh_destroy(self)
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def dg_nccl_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    _check(_c["dg_nccl_unique_id"](buf))
+    return buf.raw
+
+
+def dg_mesh_create(dim, N, L, P, rank=0, nranks=1, nccl_uid=None, stream=None) -> Mesh:
+    N3 = (list(N) + [1, 1, 1])[:3]
+    L3 = (list(L) + [1.0, 1.0, 1.0])[:3]
+    h = _vp()
+    uid = None if nccl_uid is None else bytes(nccl_uid)
+    _check(_c["dg_mesh_create"](int(dim), (_i * 3)(*N3), (_d * 3)(*L3), int(P), int(rank), int(nranks), uid,
+                                _stream_ptr(stream), ctypes.byref(h)))
+    return Mesh(h.value, dim, N3[:dim], L3[:dim], P, rank, nranks)
+
+
+def dg_mesh_destroy(m: Mesh):
+    if m._h:
+        _c["dg_mesh_destroy"](m._h)
+        m._h = None
+
+
+def dg_mesh_set_stream(m: Mesh, stream):
+    _check(_c["dg_mesh_set_stream"](m.handle, _stream_ptr(stream)))
+
+
+def dg_mesh_local_ndof(m: Mesh) -> int:
+    return int(_c["dg_mesh_local_ndof"](m.handle))
+
+
+def dg_mesh_local_elements(m: Mesh) -> int:
+    return int(_c["dg_mesh_local_elements"](m.handle))
+
+
+def dg_mesh_element_offset(m: Mesh) -> int:
+    return int(_c["dg_mesh_element_offset"](m.handle))
+
+
+def dg_mesh_launch_count(m: Mesh) -> int:
+    return int(_c["dg_mesh_launch_count"](m.handle))
+
+
+def dg_mesh_node_coords(m: Mesh, xyz):
+    _check(_c["dg_mesh_node_coords"](m.handle, _ptr(xyz)))
+
+
+def dg_mesh_mass(m: Mesh, mass):
+    _check(_c["dg_mesh_mass"](m.handle, _ptr(mass)))
+
+
+def dg_helmholtz_apply(m: Mesh, lam, nu, nu_const, u, out):
+    _check(_c["dg_helmholtz_apply"](m.handle, float(lam), _ptr(nu), float(nu_const), _ptr(u), _ptr(out)))
+
+
+def dg_helmholtz_diag(m: Mesh, lam, nu, nu_const, diag):
+    _check(_c["dg_helmholtz_diag"](m.handle, float(lam), _ptr(nu), float(nu_const), _ptr(diag)))
+
+
+def dg_pcg_solve(m: Mesh, lam, nu, nu_const, f, tol, maxit, u, raise_on_notconv=True) -> SolveInfo:
+    info = SolveInfo()
+    st = _c["dg_pcg_solve"](m.handle, float(lam), _ptr(nu), float(nu_const), _ptr(f), float(tol), int(maxit),
+                            _ptr(u), ctypes.byref(info))
+    _check(st, info, allow=() if raise_on_notconv else (DG_ENOTCONV,))
+    return info
+
+
+def dg_convect_rhs(m: Mesh, v, out):
+    vin = (_vp * 3)(*([_ptr(x) for x in v] + [None] * (3 - len(v))))
+    vout = (_vp * 3)(*([_ptr(x) for x in out] + [None] * (3 - len(out))))
+    _check(_c["dg_convect_rhs"](m.handle, vin, vout))
+
+
+def dg_helmholtz_apply_host(m: Mesh, lam, nu, nu_const, u, out):
+    _check(_c["dg_helmholtz_apply_host"](m.handle, float(lam), _hptr(nu), float(nu_const), _hptr(u), _hptr(out)))
+
+
+def dg_pcg_solve_host(m: Mesh, lam, nu, nu_const, f, tol, maxit, u) -> SolveInfo:
+    info = SolveInfo()
+    _check(_c["dg_pcg_solve_host"](m.handle, float(lam), _hptr(nu), float(nu_const), _hptr(f), float(tol),
+                                   int(maxit), _hptr(u), ctypes.byref(info)), info)
+    return info
+
+
+def dg_gll_tables(P):
+    xi = np.zeros(P + 1)
+    w = np.zeros(P + 1)
+    D = np.zeros((P + 1, P + 1))
+    _check(_c["dg_gll_tables"](int(P), xi.ctypes.data, w.ctypes.data, D.ctypes.data))
+    return xi, w, D
+
+
+def dg_check_field(m: Mesh, x, positive=True):
+    _check(_c["dg_check_field"](m.handle, _ptr(x), int(bool(positive))))
+
+

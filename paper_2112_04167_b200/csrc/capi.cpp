@@ -1,0 +1,771 @@
+// capi.cpp -- the C-ABI of libdgsip.so (include/dg.h): mesh/workspace ownership, kernel
+// orchestration on the caller's stream, the Jacobi-PCG driver with device-resident
+// scalars, NCCL halo exchange / allreduce for slab-partitioned meshes, and error plumbing.
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "dg_internal.h"
+
+namespace dg {
+
+thread_local std::string g_err;
+
+dg_status set_error(dg_status s, const std::string &msg)
+{
+    g_err = msg;
+    return s;
+}
+
+cudaError_t upload_tables()
+{
+    cudaError_t e;
+    if ((e = upload_tables_vec()) != cudaSuccess) return e;
+    if ((e = upload_tables_apply2()) != cudaSuccess) return e;
+    if ((e = upload_tables_apply3()) != cudaSuccess) return e;
+    return upload_tables_convect();
+}
+
+// ---------------------------------------------------------------------------
+// NCCL, loaded on demand (single-rank meshes never need it)
+// ---------------------------------------------------------------------------
+struct NcclApi {
+    ncclResult_t (*GetUniqueId)(ncclUniqueId *);
+    ncclResult_t (*CommInitRank)(ncclComm_t *, int, ncclUniqueId, int);
+    ncclResult_t (*CommDestroy)(ncclComm_t);
+    ncclResult_t (*Send)(const void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t);
+    ncclResult_t (*Recv)(void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t);
+    ncclResult_t (*AllReduce)(const void *, void *, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t);
+    ncclResult_t (*GroupStart)();
+    ncclResult_t (*GroupEnd)();
+    const char *(*GetErrorString)(ncclResult_t);
+    bool ok = false;
+    std::string why;
+};
+
+static NcclApi *nccl()
+{
+    static NcclApi api;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        const char *env = getenv("DG_NCCL_LIB");
+        const char *cands[] = {env ? env : "libnccl.so.2", "libnccl.so.2", "libnccl.so"};
+        void *h = nullptr;
+        for (const char *c : cands)
+            if ((h = dlopen(c, RTLD_NOW | RTLD_GLOBAL))) break;
+        if (!h) {
+            api.why = std::string("cannot dlopen NCCL (set DG_NCCL_LIB): ") + dlerror();
+            return;
+        }
+#define LOAD(field, sym)                                                      \
+    api.field = reinterpret_cast<decltype(api.field)>(dlsym(h, sym));         \
+    if (!api.field) {                                                         \
+        api.why = "NCCL symbol missing: " sym;                                \
+        return;                                                               \
+    }
+        LOAD(GetUniqueId, "ncclGetUniqueId");
+        LOAD(CommInitRank, "ncclCommInitRank");
+        LOAD(CommDestroy, "ncclCommDestroy");
+        LOAD(Send, "ncclSend");
+        LOAD(Recv, "ncclRecv");
+        LOAD(AllReduce, "ncclAllReduce");
+        LOAD(GroupStart, "ncclGroupStart");
+        LOAD(GroupEnd, "ncclGroupEnd");
+        LOAD(GetErrorString, "ncclGetErrorString");
+#undef LOAD
+        api.ok = true;
+    });
+    return &api;
+}
+
+// ---------------------------------------------------------------------------
+// Lanczos estimate of cond(D^-1 A) from the CG coefficients (tridiagonal, Sturm bisection)
+// ---------------------------------------------------------------------------
+static int sturm_count(const std::vector<double> &a, const std::vector<double> &b, double x)
+{
+    int cnt = 0;
+    double d = 1.0;
+    for (size_t i = 0; i < a.size(); ++i) {
+        const double bb = i ? b[i - 1] * b[i - 1] : 0.0;
+        d = (a[i] - x) - (i ? bb / d : 0.0);
+        if (d == 0.0) d = -1e-300;
+        if (d < 0.0) ++cnt;
+    }
+    return cnt;
+}
+
+static double lanczos_kappa(const double *hist, int k)
+{
+    if (k < 2) return NAN;
+    std::vector<double> a(k), b(k - 1);
+    for (int j = 0; j < k; ++j) {
+        const double al = hist[2 * j], be_prev = j ? hist[2 * (j - 1) + 1] : 0.0, al_prev = j ? hist[2 * (j - 1)] : 1.0;
+        a[j] = 1.0 / al + (j ? be_prev / al_prev : 0.0);
+        if (j < k - 1) b[j] = std::sqrt(std::max(hist[2 * j + 1], 0.0)) / al;
+    }
+    double lo = 1e300, hi = -1e300;
+    for (int j = 0; j < k; ++j) {
+        const double r = (j ? std::fabs(b[j - 1]) : 0.0) + (j < k - 1 ? std::fabs(b[j]) : 0.0);
+        lo = std::min(lo, a[j] - r);
+        hi = std::max(hi, a[j] + r);
+    }
+    auto kth = [&](int idx) {  // idx-th smallest eigenvalue (0-based)
+        double l = lo, h = hi;
+        for (int it = 0; it < 200; ++it) {
+            const double mid = 0.5 * (l + h);
+            if (sturm_count(a, b, mid) > idx) h = mid;
+            else l = mid;
+        }
+        return 0.5 * (l + h);
+    };
+    const double emin = kth(0), emax = kth(k - 1);
+    return emin > 0.0 ? emax / emin : NAN;
+}
+
+}  // namespace dg
+
+using namespace dg;
+
+// ---------------------------------------------------------------------------
+// mesh
+// ---------------------------------------------------------------------------
+struct dg_mesh {
+    Geom g{};
+    int rank = 0, nranks = 1, device = 0;
+    long long el_off = 0, ndof = 0, ndof_global = 0, layer = 0;  // layer: doubles per slab layer
+    cudaStream_t st = nullptr;
+    // PCG workspace
+    double *r = nullptr, *q = nullptr, *pa = nullptr, *pb = nullptr, *dinv = nullptr;
+    double *partial = nullptr;
+    int partial_cap = 0;  // in doubles
+    double *sums = nullptr, *aux = nullptr, *mass_e = nullptr, *hist = nullptr;
+    int hist_cap = 0;
+    PcgScal *scal = nullptr, *hscal = nullptr;
+    // halos (multi-rank)
+    double *h_lo = nullptr, *h_hi = nullptr, *hn_lo = nullptr, *hn_hi = nullptr;
+    double *hv_lo[3] = {nullptr, nullptr, nullptr}, *hv_hi[3] = {nullptr, nullptr, nullptr};
+    ncclComm_t comm = nullptr;
+    // host-variant staging
+    double *st_a = nullptr, *st_b = nullptr, *st_c = nullptr;
+    int *d_flag = nullptr;
+    long long launches = 0;
+};
+
+#define CK(call)                                                                                         \
+    do {                                                                                                 \
+        cudaError_t _e = (call);                                                                         \
+        if (_e != cudaSuccess)                                                                           \
+            return set_error(_e == cudaErrorNotSupported ? DG_EUNSUPPORTED : DG_ECUDA,                  \
+                             std::string(#call) + ": " + cudaGetErrorString(_e));                        \
+    } while (0)
+
+#define CKN(call)                                                                                        \
+    do {                                                                                                 \
+        ncclResult_t _r = (call);                                                                        \
+        if (_r != ncclSuccess) return set_error(DG_ENCCL, std::string(#call) + ": " + nccl()->GetErrorString(_r)); \
+    } while (0)
+
+namespace {
+
+int smem_bytes(const Geom &g, bool varnu)
+{
+    const int n = g.n;
+    const int PX = (n % 2 == 0) ? n + 1 : n;
+    const int SPE = g.dim == 3 ? PX * n * n : PX * n;
+    const int BE = g.B[0] * g.B[1] * g.B[2];
+    return ((2 + (varnu ? 1 : 0)) * BE * SPE + 64 + g.npe) * 8;
+}
+
+void choose_bricks(Geom &g)
+{
+    const int BEmax = g.dim == 3 ? (g.n >= 7 ? 8 : 16) : (g.n >= 7 ? 16 : 32);
+    g.B[0] = g.B[1] = g.B[2] = 1;
+    for (;;) {
+        int best = -1;
+        for (int d = 0; d < g.dim; ++d) {
+            const int BE = g.B[0] * g.B[1] * g.B[2];
+            if (g.Nl[d] % (2 * g.B[d]) != 0 || 2 * BE > BEmax) continue;
+            Geom t = g;
+            t.B[d] *= 2;
+            if (smem_bytes(t, true) > 200 * 1024) continue;
+            if (best < 0 || g.B[d] < g.B[best]) best = d;
+        }
+        if (best < 0) break;
+        g.B[best] *= 2;
+    }
+    for (int d = 0; d < 3; ++d) g.nbk[d] = g.Nl[d] / g.B[d];
+}
+
+long long nbricks(const Geom &g) { return (long long)g.nbk[0] * g.nbk[1] * g.nbk[2]; }
+
+int apply_grid(const Geom &g)
+{
+    const long long nb = nbricks(g);
+    return (int)std::min<long long>(nb, 148LL * 16);
+}
+
+dg_status alloc(void **p, size_t bytes)
+{
+    if (cudaMalloc(p, bytes) != cudaSuccess) {
+        cudaGetLastError();
+        return set_error(DG_ENOMEM, "cudaMalloc of " + std::to_string(bytes) + " bytes failed");
+    }
+    return DG_OK;
+}
+
+#define CKS(x)                        \
+    do {                              \
+        dg_status _s = (x);           \
+        if (_s != DG_OK) return _s;   \
+    } while (0)
+
+dg_status ensure_workspace(dg_mesh *m)
+{
+    if (m->r) return DG_OK;
+    const size_t b = sizeof(double) * (size_t)m->ndof;
+    CKS(alloc((void **)&m->r, b));
+    CKS(alloc((void **)&m->q, b));
+    CKS(alloc((void **)&m->pa, b));
+    CKS(alloc((void **)&m->pb, b));
+    CKS(alloc((void **)&m->dinv, b));
+    return DG_OK;
+}
+
+dg_status ensure_hist(dg_mesh *m, int maxit)
+{
+    if (m->hist_cap >= maxit + 2) return DG_OK;
+    if (m->hist) cudaFree(m->hist);
+    m->hist = nullptr;
+    m->hist_cap = maxit + 2;
+    return alloc((void **)&m->hist, sizeof(double) * 2 * (size_t)m->hist_cap);
+}
+
+dg_status ensure_halos(dg_mesh *m, bool vel)
+{
+    if (m->nranks == 1) return DG_OK;
+    const size_t b = sizeof(double) * (size_t)m->layer;
+    if (!m->h_lo) {
+        CKS(alloc((void **)&m->h_lo, b));
+        CKS(alloc((void **)&m->h_hi, b));
+        CKS(alloc((void **)&m->hn_lo, b));
+        CKS(alloc((void **)&m->hn_hi, b));
+    }
+    if (vel && !m->hv_lo[0])
+        for (int c = 0; c < 3; ++c) {
+            CKS(alloc((void **)&m->hv_lo[c], b));
+            CKS(alloc((void **)&m->hv_hi[c], b));
+        }
+    return DG_OK;
+}
+
+// Exchange the first/last slab layers of `field` with the neighbouring ranks (periodic ring):
+// lo <- last layer of rank-1, hi <- first layer of rank+1.  Sends are posted as
+// (last -> next, first -> prev) and receives as (lo <- prev, hi <- next), so that with two
+// ranks (prev == next) the in-order matching per peer still pairs them correctly.
+dg_status exchange(dg_mesh *m, const double *field, double *lo, double *hi)
+{
+    NcclApi *nc = nccl();
+    const int R = m->nranks, prev = (m->rank - 1 + R) % R, next = (m->rank + 1) % R;
+    const int S = m->g.dim - 1;
+    const double *first = field, *last = field + (size_t)(m->g.Nl[S] - 1) * m->layer;
+    CKN(nc->GroupStart());
+    CKN(nc->Send(last, (size_t)m->layer, ncclDouble, next, m->comm, m->st));
+    CKN(nc->Send(first, (size_t)m->layer, ncclDouble, prev, m->comm, m->st));
+    CKN(nc->Recv(lo, (size_t)m->layer, ncclDouble, prev, m->comm, m->st));
+    CKN(nc->Recv(hi, (size_t)m->layer, ncclDouble, next, m->comm, m->st));
+    CKN(nc->GroupEnd());
+    return DG_OK;
+}
+
+dg_status allreduce(dg_mesh *m, double *buf, int count)
+{
+    if (m->nranks == 1) return DG_OK;
+    CKN(nccl()->AllReduce(buf, buf, (size_t)count, ncclDouble, ncclSum, m->comm, m->st));
+    return DG_OK;
+}
+
+dg_status check_common(dg_mesh *m, double lam, const double *nu, double nu_const)
+{
+    if (!m) return set_error(DG_EINVAL, "null mesh");
+    if (!(lam >= 0.0) || !std::isfinite(lam)) return set_error(DG_EINVAL, "lambda must be finite and >= 0");
+    if (!nu && !(nu_const > 0.0 && std::isfinite(nu_const)))
+        return set_error(DG_EINVAL, "nu_const must be finite and > 0 when nu == NULL");
+    return DG_OK;
+}
+
+dg_status run_apply(dg_mesh *m, double lam, const double *nu, double nu_const, const double *u, double *out,
+                    const Halo &halo, const DotEpi &epi, const PProl &pro, int grid)
+{
+    ApplyParams a{};
+    a.g = m->g;
+    a.lam = lam;
+    a.nu_const = nu_const;
+    a.u = u;
+    a.nu = nu;
+    a.out = out;
+    a.halo = halo;
+    a.epi = epi;
+    a.pro = pro;
+    a.b0 = 0;
+    a.b1 = nbricks(m->g);
+    const bool varnu = nu != nullptr;
+    const int smem = smem_bytes(m->g, varnu);
+    const cudaError_t e = m->g.dim == 3 ? launch_apply3(a, varnu, pro.on, grid, smem, m->st)
+                                        : launch_apply2(a, varnu, pro.on, grid, smem, m->st);
+    CK(e);
+    m->launches += 1;
+    return DG_OK;
+}
+
+dg_status apply_impl(dg_mesh *m, double lam, const double *nu, double nu_const, const double *u, double *out)
+{
+    Halo h;
+    if (m->nranks > 1) {
+        CKS(ensure_halos(m, false));
+        CKS(exchange(m, u, m->h_lo, m->h_hi));
+        h.u_lo = m->h_lo;
+        h.u_hi = m->h_hi;
+        if (nu) {
+            CKS(exchange(m, nu, m->hn_lo, m->hn_hi));
+            h.nu_lo = m->hn_lo;
+            h.nu_hi = m->hn_hi;
+        }
+    }
+    return run_apply(m, lam, nu, nu_const, u, out, h, DotEpi{}, PProl{}, apply_grid(m->g));
+}
+
+dg_status diag_impl(dg_mesh *m, double lam, const double *nu, double nu_const, double *diag)
+{
+    Halo h;
+    if (m->nranks > 1 && nu) {
+        CKS(ensure_halos(m, false));
+        CKS(exchange(m, nu, m->hn_lo, m->hn_hi));
+        h.nu_lo = m->hn_lo;
+        h.nu_hi = m->hn_hi;
+    }
+    CK(m->g.dim == 3 ? launch_diag3(m->g, lam, nu, nu_const, h, diag, m->st)
+                     : launch_diag2(m->g, lam, nu, nu_const, h, diag, m->st));
+    m->launches += 1;
+    return DG_OK;
+}
+
+// reduce partial[G][2] -> sums[2] (+ allreduce) -> finalize(mode)
+dg_status reduce_fin(dg_mesh *m, int G, int mode)
+{
+    if (m->nranks == 1) {
+        CK(launch_reduce_fin(m->partial, G, 2, m->sums, mode, m->scal, m->hist, m->aux, m->st));
+        m->launches += 1;
+    } else {
+        CK(launch_reduce_s(m->partial, G, 2, m->sums,
+                           (mode == FIN_ALPHA || mode == FIN_BETA) ? m->scal : nullptr, m->st));
+        CKS(allreduce(m, m->sums, 2));
+        CK(launch_finalize(mode, m->sums, m->scal, m->hist, m->aux, m->st));
+        m->launches += 2;
+    }
+    return DG_OK;
+}
+
+dg_status pcg_impl(dg_mesh *m, double lam, const double *nu, double nu_const, const double *f, double tol,
+                   int maxit, double *u, dg_solve_info *info)
+{
+    CKS(ensure_workspace(m));
+    CKS(ensure_hist(m, maxit));
+    const Geom &g = m->g;
+    const int VG = vec_grid();
+    const bool multi = m->nranks > 1;
+
+    // scalars
+    PcgScal s0{};
+    s0.lam = lam;
+    s0.tol2 = tol * tol;
+    s0.ndof_global = m->ndof_global;
+    s0.maxit = maxit;
+    CK(cudaMemcpyAsync(m->scal, &s0, sizeof(s0), cudaMemcpyHostToDevice, m->st));
+
+    // Jacobi preconditioner
+    CKS(diag_impl(m, lam, nu, nu_const, m->q));
+    CK(launch_recip(g, m->q, m->dinv, m->st));
+    m->launches += 1;
+    Halo hnu;
+    if (multi && nu) {  // diag_impl exchanged nu already
+        hnu.nu_lo = m->hn_lo;
+        hnu.nu_hi = m->hn_hi;
+    }
+    // f mean (lam == 0) and total mass
+    CK(launch_mass_moments(g, f, m->mass_e, m->partial, m->st));
+    m->launches += 1;
+    CKS(reduce_fin(m, VG, FIN_FMEAN));
+    // r = M (f - fmean) - A u
+    CKS(apply_impl(m, lam, nu, nu_const, u, m->q));
+    CK(launch_pcg_init(g, f, m->q, m->r, m->mass_e, m->scal, m->partial, m->st));
+    m->launches += 1;
+    CKS(reduce_fin(m, VG, FIN_INIT));
+    CK(launch_pcg_init2(g, m->r, m->dinv, nullptr, m->mass_e, m->scal, nullptr, m->partial, m->st));
+    m->launches += 1;
+    CKS(reduce_fin(m, VG, FIN_INIT2));
+    CK(cudaMemsetAsync(m->pa, 0, sizeof(double) * (size_t)m->ndof, m->st));
+
+    double *p_old = m->pa, *p_new = m->pb;
+    int chunk = 4;
+    for (;;) {
+        CK(cudaMemcpyAsync(m->hscal, m->scal, sizeof(PcgScal), cudaMemcpyDeviceToHost, m->st));
+        CK(cudaStreamSynchronize(m->st));
+        if (m->hscal->done) break;
+        for (int it = 0; it < chunk; ++it) {
+            if (!multi) {
+                // q = A p with p = dinv r + beta p_old (prologue), partials p.q, sum q (epilogue)
+                PProl pro;
+                pro.on = true;
+                pro.r = m->r;
+                pro.dinv = m->dinv;
+                pro.p_old = p_old;
+                pro.p_out = p_new;
+                pro.beta = &m->scal->beta;
+                pro.done = &m->scal->done;
+                DotEpi epi;
+                epi.partial = m->partial;
+                const int grid = apply_grid(g);
+                CKS(run_apply(m, lam, nu, nu_const, nullptr, m->q, Halo{}, epi, pro, grid));
+                CKS(reduce_fin(m, grid, FIN_ALPHA));
+                CK(launch_pcg_update(g, u, m->r, p_new, m->q, m->dinv, m->mass_e, m->scal, m->partial, m->st));
+                m->launches += 1;
+                CKS(reduce_fin(m, VG, FIN_BETA));
+                std::swap(p_old, p_new);
+            } else {
+                // unfused: p = dinv r + beta p ; halo(p) ; q = A p ; p.q
+                CK(launch_pcg_pupd(g, p_old, m->r, m->dinv, m->scal, m->st));
+                m->launches += 1;
+                CKS(ensure_halos(m, false));
+                CKS(exchange(m, p_old, m->h_lo, m->h_hi));
+                Halo h = hnu;
+                h.u_lo = m->h_lo;
+                h.u_hi = m->h_hi;
+                CKS(run_apply(m, lam, nu, nu_const, p_old, m->q, h, DotEpi{}, PProl{}, apply_grid(g)));
+                CK(launch_dot_pq(g, p_old, m->q, m->scal, m->partial, m->st));
+                m->launches += 1;
+                CKS(reduce_fin(m, VG, FIN_ALPHA));
+                CK(launch_pcg_update(g, u, m->r, p_old, m->q, m->dinv, m->mass_e, m->scal, m->partial, m->st));
+                m->launches += 1;
+                CKS(reduce_fin(m, VG, FIN_BETA));
+            }
+        }
+        chunk = std::min(chunk * 2, 32);
+    }
+    // lam == 0: zero mass-weighted mean of u
+    if (lam == 0.0) {
+        CK(launch_mass_moments(g, u, m->mass_e, m->partial, m->st));
+        m->launches += 1;
+        CKS(reduce_fin(m, VG, FIN_UMEAN));
+        CK(launch_shift(g, u, m->aux, m->st));
+        m->launches += 1;
+    }
+    CK(cudaMemcpyAsync(m->hscal, m->scal, sizeof(PcgScal), cudaMemcpyDeviceToHost, m->st));
+    CK(cudaStreamSynchronize(m->st));
+    const PcgScal hs = *m->hscal;
+    if (info) {
+        info->iters = hs.iter;
+        info->rel_res = hs.fnorm2 > 0 ? std::sqrt(hs.res2 / hs.fnorm2) : std::sqrt(hs.res2);
+        info->removed_mean = hs.fmean;
+        info->f_norm = std::sqrt(hs.fnorm2);
+        info->kappa_est = NAN;
+        if (hs.iter >= 2) {
+            std::vector<double> hh(2 * (size_t)hs.iter);
+            CK(cudaMemcpy(hh.data(), m->hist, sizeof(double) * hh.size(), cudaMemcpyDeviceToHost));
+            info->kappa_est = lanczos_kappa(hh.data(), hs.iter);
+        }
+    }
+    if (hs.status == PCG_ST_BREAKDOWN) return set_error(DG_EBREAKDOWN, "PCG breakdown (p.Ap <= 0 or non-finite)");
+    if (hs.status == PCG_ST_MAXIT)
+        return set_error(DG_ENOTCONV, "PCG reached maxit=" + std::to_string(maxit) + ", rel_res=" +
+                                          std::to_string(hs.fnorm2 > 0 ? std::sqrt(hs.res2 / hs.fnorm2) : 0.0));
+    return DG_OK;
+}
+
+dg_status stage(dg_mesh *m, double **buf, size_t bytes)
+{
+    if (*buf) return DG_OK;
+    return alloc((void **)buf, bytes);
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// C-ABI
+// ---------------------------------------------------------------------------
+extern "C" {
+
+const char *dg_last_error(void) { return g_err.c_str(); }
+
+const char *dg_version(void) { return "dgsip 0.1 (sm_100a, fp64)"; }
+
+dg_status dg_nccl_unique_id(unsigned char out[128])
+{
+    if (!out) return set_error(DG_EINVAL, "null output");
+    NcclApi *nc = nccl();
+    if (!nc->ok) return set_error(DG_ENCCL, nc->why);
+    ncclUniqueId id;
+    CKN(nc->GetUniqueId(&id));
+    static_assert(sizeof(id) == 128, "ncclUniqueId size");
+    std::memcpy(out, &id, 128);
+    return DG_OK;
+}
+
+dg_status dg_mesh_create(int dim, const int N[3], const double L[3], int P, int rank, int nranks,
+                         const unsigned char *nccl_uid, void *cuda_stream, dg_mesh **out)
+{
+    if (!out || !N || !L) return set_error(DG_EINVAL, "null argument");
+    *out = nullptr;
+    if (dim != 2 && dim != 3) return set_error(DG_EINVAL, "dim must be 2 or 3");
+    if (P < 1 || P > PMAX) return set_error(DG_EINVAL, "P must be in [1, 10]");
+    if (nranks < 1 || rank < 0 || rank >= nranks) return set_error(DG_EINVAL, "bad rank / nranks");
+    for (int d = 0; d < dim; ++d) {
+        if (N[d] < 1) return set_error(DG_EINVAL, "N[d] must be >= 1");
+        if (!(L[d] > 0.0) || !std::isfinite(L[d])) return set_error(DG_EINVAL, "L[d] must be > 0");
+    }
+    const int S = dim - 1;
+    if (N[S] % nranks != 0) return set_error(DG_EINVAL, "N of the slowest direction must be divisible by nranks");
+    if (nranks > 1 && !nccl_uid) return set_error(DG_EINVAL, "nccl_uid required when nranks > 1");
+
+    dg_mesh *m = new dg_mesh();
+    Geom &g = m->g;
+    g.dim = dim;
+    g.P = P;
+    g.n = P + 1;
+    g.npe = dim == 3 ? g.n * g.n * g.n : g.n * g.n;
+    for (int d = 0; d < 3; ++d) {
+        g.N[d] = d < dim ? N[d] : 1;
+        g.Nl[d] = g.N[d];
+        g.h[d] = d < dim ? L[d] / N[d] : 1.0;
+        g.tau[d] = (double)(P + 1) * (P + 1) / g.h[d];
+    }
+    g.Nl[S] = g.N[S] / nranks;
+    g.nel = (long long)g.Nl[0] * g.Nl[1] * g.Nl[2];
+    choose_bricks(g);
+    m->rank = rank;
+    m->nranks = nranks;
+    m->st = (cudaStream_t)cuda_stream;
+    m->ndof = g.nel * g.npe;
+    m->ndof_global = m->ndof * nranks;
+    m->layer = (S == 2 ? (long long)g.Nl[0] * g.Nl[1] : (long long)g.Nl[0]) * g.npe;
+    m->el_off = (long long)rank * g.nel;
+
+    auto fail = [&](dg_status s) {
+        dg_mesh_destroy(m);
+        return s;
+    };
+    cudaGetDevice(&m->device);
+    {
+        static std::mutex mu;
+        static std::vector<int> done;
+        std::lock_guard<std::mutex> lk(mu);
+        if (std::find(done.begin(), done.end(), m->device) == done.end()) {
+            cudaError_t e = upload_tables();
+            if (e != cudaSuccess) return fail(set_error(DG_ECUDA, std::string("table upload: ") + cudaGetErrorString(e)));
+            done.push_back(m->device);
+        }
+    }
+    const int pcap = 2 * std::max(apply_grid(g), vec_grid()) + 64;
+    dg_status s;
+    if ((s = alloc((void **)&m->partial, sizeof(double) * pcap)) != DG_OK) return fail(s);
+    m->partial_cap = pcap;
+    if ((s = alloc((void **)&m->sums, sizeof(double) * 8)) != DG_OK) return fail(s);
+    if ((s = alloc((void **)&m->aux, sizeof(double) * 8)) != DG_OK) return fail(s);
+    if ((s = alloc((void **)&m->scal, sizeof(PcgScal))) != DG_OK) return fail(s);
+    if ((s = alloc((void **)&m->mass_e, sizeof(double) * g.npe)) != DG_OK) return fail(s);
+    if ((s = alloc((void **)&m->d_flag, sizeof(int))) != DG_OK) return fail(s);
+    if (cudaMallocHost((void **)&m->hscal, sizeof(PcgScal)) != cudaSuccess)
+        return fail(set_error(DG_ENOMEM, "cudaMallocHost failed"));
+    {
+        // element-local mass table m_q = prod_d w h_d/2 (uniform mesh)
+        Geom g1 = g;
+        g1.nel = 1;
+        cudaError_t e = launch_mass(g1, m->mass_e, m->st);
+        if (e != cudaSuccess) return fail(set_error(DG_ECUDA, cudaGetErrorString(e)));
+        m->launches += 1;
+    }
+    if (nranks > 1) {
+        NcclApi *nc = nccl();
+        if (!nc->ok) return fail(set_error(DG_ENCCL, nc->why));
+        ncclUniqueId id;
+        std::memcpy(&id, nccl_uid, 128);
+        ncclResult_t r = nc->CommInitRank(&m->comm, nranks, id, rank);
+        if (r != ncclSuccess) return fail(set_error(DG_ENCCL, std::string("ncclCommInitRank: ") + nc->GetErrorString(r)));
+    }
+    *out = m;
+    return DG_OK;
+}
+
+void dg_mesh_destroy(dg_mesh *m)
+{
+    if (!m) return;
+    if (m->st) cudaStreamSynchronize(m->st);
+    else cudaDeviceSynchronize();
+    double *bufs[] = {m->r, m->q, m->pa, m->pb, m->dinv, m->partial, m->sums, m->aux, m->mass_e, m->hist,
+                      m->h_lo, m->h_hi, m->hn_lo, m->hn_hi, m->st_a, m->st_b, m->st_c};
+    for (double *b : bufs)
+        if (b) cudaFree(b);
+    for (int c = 0; c < 3; ++c) {
+        if (m->hv_lo[c]) cudaFree(m->hv_lo[c]);
+        if (m->hv_hi[c]) cudaFree(m->hv_hi[c]);
+    }
+    if (m->scal) cudaFree(m->scal);
+    if (m->d_flag) cudaFree(m->d_flag);
+    if (m->hscal) cudaFreeHost(m->hscal);
+    if (m->comm) nccl()->CommDestroy(m->comm);
+    delete m;
+}
+
+dg_status dg_mesh_set_stream(dg_mesh *m, void *cuda_stream)
+{
+    if (!m) return set_error(DG_EINVAL, "null mesh");
+    m->st = (cudaStream_t)cuda_stream;
+    return DG_OK;
+}
+
+long long dg_mesh_local_ndof(const dg_mesh *m) { return m ? m->ndof : -1; }
+long long dg_mesh_local_elements(const dg_mesh *m) { return m ? m->g.nel : -1; }
+long long dg_mesh_element_offset(const dg_mesh *m) { return m ? m->el_off : -1; }
+long long dg_mesh_launch_count(const dg_mesh *m) { return m ? m->launches : -1; }
+
+dg_status dg_mesh_node_coords(const dg_mesh *m, double *xyz)
+{
+    if (!m || !xyz) return set_error(DG_EINVAL, "null argument");
+    CK(launch_coords(m->g, m->el_off, xyz, m->st));
+    const_cast<dg_mesh *>(m)->launches += 1;
+    return DG_OK;
+}
+
+dg_status dg_mesh_mass(const dg_mesh *m, double *mass)
+{
+    if (!m || !mass) return set_error(DG_EINVAL, "null argument");
+    CK(launch_mass(m->g, mass, m->st));
+    const_cast<dg_mesh *>(m)->launches += 1;
+    return DG_OK;
+}
+
+dg_status dg_helmholtz_apply(dg_mesh *m, double lam, const double *nu, double nu_const, const double *u, double *out)
+{
+    CKS(check_common(m, lam, nu, nu_const));
+    if (!u || !out) return set_error(DG_EINVAL, "null field pointer");
+    if (u == out) return set_error(DG_EINVAL, "u and out must not alias");
+    return apply_impl(m, lam, nu, nu_const, u, out);
+}
+
+dg_status dg_helmholtz_diag(dg_mesh *m, double lam, const double *nu, double nu_const, double *diag)
+{
+    CKS(check_common(m, lam, nu, nu_const));
+    if (!diag) return set_error(DG_EINVAL, "null field pointer");
+    return diag_impl(m, lam, nu, nu_const, diag);
+}
+
+dg_status dg_pcg_solve(dg_mesh *m, double lam, const double *nu, double nu_const, const double *f, double tol,
+                       int maxit, double *u, dg_solve_info *info)
+{
+    CKS(check_common(m, lam, nu, nu_const));
+    if (!f || !u) return set_error(DG_EINVAL, "null field pointer");
+    if (!(tol > 0.0)) return set_error(DG_EINVAL, "tol must be > 0");
+    if (maxit < 1) return set_error(DG_EINVAL, "maxit must be >= 1");
+    return pcg_impl(m, lam, nu, nu_const, f, tol, maxit, u, info);
+}
+
+dg_status dg_convect_rhs(dg_mesh *m, const double *const v[3], double *const out[3])
+{
+    if (!m || !v || !out) return set_error(DG_EINVAL, "null argument");
+    const int dim = m->g.dim;
+    for (int c = 0; c < dim; ++c) {
+        if (!v[c] || !out[c]) return set_error(DG_EINVAL, "null component pointer");
+        for (int c2 = 0; c2 < dim; ++c2)
+            if (out[c] == v[c2]) return set_error(DG_EINVAL, "out must not alias v");
+    }
+    ConvParams a{};
+    a.g = m->g;
+    for (int c = 0; c < 3; ++c) {
+        a.v[c] = c < dim ? v[c] : nullptr;
+        a.out[c] = c < dim ? out[c] : nullptr;
+    }
+    if (m->nranks > 1) {
+        CKS(ensure_halos(m, true));
+        for (int c = 0; c < dim; ++c) {
+            CKS(exchange(m, v[c], m->hv_lo[c], m->hv_hi[c]));
+            a.lo[c] = m->hv_lo[c];
+            a.hi[c] = m->hv_hi[c];
+        }
+    }
+    CK(launch_convect_k(a, m->st));
+    m->launches += 1;
+    return DG_OK;
+}
+
+dg_status dg_helmholtz_apply_host(dg_mesh *m, double lam, const double *nu_host, double nu_const,
+                                  const double *u_host, double *out_host)
+{
+    CKS(check_common(m, lam, nu_host, nu_const));
+    if (!u_host || !out_host) return set_error(DG_EINVAL, "null field pointer");
+    const size_t b = sizeof(double) * (size_t)m->ndof;
+    CKS(stage(m, &m->st_a, b));
+    CKS(stage(m, &m->st_b, b));
+    if (nu_host) CKS(stage(m, &m->st_c, b));
+    CK(cudaMemcpyAsync(m->st_a, u_host, b, cudaMemcpyHostToDevice, m->st));
+    if (nu_host) CK(cudaMemcpyAsync(m->st_c, nu_host, b, cudaMemcpyHostToDevice, m->st));
+    CKS(apply_impl(m, lam, nu_host ? m->st_c : nullptr, nu_const, m->st_a, m->st_b));
+    CK(cudaMemcpyAsync(out_host, m->st_b, b, cudaMemcpyDeviceToHost, m->st));
+    CK(cudaStreamSynchronize(m->st));
+    return DG_OK;
+}
+
+dg_status dg_pcg_solve_host(dg_mesh *m, double lam, const double *nu_host, double nu_const, const double *f_host,
+                            double tol, int maxit, double *u_host, dg_solve_info *info)
+{
+    CKS(check_common(m, lam, nu_host, nu_const));
+    if (!f_host || !u_host) return set_error(DG_EINVAL, "null field pointer");
+    if (!(tol > 0.0)) return set_error(DG_EINVAL, "tol must be > 0");
+    if (maxit < 1) return set_error(DG_EINVAL, "maxit must be >= 1");
+    const size_t b = sizeof(double) * (size_t)m->ndof;
+    CKS(stage(m, &m->st_a, b));
+    CKS(stage(m, &m->st_b, b));
+    if (nu_host) CKS(stage(m, &m->st_c, b));
+    CK(cudaMemcpyAsync(m->st_a, f_host, b, cudaMemcpyHostToDevice, m->st));
+    CK(cudaMemcpyAsync(m->st_b, u_host, b, cudaMemcpyHostToDevice, m->st));
+    if (nu_host) CK(cudaMemcpyAsync(m->st_c, nu_host, b, cudaMemcpyHostToDevice, m->st));
+    dg_status s = pcg_impl(m, lam, nu_host ? m->st_c : nullptr, nu_const, m->st_a, tol, maxit, m->st_b, info);
+    if (s != DG_OK && s != DG_ENOTCONV) return s;
+    CK(cudaMemcpyAsync(u_host, m->st_b, b, cudaMemcpyDeviceToHost, m->st));
+    CK(cudaStreamSynchronize(m->st));
+    return s;
+}
+
+dg_status dg_gll_tables(int P, double *xi, double *w, double *D)
+{
+    if (P < 1 || P > PMAX) return set_error(DG_EINVAL, "P must be in [1, 10]");
+    if (!xi || !w || !D) return set_error(DG_EINVAL, "null argument");
+    const Tab &t = host_tab(P);
+    for (int i = 0; i <= P; ++i) {
+        xi[i] = t.xi[i];
+        w[i] = t.w[i];
+        for (int j = 0; j <= P; ++j) D[i * (P + 1) + j] = t.D[i][j];
+    }
+    return DG_OK;
+}
+
+dg_status dg_check_field(dg_mesh *m, const double *x, int positive)
+{
+    if (!m || !x) return set_error(DG_EINVAL, "null argument");
+    CK(cudaMemsetAsync(m->d_flag, 0, sizeof(int), m->st));
+    CK(launch_check_field(m->ndof, x, positive, m->d_flag, m->st));
+    m->launches += 1;
+    int bad = 0;
+    CK(cudaMemcpyAsync(&bad, m->d_flag, sizeof(int), cudaMemcpyDeviceToHost, m->st));
+    CK(cudaStreamSynchronize(m->st));
+    if (bad) return set_error(DG_EINVAL, positive ? "field has non-finite or non-positive entries"
+                                                  : "field has non-finite entries");
+    return DG_OK;
+}
+
+}  // extern "C"

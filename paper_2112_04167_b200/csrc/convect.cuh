@@ -1,0 +1,338 @@
+// convect.cuh -- explicit DG convective tendency with local Lax-Friedrichs fluxes.
+//
+// F_c = -div(v v), DG-SEM "with consistent integration and local Lax-Friedrichs
+// fluxes for convection":
+//   M F_c,c = sum_K sum_{q in Gauss^d} W_q sum_e v_c v_e d_e phi_I
+//           - sum_F sum_{q in Gauss^{d-1}} W_q h_c [phi_I],
+//   h = 1/2 ((v^-.n) v^- + (v^+.n) v^+) + 1/2 Lambda (v^- - v^+), Lambda = 2 max|v^+-.n|
+// (readings A12-A14: Q = floor(3P/2)+1 Gauss points per direction, GLL-lumped M).
+//
+// One CTA per element.  Sum-factorised: v is interpolated GLL -> Gauss by three 1-D
+// contractions with Bq; the volume term is tested back with three passes that apply
+// Bq^T or Gq^T per direction, the three directional terms sharing the x pass; each face
+// interpolates its own and the neighbour's trace (GLL end nodes are exact traces) to the
+// face Gauss points, forms the LLF flux and projects back with Bq^T.  FP64-ALU bound
+// (~400 flop per component-DOF at P=7), shared-memory resident.
+#pragma once
+
+#include "dev_common.cuh"
+
+namespace dg {
+
+template <int DIM, int P>
+struct CCfg {
+    static constexpr int n = P + 1;
+    static constexpr int Q = (3 * P) / 2 + 1;
+    static constexpr int NZ = DIM == 3 ? n : 1;
+    static constexpr int QZ = DIM == 3 ? Q : 1;
+    static constexpr int NPE = n * n * NZ;
+    static constexpr int NQ = Q * Q * QZ;
+    static constexpr int T12 = 3 * NZ * n * Q + 3 * NZ * Q * Q;
+    static constexpr int STG = (DIM == 3) ? (3 * n * Q * Q + 2 * n * n * Q) : (2 * n * Q);
+    static constexpr int FACE = 2 * 3 * n * n + 2 * 3 * n * Q + 2 * 3 * Q * Q + 3 * Q * Q + 3 * Q * n;
+    static constexpr int SCR = T12 > STG ? (T12 > FACE ? T12 : FACE) : (STG > FACE ? STG : FACE);
+    static constexpr int SMEM = (3 * NPE + 3 * NQ + 3 * NPE + SCR + 2 * Q * n + Q) * 8;
+};
+
+template <int DIM, int P>
+__global__ void __launch_bounds__(256) k_convect(const ConvParams a)
+{
+    using C = CCfg<DIM, P>;
+    constexpr int n = C::n, Q = C::Q, NZ = C::NZ, QZ = C::QZ, NPE = C::NPE, NQ = C::NQ;
+    const Geom &g = a.g;
+    const DevTab &T = c_tab[P];
+    extern __shared__ double sm[];
+    double *sv = sm;                 // [3][NPE]
+    double *vg = sv + 3 * NPE;       // [3][NQ]
+    double *sy = vg + 3 * NQ;        // [3][NPE]
+    double *scr = sy + 3 * NPE;      // scratch
+    double *sB = scr + C::SCR;       // [Q][n] interpolation, staged from __constant__
+    double *sG = sB + Q * n;         // [Q][n] derivative interpolation
+    double *swq = sG + Q * n;        // [Q] Gauss weights
+    const int tid = threadIdx.x, nth = blockDim.x;
+    for (int t = tid; t < Q * n; t += nth) {
+        sB[t] = T.Bq[t / n][t % n];
+        sG[t] = T.Gq[t / n][t % n];
+    }
+    for (int t = tid; t < Q; t += nth) swq[t] = T.wq[t];
+
+    for (long long e = blockIdx.x; e < g.nel; e += gridDim.x) {
+        const int ec[3] = {(int)(e % g.Nl[0]), (int)((e / g.Nl[0]) % g.Nl[1]),
+                           (int)(e / ((long long)g.Nl[0] * g.Nl[1]))};
+        __syncthreads();
+        for (int t = tid; t < DIM * NPE; t += nth) {
+            const int c = t / NPE, q = t - c * NPE;
+            sv[t] = a.v[c][e * NPE + q];
+            sy[t] = 0.0;
+        }
+        __syncthreads();
+        // ---- interpolate to Gauss points: T1[c][k][j][qx], T2[c][k][qy][qx], vg[c][qz][qy][qx]
+        double *T1 = scr, *T2 = scr + 3 * NZ * n * Q;
+        for (int t = tid; t < DIM * NZ * n * Q; t += nth) {
+            const int qx = t % Q, j = (t / Q) % n, k = (t / (Q * n)) % NZ, c = t / (Q * n * NZ);
+            const double *src = sv + c * NPE + n * (j + n * k);
+            double s = 0.0;
+#pragma unroll
+            for (int i = 0; i < n; ++i) s = fma(sB[(qx) * n + (i)], src[i], s);
+            T1[t] = s;
+        }
+        __syncthreads();
+        for (int t = tid; t < DIM * NZ * Q * Q; t += nth) {
+            const int qx = t % Q, qy = (t / Q) % Q, k = (t / (Q * Q)) % NZ, c = t / (Q * Q * NZ);
+            const double *src = T1 + ((c * NZ + k) * n) * Q + qx;
+            double s = 0.0;
+#pragma unroll
+            for (int j = 0; j < n; ++j) s = fma(sB[(qy) * n + (j)], src[j * Q], s);
+            if (DIM == 3) T2[t] = s;
+            else vg[c * NQ + qx + Q * qy] = s;
+        }
+        __syncthreads();
+        if (DIM == 3) {
+            for (int t = tid; t < DIM * NQ; t += nth) {
+                const int qx = t % Q, qy = (t / Q) % Q, qz = (t / (Q * Q)) % QZ, c = t / NQ;
+                const double *src = T2 + (c * NZ) * Q * Q + qx + Q * qy;
+                double s = 0.0;
+#pragma unroll
+                for (int k = 0; k < NZ; ++k) s = fma(sB[(qz) * n + (k)], src[k * Q * Q], s);
+                vg[t] = s;
+            }
+            __syncthreads();
+        }
+        // ---- volume term, one component at a time
+        const double hx2 = 0.5 * g.h[0], hy2 = 0.5 * g.h[1], hz2 = DIM == 3 ? 0.5 * g.h[2] : 1.0;
+        const double Wc = hx2 * hy2 * hz2;
+        for (int c = 0; c < DIM; ++c) {
+            if (DIM == 3) {
+                double *Ax = scr, *Ay = Ax + n * Q * Q, *Az = Ay + n * Q * Q;
+                double *D1 = Az + n * Q * Q, *D2 = D1 + n * n * Q;
+                for (int t = tid; t < n * Q * Q; t += nth) {
+                    const int qx = t % Q, qy = (t / Q) % Q, k = t / (Q * Q);
+                    double sx = 0.0, sy_ = 0.0, sz = 0.0;
+                    const double wxy = swq[qx] * swq[qy] * Wc;
+#pragma unroll
+                    for (int qz = 0; qz < QZ; ++qz) {
+                        const int qi = qx + Q * (qy + Q * qz);
+                        const double vc = vg[c * NQ + qi];
+                        const double w = wxy * swq[qz] * vc;
+                        const double fx = w * vg[0 * NQ + qi], fy = w * vg[1 * NQ + qi], fz = w * vg[2 * NQ + qi];
+                        sx = fma(sB[(qz) * n + (k)], fx, sx);
+                        sy_ = fma(sB[(qz) * n + (k)], fy, sy_);
+                        sz = fma(sG[(qz) * n + (k)], fz, sz);
+                    }
+                    Ax[t] = sx;
+                    Ay[t] = sy_;
+                    Az[t] = sz * (2.0 / g.h[2]);
+                }
+                __syncthreads();
+                for (int t = tid; t < n * n * Q; t += nth) {
+                    const int qx = t % Q, j = (t / Q) % n, k = t / (Q * n);
+                    double d1 = 0.0, d2a = 0.0, d2b = 0.0;
+#pragma unroll
+                    for (int qy = 0; qy < Q; ++qy) {
+                        const int si = qx + Q * (qy + Q * k);
+                        d1 = fma(sB[(qy) * n + (j)], Ax[si], d1);
+                        d2a = fma(sG[(qy) * n + (j)], Ay[si], d2a);
+                        d2b = fma(sB[(qy) * n + (j)], Az[si], d2b);
+                    }
+                    D1[t] = d1;
+                    D2[t] = fma(d2a, 2.0 / g.h[1], d2b);
+                }
+                __syncthreads();
+                for (int t = tid; t < NPE; t += nth) {
+                    const int i = t % n, j = (t / n) % n, k = t / (n * n);
+                    double s1 = 0.0, s2 = 0.0;
+#pragma unroll
+                    for (int qx = 0; qx < Q; ++qx) {
+                        const int si = qx + Q * (j + n * k);
+                        s1 = fma(sG[(qx) * n + (i)], D1[si], s1);
+                        s2 = fma(sB[(qx) * n + (i)], D2[si], s2);
+                    }
+                    sy[c * NPE + t] += fma(s1, 2.0 / g.h[0], s2);
+                }
+                __syncthreads();
+            } else {
+                double *D1 = scr, *D2 = scr + n * Q;
+                for (int t = tid; t < n * Q; t += nth) {
+                    const int qx = t % Q, j = t / Q;
+                    double d1 = 0.0, d2 = 0.0;
+#pragma unroll
+                    for (int qy = 0; qy < Q; ++qy) {
+                        const int qi = qx + Q * qy;
+                        const double w = swq[qx] * swq[qy] * Wc * vg[c * NQ + qi];
+                        d1 = fma(sB[(qy) * n + (j)], w * vg[0 * NQ + qi], d1);
+                        d2 = fma(sG[(qy) * n + (j)], w * vg[1 * NQ + qi], d2);
+                    }
+                    D1[t] = d1;
+                    D2[t] = d2 * (2.0 / g.h[1]);
+                }
+                __syncthreads();
+                for (int t = tid; t < NPE; t += nth) {
+                    const int i = t % n, j = t / n;
+                    double s1 = 0.0, s2 = 0.0;
+#pragma unroll
+                    for (int qx = 0; qx < Q; ++qx) {
+                        s1 = fma(sG[(qx) * n + (i)], D1[qx + Q * j], s1);
+                        s2 = fma(sB[(qx) * n + (i)], D2[qx + Q * j], s2);
+                    }
+                    sy[c * NPE + t] += fma(s1, 2.0 / g.h[0], s2);
+                }
+                __syncthreads();
+            }
+        }
+        // ---- faces
+        constexpr int NF = DIM == 3 ? n * n : n;  // face nodes
+        constexpr int QF = DIM == 3 ? Q * Q : Q;  // face Gauss points
+        double *fo = scr, *fn = fo + 3 * NF;               // [3][NF] own / neighbour traces
+        double *F1o = fn + 3 * NF, *F1n = F1o + 3 * n * Q; // 3-D intermediates [3][b][qa]
+        double *Go = F1n + 3 * n * Q, *Gn = Go + 3 * QF;   // [3][QF]
+        double *H = Gn + 3 * QF;                           // [3][QF]
+        double *P1 = H + 3 * QF;                           // [3][qb][a]
+        for (int d = 0; d < DIM; ++d) {
+            const int o1 = (d == 0) ? 1 : 0;
+            const int o2 = (d == 2) ? 1 : 2;
+            const double ho1 = 0.5 * g.h[o1], ho2 = DIM == 3 ? 0.5 * g.h[o2] : 1.0;
+            for (int side = -1; side <= 1; side += 2) {
+                const int a_own = side > 0 ? P : 0, a_nb = side > 0 ? 0 : P;
+                int cn[3] = {ec[0], ec[1], ec[2]};
+                cn[d] += side;
+                for (int t = tid; t < DIM * NF; t += nth) {
+                    const int c = t / NF, f = t - c * NF;
+                    const int fa = f % n, fb = f / n;
+                    int nd[3] = {0, 0, 0};
+                    nd[o1] = fa;
+                    if (DIM == 3) nd[o2] = fb;
+                    nd[d] = a_own;
+                    const int qo = nd[0] + n * (nd[1] + n * nd[2]);
+                    nd[d] = a_nb;
+                    const int qn = nd[0] + n * (nd[1] + n * nd[2]);
+                    fo[t] = sv[c * NPE + qo];
+                    fn[t] = __ldg(elem_ptr(g, a.v[c], a.lo[c], a.hi[c], cn[0], cn[1], cn[2]) + qn);
+                }
+                __syncthreads();
+                if (DIM == 3) {
+                    for (int t = tid; t < 2 * DIM * n * Q; t += nth) {
+                        const int side2 = t / (DIM * n * Q), r = t - side2 * DIM * n * Q;
+                        const int qa = r % Q, b = (r / Q) % n, c = r / (Q * n);
+                        const double *src = (side2 ? fn : fo) + c * NF + b * n;
+                        double s = 0.0;
+#pragma unroll
+                        for (int aa = 0; aa < n; ++aa) s = fma(sB[(qa) * n + (aa)], src[aa], s);
+                        (side2 ? F1n : F1o)[r] = s;
+                    }
+                    __syncthreads();
+                    for (int t = tid; t < 2 * DIM * QF; t += nth) {
+                        const int side2 = t / (DIM * QF), r = t - side2 * DIM * QF;
+                        const int qa = r % Q, qb = (r / Q) % Q, c = r / QF;
+                        const double *src = (side2 ? F1n : F1o) + c * n * Q + qa;
+                        double s = 0.0;
+#pragma unroll
+                        for (int b = 0; b < n; ++b) s = fma(sB[(qb) * n + (b)], src[b * Q], s);
+                        (side2 ? Gn : Go)[r] = s;
+                    }
+                } else {
+                    for (int t = tid; t < 2 * DIM * QF; t += nth) {
+                        const int side2 = t / (DIM * QF), r = t - side2 * DIM * QF;
+                        const int qa = r % Q, c = r / Q;
+                        const double *src = (side2 ? fn : fo) + c * NF;
+                        double s = 0.0;
+#pragma unroll
+                        for (int aa = 0; aa < n; ++aa) s = fma(sB[(qa) * n + (aa)], src[aa], s);
+                        (side2 ? Gn : Go)[r] = s;
+                    }
+                }
+                __syncthreads();
+                for (int t = tid; t < QF; t += nth) {
+                    const int qa = t % Q, qb = t / Q;
+                    const double WF = swq[qa] * ho1 * (DIM == 3 ? swq[qb] * ho2 : 1.0);
+                    const double sgn = side > 0 ? 1.0 : -1.0;
+                    const double *vm = side > 0 ? Go : Gn, *vp = side > 0 ? Gn : Go;
+                    const double vnm = vm[d * QF + t], vnp = vp[d * QF + t];
+                    const double Lam = 2.0 * fmax(fabs(vnm), fabs(vnp));
+                    for (int c = 0; c < DIM; ++c) {
+                        const double hc = 0.5 * (vnm * vm[c * QF + t] + vnp * vp[c * QF + t]) +
+                                          0.5 * Lam * (vm[c * QF + t] - vp[c * QF + t]);
+                        H[c * QF + t] = sgn * WF * hc;
+                    }
+                }
+                __syncthreads();
+                if (DIM == 3) {
+                    for (int t = tid; t < DIM * Q * n; t += nth) {
+                        const int aa = t % n, qb = (t / n) % Q, c = t / (n * Q);
+                        const double *src = H + c * QF + Q * qb;
+                        double s = 0.0;
+#pragma unroll
+                        for (int qa = 0; qa < Q; ++qa) s = fma(sB[(qa) * n + (aa)], src[qa], s);
+                        P1[t] = s;
+                    }
+                    __syncthreads();
+                }
+                for (int t = tid; t < DIM * NF; t += nth) {
+                    const int c = t / NF, f = t - c * NF;
+                    const int fa = f % n, fb = f / n;
+                    double s = 0.0;
+                    if (DIM == 3) {
+                        const double *src = P1 + c * Q * n + fa;
+#pragma unroll
+                        for (int qb = 0; qb < Q; ++qb) s = fma(sB[(qb) * n + (fb)], src[qb * n], s);
+                    } else {
+                        const double *src = H + c * QF;
+#pragma unroll
+                        for (int qa = 0; qa < Q; ++qa) s = fma(sB[(qa) * n + (fa)], src[qa], s);
+                    }
+                    int nd[3] = {0, 0, 0};
+                    nd[o1] = fa;
+                    if (DIM == 3) nd[o2] = fb;
+                    nd[d] = a_own;
+                    sy[c * NPE + nd[0] + n * (nd[1] + n * nd[2])] -= s;
+                }
+                __syncthreads();
+            }
+        }
+        // ---- M^-1 (GLL-lumped) and store
+        for (int t = tid; t < DIM * NPE; t += nth) {
+            const int c = t / NPE, q = t - c * NPE;
+            const int i = q % n, j = (q / n) % n, k = q / (n * n);
+            double m = T.w[i] * hx2 * T.w[j] * hy2;
+            if (DIM == 3) m *= T.w[k] * hz2;
+            a.out[c][e * NPE + q] = sy[t] / m;
+        }
+    }
+}
+
+template <int DIM>
+struct ConvDispatch {
+    template <int P>
+    static cudaError_t go(const ConvParams &a, cudaStream_t st)
+    {
+        constexpr int smem = CCfg<DIM, P>::SMEM;
+        if constexpr (smem > 227 * 1024) {
+            return cudaErrorNotSupported;  // shared-memory tile too large (3-D P=10)
+        } else {
+        auto kern = k_convect<DIM, P>;
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (e != cudaSuccess) return e;
+        long long grid = a.g.nel;
+        if (grid > 148 * 16) grid = 148 * 16;
+        kern<<<(int)grid, 256, smem, st>>>(a);
+        return cudaGetLastError();
+        }
+    }
+    static cudaError_t run(const ConvParams &a, cudaStream_t st)
+    {
+        switch (a.g.P) {
+        case 1: if constexpr (DG_HAS_P(1)) return go<1>(a, st); else return cudaErrorNotSupported;
+        case 2: if constexpr (DG_HAS_P(2)) return go<2>(a, st); else return cudaErrorNotSupported;
+        case 3: if constexpr (DG_HAS_P(3)) return go<3>(a, st); else return cudaErrorNotSupported;
+        case 4: if constexpr (DG_HAS_P(4)) return go<4>(a, st); else return cudaErrorNotSupported;
+        case 5: if constexpr (DG_HAS_P(5)) return go<5>(a, st); else return cudaErrorNotSupported;
+        case 6: if constexpr (DG_HAS_P(6)) return go<6>(a, st); else return cudaErrorNotSupported;
+        case 7: if constexpr (DG_HAS_P(7)) return go<7>(a, st); else return cudaErrorNotSupported;
+        case 8: if constexpr (DG_HAS_P(8)) return go<8>(a, st); else return cudaErrorNotSupported;
+        case 9: if constexpr (DG_HAS_P(9)) return go<9>(a, st); else return cudaErrorNotSupported;
+        case 10: if constexpr (DG_HAS_P(10)) return go<10>(a, st); else return cudaErrorNotSupported;
+        default: return cudaErrorInvalidValue;
+        }
+    }
+};
+
+}  // namespace dg

@@ -1,0 +1,146 @@
+// dg_internal.h -- internal declarations of libdgsip.so (product path; no oracle code).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+
+#include "dg.h"
+
+namespace dg {
+
+constexpr int PMAX = 10;         // highest compiled degree
+constexpr int NMAX = PMAX + 1;   // GLL points per direction
+constexpr int QMAX = (3 * PMAX) / 2 + 1;  // Gauss points for convection (reading A13)
+
+// Per-degree 1-D tables (host copy; uploaded to __constant__ memory by the kernels TU).
+struct Tab {
+    double xi[NMAX];          // GLL nodes on [-1,1]
+    double w[NMAX];           // GLL weights
+    double D[NMAX][NMAX];     // D[i][j] = l_j'(xi_i), closed form
+    int Q;                    // Gauss points, floor(3P/2)+1        (reading A13)
+    double zq[QMAX];          // Gauss nodes
+    double wq[QMAX];          // Gauss weights
+    double Bq[QMAX][NMAX];    // Bq[q][j] = l_j(zq_q)  (barycentric form)
+    double Gq[QMAX][NMAX];    // Gq[q][j] = l_j'(zq_q) = (Bq D)[q][j]
+};
+
+// tables.cpp
+void build_tab(int P, Tab *t);
+const Tab &host_tab(int P);
+
+// error plumbing (capi.cpp)
+dg_status set_error(dg_status s, const std::string &msg);
+
+// ---------------------------------------------------------------------------
+// kernel launch interface (kernels.cu)
+// ---------------------------------------------------------------------------
+struct Geom {
+    int dim, P, n, npe;
+    int N[3];        // global elements per direction (N[2] = 1 in 2-D)
+    int Nl[3];       // local elements per direction (slowest one split by ranks)
+    int B[3];        // brick (elements per CTA) per direction
+    int nbk[3];      // bricks per direction (local)
+    double h[3];     // element size per direction
+    double tau[3];   // penalty (P+1)^2 / h_d (reading A1)
+    long long nel;   // local elements
+};
+
+struct Halo {        // neighbour element layers of the slowest direction (multi-rank)
+    const double *u_lo = nullptr, *u_hi = nullptr;
+    const double *nu_lo = nullptr, *nu_hi = nullptr;
+};
+
+// Fused epilogue for the PCG apply: partial[blk*2 + 0] += dotv . out,  partial[blk*2+1] += sum(out)
+struct DotEpi {
+    const double *dotv = nullptr;
+    double *partial = nullptr;
+};
+
+// Prologue for the PCG apply: the operand is p = dinv .* r + beta * p_old (computed on the
+// fly, also for neighbour lines), and p is written to p_out for the owned elements.
+struct PProl {
+    bool on = false;
+    const double *r = nullptr, *dinv = nullptr, *p_old = nullptr;
+    double *p_out = nullptr;
+    const double *beta = nullptr;  // device scalar
+    const int *done = nullptr;     // device flag: skip all work when set
+};                                 // (single-rank only; multi-rank runs the unfused path)
+
+struct ApplyParams {
+    Geom g;
+    double lam, nu_const;
+    const double *u, *nu;
+    double *out;
+    Halo halo;
+    DotEpi epi;
+    PProl pro;
+    long long b0, b1;   // brick range [b0, b1)
+};
+
+struct ConvParams {
+    Geom g;
+    const double *v[3];
+    double *out[3];
+    const double *lo[3];
+    const double *hi[3];
+};
+
+// apply2.cu / apply3.cu / convect.cu
+cudaError_t launch_apply2(const ApplyParams &a, bool varnu, bool pcg, int grid, int smem, cudaStream_t st);
+cudaError_t launch_apply3(const ApplyParams &a, bool varnu, bool pcg, int grid, int smem, cudaStream_t st);
+cudaError_t launch_diag2(const Geom &g, double lam, const double *nu, double nuc, const Halo &h, double *d,
+                         cudaStream_t st);
+cudaError_t launch_diag3(const Geom &g, double lam, const double *nu, double nuc, const Halo &h, double *d,
+                         cudaStream_t st);
+cudaError_t launch_convect_k(const ConvParams &a, cudaStream_t st);
+cudaError_t launch_coords(const Geom &g, long long el_offset, double *xyz, cudaStream_t st);
+cudaError_t launch_mass(const Geom &g, double *mass, cudaStream_t st);
+cudaError_t upload_tables();   // all kernel TUs (capi.cpp)
+cudaError_t upload_tables_vec();
+cudaError_t upload_tables_apply2();
+cudaError_t upload_tables_apply3();
+cudaError_t upload_tables_convect();
+
+// PCG vector kernels -------------------------------------------------------
+struct PcgScal {                 // device-resident scalars of one solve
+    double rz, pq, alpha, beta, qmean, res2, fnorm2, fmean, sum_m, tol2;
+    double lam;
+    long long ndof_global;
+    int iter, done, status, maxit;
+};
+enum { PCG_ST_RUN = 0, PCG_ST_CONV = 1, PCG_ST_MAXIT = 2, PCG_ST_BREAKDOWN = 3 };
+
+int vec_grid();
+// partial sums of m*f and m over the local slab -> partial[blk*2 + {0,1}]
+cudaError_t launch_mass_moments(const Geom &g, const double *f, const double *mass_e, double *partial,
+                                cudaStream_t st);
+// r = m (f - fmean) - Ar ; partial: sum r, sum (f-fmean)^2
+cudaError_t launch_pcg_init(const Geom &g, const double *f, const double *Ar, double *r, const double *mass_e,
+                            const PcgScal *s, double *partial, cudaStream_t st);
+// r -= rsum/N (lam==0) ; z = dinv r ; p = z ; partial: r.z, sum (r/m)^2
+cudaError_t launch_pcg_init2(const Geom &g, double *r, const double *dinv, double *p, const double *mass_e,
+                             const PcgScal *s, const double *rsum_global, double *partial, cudaStream_t st);
+// x += a p ; r -= a (q - qmean) ; partial: r.(dinv r), sum (r/m)^2
+cudaError_t launch_pcg_update(const Geom &g, double *x, double *r, const double *p, const double *q,
+                              const double *dinv, const double *mass_e, const PcgScal *s, double *partial,
+                              cudaStream_t st);
+// u -= (sum m u)/(sum m)  (lam == 0), partial for the moment is computed separately
+cudaError_t launch_shift(const Geom &g, double *x, const double *shift, cudaStream_t st);
+// deterministic reduction of partial[G][K] into sums[K] (single CTA, fixed order)
+cudaError_t launch_reduce(const double *partial, int G, int K, double *sums, cudaStream_t st);
+// scalar finalisation steps (single thread), mode-dependent
+enum FinMode { FIN_FMEAN = 0, FIN_INIT = 1, FIN_INIT2 = 2, FIN_ALPHA = 3, FIN_BETA = 4, FIN_UMEAN = 5 };
+cudaError_t launch_finalize(int mode, const double *sums, PcgScal *s, double *hist, double *aux, cudaStream_t st);
+cudaError_t launch_reduce_s(const double *partial, int G, int K, double *sums, const PcgScal *s, cudaStream_t st);
+cudaError_t launch_reduce_fin(const double *partial, int G, int K, double *sums, int mode, PcgScal *s, double *hist,
+                              double *aux, cudaStream_t st);
+cudaError_t launch_pcg_pupd(const Geom &g, double *p, const double *r, const double *dinv, const PcgScal *s,
+                            cudaStream_t st);
+cudaError_t launch_dot_pq(const Geom &g, const double *p, const double *q, const PcgScal *s, double *partial,
+                          cudaStream_t st);
+cudaError_t launch_recip(const Geom &g, const double *d, double *dinv, cudaStream_t st);
+cudaError_t launch_check_field(long long n, const double *x, int positive, int *bad, cudaStream_t st);
+
+}  // namespace dg

@@ -1,0 +1,297 @@
+"""GPU parity: CUDA path (through the C-ABI) vs the CPU oracle on identical seeded inputs.
+
+Tolerances (BASELINE.json north_star): relative L2 <= 1e-12 for operator application,
+diagonal and convection; <= 1e-9 for solutions converged to a residual of 1e-11.
+Relative L2 = ||y_gpu - y_ora||_2 / ||y_ora||_2 over the compared entries (reading A17).
+At the full BASELINE sizes the oracle computes sampled elements one by one (rows of the
+apply / convect are element-local given the neighbours), in the launch configuration the
+bench times (same mesh, same brick decomposition).
+"""
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+from workloads import config
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs CUDA", allow_module_level=True)
+
+import paper_2112_04167_b200 as dg  # noqa: E402
+
+DEV = torch.device("cuda:0")
+TWO_PI = 2 * math.pi
+
+
+def rel(a, b):
+    a = np.asarray(a).reshape(-1)
+    b = np.asarray(b).reshape(-1)
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+def T(a):
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).to(DEV)
+
+
+def H(t):
+    torch.cuda.synchronize()
+    return t.cpu().numpy()
+
+
+def meshes(dim, N, L, P):
+    return dg.dg_mesh_create(dim, N, L, P, stream=torch.cuda.current_stream()), oracle.Mesh(dim, N, L, P)
+
+
+def sample_elements(N, dim, k, seed):
+    """k random elements plus every periodic-seam corner/edge element class."""
+    rng = np.random.default_rng(seed)
+    nel = int(np.prod(N[:dim]))
+    pick = set(rng.choice(nel, size=min(k, nel), replace=False).tolist())
+    for c in np.ndindex(*([2] * dim)):
+        ec = [0 if b == 0 else N[d] - 1 for d, b in enumerate(c)]
+        e = ec[0] + N[0] * (ec[1] + (N[1] * ec[2] if dim == 3 else 0))
+        pick.add(int(e))
+    return np.array(sorted(pick), dtype=np.int64)
+
+
+# ---------------------------------------------------------------------------
+# apply / diag on small meshes (several bricks, ragged tails, N=1 and N=2 cases)
+# ---------------------------------------------------------------------------
+SMALL = [
+    (2, (4, 4), 4), (2, (3, 5), 3), (2, (1, 2), 2), (2, (6, 1), 8), (2, (5, 7), 1), (2, (2, 3), 10),
+    (3, (2, 2, 2), 3), (3, (3, 2, 5), 4), (3, (1, 1, 1), 2), (3, (4, 1, 3), 5), (3, (2, 3, 2), 7),
+    (3, (3, 3, 3), 6), (3, (2, 2, 1), 1), (3, (2, 1, 2), 9), (3, (1, 2, 2), 10),
+]
+
+
+@pytest.mark.parametrize("dim,N,P", SMALL)
+@pytest.mark.parametrize("varnu", [False, True])
+def test_apply_diag_small(dim, N, P, varnu):
+    L = (1.0, 1.7, 0.6)[:dim]
+    m, om = meshes(dim, N, L, P)
+    rng = np.random.default_rng(P * 100 + dim)
+    u = rng.uniform(-1, 1, (om.n_el, om.npe))
+    nu = (0.2 + rng.uniform(0, 1, u.shape)) if varnu else None
+    for lam in (0.0, 2.3):
+        out = torch.empty(u.shape, dtype=torch.float64, device=DEV)
+        dg.dg_helmholtz_apply(m, lam, None if nu is None else T(nu), 0.37, T(u), out)
+        ref = oracle.sip_apply(om, lam, u, nu=nu, nu_const=0.37)
+        assert rel(H(out), ref) <= 1e-12
+        d = torch.empty_like(out)
+        dg.dg_helmholtz_diag(m, lam, None if nu is None else T(nu), 0.37, d)
+        assert rel(H(d), oracle.sip_diag(om, lam, nu=nu, nu_const=0.37)) <= 1e-12
+
+
+@pytest.mark.parametrize("dim,N,P", [(2, (2, 2), 4), (2, (2, 2), 8), (3, (2, 2, 2), 3), (3, (2, 2, 2), 2)])
+def test_matrix_reconstruction_2x2(dim, N, P):
+    """Q11: GPU operator column by column from unit vectors == brute-force dense matrix."""
+    L = (TWO_PI,) * dim
+    m, om = meshes(dim, N, L, P)
+    rng = np.random.default_rng(5)
+    nu = 0.3 + rng.uniform(0, 1, (om.n_el, om.npe))
+    A = oracle.sip_dense(om, 1.5, nu=nu)
+    n = om.ndof
+    E = torch.eye(n, dtype=torch.float64, device=DEV)
+    cols = torch.empty((n, n), dtype=torch.float64, device=DEV)
+    dnu = T(nu)
+    for j in range(n):
+        dg.dg_helmholtz_apply(m, 1.5, dnu, 0.0, E[j].contiguous(), cols[j])
+    G = H(cols).T
+    assert np.abs(G - A).max() <= 1e-13 * np.abs(A).max()
+    assert np.abs(G - G.T).max() <= 1e-13 * np.abs(A).max()
+
+
+# ---------------------------------------------------------------------------
+# BASELINE configs
+# ---------------------------------------------------------------------------
+def cfg_mesh(c, P=None):
+    P = c.P if P is None else P
+    return meshes(c.dim, c.N[: c.dim], c.L[: c.dim], P)
+
+
+@pytest.mark.parametrize("cid", [1, 2, 3])
+def test_apply_configs_full(cid):
+    c = config(cid)
+    m, om = cfg_mesh(c)
+    u = c.apply_input()
+    nu = c.nu()
+    out = torch.empty(u.shape, dtype=torch.float64, device=DEV)
+    dg.dg_helmholtz_apply(m, c.lam, None if nu is None else T(nu), c.nu0, T(u), out)
+    ref = oracle.sip_apply(om, c.lam, u, nu=nu, nu_const=c.nu0)
+    assert rel(H(out), ref) <= 1e-12
+    d = torch.empty_like(out)
+    dg.dg_helmholtz_diag(m, c.lam, None if nu is None else T(nu), c.nu0, d)
+    el = sample_elements(c.N, c.dim, 16, cid)
+    assert rel(H(d)[el], oracle.sip_diag(om, c.lam, nu=nu, nu_const=c.nu0, elems=el)) <= 1e-12
+
+
+@pytest.mark.parametrize("cid", [4, 5])
+def test_apply_configs_sampled(cid):
+    c = config(cid)
+    m, om = cfg_mesh(c)
+    u = c.apply_input()
+    nu = c.nu()
+    out = torch.empty(u.shape, dtype=torch.float64, device=DEV)
+    dg.dg_helmholtz_apply(m, c.lam, None if nu is None else T(nu), c.nu0, T(u), out)
+    el = sample_elements(c.N, c.dim, 96, cid)
+    ref = oracle.sip_apply(om, c.lam, u, nu=nu, nu_const=c.nu0, elems=el)
+    got = H(out)[el]
+    assert rel(got, ref) <= 1e-12
+    # property at any size: A 1 = lam M 1 (the SIP form annihilates constants)
+    one = torch.ones_like(out)
+    dg.dg_helmholtz_apply(m, c.lam, None if nu is None else T(nu), c.nu0, one, out)
+    mass = torch.empty_like(out)
+    dg.dg_mesh_mass(m, mass)
+    o, ms = H(out), H(mass)
+    assert np.abs(o - c.lam * ms).max() <= 1e-12 * np.abs(c.lam * ms).max()
+
+
+def test_apply_deterministic_and_host_variant():
+    c = config(3)
+    m, om = cfg_mesh(c)
+    u = c.apply_input()
+    a = torch.empty(u.shape, dtype=torch.float64, device=DEV)
+    b = torch.empty_like(a)
+    du = T(u)
+    dg.dg_helmholtz_apply(m, c.lam, None, c.nu0, du, a)
+    dg.dg_helmholtz_apply(m, c.lam, None, c.nu0, du, b)
+    assert torch.equal(a, b)
+    hout = np.empty_like(u)
+    dg.dg_helmholtz_apply_host(m, c.lam, None, c.nu0, np.ascontiguousarray(u), hout)
+    assert np.array_equal(hout, H(a))
+
+
+# ---------------------------------------------------------------------------
+# solves
+# ---------------------------------------------------------------------------
+def test_pcg_c1_dense_and_mms():
+    """Config 1(b): f from u = sin x sin y; vs LAPACK dense solve of the oracle matrix."""
+    c = config(1)
+    m, om = cfg_mesh(c)
+    f = c.rhs()
+    u = torch.zeros(f.shape, dtype=torch.float64, device=DEV)
+    info = dg.dg_pcg_solve(m, c.lam, None, c.nu0, T(f), c.tol, 2000, u)
+    assert info.rel_res <= c.tol
+    A = oracle.sip_dense(om, c.lam, nu_const=c.nu0)
+    ref = np.linalg.solve(A, oracle.mass(om).reshape(-1) * f.reshape(-1))
+    assert rel(H(u), ref) <= 1e-9
+    X = c.coords()
+    uex = np.sin(X[0]) * np.sin(X[1])
+    assert math.sqrt(np.mean((H(u) - uex) ** 2)) < 2e-4   # spatial error of the P=4 4x4 mesh
+
+
+@pytest.mark.parametrize("lam_case", ["helmholtz", "poisson"])
+def test_pcg_c2(lam_case):
+    c = config(2)
+    m, om = cfg_mesh(c)
+    nu = c.nu()
+    f = c.rhs()
+    lam = c.lam if lam_case == "helmholtz" else 0.0
+    u = torch.zeros(f.shape, dtype=torch.float64, device=DEV)
+    info = dg.dg_pcg_solve(m, lam, T(nu), 0.0, T(f), c.tol, 20000, u)
+    assert info.rel_res <= c.tol
+    ref, it, rr, rm, st = oracle.pcg_solve(om, lam, f, nu=nu, tol=1e-14)
+    assert rel(H(u), ref) <= 1e-9, (info.as_dict(), rr)
+    if lam == 0.0:
+        assert abs(info.removed_mean - rm) <= 1e-12 * max(1.0, abs(rm))
+
+
+def test_pcg_c3_helmholtz():
+    c = config(3)
+    m, om = cfg_mesh(c)
+    for comp in range(3):
+        f = c.rhs(comp)
+        u = torch.zeros(f.shape, dtype=torch.float64, device=DEV)
+        info = dg.dg_pcg_solve(m, c.lam, None, c.nu0, T(f), 1e-11, 2000, u)
+        ref, it, rr, _, _ = oracle.pcg_solve(om, c.lam, f, nu_const=c.nu0, tol=1e-14)
+        assert rel(H(u), ref) <= 1e-9, info.as_dict()
+        assert 4 <= info.iters <= 30
+
+
+def test_pcg_c3_poisson_residual_crosscheck():
+    """Config 3 pressure Poisson (P_p = P-1 = 6, lam = 0) at the config tolerance; checked with
+    the ORACLE's operator: ||M^-1 (M f' - A u)|| / ||f'|| <= 1.1 tol (Q14)."""
+    c = config(3)
+    m, om = cfg_mesh(c, P=c.P_p)
+    f = c.poisson_rhs_raw()
+    u = torch.zeros(f.shape, dtype=torch.float64, device=DEV)
+    info = dg.dg_pcg_solve(m, 0.0, None, 1.0, T(f), c.tol, 20000, u)
+    mass = oracle.mass(om)
+    fp = f - (mass * f).sum() / mass.sum()
+    uh = H(u)
+    r = mass * fp - oracle.sip_apply(om, 0.0, uh, nu_const=1.0)
+    res = np.linalg.norm(r / mass) / np.linalg.norm(fp)
+    assert res <= 1.1 * c.tol, (res, info.as_dict())
+    assert abs((mass * uh).sum()) <= 1e-10 * np.abs(uh).max() * mass.sum()
+    assert 300 <= info.iters <= 1500
+
+
+def test_pcg_small_poisson_vs_oracle():
+    dim, N, L, P = 3, (4, 4, 4), (TWO_PI,) * 3, 6
+    m, om = meshes(dim, N, L, P)
+    f = np.random.default_rng(3).uniform(-1, 1, (om.n_el, om.npe))
+    u = torch.zeros(f.shape, dtype=torch.float64, device=DEV)
+    dg.dg_pcg_solve(m, 0.0, None, 1.0 / 1600, T(f), 1e-11, 20000, u)
+    ref, *_ = oracle.pcg_solve(om, 0.0, f, nu_const=1.0 / 1600, tol=1e-14)
+    assert rel(H(u), ref) <= 1e-9
+
+
+def test_pcg_notconv_and_einval():
+    c = config(1)
+    m, om = cfg_mesh(c)
+    f = T(c.rhs())
+    u = torch.zeros_like(f)
+    with pytest.raises(dg.DGError) as ei:
+        dg.dg_pcg_solve(m, c.lam, None, c.nu0, f, 1e-14, 2, u)
+    assert ei.value.status == dg.DG_ENOTCONV and ei.value.info.iters == 2
+    with pytest.raises(dg.DGError) as ei:
+        dg.dg_pcg_solve(m, -1.0, None, c.nu0, f, 1e-10, 10, u)
+    assert ei.value.status == dg.DG_EINVAL
+    with pytest.raises(dg.DGError) as ei:
+        dg.dg_helmholtz_apply(m, 1.0, None, 1.0, f, f)
+    assert ei.value.status == dg.DG_EINVAL
+    bad = f.clone()
+    bad[0, 0] = float("nan")
+    with pytest.raises(dg.DGError):
+        dg.dg_check_field(m, bad, positive=False)
+
+
+# ---------------------------------------------------------------------------
+# convection
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("dim,N,P", [(3, (2, 3, 2), 3), (3, (3, 2, 2), 7), (2, (4, 3), 5), (3, (1, 2, 2), 4),
+                                     (2, (2, 1), 8), (3, (2, 2, 2), 5)])
+def test_convect_small(dim, N, P):
+    L = (1.0, 1.4, 0.8)[:dim]
+    m, om = meshes(dim, N, L, P)
+    rng = np.random.default_rng(P)
+    v = [rng.uniform(-1, 1, (om.n_el, om.npe)) for _ in range(dim)]
+    dv = [T(a) for a in v]
+    do = [torch.empty_like(dv[0]) for _ in range(dim)]
+    dg.dg_convect_rhs(m, dv, do)
+    ref = oracle.convect(om, v)
+    for cc in range(dim):
+        assert rel(H(do[cc]), ref[cc]) <= 1e-12
+
+
+def test_convect_c4_sampled():
+    c = config(4)
+    m, om = cfg_mesh(c)
+    v = c.tg_velocity()
+    dv = [T(a) for a in v]
+    do = [torch.empty_like(dv[0]) for _ in range(3)]
+    dg.dg_convect_rhs(m, dv, do)
+    el = sample_elements(c.N, 3, 24, 4)
+    ref = oracle.convect(om, v, elems=el)
+    for cc in range(3):
+        assert rel(H(do[cc])[el], ref[cc]) <= 1e-12
+    # conservation over the whole field (any size): sum_I m_I F_c,I = 0
+    mass = torch.empty_like(dv[0])
+    dg.dg_mesh_mass(m, mass)
+    for cc in range(3):
+        tot = float((mass * do[cc]).sum())
+        assert abs(tot) <= 1e-12 * float((mass * do[cc].abs()).sum())
