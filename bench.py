@@ -1,0 +1,394 @@
+"""Benchmark of the SIP-DG implicit-stage hot path on B200 (contract: one JSON line on rank 0).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl product|reference] [--workload c5]
+
+Workload: BASELINE.json configs[4] (c5), the largest single-GPU
+config and the one the north star's scaling target names: periodic [0,2pi]^3, 64^3 hexes,
+P = 5 (56.6 M DOF), variable nu = 1e-3 (1 + 0.5 tanh(4 sin x sin y sin z)), lam = 229.43.
+
+step  = one SIP-DG Helmholtz apply (BASELINE metric "GDOF/s SIP-DG Helmholtz apply") of the
+        whole mesh; value = global DOF / step time (GDOF/s), max over ranks (strong scaling).
+pcg   = Jacobi-PCG solves of the same workload to tol 1e-10 from u0 = 0 (iterations/s).
+e2e   = the same apply metric through the C-ABI host-buffer call (H2D of u and nu and D2H
+        of the result inside the timed region).
+Inputs (453 MB per field) are larger than L2 (126 MB): no explicit flush is needed.
+
+--impl reference times the CPU oracle (oracle/, C + OpenMP, explicit quadrature) on a
+bounded sample of the same workload (the tier's reference arm); under torchrun only
+rank 0 runs it.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from workloads import config as get_config  # noqa: E402
+
+WORKLOADS = {"c5": 5, "c4": 4, "c3": 3, "c2": 2, "c1": 1}
+BYTES_PER_DOF = {True: 24.0, False: 16.0}  # algorithmic bytes per DOF per apply (var / const nu)
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+# ---------------------------------------------------------------------------
+# clocks sampler (nvidia-smi during the timed region)
+# ---------------------------------------------------------------------------
+class Clocks:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.Q,
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = float(f[2])
+            except ValueError:
+                continue
+            for nm, val in zip(names, f[5:9]):
+                if val.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# seeded inputs for one rank's slab (identical values to the global canonical arrays)
+# ---------------------------------------------------------------------------
+def slab_inputs(c, el_off, nel):
+    npe = c.n ** c.dim
+    from workloads.inputs import rng
+
+    g = rng(c.cid, 0)
+    g.bit_generator.advance(int(el_off) * npe)
+    u = g.uniform(-1.0, 1.0, size=(nel, npe))
+    g = rng(c.cid, 10)
+    g.bit_generator.advance(int(el_off) * npe)
+    f = g.uniform(-1.0, 1.0, size=(nel, npe))
+    nu = None
+    if c.variable_nu:
+        nu = c.nu()[el_off:el_off + nel] if nel * npe < 4_000_000 else _slab_nu(c, el_off, nel)
+    return u, f, nu
+
+
+def _slab_nu(c, el_off, nel):
+    from workloads.inputs import gll_points_for_sampling
+
+    n = c.n
+    xi = gll_points_for_sampling(c.P)
+    e = np.arange(el_off, el_off + nel)
+    N = c.N
+    ex, ey, ez = e % N[0], (e // N[0]) % N[1], e // (N[0] * N[1])
+    h = [c.L[d] / N[d] for d in range(3)]
+    x = ex[:, None, None, None] * h[0] + ((xi + 1) * 0.5 * h[0])[None, None, None, :]
+    y = ey[:, None, None, None] * h[1] + ((xi + 1) * 0.5 * h[1])[None, None, :, None]
+    z = ez[:, None, None, None] * h[2] + ((xi + 1) * 0.5 * h[2])[None, :, None, None]
+    x, y, z = np.broadcast_arrays(x, y, z)
+    X = [a.reshape(nel, n ** 3) for a in (x, y, z)]
+    if c.cid == 5:
+        return c.nu0 * (1.0 + 0.5 * np.tanh(4.0 * np.sin(X[0]) * np.sin(X[1]) * np.sin(X[2])))
+    raise ValueError
+
+
+# ---------------------------------------------------------------------------
+# reference arm / cpu baseline: the oracle on a bounded sample
+# ---------------------------------------------------------------------------
+def time_oracle(c, budget_s=12.0):
+    import oracle
+
+    om = oracle.Mesh(c.dim, c.N[: c.dim], c.L[: c.dim], c.P)
+    nel_s = min(c.n_el, 2048)
+    u, _, nu = slab_inputs(c, 0, c.n_el) if c.n_el <= 4096 else (None, None, None)
+    if u is None:  # full-size input arrays are needed by the oracle (neighbour reads)
+        u = c.apply_input()
+        nu = c.nu()
+    rng = np.random.default_rng(99)
+    elems = np.sort(rng.choice(c.n_el, size=nel_s, replace=False))
+    t0 = time.perf_counter()
+    oracle.sip_apply(om, c.lam, u, nu=nu, nu_const=c.nu0, elems=elems)
+    t1 = time.perf_counter() - t0
+    reps = max(1, int(budget_s / max(t1, 1e-3)))
+    reps = min(reps, 200)
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        oracle.sip_apply(om, c.lam, u, nu=nu, nu_const=c.nu0, elems=elems)
+    t = (time.perf_counter() - t0) / reps
+    cores = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
+    gdofs = nel_s * c.n ** c.dim / t / 1e9
+    return {"value": gdofs, "unit": "GDOF/s", "cores": cores, "kind": "oracle",
+            "sample": "oracle_sip_apply (explicit GLL quadrature, C/OpenMP) on %d random elements of %s "
+                      "(%d DOF), mean of %d repetitions" % (nel_s, c.name, nel_s * c.n ** c.dim, reps),
+            "seconds_per_sample": t}
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    c = get_config(WORKLOADS[args.workload])
+    cb = time_oracle(c)
+    steps_t = []
+    import oracle
+
+    om = oracle.Mesh(c.dim, c.N[: c.dim], c.L[: c.dim], c.P)
+    u, nu = c.apply_input(), c.nu()
+    elems = np.sort(np.random.default_rng(7).choice(c.n_el, size=min(c.n_el, 2048), replace=False))
+    for i in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        oracle.sip_apply(om, c.lam, u, nu=nu, nu_const=c.nu0, elems=elems)
+        dt = time.perf_counter() - t0
+        if i >= args.warmup:
+            steps_t.append(dt)
+    t = statistics.mean(steps_t)
+    val = len(elems) * c.n ** c.dim / t / 1e9
+    line = {"metric": "GDOF/s SIP-DG Helmholtz apply", "value": val, "unit": "GDOF/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
+            "config": {"workload": c.name, "N": list(c.N), "P": c.P, "ndof": c.ndof,
+                       "sample_elements": int(len(elems))},
+            "cpu_baseline": cb, "e2e": {"value": val, "unit": "GDOF/s", "h2d_bytes_per_step": 0,
+                                        "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# product arm
+# ---------------------------------------------------------------------------
+def run_product(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2112_04167_b200 as dg
+
+    c = get_config(WORKLOADS[args.workload])
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    stream = torch.cuda.current_stream()
+    uid = None
+    if world > 1:
+        obj = [dg.dg_nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        uid = obj[0]
+    m = dg.dg_mesh_create(c.dim, c.N[: c.dim], c.L[: c.dim], c.P, rank=rank, nranks=world, nccl_uid=uid,
+                          stream=stream)
+    nel, off = m.n_el, m.element_offset
+    u_h, f_h, nu_h = slab_inputs(c, off, nel)
+    u = torch.from_numpy(u_h).to(dev)
+    f = torch.from_numpy(f_h).to(dev)
+    nu = torch.from_numpy(nu_h).to(dev) if nu_h is not None else None
+    out = torch.empty_like(u)
+    ndof_global = c.ndof
+    varnu = nu is not None
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # ---- device-timed apply steps
+    for _ in range(args.warmup):
+        dg.dg_helmholtz_apply(m, c.lam, nu, c.nu0, u, out)
+    barrier()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2 * args.steps)]
+    l0 = dg.dg_mesh_launch_count(m)
+    with Clocks(local_rank) as clk:
+        barrier()
+        t_start = torch.cuda.Event(enable_timing=True)
+        t_end = torch.cuda.Event(enable_timing=True)
+        t_start.record(stream)
+        for k in range(args.steps):
+            ev[2 * k].record(stream)
+            dg.dg_helmholtz_apply(m, c.lam, nu, c.nu0, u, out)
+            ev[2 * k + 1].record(stream)
+        t_end.record(stream)
+        barrier()
+    launches = dg.dg_mesh_launch_count(m) - l0
+    total_ms = max_over_ranks(t_start.elapsed_time(t_end))
+    per_launch_ms = statistics.mean(ev[2 * k].elapsed_time(ev[2 * k + 1]) for k in range(args.steps))
+    per_launch_ms = max_over_ranks(per_launch_ms)
+    ms_step = total_ms / args.steps
+    value = ndof_global / (ms_step * 1e-3) / 1e9
+
+    # ---- PCG solves (iterations/s)
+    solve_ms, iters, infos = [], [], []
+    for k in range(args.solve_warmup + args.solves):
+        x = torch.zeros_like(u)
+        barrier()
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        info = dg.dg_pcg_solve(m, c.lam, nu, c.nu0, f, c.tol, 5000, x)
+        b.record(stream)
+        barrier()
+        if k >= args.solve_warmup:
+            solve_ms.append(max_over_ranks(a.elapsed_time(b)))
+            iters.append(info.iters)
+            infos.append(info.as_dict())
+    t_solve = statistics.mean(solve_ms)
+    it = statistics.mean(iters)
+
+    # ---- e2e through the host-buffer C-ABI call (rank-local slab)
+    u_np = np.ascontiguousarray(u_h)
+    nu_np = None if nu_h is None else np.ascontiguousarray(nu_h)
+    import torch as _t
+
+    u_pin = _t.from_numpy(u_np).pin_memory().numpy()
+    nu_pin = None if nu_np is None else _t.from_numpy(nu_np).pin_memory().numpy()
+    o_pin = _t.empty(u_np.shape, dtype=_t.float64).pin_memory().numpy()
+    for _ in range(max(1, args.warmup)):
+        dg.dg_helmholtz_apply_host(m, c.lam, nu_pin, c.nu0, u_pin, o_pin)
+    barrier()
+    e2e_steps = max(3, args.steps // 4)
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        dg.dg_helmholtz_apply_host(m, c.lam, nu_pin, c.nu0, u_pin, o_pin)
+    barrier()
+    e2e_s = max_over_ranks((time.perf_counter() - t0) / e2e_steps)
+    h2d = u_np.nbytes * world + (nu_np.nbytes * world if nu_np is not None else 0)
+    d2h = u_np.nbytes * world
+
+    if rank != 0:
+        return
+    peak, peak_kind = measured_peaks()
+    bpd = BYTES_PER_DOF[varnu]
+    nd_local = m.ndof
+    achieved = nd_local * bpd / (per_launch_ms * 1e-3) / 1e9
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    if os.path.exists(prof):
+        try:
+            with open(prof) as fh:
+                traffic = json.load(fh).get(args.workload, {}).get("apply_dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+    cb = None
+    if world == 1 and not args.no_cpu_baseline:
+        cb = time_oracle(c)
+    line = {
+        "metric": "GDOF/s SIP-DG Helmholtz apply",
+        "value": value,
+        "unit": "GDOF/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": ms_step,
+        "higher_is_better": True,
+        "scaling": "strong",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic",
+        "impl": "product",
+        "config": {"workload": c.name, "N": list(c.N), "P": c.P, "ndof": ndof_global, "lam": c.lam,
+                   "nu": "1e-3(1+0.5tanh(4 sin x sin y sin z)) at GLL nodes", "parallelism": "z-slabs x%d" % world,
+                   "bricks": None, "l2": "inputs larger than L2 (%.0f MB per field)" % (ndof_global * 8 / 1e6)},
+        "pcg": {"iters_per_s": it / (t_solve * 1e-3), "iters": it, "ms_per_solve": t_solve, "tol": c.tol,
+                "solves": args.solves, "rel_res": infos[-1]["rel_res"], "kappa_est": infos[-1]["kappa_est"],
+                "gdof_iter_per_s": ndof_global * it / (t_solve * 1e-3) / 1e9},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": traffic, "kernel": "k_apply<3,%d,%s,false>" % (c.P, "true" if varnu else "false"),
+                     "bytes_per_dof": bpd, "peak_kind": peak_kind, "launch_ms": per_launch_ms},
+        "e2e": {"value": ndof_global / e2e_s / 1e9, "unit": "GDOF/s", "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h, "ms_per_step": e2e_s * 1e3},
+        "gpu_launches": launches,
+        "clocks": clk.summary(),
+        "cpu_baseline": cb,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--solves", type=int, default=3)
+    ap.add_argument("--solve-warmup", type=int, default=1)
+    ap.add_argument("--impl", default="product", choices=["product", "reference"])
+    ap.add_argument("--workload", default="c5", choices=sorted(WORKLOADS))
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    try:
+        run_product(args, rank, world, local_rank)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -80,14 +80,15 @@ def build(pset: str | None = None, jobs: int | None = None, force: bool = False,
     hdr = _digest(headers(), " ".join(flags))
     stamp = os.path.join(BUILD, "stamp")
     want = _digest(sources(), hdr)
-    if not force and os.path.exists(LIB) and os.path.exists(stamp) and open(stamp).read() == want:
+    if not force and not verbose and os.path.exists(LIB) and os.path.exists(stamp) and open(stamp).read() == want:
         return LIB
 
     def compile_one(src):
         obj = os.path.join(BUILD, os.path.basename(src) + ".o")
         tag = obj + ".sha"
         key = _digest([src], hdr)
-        if not force and os.path.exists(obj) and os.path.exists(tag) and open(tag).read() == key:
+        if not force and os.path.exists(obj) and os.path.exists(tag) and open(tag).read() == key and \
+                (not verbose or os.path.exists(obj + ".ptxas.log")):
             return obj
         cmd = [nvcc()] + ARCH + flags + ["-Xptxas", "-v"] * bool(verbose) + ["-c", src, "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)

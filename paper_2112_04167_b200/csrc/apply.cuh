@@ -27,6 +27,9 @@
 // the epilogue.
 #pragma once
 
+#include <algorithm>
+#include <cstdlib>
+
 #include "dev_common.cuh"
 
 namespace dg {
@@ -78,200 +81,11 @@ __device__ __forceinline__ double end_flux(const DevTab &T, const double (&v)[P 
     return nu * sd * g;
 }
 
-// ---------------------------------------------------------------------------
-// one direction pass over the brick
-// ---------------------------------------------------------------------------
-template <int DIM, int P, bool VARNU, bool PCG, int D>
-__device__ __forceinline__ void apply_pass(const ApplyParams &a, const DevTab &T, const double *su,
-                                           const double *snu, double *sacc, const int (&e0)[3], double beta)
-{
-    using C = Cfg<DIM, P>;
-    constexpr int n = C::n;
-    constexpr int O1 = (D == 0) ? 1 : 0;
-    constexpr int O2 = (DIM == 3) ? ((D == 2) ? 1 : 2) : 2;
-    const Geom &g = a.g;
-    const int Bd = g.B[D];
-    const int BE = g.B[0] * g.B[1] * g.B[2];
-    const int ncross = BE / Bd;
-    const int nlines = ncross * C::NT;
-    // shared-memory strides per node coordinate (x pitch PX), global strides (pitch n)
-    constexpr int SS[3] = {1, C::PX, C::PX * n};
-    constexpr int GS[3] = {1, n, n * n};
-    const double sd = 2.0 / g.h[D];
-    const double tau = g.tau[D];
+}  // namespace dg
 
-    for (int L = threadIdx.x; L < nlines; L += blockDim.x) {
-        const int tn = L % C::NT, ce = L / C::NT;
-        const int ta = tn % n, tb = (DIM == 3) ? tn / n : 0;
-        int lc[3] = {0, 0, 0};
-        lc[O1] = ce % g.B[O1];
-        if (DIM == 3) lc[O2] = ce / g.B[O1];
-        int nd[3] = {0, 0, 0};
-        nd[O1] = ta;
-        if (DIM == 3) nd[O2] = tb;
-        const int soff = nd[0] * SS[0] + nd[1] * SS[1] + nd[2] * SS[2];  // node offset, i_D = 0
-        const int goff = nd[0] * GS[0] + nd[1] * GS[1] + nd[2] * GS[2];
-        double W = T.w[ta] * 0.5 * g.h[O1];
-        if (DIM == 3) W *= T.w[tb] * 0.5 * g.h[O2];
+#include "apply_kernel.cuh"
 
-        auto slot = [&](int l) {
-            int c[3] = {lc[0], lc[1], lc[2]};
-            c[D] = l;
-            return c[0] + g.B[0] * (c[1] + g.B[1] * c[2]);
-        };
-        // global neighbour line (outside the brick) along D at brick-row position l (-1 or Bd)
-        auto load_global = [&](int l, double (&v)[n], double &nu_face, int face_node) {
-            int c[3] = {e0[0] + lc[0], e0[1] + lc[1], e0[2] + lc[2]};
-            c[D] = e0[D] + l;
-            const double *pu;
-            if (PCG) {
-                const double *pr = elem_ptr(g, a.pro.r, nullptr, nullptr, c[0], c[1], c[2]) + goff;
-                const double *pd = elem_ptr(g, a.pro.dinv, nullptr, nullptr, c[0], c[1], c[2]) + goff;
-                const double *pp = elem_ptr(g, a.pro.p_old, nullptr, nullptr, c[0], c[1], c[2]) + goff;
-#pragma unroll
-                for (int i = 0; i < n; ++i)
-                    v[i] = fma(beta, __ldg(pp + i * GS[D]), __ldg(pd + i * GS[D]) * __ldg(pr + i * GS[D]));
-            } else {
-                pu = elem_ptr(g, a.u, a.halo.u_lo, a.halo.u_hi, c[0], c[1], c[2]) + goff;
-#pragma unroll
-                for (int i = 0; i < n; ++i) v[i] = __ldg(pu + i * GS[D]);
-            }
-            if (VARNU) {
-                const double *pn = elem_ptr(g, a.nu, a.halo.nu_lo, a.halo.nu_hi, c[0], c[1], c[2]) + goff;
-                nu_face = __ldg(pn + face_node * GS[D]);
-            } else {
-                nu_face = a.nu_const;
-            }
-        };
-        auto load_smem = [&](int l, double (&v)[n], double (&vn)[n]) {
-            const int base = slot(l) * C::SPE + soff;
-#pragma unroll
-            for (int i = 0; i < n; ++i) v[i] = su[base + i * SS[D]];
-            if (VARNU) {
-#pragma unroll
-                for (int i = 0; i < n; ++i) vn[i] = snu[base + i * SS[D]];
-            }
-        };
-
-        double cur[n], cnu[n], nxt[n], nnu[n];
-        double uL, sL, nuL;
-        {
-            double nb[n];
-            load_global(-1, nb, nuL, P);
-            uL = nb[P];
-            sL = end_flux<P>(T, nb, 1, nuL, sd);
-        }
-        load_smem(0, cur, cnu);
-        for (int l = 0; l < Bd; ++l) {
-            double uR, sR, nuR;
-            if (l + 1 < Bd) {
-                load_smem(l + 1, nxt, nnu);
-                nuR = VARNU ? nnu[0] : a.nu_const;
-            } else {
-                load_global(Bd, nxt, nuR, 0);
-            }
-            uR = nxt[0];
-            sR = end_flux<P>(T, nxt, 0, nuR, sd);
-            double r[n], sP;
-            line_op<P, VARNU>(T, cur, cnu, a.nu_const, uL, sL, nuL, uR, sR, nuR, sd, tau, r, sP);
-            const int base = slot(l) * C::SPE + soff;
-#pragma unroll
-            for (int i = 0; i < n; ++i) sacc[base + i * SS[D]] += W * r[i];
-            uL = cur[P];
-            sL = sP;
-            nuL = VARNU ? cnu[P] : a.nu_const;
-#pragma unroll
-            for (int i = 0; i < n; ++i) {
-                cur[i] = nxt[i];
-                if (VARNU) cnu[i] = nnu[i];
-            }
-        }
-    }
-}
-
-// ---------------------------------------------------------------------------
-// apply kernel
-// ---------------------------------------------------------------------------
-template <int DIM, int P, bool VARNU, bool PCG>
-__global__ void __launch_bounds__(256, 1) k_apply(const ApplyParams a)
-{
-    using C = Cfg<DIM, P>;
-    constexpr int n = C::n;
-    const Geom &g = a.g;
-    const DevTab &T = c_tab[P];
-    extern __shared__ double sm[];
-    const int BE = g.B[0] * g.B[1] * g.B[2];
-    double *su = sm;
-    double *snu = su + BE * C::SPE;
-    double *sacc = snu + (VARNU ? BE * C::SPE : 0);
-    double *sred = sacc + BE * C::SPE;  // 64 doubles
-    double *smass = sred + 64;          // NPE doubles: element mass m_q
-    if (PCG && *a.pro.done) return;
-    const double beta = PCG ? *a.pro.beta : 0.0;
-
-    for (int q = threadIdx.x; q < C::NPE; q += blockDim.x) {
-        const int i = q % n, j = (q / n) % n, k = q / (n * n);
-        double m = T.w[i] * 0.5 * g.h[0] * T.w[j] * 0.5 * g.h[1];
-        if (DIM == 3) m *= T.w[k] * 0.5 * g.h[2];
-        smass[q] = m;
-    }
-    double acc2[2] = {0.0, 0.0};
-
-    for (long long bk = a.b0 + blockIdx.x; bk < a.b1; bk += gridDim.x) {
-        const int bx = (int)(bk % g.nbk[0]);
-        const int by = (int)((bk / g.nbk[0]) % g.nbk[1]);
-        const int bz = (int)(bk / ((long long)g.nbk[0] * g.nbk[1]));
-        const int e0[3] = {bx * g.B[0], by * g.B[1], bz * g.B[2]};
-        __syncthreads();
-        // ---- stage the brick (coalesced per element chunk)
-        for (int t = threadIdx.x; t < BE * C::NPE; t += blockDim.x) {
-            const int el = t / C::NPE, q = t - el * C::NPE;
-            const int lx = el % g.B[0], ly = (el / g.B[0]) % g.B[1], lz = el / (g.B[0] * g.B[1]);
-            const long long gi = elem_index(g, e0[0] + lx, e0[1] + ly, e0[2] + lz) * C::NPE + q;
-            const int si = el * C::SPE + (q % n) + C::PX * (q / n);
-            double val;
-            if (PCG) {
-                val = fma(beta, a.pro.p_old[gi], a.pro.dinv[gi] * a.pro.r[gi]);
-                a.pro.p_out[gi] = val;
-            } else {
-                val = a.u[gi];
-            }
-            su[si] = val;
-            if (VARNU) snu[si] = a.nu[gi];
-            sacc[si] = 0.0;
-        }
-        __syncthreads();
-        apply_pass<DIM, P, VARNU, PCG, 0>(a, T, su, snu, sacc, e0, beta);
-        __syncthreads();
-        apply_pass<DIM, P, VARNU, PCG, 1>(a, T, su, snu, sacc, e0, beta);
-        __syncthreads();
-        if (DIM == 3) {
-            apply_pass<DIM, P, VARNU, PCG, (DIM == 3 ? 2 : 1)>(a, T, su, snu, sacc, e0, beta);
-            __syncthreads();
-        }
-        // ---- write out = acc + lam m u
-        for (int t = threadIdx.x; t < BE * C::NPE; t += blockDim.x) {
-            const int el = t / C::NPE, q = t - el * C::NPE;
-            const int lx = el % g.B[0], ly = (el / g.B[0]) % g.B[1], lz = el / (g.B[0] * g.B[1]);
-            const long long gi = elem_index(g, e0[0] + lx, e0[1] + ly, e0[2] + lz) * C::NPE + q;
-            const int si = el * C::SPE + (q % n) + C::PX * (q / n);
-            const double uu = su[si];
-            const double o = fma(a.lam * smass[q], uu, sacc[si]);
-            a.out[gi] = o;
-            if (PCG) {
-                acc2[0] = fma(uu, o, acc2[0]);
-                acc2[1] += o;
-            }
-        }
-    }
-    if (PCG) {
-        block_sum<2>(acc2, sred);
-        if (threadIdx.x == 0) {
-            a.epi.partial[2 * blockIdx.x + 0] = acc2[0];
-            a.epi.partial[2 * blockIdx.x + 1] = acc2[1];
-        }
-    }
-}
+namespace dg {
 
 // ---------------------------------------------------------------------------
 // Jacobi diagonal: diag_I = lam m_I + sum_d W_perp,d (K_d e_I)_I, evaluated by the same
@@ -341,34 +155,94 @@ __global__ void __launch_bounds__(256) k_diag(const Geom g, double lam, const do
 // ---------------------------------------------------------------------------
 template <int DIM>
 struct ApplyDispatch {
-    template <int P, bool VARNU, bool PCG>
-    static cudaError_t go(const ApplyParams &a, int grid, int smem, cudaStream_t st)
+    // launch one compile-time brick shape (persistent grid: #SM x occupancy, <= 148 x 8)
+    template <int P, bool VARNU, int MODE, int BX, int BY, int BZ>
+    static cudaError_t go(ApplyParams a, int *grid, cudaStream_t st)
     {
-        auto kern = k_apply<DIM, P, VARNU, PCG>;
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        if (e != cudaSuccess) return e;
-        kern<<<grid, 256, smem, st>>>(a);
-        return cudaGetLastError();
+        using K = KC<DIM, P, VARNU, MODE, BX, BY, BZ>;
+        if constexpr (K::SMEM_BYTES > 227 * 1024) {
+            return cudaErrorNotSupported;
+        } else {
+            auto kern = k_apply<DIM, P, VARNU, MODE, BX, BY, BZ>;
+            static int occ = -1, nsm = 0;  // per instantiation (one device per process is assumed)
+            cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, K::SMEM_BYTES);
+            if (e != cudaSuccess) return e;
+            if (occ < 0) {
+                int dev = 0;
+                cudaGetDevice(&dev);
+                cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+                e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, K::NT, K::SMEM_BYTES);
+                if (e != cudaSuccess) return e;
+                if (occ < 1) return cudaErrorInvalidConfiguration;
+            }
+            a.g.B[0] = BX;
+            a.g.B[1] = BY;
+            a.g.B[2] = BZ;
+            for (int d = 0; d < 3; ++d) a.g.nbk[d] = a.g.Nl[d] / a.g.B[d];
+            a.b0 = 0;
+            a.b1 = (long long)a.g.nbk[0] * a.g.nbk[1] * a.g.nbk[2];
+            long long gsz = (long long)nsm * std::min(occ, 8);
+            // column segments along the slowest direction: enough units (>= 3 per CTA) for
+            // balance, as long as possible for the on-chip slowest-direction traces
+            const int S = DIM - 1;
+            const long long ncols = DIM == 3 ? (long long)a.g.nbk[0] * a.g.nbk[1] : a.g.nbk[0];
+            const int nbS = a.g.nbk[S];
+            int nseg = 1;
+            while (ncols * nseg < 3 * gsz && nbS % (2 * nseg) == 0) nseg *= 2;
+            a.nseg = nseg;
+            a.seglen = nbS / nseg;
+            const long long nunits = ncols * nseg;
+            if (gsz > nunits) gsz = nunits;
+            if (gsz < 1) gsz = 1;
+            *grid = (int)gsz;
+            kern<<<(int)gsz, K::NT, K::SMEM_BYTES, st>>>(a);
+            return cudaGetLastError();
+        }
+    }
+    // brick shape: the largest of the candidates that divides the local mesh and fits the
+    // shared-memory budget (default 110 KB = two CTAs per SM; DG_SMEM_BUDGET_KB overrides)
+    template <int P, bool VARNU, int MODE>
+    static cudaError_t pick(const ApplyParams &a, int *grid, cudaStream_t st)
+    {
+        static const int budget = [] {
+            const char *e = getenv("DG_SMEM_BUDGET_KB");
+            return (e ? atoi(e) : 110) * 1024;
+        }();
+        const int *N = a.g.Nl;
+        if constexpr (DIM == 3) {
+            if (N[0] % 2 == 0 && N[1] % 2 == 0 && N[2] % 2 == 0 && KC<3, P, VARNU, MODE, 2, 2, 2>::SMEM_BYTES <= budget)
+                return go<P, VARNU, MODE, 2, 2, 2>(a, grid, st);
+            if (N[0] % 2 == 0 && N[1] % 2 == 0 && KC<3, P, VARNU, MODE, 2, 2, 1>::SMEM_BYTES <= budget)
+                return go<P, VARNU, MODE, 2, 2, 1>(a, grid, st);
+            return go<P, VARNU, MODE, 1, 1, 1>(a, grid, st);
+        } else {
+            if (N[0] % 4 == 0 && N[1] % 4 == 0 && KC<2, P, VARNU, MODE, 4, 4, 1>::SMEM_BYTES <= budget)
+                return go<P, VARNU, MODE, 4, 4, 1>(a, grid, st);
+            if (N[0] % 2 == 0 && N[1] % 2 == 0 && KC<2, P, VARNU, MODE, 2, 2, 1>::SMEM_BYTES <= budget)
+                return go<P, VARNU, MODE, 2, 2, 1>(a, grid, st);
+            return go<P, VARNU, MODE, 1, 1, 1>(a, grid, st);
+        }
     }
     template <int P>
-    static cudaError_t go_p(const ApplyParams &a, bool varnu, bool pcg, int grid, int smem, cudaStream_t st)
+    static cudaError_t go_p(const ApplyParams &a, bool varnu, bool pcg, int *grid, cudaStream_t st)
     {
-        if (varnu) return pcg ? go<P, true, true>(a, grid, smem, st) : go<P, true, false>(a, grid, smem, st);
-        return pcg ? go<P, false, true>(a, grid, smem, st) : go<P, false, false>(a, grid, smem, st);
+        if (varnu) return pcg ? pick<P, true, 1>(a, grid, st) : pick<P, true, 0>(a, grid, st);
+        return pcg ? pick<P, false, 1>(a, grid, st) : pick<P, false, 0>(a, grid, st);
     }
-    static cudaError_t apply(const ApplyParams &a, bool varnu, bool pcg, int grid, int smem, cudaStream_t st)
+    static cudaError_t apply(const ApplyParams &a, bool varnu, bool pcg, int *grid, int smem, cudaStream_t st)
     {
+        (void)smem;
         switch (a.g.P) {
-        case 1: if constexpr (DG_HAS_P(1)) return go_p<1>(a, varnu, pcg, grid, smem, st); else return cudaErrorNotSupported;
-        case 2: if constexpr (DG_HAS_P(2)) return go_p<2>(a, varnu, pcg, grid, smem, st); else return cudaErrorNotSupported;
-        case 3: if constexpr (DG_HAS_P(3)) return go_p<3>(a, varnu, pcg, grid, smem, st); else return cudaErrorNotSupported;
-        case 4: if constexpr (DG_HAS_P(4)) return go_p<4>(a, varnu, pcg, grid, smem, st); else return cudaErrorNotSupported;
-        case 5: if constexpr (DG_HAS_P(5)) return go_p<5>(a, varnu, pcg, grid, smem, st); else return cudaErrorNotSupported;
-        case 6: if constexpr (DG_HAS_P(6)) return go_p<6>(a, varnu, pcg, grid, smem, st); else return cudaErrorNotSupported;
-        case 7: if constexpr (DG_HAS_P(7)) return go_p<7>(a, varnu, pcg, grid, smem, st); else return cudaErrorNotSupported;
-        case 8: if constexpr (DG_HAS_P(8)) return go_p<8>(a, varnu, pcg, grid, smem, st); else return cudaErrorNotSupported;
-        case 9: if constexpr (DG_HAS_P(9)) return go_p<9>(a, varnu, pcg, grid, smem, st); else return cudaErrorNotSupported;
-        case 10: if constexpr (DG_HAS_P(10)) return go_p<10>(a, varnu, pcg, grid, smem, st); else return cudaErrorNotSupported;
+        case 1: if constexpr (DG_HAS_P(1)) return go_p<1>(a, varnu, pcg, grid, st); else return cudaErrorNotSupported;
+        case 2: if constexpr (DG_HAS_P(2)) return go_p<2>(a, varnu, pcg, grid, st); else return cudaErrorNotSupported;
+        case 3: if constexpr (DG_HAS_P(3)) return go_p<3>(a, varnu, pcg, grid, st); else return cudaErrorNotSupported;
+        case 4: if constexpr (DG_HAS_P(4)) return go_p<4>(a, varnu, pcg, grid, st); else return cudaErrorNotSupported;
+        case 5: if constexpr (DG_HAS_P(5)) return go_p<5>(a, varnu, pcg, grid, st); else return cudaErrorNotSupported;
+        case 6: if constexpr (DG_HAS_P(6)) return go_p<6>(a, varnu, pcg, grid, st); else return cudaErrorNotSupported;
+        case 7: if constexpr (DG_HAS_P(7)) return go_p<7>(a, varnu, pcg, grid, st); else return cudaErrorNotSupported;
+        case 8: if constexpr (DG_HAS_P(8)) return go_p<8>(a, varnu, pcg, grid, st); else return cudaErrorNotSupported;
+        case 9: if constexpr (DG_HAS_P(9)) return go_p<9>(a, varnu, pcg, grid, st); else return cudaErrorNotSupported;
+        case 10: if constexpr (DG_HAS_P(10)) return go_p<10>(a, varnu, pcg, grid, st); else return cudaErrorNotSupported;
         default: return cudaErrorInvalidValue;
         }
     }

@@ -5,7 +5,7 @@ DG_DEFINE_CONST_TABLES(upload_tables_apply2)
 }
 #include "apply.cuh"
 namespace dg {
-cudaError_t launch_apply2(const ApplyParams &a, bool varnu, bool pcg, int grid, int smem, cudaStream_t st)
+cudaError_t launch_apply2(const ApplyParams &a, bool varnu, bool pcg, int *grid, int smem, cudaStream_t st)
 {
     return ApplyDispatch<2>::apply(a, varnu, pcg, grid, smem, st);
 }

@@ -142,7 +142,7 @@ struct dg_mesh {
     long long el_off = 0, ndof = 0, ndof_global = 0, layer = 0;  // layer: doubles per slab layer
     cudaStream_t st = nullptr;
     // PCG workspace
-    double *r = nullptr, *q = nullptr, *pa = nullptr, *pb = nullptr, *dinv = nullptr;
+    double *r = nullptr, *q = nullptr, *pa = nullptr, *pb = nullptr, *dinv = nullptr, *z = nullptr;
     double *partial = nullptr;
     int partial_cap = 0;  // in doubles
     double *sums = nullptr, *aux = nullptr, *mass_e = nullptr, *hist = nullptr;
@@ -174,42 +174,9 @@ struct dg_mesh {
 
 namespace {
 
-int smem_bytes(const Geom &g, bool varnu)
-{
-    const int n = g.n;
-    const int PX = (n % 2 == 0) ? n + 1 : n;
-    const int SPE = g.dim == 3 ? PX * n * n : PX * n;
-    const int BE = g.B[0] * g.B[1] * g.B[2];
-    return ((2 + (varnu ? 1 : 0)) * BE * SPE + 64 + g.npe) * 8;
-}
-
-void choose_bricks(Geom &g)
-{
-    const int BEmax = g.dim == 3 ? (g.n >= 7 ? 8 : 16) : (g.n >= 7 ? 16 : 32);
-    g.B[0] = g.B[1] = g.B[2] = 1;
-    for (;;) {
-        int best = -1;
-        for (int d = 0; d < g.dim; ++d) {
-            const int BE = g.B[0] * g.B[1] * g.B[2];
-            if (g.Nl[d] % (2 * g.B[d]) != 0 || 2 * BE > BEmax) continue;
-            Geom t = g;
-            t.B[d] *= 2;
-            if (smem_bytes(t, true) > 200 * 1024) continue;
-            if (best < 0 || g.B[d] < g.B[best]) best = d;
-        }
-        if (best < 0) break;
-        g.B[best] *= 2;
-    }
-    for (int d = 0; d < 3; ++d) g.nbk[d] = g.Nl[d] / g.B[d];
-}
-
 long long nbricks(const Geom &g) { return (long long)g.nbk[0] * g.nbk[1] * g.nbk[2]; }
 
-int apply_grid(const Geom &g)
-{
-    const long long nb = nbricks(g);
-    return (int)std::min<long long>(nb, 148LL * 16);
-}
+constexpr int APPLY_GRID_MAX = 148 * 8;
 
 dg_status alloc(void **p, size_t bytes)
 {
@@ -235,6 +202,7 @@ dg_status ensure_workspace(dg_mesh *m)
     CKS(alloc((void **)&m->pa, b));
     CKS(alloc((void **)&m->pb, b));
     CKS(alloc((void **)&m->dinv, b));
+    CKS(alloc((void **)&m->z, b));
     return DG_OK;
 }
 
@@ -301,7 +269,7 @@ dg_status check_common(dg_mesh *m, double lam, const double *nu, double nu_const
 }
 
 dg_status run_apply(dg_mesh *m, double lam, const double *nu, double nu_const, const double *u, double *out,
-                    const Halo &halo, const DotEpi &epi, const PProl &pro, int grid)
+                    const Halo &halo, const DotEpi &epi, const PProl &pro, int *grid_out = nullptr)
 {
     ApplyParams a{};
     a.g = m->g;
@@ -314,12 +282,13 @@ dg_status run_apply(dg_mesh *m, double lam, const double *nu, double nu_const, c
     a.epi = epi;
     a.pro = pro;
     a.b0 = 0;
-    a.b1 = nbricks(m->g);
+    a.b1 = nbricks(a.g);
     const bool varnu = nu != nullptr;
-    const int smem = smem_bytes(m->g, varnu);
-    const cudaError_t e = m->g.dim == 3 ? launch_apply3(a, varnu, pro.on, grid, smem, m->st)
-                                        : launch_apply2(a, varnu, pro.on, grid, smem, m->st);
+    int grid = 0;
+    const cudaError_t e = m->g.dim == 3 ? launch_apply3(a, varnu, pro.on, &grid, 0, m->st)
+                                        : launch_apply2(a, varnu, pro.on, &grid, 0, m->st);
     CK(e);
+    if (grid_out) *grid_out = grid;
     m->launches += 1;
     return DG_OK;
 }
@@ -338,7 +307,7 @@ dg_status apply_impl(dg_mesh *m, double lam, const double *nu, double nu_const, 
             h.nu_hi = m->hn_hi;
         }
     }
-    return run_apply(m, lam, nu, nu_const, u, out, h, DotEpi{}, PProl{}, apply_grid(m->g));
+    return run_apply(m, lam, nu, nu_const, u, out, h, DotEpi{}, PProl{});
 }
 
 dg_status diag_impl(dg_mesh *m, double lam, const double *nu, double nu_const, double *diag)
@@ -407,7 +376,7 @@ dg_status pcg_impl(dg_mesh *m, double lam, const double *nu, double nu_const, co
     CK(launch_pcg_init(g, f, m->q, m->r, m->mass_e, m->scal, m->partial, m->st));
     m->launches += 1;
     CKS(reduce_fin(m, VG, FIN_INIT));
-    CK(launch_pcg_init2(g, m->r, m->dinv, nullptr, m->mass_e, m->scal, nullptr, m->partial, m->st));
+    CK(launch_pcg_init2(g, m->r, m->dinv, m->z, m->mass_e, m->scal, m->partial, m->st));
     m->launches += 1;
     CKS(reduce_fin(m, VG, FIN_INIT2));
     CK(cudaMemsetAsync(m->pa, 0, sizeof(double) * (size_t)m->ndof, m->st));
@@ -423,35 +392,34 @@ dg_status pcg_impl(dg_mesh *m, double lam, const double *nu, double nu_const, co
                 // q = A p with p = dinv r + beta p_old (prologue), partials p.q, sum q (epilogue)
                 PProl pro;
                 pro.on = true;
-                pro.r = m->r;
-                pro.dinv = m->dinv;
+                pro.z = m->z;
                 pro.p_old = p_old;
                 pro.p_out = p_new;
                 pro.beta = &m->scal->beta;
                 pro.done = &m->scal->done;
                 DotEpi epi;
                 epi.partial = m->partial;
-                const int grid = apply_grid(g);
-                CKS(run_apply(m, lam, nu, nu_const, nullptr, m->q, Halo{}, epi, pro, grid));
+                int grid = 0;
+                CKS(run_apply(m, lam, nu, nu_const, nullptr, m->q, Halo{}, epi, pro, &grid));
                 CKS(reduce_fin(m, grid, FIN_ALPHA));
-                CK(launch_pcg_update(g, u, m->r, p_new, m->q, m->dinv, m->mass_e, m->scal, m->partial, m->st));
+                CK(launch_pcg_update(g, u, m->r, p_new, m->q, m->dinv, m->z, m->mass_e, m->scal, m->partial, m->st));
                 m->launches += 1;
                 CKS(reduce_fin(m, VG, FIN_BETA));
                 std::swap(p_old, p_new);
             } else {
                 // unfused: p = dinv r + beta p ; halo(p) ; q = A p ; p.q
-                CK(launch_pcg_pupd(g, p_old, m->r, m->dinv, m->scal, m->st));
+                CK(launch_pcg_pupd(g, p_old, m->z, m->scal, m->st));
                 m->launches += 1;
                 CKS(ensure_halos(m, false));
                 CKS(exchange(m, p_old, m->h_lo, m->h_hi));
                 Halo h = hnu;
                 h.u_lo = m->h_lo;
                 h.u_hi = m->h_hi;
-                CKS(run_apply(m, lam, nu, nu_const, p_old, m->q, h, DotEpi{}, PProl{}, apply_grid(g)));
+                CKS(run_apply(m, lam, nu, nu_const, p_old, m->q, h, DotEpi{}, PProl{}));
                 CK(launch_dot_pq(g, p_old, m->q, m->scal, m->partial, m->st));
                 m->launches += 1;
                 CKS(reduce_fin(m, VG, FIN_ALPHA));
-                CK(launch_pcg_update(g, u, m->r, p_old, m->q, m->dinv, m->mass_e, m->scal, m->partial, m->st));
+                CK(launch_pcg_update(g, u, m->r, p_old, m->q, m->dinv, m->z, m->mass_e, m->scal, m->partial, m->st));
                 m->launches += 1;
                 CKS(reduce_fin(m, VG, FIN_BETA));
             }
@@ -547,7 +515,10 @@ dg_status dg_mesh_create(int dim, const int N[3], const double L[3], int P, int 
     }
     g.Nl[S] = g.N[S] / nranks;
     g.nel = (long long)g.Nl[0] * g.Nl[1] * g.Nl[2];
-    choose_bricks(g);
+    for (int d = 0; d < 3; ++d) {  // brick shape is chosen per launch by the apply dispatch
+        g.B[d] = 1;
+        g.nbk[d] = g.Nl[d];
+    }
     m->rank = rank;
     m->nranks = nranks;
     m->st = (cudaStream_t)cuda_stream;
@@ -571,7 +542,7 @@ dg_status dg_mesh_create(int dim, const int N[3], const double L[3], int P, int 
             done.push_back(m->device);
         }
     }
-    const int pcap = 2 * std::max(apply_grid(g), vec_grid()) + 64;
+    const int pcap = 2 * std::max(APPLY_GRID_MAX, vec_grid()) + 64;
     dg_status s;
     if ((s = alloc((void **)&m->partial, sizeof(double) * pcap)) != DG_OK) return fail(s);
     m->partial_cap = pcap;
@@ -607,7 +578,7 @@ void dg_mesh_destroy(dg_mesh *m)
     if (!m) return;
     if (m->st) cudaStreamSynchronize(m->st);
     else cudaDeviceSynchronize();
-    double *bufs[] = {m->r, m->q, m->pa, m->pb, m->dinv, m->partial, m->sums, m->aux, m->mass_e, m->hist,
+    double *bufs[] = {m->r, m->q, m->pa, m->pb, m->dinv, m->z, m->partial, m->sums, m->aux, m->mass_e, m->hist,
                       m->h_lo, m->h_hi, m->hn_lo, m->hn_hi, m->st_a, m->st_b, m->st_c};
     for (double *b : bufs)
         if (b) cudaFree(b);

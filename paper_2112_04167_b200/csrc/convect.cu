@@ -1,7 +1,7 @@
 // convect.cu -- instantiations of the LLF convection kernel (see convect.cuh).
 #include "dev_common.cuh"
 namespace dg {
-DG_DEFINE_CONST_TABLES(upload_tables_convect)
+DG_DEFINE_CONV_TABLES(upload_tables_convect)
 }
 #include "convect.cuh"
 namespace dg {

@@ -40,7 +40,7 @@ __global__ void __launch_bounds__(256) k_convect(const ConvParams a)
     using C = CCfg<DIM, P>;
     constexpr int n = C::n, Q = C::Q, NZ = C::NZ, QZ = C::QZ, NPE = C::NPE, NQ = C::NQ;
     const Geom &g = a.g;
-    const DevTab &T = c_tab[P];
+    const CvTab &T = c_ctab[P];
     extern __shared__ double sm[];
     double *sv = sm;                 // [3][NPE]
     double *vg = sv + 3 * NPE;       // [3][NQ]

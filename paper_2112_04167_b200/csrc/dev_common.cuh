@@ -17,11 +17,18 @@
 
 namespace dg {
 
+// operator tables (apply / diag / vec TUs)
 struct DevTab {
     double xi[NMAX];
     double w[NMAX];
     double D[NMAX][NMAX];
-    double Q;  // stored as double to keep the struct 8-byte homogeneous
+    double Kref[NMAX][NMAX];
+    EOTab eD, eE, eK;
+};
+
+// convection tables (convect TU)
+struct CvTab {
+    double w[NMAX];
     double zq[QMAX];
     double wq[QMAX];
     double Bq[QMAX][NMAX];
@@ -33,9 +40,19 @@ inline void to_devtab(const Tab &t, DevTab *d)
     for (int i = 0; i < NMAX; ++i) {
         d->xi[i] = t.xi[i];
         d->w[i] = t.w[i];
-        for (int j = 0; j < NMAX; ++j) d->D[i][j] = t.D[i][j];
+        for (int j = 0; j < NMAX; ++j) {
+            d->D[i][j] = t.D[i][j];
+            d->Kref[i][j] = t.Kref[i][j];
+        }
     }
-    d->Q = t.Q;
+    d->eD = t.eD;
+    d->eE = t.eE;
+    d->eK = t.eK;
+}
+
+inline void to_cvtab(const Tab &t, CvTab *d)
+{
+    for (int i = 0; i < NMAX; ++i) d->w[i] = t.w[i];
     for (int q = 0; q < QMAX; ++q) {
         d->zq[q] = t.zq[q];
         d->wq[q] = t.wq[q];
@@ -53,6 +70,15 @@ inline void to_devtab(const Tab &t, DevTab *d)
         static DevTab h[PMAX + 1];                                                          \
         for (int p = 1; p <= PMAX; ++p) to_devtab(host_tab(p), &h[p]);                      \
         return cudaMemcpyToSymbol(c_tab, h, sizeof(h));                                     \
+    }
+
+#define DG_DEFINE_CONV_TABLES(fn_name)                                                      \
+    static __constant__ CvTab c_ctab[PMAX + 1];                                             \
+    cudaError_t fn_name()                                                                   \
+    {                                                                                       \
+        static CvTab h[PMAX + 1];                                                           \
+        for (int p = 1; p <= PMAX; ++p) to_cvtab(host_tab(p), &h[p]);                       \
+        return cudaMemcpyToSymbol(c_ctab, h, sizeof(h));                                    \
     }
 
 template <int DIM, int P>

@@ -14,6 +14,21 @@ constexpr int PMAX = 10;         // highest compiled degree
 constexpr int NMAX = PMAX + 1;   // GLL points per direction
 constexpr int QMAX = (3 * PMAX) / 2 + 1;  // Gauss points for convection (reading A13)
 
+constexpr int HMAX = NMAX / 2 + 1;  // even-odd half size
+
+// Even-odd (Kopriva) factorisation of an n x n matrix X that is centro-symmetric (sym:
+// X[P-i][P-j] = X[i][j]) or anti-centro-symmetric (anti: X[P-i][P-j] = -X[i][j]).
+// h = n/2, mid = P/2 (odd n only):
+//   Te[i][j] = (X[i][j] + X[i][P-j])/2,  To[i][j] = (X[i][j] - X[i][P-j])/2   (i, j < h)
+//   Tc[i] = X[i][mid],  Mr[j] = X[mid][j],  Mmid = X[mid][mid]
+struct EOTab {
+    double Te[HMAX][HMAX];
+    double To[HMAX][HMAX];
+    double Tc[HMAX];
+    double Mr[HMAX];
+    double Mmid;
+};
+
 // Per-degree 1-D tables (host copy; uploaded to __constant__ memory by the kernels TU).
 struct Tab {
     double xi[NMAX];          // GLL nodes on [-1,1]
@@ -24,6 +39,12 @@ struct Tab {
     double wq[QMAX];          // Gauss weights
     double Bq[QMAX][NMAX];    // Bq[q][j] = l_j(zq_q)  (barycentric form)
     double Gq[QMAX][NMAX];    // Gq[q][j] = l_j'(zq_q) = (Bq D)[q][j]
+    // Reference SIP line matrix for constant nu (reading A1: tau = (P+1)^2/h = (P+1)^2/2 * (2/h)):
+    //   Kref = Kvol + F1 + (P+1)^2/2 F2,  Kvol[i][j] = sum_k w_k D[k][i] D[k][j],
+    //   F1 = -1/2 (e_P D[P]^T + D[P] e_P^T) + 1/2 (e_0 D[0]^T + D[0] e_0^T),  F2 = e_0 e_0^T + e_P e_P^T
+    // so that one element line contributes  (nu 2/h) Kref v  plus the neighbour terms.
+    double Kref[NMAX][NMAX];
+    EOTab eD, eE, eK;         // even-odd forms of D (anti), D^T (anti), Kref (sym)
 };
 
 // tables.cpp
@@ -58,11 +79,11 @@ struct DotEpi {
     double *partial = nullptr;
 };
 
-// Prologue for the PCG apply: the operand is p = dinv .* r + beta * p_old (computed on the
-// fly, also for neighbour lines), and p is written to p_out for the owned elements.
+// Prologue for the PCG apply: the operand is p = z + beta * p_old (computed on the fly, also
+// for neighbour lines), and p is written to p_out for the owned elements.
 struct PProl {
     bool on = false;
-    const double *r = nullptr, *dinv = nullptr, *p_old = nullptr;
+    const double *z = nullptr, *p_old = nullptr;   // z = D^-1 r (written by the update kernel)
     double *p_out = nullptr;
     const double *beta = nullptr;  // device scalar
     const int *done = nullptr;     // device flag: skip all work when set
@@ -77,6 +98,7 @@ struct ApplyParams {
     DotEpi epi;
     PProl pro;
     long long b0, b1;   // brick range [b0, b1)
+    int seglen = 1, nseg = 1;  // column segments along the slowest direction (apply kernel)
 };
 
 struct ConvParams {
@@ -88,8 +110,9 @@ struct ConvParams {
 };
 
 // apply2.cu / apply3.cu / convect.cu
-cudaError_t launch_apply2(const ApplyParams &a, bool varnu, bool pcg, int grid, int smem, cudaStream_t st);
-cudaError_t launch_apply3(const ApplyParams &a, bool varnu, bool pcg, int grid, int smem, cudaStream_t st);
+// grid: out, the number of CTAs launched (persistent; <= 148 x 8)
+cudaError_t launch_apply2(const ApplyParams &a, bool varnu, bool pcg, int *grid, int smem, cudaStream_t st);
+cudaError_t launch_apply3(const ApplyParams &a, bool varnu, bool pcg, int *grid, int smem, cudaStream_t st);
 cudaError_t launch_diag2(const Geom &g, double lam, const double *nu, double nuc, const Halo &h, double *d,
                          cudaStream_t st);
 cudaError_t launch_diag3(const Geom &g, double lam, const double *nu, double nuc, const Halo &h, double *d,
@@ -119,12 +142,12 @@ cudaError_t launch_mass_moments(const Geom &g, const double *f, const double *ma
 // r = m (f - fmean) - Ar ; partial: sum r, sum (f-fmean)^2
 cudaError_t launch_pcg_init(const Geom &g, const double *f, const double *Ar, double *r, const double *mass_e,
                             const PcgScal *s, double *partial, cudaStream_t st);
-// r -= rsum/N (lam==0) ; z = dinv r ; p = z ; partial: r.z, sum (r/m)^2
-cudaError_t launch_pcg_init2(const Geom &g, double *r, const double *dinv, double *p, const double *mass_e,
-                             const PcgScal *s, const double *rsum_global, double *partial, cudaStream_t st);
-// x += a p ; r -= a (q - qmean) ; partial: r.(dinv r), sum (r/m)^2
+// r -= rmean (lam==0) ; z = dinv r ; partial: r.z, sum (r/m)^2
+cudaError_t launch_pcg_init2(const Geom &g, double *r, const double *dinv, double *z, const double *mass_e,
+                             const PcgScal *s, double *partial, cudaStream_t st);
+// x += a p ; r -= a (q - qmean) ; z = dinv r ; partial: r.z, sum (r/m)^2
 cudaError_t launch_pcg_update(const Geom &g, double *x, double *r, const double *p, const double *q,
-                              const double *dinv, const double *mass_e, const PcgScal *s, double *partial,
+                              const double *dinv, double *z, const double *mass_e, const PcgScal *s, double *partial,
                               cudaStream_t st);
 // u -= (sum m u)/(sum m)  (lam == 0), partial for the moment is computed separately
 cudaError_t launch_shift(const Geom &g, double *x, const double *shift, cudaStream_t st);
@@ -136,8 +159,7 @@ cudaError_t launch_finalize(int mode, const double *sums, PcgScal *s, double *hi
 cudaError_t launch_reduce_s(const double *partial, int G, int K, double *sums, const PcgScal *s, cudaStream_t st);
 cudaError_t launch_reduce_fin(const double *partial, int G, int K, double *sums, int mode, PcgScal *s, double *hist,
                               double *aux, cudaStream_t st);
-cudaError_t launch_pcg_pupd(const Geom &g, double *p, const double *r, const double *dinv, const PcgScal *s,
-                            cudaStream_t st);
+cudaError_t launch_pcg_pupd(const Geom &g, double *p, const double *z, const PcgScal *s, cudaStream_t st);
 cudaError_t launch_dot_pq(const Geom &g, const double *p, const double *q, const PcgScal *s, double *partial,
                           cudaStream_t st);
 cudaError_t launch_recip(const Geom &g, const double *d, double *dinv, cudaStream_t st);

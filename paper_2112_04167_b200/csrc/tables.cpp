@@ -35,6 +35,8 @@ const long double PI_L = 3.14159265358979323846264338327950288L;
 
 }  // namespace
 
+static void build_eo(int P, const long double X[NMAX][NMAX], EOTab *e);
+
 void build_tab(int P, Tab *t)
 {
     const int n = P + 1;
@@ -68,6 +70,31 @@ void build_tab(int P, Tab *t)
             else D[i][j] = 0.0L;
             t->D[i][j] = (double)D[i][j];
         }
+
+    // constant-nu reference line matrix and even-odd tables
+    {
+        long double Kr[NMAX][NMAX], Dt[NMAX][NMAX];
+        long double wl[NMAX];
+        for (int i = 0; i < n; ++i) wl[i] = 2.0L / ((long double)P * (P + 1) * lp[i] * lp[i]);
+        const long double kap = (long double)(P + 1) * (P + 1) / 2.0L;
+        for (int i = 0; i < n; ++i)
+            for (int j = 0; j < n; ++j) {
+                long double s = 0.0L;
+                for (int k = 0; k < n; ++k) s += wl[k] * D[k][i] * D[k][j];
+                if (i == P) s += -0.5L * D[P][j];
+                if (j == P) s += -0.5L * D[P][i];
+                if (i == 0) s += 0.5L * D[0][j];
+                if (j == 0) s += 0.5L * D[0][i];
+                if (i == j && (i == 0 || i == P)) s += kap;
+                Kr[i][j] = s;
+                Dt[i][j] = D[j][i];
+            }
+        for (int i = 0; i < NMAX; ++i)
+            for (int j = 0; j < NMAX; ++j) t->Kref[i][j] = (i < n && j < n) ? (double)Kr[i][j] : 0.0;
+        build_eo(P, D, &t->eD);
+        build_eo(P, Dt, &t->eE);
+        build_eo(P, Kr, &t->eK);
+    }
 
     // Gauss-Legendre points for convection
     const int Q = (3 * P) / 2 + 1;
@@ -104,6 +131,28 @@ void build_tab(int P, Tab *t)
             for (int k = 0; k < n; ++k) g += B[k] * D[k][j];
             t->Gq[qa][j] = (double)g;
         }
+    }
+}
+
+static void build_eo(int P, const long double X[NMAX][NMAX], EOTab *e)
+{
+    const int n = P + 1, h = n / 2, mid = P / 2;
+    for (int i = 0; i < HMAX; ++i) {
+        for (int j = 0; j < HMAX; ++j) e->Te[i][j] = e->To[i][j] = 0.0;
+        e->Tc[i] = e->Mr[i] = 0.0;
+    }
+    e->Mmid = 0.0;
+    for (int i = 0; i < h; ++i)
+        for (int j = 0; j < h; ++j) {
+            e->Te[i][j] = (double)((X[i][j] + X[i][P - j]) / 2.0L);
+            e->To[i][j] = (double)((X[i][j] - X[i][P - j]) / 2.0L);
+        }
+    if (n % 2 == 1) {
+        for (int i = 0; i < h; ++i) {
+            e->Tc[i] = (double)X[i][mid];
+            e->Mr[i] = (double)X[mid][i];
+        }
+        e->Mmid = (double)X[mid][mid];
     }
 }
 

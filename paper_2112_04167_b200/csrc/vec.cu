@@ -56,7 +56,7 @@ __global__ void k_pcg_init(long long ndof, int npe, const double *__restrict__ f
 }
 
 __global__ void k_pcg_init2(long long ndof, int npe, double *__restrict__ r, const double *__restrict__ dinv,
-                            const double *__restrict__ me, const PcgScal *s, double *partial)
+                            double *__restrict__ z, const double *__restrict__ me, const PcgScal *s, double *partial)
 {
     const double rmean = s->qmean;  // FIN_INIT stores the mean of r here (lam == 0), else 0
     double v[2] = {0.0, 0.0};
@@ -64,7 +64,9 @@ __global__ void k_pcg_init2(long long ndof, int npe, double *__restrict__ r, con
         const double m = __ldg(me + (int)(i % npe));
         const double ri = r[i] - rmean;
         r[i] = ri;
-        v[0] = fma(ri, dinv[i] * ri, v[0]);
+        const double zi = dinv[i] * ri;
+        z[i] = zi;
+        v[0] = fma(ri, zi, v[0]);
         const double rm = ri / m;
         v[1] = fma(rm, rm, v[1]);
     }
@@ -73,8 +75,8 @@ __global__ void k_pcg_init2(long long ndof, int npe, double *__restrict__ r, con
 
 __global__ void k_pcg_update(long long ndof, int npe, double *__restrict__ x, double *__restrict__ r,
                              const double *__restrict__ p, const double *__restrict__ q,
-                             const double *__restrict__ dinv, const double *__restrict__ me, const PcgScal *s,
-                             double *partial)
+                             const double *__restrict__ dinv, double *__restrict__ z, const double *__restrict__ me,
+                             const PcgScal *s, double *partial)
 {
     if (s->done) return;
     const double alpha = s->alpha, qmean = s->qmean;
@@ -84,21 +86,22 @@ __global__ void k_pcg_update(long long ndof, int npe, double *__restrict__ x, do
         x[i] = fma(alpha, p[i], x[i]);
         const double ri = fma(-alpha, q[i] - qmean, r[i]);
         r[i] = ri;
-        v[0] = fma(ri, dinv[i] * ri, v[0]);
+        const double zi = dinv[i] * ri;
+        z[i] = zi;
+        v[0] = fma(ri, zi, v[0]);
         const double rm = ri / m;
         v[1] = fma(rm, rm, v[1]);
     }
     write_partials<2>(v, partial);
 }
 
-// p = dinv r + beta p (multi-rank path, where the apply prologue is not used)
-__global__ void k_pcg_pupd(long long ndof, double *__restrict__ p, const double *__restrict__ r,
-                           const double *__restrict__ dinv, const PcgScal *s)
+// p = z + beta p (multi-rank path, where the apply prologue is not used)
+__global__ void k_pcg_pupd(long long ndof, double *__restrict__ p, const double *__restrict__ z, const PcgScal *s)
 {
     if (s->done) return;
     const double beta = s->beta;
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < ndof; i += (long long)gridDim.x * blockDim.x)
-        p[i] = fma(beta, p[i], dinv[i] * r[i]);
+        p[i] = fma(beta, p[i], z[i]);
 }
 
 // partial p.q and sum q (multi-rank path)
@@ -282,27 +285,24 @@ cudaError_t launch_pcg_init(const Geom &g, const double *f, const double *Ar, do
     return cudaGetLastError();
 }
 
-cudaError_t launch_pcg_init2(const Geom &g, double *r, const double *dinv, double *p, const double *mass_e,
-                             const PcgScal *s, const double *rsum_global, double *partial, cudaStream_t st)
+cudaError_t launch_pcg_init2(const Geom &g, double *r, const double *dinv, double *z, const double *mass_e,
+                             const PcgScal *s, double *partial, cudaStream_t st)
 {
-    (void)p;
-    (void)rsum_global;
-    k_pcg_init2<<<vec_grid(), 256, 0, st>>>(nd(g), g.npe, r, dinv, mass_e, s, partial);
+    k_pcg_init2<<<vec_grid(), 256, 0, st>>>(nd(g), g.npe, r, dinv, z, mass_e, s, partial);
     return cudaGetLastError();
 }
 
 cudaError_t launch_pcg_update(const Geom &g, double *x, double *r, const double *p, const double *q,
-                              const double *dinv, const double *mass_e, const PcgScal *s, double *partial,
+                              const double *dinv, double *z, const double *mass_e, const PcgScal *s, double *partial,
                               cudaStream_t st)
 {
-    k_pcg_update<<<vec_grid(), 256, 0, st>>>(nd(g), g.npe, x, r, p, q, dinv, mass_e, s, partial);
+    k_pcg_update<<<vec_grid(), 256, 0, st>>>(nd(g), g.npe, x, r, p, q, dinv, z, mass_e, s, partial);
     return cudaGetLastError();
 }
 
-cudaError_t launch_pcg_pupd(const Geom &g, double *p, const double *r, const double *dinv, const PcgScal *s,
-                            cudaStream_t st)
+cudaError_t launch_pcg_pupd(const Geom &g, double *p, const double *z, const PcgScal *s, cudaStream_t st)
 {
-    k_pcg_pupd<<<vec_grid(), 256, 0, st>>>(nd(g), p, r, dinv, s);
+    k_pcg_pupd<<<vec_grid(), 256, 0, st>>>(nd(g), p, z, s);
     return cudaGetLastError();
 }
 
