@@ -28,6 +28,7 @@
 #pragma once
 
 #include <algorithm>
+#include <cstdint>
 #include <cstdlib>
 
 #include "dev_common.cuh"
@@ -84,6 +85,7 @@ __device__ __forceinline__ double end_flux(const DevTab &T, const double (&v)[P 
 }  // namespace dg
 
 #include "apply_kernel.cuh"
+#include "apply5.cuh"
 
 namespace dg {
 
@@ -199,6 +201,54 @@ struct ApplyDispatch {
             return cudaGetLastError();
         }
     }
+    // v5 (3-D): warp-specialised TMA/mbarrier kernel on 2x2x2 bricks (apply5.cuh)
+    template <int P, bool VARNU, int MODE>
+    static cudaError_t go5(ApplyParams a, int *grid, cudaStream_t st)
+    {
+        using K = v5::KC5<P, VARNU, MODE>;
+        if constexpr (K::SMEM_BYTES > 227 * 1024) {
+            return cudaErrorNotSupported;
+        } else {
+            auto kern = v5::k_apply5<P, VARNU, MODE>;
+            static int occ = -1, nsm = 0;
+            cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, K::SMEM_BYTES);
+            if (e != cudaSuccess) return e;
+            if (occ < 0) {
+                int dev = 0;
+                cudaGetDevice(&dev);
+                cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+                e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, K::NT, K::SMEM_BYTES);
+                if (e != cudaSuccess) return e;
+                if (occ < 1) return cudaErrorInvalidConfiguration;
+            }
+            long long gsz = (long long)nsm * std::min(occ, 4);
+            const long long ncols = (long long)(a.g.Nl[0] / 2) * (a.g.Nl[1] / 2);
+            const int nbS = a.g.Nl[2] / 2;
+            int nseg = 1;
+            while (ncols * nseg < 3 * gsz && nbS % (2 * nseg) == 0) nseg *= 2;
+            a.nseg = nseg;
+            a.seglen = nbS / nseg;
+            const long long nunits = ncols * nseg;
+            if (gsz > nunits) gsz = nunits;
+            if (gsz < 1) gsz = 1;
+            *grid = (int)gsz;
+            kern<<<(int)gsz, K::NT, K::SMEM_BYTES, st>>>(a);
+            return cudaGetLastError();
+        }
+    }
+    static bool v5_ok(const ApplyParams &a, bool pcg)
+    {
+        static const bool off = [] {
+            const char *e = getenv("DG_APPLY_IMPL");
+            return e && e[0] == 'v' && e[1] == '4';
+        }();
+        if (off || DIM != 3) return false;
+        for (int d = 0; d < 3; ++d)
+            if (a.g.Nl[d] % 2) return false;
+        auto al = [](const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+        if (pcg) return al(a.pro.z) && al(a.pro.p_old) && al(a.pro.p_out) && (!a.nu || al(a.nu));
+        return al(a.u) && (!a.nu || al(a.nu));
+    }
     // brick shape: the largest of the candidates that divides the local mesh and fits the
     // shared-memory budget (default 110 KB = two CTAs per SM; DG_SMEM_BUDGET_KB overrides)
     template <int P, bool VARNU, int MODE>
@@ -210,6 +260,10 @@ struct ApplyDispatch {
         }();
         const int *N = a.g.Nl;
         if constexpr (DIM == 3) {
+            if (v5_ok(a, MODE == 1)) {
+                const cudaError_t e = go5<P, VARNU, MODE>(a, grid, st);
+                if (e != cudaErrorNotSupported) return e;
+            }
             if (N[0] % 2 == 0 && N[1] % 2 == 0 && N[2] % 2 == 0 && KC<3, P, VARNU, MODE, 2, 2, 2>::SMEM_BYTES <= budget)
                 return go<P, VARNU, MODE, 2, 2, 2>(a, grid, st);
             if (N[0] % 2 == 0 && N[1] % 2 == 0 && KC<3, P, VARNU, MODE, 2, 2, 1>::SMEM_BYTES <= budget)

@@ -512,6 +512,14 @@ dg_status dg_mesh_create(int dim, const int N[3], const double L[3], int P, int 
         g.Nl[d] = g.N[d];
         g.h[d] = d < dim ? L[d] / N[d] : 1.0;
         g.tau[d] = (double)(P + 1) * (P + 1) / g.h[d];
+        g.sd[d] = 2.0 / g.h[d];
+    }
+    g.mfac = 1.0;
+    for (int d = 0; d < dim; ++d) g.mfac *= 0.5 * g.h[d];
+    for (int d = 0; d < 3; ++d) {
+        g.wfac[d] = 1.0;
+        for (int d2 = 0; d2 < dim; ++d2)
+            if (d2 != d) g.wfac[d] *= 0.5 * g.h[d2];
     }
     g.Nl[S] = g.N[S] / nranks;
     g.nel = (long long)g.Nl[0] * g.Nl[1] * g.Nl[2];

@@ -65,6 +65,9 @@ struct Geom {
     int nbk[3];      // bricks per direction (local)
     double h[3];     // element size per direction
     double tau[3];   // penalty (P+1)^2 / h_d (reading A1)
+    double sd[3];    // 2 / h_d (reference-to-physical derivative factor)
+    double wfac[3];  // transverse Jacobian of a line along d: prod_{d' != d} h_d'/2
+    double mfac;     // element Jacobian prod_d h_d/2 (GLL mass m_I = w_i w_j (w_k) mfac)
     long long nel;   // local elements
 };
 
