@@ -135,7 +135,7 @@ struct KC5 {
     static constexpr int OFF_TR = OFF_ACC + BRK;
     static constexpr int OFF_RED = OFF_TR + 2 * TRB;
     static constexpr int OFF_BAR = OFF_RED + 64;  // 4 mbarriers (uint64)
-    static constexpr int SMEM_DOUBLES = OFF_BAR + 6;
+    static constexpr int SMEM_DOUBLES = OFF_BAR + 4;
     static constexpr int SMEM_BYTES = SMEM_DOUBLES * 8;
     static constexpr int KTD = (2 * LN + NP - 1) / NP;  // producer trace tasks per thread per direction
     static constexpr int MINB = (SMEM_BYTES + 1024) * 2 <= 228 * 1024 ? 2 : 1;
@@ -156,15 +156,27 @@ struct Tr {
 // ---------------------------------------------------------------------------
 // consumer: one direction pass over the brick
 // ---------------------------------------------------------------------------
+// z-pass carry of one consumer thread (its z line L is the same in every brick): the output
+// of the brick's TOP element line is held back until the next brick of the column supplies
+// the other side of the shared face, so no brick ever waits for its upper neighbour.
+template <int n>
+struct ZCarry {
+    bool held = false;
+    double o[n];          // top-element output without its top-face terms
+    double *po = nullptr; // its destination
+    double u, gP, nu;     // top-face own trace: u_P, (D v)_P, nu_P
+};
+
 template <class K, int D, bool FIRST, bool LAST>
 __device__ __forceinline__ void cpass(const ApplyParams &a, const DevTab &T, const double *su, const double *snu,
-                                      double *sacc, const double *tr, double *trnext, long long ebase, int L,
-                                      double &epi0, double &epi1)
+                                      double *sacc, const double *tr, long long ebase, int L, double &epi0,
+                                      double &epi1, ZCarry<K::n> &zc, bool zfirst, bool zlast)
 {
     constexpr int P = K::P, n = K::n, NN = K::NN, NPE = K::NPE, B = K::B, LN = K::LN, NV = K::NV;
     constexpr int O1 = Tr<D>::O1, O2 = Tr<D>::O2;
     constexpr int SS[3] = {1, n, NN};                         // node strides (smem == global)
     constexpr int ES[3] = {NPE, B * NPE, B * B * NPE};        // element strides in the brick
+    constexpr bool ZC = (D == 2) && LAST;                     // column carry active in this pass
     if (L >= LN) return;
     const Geom &g = a.g;
     const int ce = L / NN, tn = L - ce * NN;
@@ -175,10 +187,23 @@ __device__ __forceinline__ void cpass(const ApplyParams &a, const DevTab &T, con
     const double sd = g.sd[D], htau = 0.5 * g.tau[D];
     const double *trd = tr + D * K::TRD;
     // brick-face traces: side 0 (left/bottom neighbour, its node P), side 1 (its node 0)
-    const double uLb = trd[0 * LN + L], sLb = trd[1 * LN + L];
-    const double uRb = trd[NV * LN + L], sRb = trd[(NV + 1) * LN + L];
-    const double nuLb = K::VARNU ? trd[2 * LN + L] : a.nu_const;
-    const double nuRb = K::VARNU ? trd[(NV + 2) * LN + L] : a.nu_const;
+    const bool use_lo = !ZC || zfirst, use_hi = !ZC || zlast;
+    const double nu_c = a.nu_const;
+    double uLb, sLb, nuLb, uRb = 0.0, sRb = 0.0, nuRb = nu_c;
+    if (use_lo) {
+        uLb = trd[0 * LN + L];
+        sLb = trd[1 * LN + L];
+        nuLb = K::VARNU ? trd[2 * LN + L] : nu_c;
+    } else {
+        uLb = zc.u;
+        nuLb = K::VARNU ? zc.nu : nu_c;
+        sLb = nuLb * sd * zc.gP;
+    }
+    if (use_hi) {
+        uRb = trd[NV * LN + L];
+        sRb = trd[(NV + 1) * LN + L];
+        nuRb = K::VARNU ? trd[(NV + 2) * LN + L] : nu_c;
+    }
 
     double v[B][n], nv[B][n];
 #pragma unroll
@@ -211,8 +236,25 @@ __device__ __forceinline__ void cpass(const ApplyParams &a, const DevTab &T, con
         }
     }
 
-    // accumulate / store the line result r of element l of the brick row
-    auto emit = [&](int l, const double (&r)[n]) {
+    // release the held top element of the previous brick: add its top-face terms
+    // dr_i = c D_{P,i} + [i == P] f0 (c: lifting / neighbour-value coefficient, f0: flux part)
+    auto release = [&](double c, double f0) {
+        double s1 = 0.0;
+#pragma unroll
+        for (int i = 0; i < n; ++i) {
+            const double d = W * fma(c, T.D[P][i], i == P ? f0 : 0.0);
+            zc.po[i * SS[D]] = zc.o[i] + d;
+            s1 += d;
+        }
+        if (K::MODE == 1) {
+            epi0 = fma(W, fma(c, zc.gP, f0 * zc.u), epi0);  // sum_i v_i dr_i W
+            epi1 += s1;
+        }
+        zc.held = false;
+    };
+
+    // accumulate / store (or hold) the line result r of element l of the brick row
+    auto emit = [&](int l, const double (&r)[n], bool hold) {
         double *pa = sacc + soff + l * ES[D];
         if (FIRST) {
 #pragma unroll
@@ -227,18 +269,19 @@ __device__ __forceinline__ void cpass(const ApplyParams &a, const DevTab &T, con
             lc[D] = l;
             const long long ge = ebase + lc[0] + (long long)g.Nl[0] * (lc[1] + (long long)g.Nl[1] * lc[2]);
             double *po = a.out + ge * NPE + ta * SS[O1] + tb * SS[O2];
-            const double *pu = su + soff + l * ES[D];
             const double lw = a.lam * W * (0.5 * g.h[D]);  // lam m_I = lam W w_i h_D/2
 #pragma unroll
             for (int i = 0; i < n; ++i) {
-                const double ui = pu[i * SS[D]];
+                const double ui = v[l][i];
                 const double o = fma(lw * T.w[i], ui, fma(W, r[i], pa[i * SS[D]]));
-                po[i * SS[D]] = o;
+                if (ZC && hold) zc.o[i] = o;
+                else po[i * SS[D]] = o;
                 if (K::MODE == 1) {
                     epi0 = fma(ui, o, epi0);
                     epi1 += o;
                 }
             }
+            if (ZC && hold) zc.po = po;
         }
     };
 
@@ -260,12 +303,11 @@ __device__ __forceinline__ void cpass(const ApplyParams &a, const DevTab &T, con
             J[f] = um - up;
             F[f] = fma(htau * (nm + np), J[f], -0.5 * (sm + sp));
         }
-        if (D == 2 && trnext) {  // carry: our top-face traces are the next brick's bottom traces
-            double *tz = trnext + 2 * K::TRD;
-            tz[L] = v[B - 1][P];
-            tz[LN + L] = nv[B - 1][P] * sd * gg[B - 1][P];
-            tz[2 * LN + L] = nv[B - 1][P];
+        if (ZC && !use_hi) {  // top face deferred to the next brick
+            F[B] = 0.0;
+            J[B] = 0.0;
         }
+        if (ZC && !use_lo && zc.held) release(-0.5 * sd * zc.nu * J[0], F[0]);
 #pragma unroll
         for (int l = 0; l < B; ++l) {
             double t[n], r[n];
@@ -277,10 +319,16 @@ __device__ __forceinline__ void cpass(const ApplyParams &a, const DevTab &T, con
             eo<P, true>(T.eE, t, r);
             r[P] += F[l + 1];
             r[0] -= F[l];
-            emit(l, r);
+            emit(l, r, l == B - 1 && !use_hi);
+        }
+        if (ZC && !use_hi) {
+            zc.held = true;
+            zc.u = v[B - 1][P];
+            zc.gP = gg[B - 1][P];
+            zc.nu = nv[B - 1][P];
         }
     } else {
-        const double c = a.nu_const * sd;
+        const double c = nu_c * sd;
         const double ck = c * (0.5 * (P + 1) * (P + 1));
         double d0[B], dP[B];
 #pragma unroll
@@ -288,11 +336,8 @@ __device__ __forceinline__ void cpass(const ApplyParams &a, const DevTab &T, con
             d0[l] = rdot<P>(T, 0, v[l]);
             dP[l] = rdot<P>(T, P, v[l]);
         }
-        if (D == 2 && trnext) {  // carry (see above)
-            double *tz = trnext + 2 * K::TRD;
-            tz[L] = v[B - 1][P];
-            tz[LN + L] = c * dP[B - 1];
-        }
+        // previous top element: neighbour terms (1/2 c u+) D_P + [P] (-1/2 s+ - c kappa u+)
+        if (ZC && !use_lo && zc.held) release(0.5 * c * v[0][0], fma(-ck, v[0][0], -0.5 * c * d0[0]));
 #pragma unroll
         for (int l = 0; l < B; ++l) {
             const double uL = l == 0 ? uLb : v[l - 1][P];
@@ -306,7 +351,12 @@ __device__ __forceinline__ void cpass(const ApplyParams &a, const DevTab &T, con
             for (int i = 0; i < n; ++i) r[i] = fma(c, kv[i], fma(aR, T.D[P][i], aL * T.D[0][i]));
             r[P] += fma(-ck, uR, -0.5 * sR);
             r[0] += fma(-ck, uL, 0.5 * sL);
-            emit(l, r);
+            emit(l, r, l == B - 1 && !use_hi);
+        }
+        if (ZC && !use_hi) {
+            zc.held = true;
+            zc.u = v[B - 1][P];
+            zc.gP = dP[B - 1];
         }
     }
 }
@@ -391,28 +441,6 @@ __device__ __noinline__ void ptraces(const ApplyParams &a, const DevTab &T, doub
     }
 }
 
-// z-top (side 1) traces of the previous brick of the column: the right neighbour lines are
-// the bottom element layer of the brick just staged in shared memory (su, snu)
-template <class K>
-__device__ __forceinline__ void ptop_smem(const ApplyParams &a, const DevTab &T, double *trprev, const double *su,
-                                          const double *snu, int ptid)
-{
-    constexpr int P = K::P, n = K::n, NN = K::NN, NPE = K::NPE, B = K::B, LN = K::LN, NV = K::NV;
-    const double sd = a.g.sd[2];
-    double *trd = trprev + 2 * K::TRD;
-    for (int L = ptid; L < LN; L += K::NP) {
-        const int ce = L / NN, tn = L - ce * NN;
-        const int base = ((ce % B) + B * (ce / B)) * NPE + tn;  // (lx, ly, lz = 0), node (ta, tb, 0)
-        double v[n];
-#pragma unroll
-        for (int i = 0; i < n; ++i) v[i] = su[base + i * NN];
-        const double nuf = K::VARNU ? snu[base] : a.nu_const;
-        trd[NV * LN + L] = v[0];
-        trd[(NV + 1) * LN + L] = nuf * sd * rdot<P>(T, 0, v);
-        if (K::VARNU) trd[(NV + 2) * LN + L] = nuf;
-    }
-}
-
 template <int P, bool VARNU, int MODE>
 __global__ void __launch_bounds__((KC5<P, VARNU, MODE>::NT)) __maxnreg__((KC5<P, VARNU, MODE>::MAXREG)) k_apply5(const __grid_constant__ ApplyParams a)
 {
@@ -421,7 +449,7 @@ __global__ void __launch_bounds__((KC5<P, VARNU, MODE>::NT)) __maxnreg__((KC5<P,
     const Geom &g = a.g;
     const DevTab &T = c_tab[P];
     extern __shared__ __align__(16) double sm[];
-    // full[0..1] (producers + TMA bytes), empty[0..1] (consumers), ztop[0..1] (producers)
+    // full[0..1] (producers + TMA bytes), empty[0..1] (consumers)
     uint64_t *bar = reinterpret_cast<uint64_t *>(sm + K::OFF_BAR);
     const int tid = threadIdx.x;
     if (MODE == 1 && *a.pro.done) return;
@@ -431,8 +459,6 @@ __global__ void __launch_bounds__((KC5<P, VARNU, MODE>::NT)) __maxnreg__((KC5<P,
         mbar_init(&bar[1], NP);
         mbar_init(&bar[2], NC);
         mbar_init(&bar[3], NC);
-        mbar_init(&bar[4], NP);
-        mbar_init(&bar[5], NP);
         fence_proxy_async();
     }
     __syncthreads();
@@ -485,16 +511,10 @@ __global__ void __launch_bounds__((KC5<P, VARNU, MODE>::NT)) __maxnreg__((KC5<P,
                 ptraces<K, 0>(a, T, tr, e0, ptid, beta, 3);
                 ptraces<K, 1>(a, T, tr, e0, ptid, beta, 3);
                 // z faces: from global memory only at segment ends; inside a segment the
-                // bottom traces are carried by the consumers and the top traces of the
-                // previous brick come from this brick's staged bottom layer
+                // consumers carry the shared face from one brick to the next (ZCarry)
                 const int zm = (j == 0 ? 1 : 0) | (j == seglen - 1 ? 2 : 0);
                 if (zm) ptraces<K, 2>(a, T, tr, e0, ptid, beta, zm);
                 mbar_arrive(&bar[buf]);
-                if (j > 0) {
-                    mbar_wait(&bar[buf], (it >> 1) & 1);  // staged data (TMA / p) of this brick landed
-                    ptop_smem<K>(a, T, sm + K::OFF_TR + (buf ^ 1) * K::TRB, su, snu, ptid);
-                    mbar_arrive(&bar[4 + (buf ^ 1)]);
-                }
             }
         }
         return;
@@ -502,7 +522,8 @@ __global__ void __launch_bounds__((KC5<P, VARNU, MODE>::NT)) __maxnreg__((KC5<P,
 
     // ------------------------------- consumers -------------------------------
     double epi0 = 0.0, epi1 = 0.0;
-    int it = 0, zpar = 0;
+    int it = 0;
+    ZCarry<K::n> zc;
     double *sacc = sm + K::OFF_ACC;
     for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
         const int col = u % ncols, zs = u / ncols;
@@ -514,17 +535,12 @@ __global__ void __launch_bounds__((KC5<P, VARNU, MODE>::NT)) __maxnreg__((KC5<P,
             const double *tr = sm + K::OFF_TR + buf * K::TRB;
             const long long eb = e0[0] + s1 * e0[1] + s2 * e0[2];
             mbar_wait(&bar[buf], (it >> 1) & 1);
-            cpass<K, 0, true, false>(a, T, su, snu, sacc, tr, nullptr, eb, tid, epi0, epi1);
+            const bool zf = j == 0, zl = j == seglen - 1;
+            cpass<K, 0, true, false>(a, T, su, snu, sacc, tr, eb, tid, epi0, epi1, zc, zf, zl);
             named_sync(1, NC);
-            cpass<K, 1, false, false>(a, T, su, snu, sacc, tr, nullptr, eb, tid, epi0, epi1);
-            const bool more = j < seglen - 1;
-            if (more) {  // z-top traces of this brick (from the next brick's staged data)
-                mbar_wait(&bar[4 + buf], (zpar >> buf) & 1);
-                zpar ^= 1 << buf;
-            }
+            cpass<K, 1, false, false>(a, T, su, snu, sacc, tr, eb, tid, epi0, epi1, zc, zf, zl);
             named_sync(1, NC);
-            cpass<K, 2, false, true>(a, T, su, snu, sacc, tr, more ? sm + K::OFF_TR + (buf ^ 1) * K::TRB : nullptr, eb,
-                                     tid, epi0, epi1);
+            cpass<K, 2, false, true>(a, T, su, snu, sacc, tr, eb, tid, epi0, epi1, zc, zf, zl);
             mbar_arrive(&bar[2 + buf]);
             named_sync(1, NC);  // ACC is rewritten by the next brick's x pass
         }

@@ -45,3 +45,6 @@ ts = sum(v[1] for v in data.values()) or 1
 print(first_fn, "total warp-inst", tot)
 for k, v in sorted(data.items(), key=lambda kv: -kv[1][0])[:N]:
     print("%10d %5.1f%% st %5.1f%%  %s:%d  %s" % (v[0], 100 * v[0] / tot, 100 * v[1] / ts, k[0], k[1], v[2]))
+print("--- by stall samples")
+for k, v in sorted(data.items(), key=lambda kv: -kv[1][1])[:N]:
+    print("%10d %5.1f%% st %5.1f%%  %s:%d  %s" % (v[0], 100 * v[0] / tot, 100 * v[1] / ts, k[0], k[1], v[2]))
