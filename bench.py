@@ -106,41 +106,11 @@ class Clocks:
 
 
 # ---------------------------------------------------------------------------
-# seeded inputs for one rank's slab (identical values to the global canonical arrays)
+# seeded inputs for one rank's slab (identical values to the global canonical arrays;
+# tests/test_multirank_gloo.py checks that)
 # ---------------------------------------------------------------------------
 def slab_inputs(c, el_off, nel):
-    npe = c.n ** c.dim
-    from workloads.inputs import rng
-
-    g = rng(c.cid, 0)
-    g.bit_generator.advance(int(el_off) * npe)
-    u = g.uniform(-1.0, 1.0, size=(nel, npe))
-    g = rng(c.cid, 10)
-    g.bit_generator.advance(int(el_off) * npe)
-    f = g.uniform(-1.0, 1.0, size=(nel, npe))
-    nu = None
-    if c.variable_nu:
-        nu = c.nu()[el_off:el_off + nel] if nel * npe < 4_000_000 else _slab_nu(c, el_off, nel)
-    return u, f, nu
-
-
-def _slab_nu(c, el_off, nel):
-    from workloads.inputs import gll_points_for_sampling
-
-    n = c.n
-    xi = gll_points_for_sampling(c.P)
-    e = np.arange(el_off, el_off + nel)
-    N = c.N
-    ex, ey, ez = e % N[0], (e // N[0]) % N[1], e // (N[0] * N[1])
-    h = [c.L[d] / N[d] for d in range(3)]
-    x = ex[:, None, None, None] * h[0] + ((xi + 1) * 0.5 * h[0])[None, None, None, :]
-    y = ey[:, None, None, None] * h[1] + ((xi + 1) * 0.5 * h[1])[None, None, :, None]
-    z = ez[:, None, None, None] * h[2] + ((xi + 1) * 0.5 * h[2])[None, :, None, None]
-    x, y, z = np.broadcast_arrays(x, y, z)
-    X = [a.reshape(nel, n ** 3) for a in (x, y, z)]
-    if c.cid == 5:
-        return c.nu0 * (1.0 + 0.5 * np.tanh(4.0 * np.sin(X[0]) * np.sin(X[1]) * np.sin(X[2])))
-    raise ValueError
+    return c.apply_input_slab(el_off, nel), c.rhs_slab(0, el_off, nel), c.nu_slab(el_off, nel)
 
 
 # ---------------------------------------------------------------------------

@@ -128,6 +128,28 @@ __global__ void __launch_bounds__(256) k_diag(const Geom g, double lam, const do
                 vn[k] = VARNU ? __ldg(nu + e * C::NPE + goff + k * GS) : nu_const;
             }
             const bool self = (g.N[D] == 1);
+            if (!self) {
+                // closed form: (2/h) sum_k w_k nu_k D_ki^2, plus at node P
+                // -nu_P (2/h) D_PP + tau (nu_P + nu_R)/2 and at node 0 +nu_0 (2/h) D_00 + tau (nu_0 + nu_L)/2
+                double acc = 0.0;
+#pragma unroll
+                for (int k = 0; k < n; ++k) {
+                    const double nk = VARNU ? __ldg(nu + e * C::NPE + goff + k * GS) : nu_const;
+                    acc = fma(T.w[k] * T.D[k][i] * T.D[k][i], nk, acc);
+                }
+                acc *= sd;
+                if (i == P || i == 0) {
+                    int cn[3] = {ec[0], ec[1], ec[2]};
+                    cn[D] += (i == P) ? 1 : -1;
+                    const double nown = VARNU ? __ldg(nu + e * C::NPE + goff + i * GS) : nu_const;
+                    const double nnb = VARNU ? __ldg(elem_ptr(g, nu, halo.nu_lo, halo.nu_hi, cn[0], cn[1], cn[2]) + goff +
+                                                      (i == P ? 0 : P * GS))
+                                             : nu_const;
+                    acc += (i == P ? -1.0 : 1.0) * nown * sd * T.D[i][i] + 0.5 * g.tau[D] * (nown + nnb);
+                }
+                dg += W * acc;
+                continue;
+            }
             double uL, sL, nuL, uR, sR, nuR;
             if (self) {
                 uL = v[P]; nuL = vn[P]; sL = end_flux<P>(T, v, 1, nuL, sd);

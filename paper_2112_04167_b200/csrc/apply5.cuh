@@ -312,7 +312,7 @@ __device__ __forceinline__ void cpass(const ApplyParams &a, const DevTab &T, con
         for (int l = 0; l < B; ++l) {
             double t[n], r[n];
 #pragma unroll
-            for (int k = 0; k < n; ++k) t[k] = (T.w[k] * sd) * (nv[l][k] * gg[l][k]);
+            for (int k = 0; k < n; ++k) t[k] = g.wsd[D][k] * (nv[l][k] * gg[l][k]);
             // symmetry (lifting) terms -1/2 nu (2/h) D_{end,i} J folded into the D^T operand
             t[P] = fma(-0.5 * sd * nv[l][P], J[l + 1], t[P]);
             t[0] = fma(-0.5 * sd * nv[l][0], J[l], t[0]);

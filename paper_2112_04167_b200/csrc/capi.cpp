@@ -516,6 +516,8 @@ dg_status dg_mesh_create(int dim, const int N[3], const double L[3], int P, int 
     }
     g.mfac = 1.0;
     for (int d = 0; d < dim; ++d) g.mfac *= 0.5 * g.h[d];
+    for (int d = 0; d < 3; ++d)
+        for (int k = 0; k < NMAX; ++k) g.wsd[d][k] = k <= P ? host_tab(P).w[k] * g.sd[d] : 0.0;
     for (int d = 0; d < 3; ++d) {
         g.wfac[d] = 1.0;
         for (int d2 = 0; d2 < dim; ++d2)

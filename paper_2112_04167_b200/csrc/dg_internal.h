@@ -68,6 +68,7 @@ struct Geom {
     double sd[3];    // 2 / h_d (reference-to-physical derivative factor)
     double wfac[3];  // transverse Jacobian of a line along d: prod_{d' != d} h_d'/2
     double mfac;     // element Jacobian prod_d h_d/2 (GLL mass m_I = w_i w_j (w_k) mfac)
+    double wsd[3][NMAX];  // w_k * 2/h_d (GLL weight times derivative factor)
     long long nel;   // local elements
 };
 

@@ -126,6 +126,49 @@ class Config:
             return (self.lam + 2.0 * self.nu0) * np.sin(X[0]) * np.sin(X[1])
         return uniform_field(self.cid, 10 + comp, (self.n_el, self.n ** self.dim))
 
+    # ---- rank slabs (multi-GPU): the same values as the global arrays' slices ----------
+    def _slab_uniform(self, field: int, el_off: int, nel: int, npe: int):
+        g = rng(self.cid, field)
+        g.bit_generator.advance(int(el_off) * npe)  # PCG64 draws one 64-bit word per double
+        return g.uniform(-1.0, 1.0, size=(nel, npe))
+
+    def coords_slab(self, el_off: int, nel: int, P=None):
+        """Node coordinates of the global elements [el_off, el_off + nel) (canonical order)."""
+        P = self.P if P is None else P
+        n = P + 1
+        xi = gll_points_for_sampling(P)
+        N = list(self.N[: self.dim])
+        e = np.arange(el_off, el_off + nel)
+        ec = [e % N[0], (e // N[0]) % N[1]] + ([e // (N[0] * N[1])] if self.dim == 3 else [])
+        out = []
+        for d in range(self.dim):
+            h = self.L[d] / N[d]
+            shape = [nel] + [1] * self.dim
+            shape[self.dim - d] = n            # node axes (k, j, i): x fastest
+            loc = ((xi + 1.0) * 0.5 * h).reshape(shape[1:])
+            x = ec[d].reshape([nel] + [1] * self.dim) * h + loc[None]
+            out.append(np.ascontiguousarray(np.broadcast_to(x, [nel] + [n] * self.dim)).reshape(nel, n ** self.dim))
+        return out
+
+    def apply_input_slab(self, el_off: int, nel: int):
+        return self._slab_uniform(0, el_off, nel, self.n ** self.dim)
+
+    def rhs_slab(self, comp: int, el_off: int, nel: int):
+        if self.cid == 1:
+            X = self.coords_slab(el_off, nel)
+            return (self.lam + 2.0 * self.nu0) * np.sin(X[0]) * np.sin(X[1])
+        return self._slab_uniform(10 + comp, el_off, nel, self.n ** self.dim)
+
+    def nu_slab(self, el_off: int, nel: int):
+        if not self.variable_nu:
+            return None
+        X = self.coords_slab(el_off, nel)
+        if self.cid == 2:
+            return self.nu0 * (1.0 + 0.5 * np.sin(X[0]) * np.cos(X[1]))
+        if self.cid == 5:
+            return self.nu0 * (1.0 + 0.5 * np.tanh(4.0 * np.sin(X[0]) * np.sin(X[1]) * np.sin(X[2])))
+        raise ValueError("no variable nu for config %d" % self.cid)
+
     def poisson_rhs_raw(self):
         """Seeded U[-1,1] Poisson rhs on the pressure mesh (mass-mean removed by the solver)."""
         n_p = self.P_p + 1
