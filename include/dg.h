@@ -116,6 +116,34 @@ dg_status dg_pcg_solve(dg_mesh *m, double lam, const double *nu, double nu_const
  * out must not alias v. */
 dg_status dg_convect_rhs(dg_mesh *m, const double *const v[3], double *const out[3]);
 
+/* One IMEX-RK stage i = 2 of Alg. 3 for constant viscosity nu, F_s = 0 and
+ * periodic boundaries (the config-4 composition):
+ *   line 4: v' = v + dt a_ex21 (F_c(v) + F_d1(v)),  F_c by dg_convect_rhs (LLF),
+ *           F_d1 = -M^-1 A_0 v (the SIP operator at lam = 0, P:693 F_d1 = div nu grad v);
+ *           the grad-div terms F_d2 + F_d3 (they cancel the divergence part) are not formed;
+ *   line 5: -lap psi = -div v' on the pressure mesh mp (degree P-1; reading A9) with
+ *           the STAND-IN rhs of SURVEY a8: the broken (element-local collocation) divergence of
+ *           v' interpolated to the pressure GLL nodes; solved by dg_pcg_solve (lam = 0: mean
+ *           projection, reading A8) from psi = 0;
+ *   line 6: v'' = v' (the DG gradient projection is SURVEY NEXT-1, not built);
+ *   line 8: g = v'' + dt (a_im21 - a_ex21) F_d1(v);
+ *   line 9: per component, solve v - dt a_im22 nu lap v = g, i.e. lam = 1/(dt a_im22),
+ *           f = lam g (reading A4), by dg_pcg_solve from the initial guess v''.
+ * mv: velocity mesh (degree P >= 2); mp: pressure mesh with the same dim, N, L, rank/nranks
+ * and degree P-1.  v[c], vout[c] (c < dim): DEVICE [local_ndof of mv], vout must not alias
+ * v; psi: DEVICE [local_ndof of mp].  Runs on mv's stream; synchronous (it contains solves).
+ * The stage workspace (dim+1 velocity fields, one pressure field) is allocated on first use
+ * and owned by the meshes.  Errors: DG_EINVAL for mismatched meshes or non-positive dt,
+ * a_im22, nu, tol or maxit; solver errors as dg_pcg_solve (info holds every solve). */
+typedef struct {
+    dg_solve_info pressure;
+    dg_solve_info velocity[3];
+} dg_stage_info;
+
+dg_status dg_imex_stage(dg_mesh *mv, dg_mesh *mp, double dt, double a_ex21, double a_im21, double a_im22,
+                        double nu, const double *const v[3], double *const vout[3], double *psi, double tol,
+                        int maxit, dg_stage_info *info);
+
 /* Host-buffer variants: same operations on HOST arrays; H2D and D2H copies through
  * mesh-owned device staging buffers are part of the call (allocated on first use). */
 dg_status dg_helmholtz_apply_host(dg_mesh *m, double lam, const double *nu_host, double nu_const,

@@ -205,3 +205,58 @@ def mass(mesh: Mesh):
     else:
         m = (wd[2][:, None, None] * wd[1][None, :, None] * wd[0][None, None, :]).reshape(-1)
     return np.broadcast_to(m, (mesh.n_el, mesh.npe)).copy()
+
+
+# ---------------------------------------------------------------------------
+# IMEX-RK stage -- plain numpy composition of the functions above.
+# ---------------------------------------------------------------------------
+def _lagrange_matrix(P, xi, pts):
+    """B[a, j] = l_j(pts[a]), dB[a, j] = l_j'(pts[a]) on the nodes xi (product formula)."""
+    B = np.zeros((len(pts), P + 1))
+    dB = np.zeros((len(pts), P + 1))
+    for a, x in enumerate(pts):
+        B[a], dB[a] = lagrange(P, xi, x)
+    return B, dB
+
+
+def broken_divergence_p1(mesh: Mesh, v):
+    """Element-local (broken) collocation divergence of the nodal velocity v at the GLL
+    nodes of degree P, interpolated to the GLL nodes of degree P-1, returned as
+    [N_el, P^d] (pressure-mesh layout).  The stand-in Poisson rhs of SURVEY §8(a) a8:
+    div v (x_q) = sum_d (2/h_d) sum_j l_j'(xi_{q_d}) v_d(.., x_j, ..) at the velocity nodes,
+    then the degree-P interpolant evaluated at the degree-(P-1) nodes."""
+    P, dim, n = mesh.P, mesh.dim, mesh.P + 1
+    xi, _ = gll(P)
+    xp, _ = gll(P - 1)
+    _, Dm = _lagrange_matrix(P, xi, xi)        # Dm[i, j] = l_j'(xi_i)
+    Ip, _ = _lagrange_matrix(P, xi, xp)        # Ip[a, j] = l_j(xp_a)
+    shp = (mesh.n_el,) + (n,) * dim            # node axes (k, j, i): x last
+    div = np.zeros(shp)
+    for d in range(dim):
+        vd = np.asarray(v[d], dtype=np.float64).reshape(shp)
+        ax = dim - d                            # array axis of direction d
+        div += (2.0 * mesh.N[d] / mesh.L[d]) * np.moveaxis(np.tensordot(Dm, vd, axes=([1], [ax])), 0, ax)
+    for d in range(dim):
+        ax = dim - d
+        div = np.moveaxis(np.tensordot(Ip, div, axes=([1], [ax])), 0, ax)
+    return div.reshape(mesh.n_el, P ** dim)
+
+
+def imex_stage(mv: Mesh, mp: Mesh, dt, a_ex21, a_im21, a_im22, nu, v, tol=1e-14):
+    """Alg. 3 stage i = 2, constant nu, F_s = 0, under the readings of
+    include/dg.h dg_imex_stage: returns (vout[dim], psi, v').  Exact discrete solves
+    (oracle PCG to tol)."""
+    dim = mv.dim
+    m = mass(mv)
+    Fc = convect(mv, v)                                                     # F_c(v)   (P:693)
+    Fd = [-sip_apply(mv, 0.0, v[c], nu_const=nu) / m for c in range(dim)]  # F_d1(v) = -M^-1 A_0 v
+    vp = [np.asarray(v[c]) + dt * a_ex21 * (Fc[c] + Fd[c]) for c in range(dim)]         # line 4
+    fp = -broken_divergence_p1(mv, vp)                                       # line 5 rhs: -div v'
+    psi, *_ = pcg_solve(mp, 0.0, fp, nu_const=1.0, tol=tol)                 # line 5 (lam = 0)
+    lam = 1.0 / (dt * a_im22)
+    out = []
+    for c in range(dim):
+        g = vp[c] + dt * (a_im21 - a_ex21) * Fd[c]                          # line 8 (v'' = v')
+        u, *_ = pcg_solve(mv, lam, lam * g, nu_const=nu, tol=tol)           # line 9
+        out.append(u)
+    return out, psi, vp

@@ -19,12 +19,14 @@ from ._capi import (  # noqa: F401
     DGError,
     Mesh,
     SolveInfo,
+    StageInfo,
     dg_check_field,
     dg_convect_rhs,
     dg_gll_tables,
     dg_helmholtz_apply,
     dg_helmholtz_apply_host,
     dg_helmholtz_diag,
+    dg_imex_stage,
     dg_last_error,
     dg_mesh_create,
     dg_mesh_destroy,

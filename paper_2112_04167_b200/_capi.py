@@ -36,6 +36,13 @@ class SolveInfo(ctypes.Structure):
         return {k: getattr(self, k) for k, _ in self._fields_}
 
 
+class StageInfo(ctypes.Structure):
+    _fields_ = [("pressure", SolveInfo), ("velocity", SolveInfo * 3)]
+
+    def as_dict(self):
+        return {"pressure": self.pressure.as_dict(), "velocity": [x.as_dict() for x in self.velocity]}
+
+
 def _sig(name, res, args):
     f = getattr(_lib, name)
     f.restype = res
@@ -59,6 +66,8 @@ _c = {
     "dg_helmholtz_diag": _sig("dg_helmholtz_diag", _i, [_vp, _d, _vp, _d, _vp]),
     "dg_pcg_solve": _sig("dg_pcg_solve", _i, [_vp, _d, _vp, _d, _vp, _d, _i, _vp, ctypes.POINTER(SolveInfo)]),
     "dg_convect_rhs": _sig("dg_convect_rhs", _i, [_vp, ctypes.POINTER(_vp), ctypes.POINTER(_vp)]),
+    "dg_imex_stage": _sig("dg_imex_stage", _i, [_vp, _vp, _d, _d, _d, _d, _d, ctypes.POINTER(_vp),
+                                                ctypes.POINTER(_vp), _vp, _d, _i, ctypes.POINTER(StageInfo)]),
     "dg_helmholtz_apply_host": _sig("dg_helmholtz_apply_host", _i, [_vp, _d, _vp, _d, _vp, _vp]),
     "dg_pcg_solve_host": _sig("dg_pcg_solve_host", _i, [_vp, _d, _vp, _d, _vp, _d, _i, _vp,
                                                         ctypes.POINTER(SolveInfo)]),
@@ -241,6 +250,16 @@ def dg_convect_rhs(m: Mesh, v, out):
     vin = (_vp * 3)(*([_ptr(x) for x in v] + [None] * (3 - len(v))))
     vout = (_vp * 3)(*([_ptr(x) for x in out] + [None] * (3 - len(out))))
     _check(_c["dg_convect_rhs"](m.handle, vin, vout))
+
+
+def dg_imex_stage(mv: Mesh, mp: Mesh, dt, a_ex21, a_im21, a_im22, nu, v, vout, psi, tol, maxit) -> StageInfo:
+    """One IMEX-RK stage (Alg. 3 lines 4-9) -- see include/dg.h."""
+    vin = (_vp * 3)(*([_ptr(x) for x in v] + [None] * (3 - len(v))))
+    vo = (_vp * 3)(*([_ptr(x) for x in vout] + [None] * (3 - len(vout))))
+    info = StageInfo()
+    _check(_c["dg_imex_stage"](mv.handle, mp.handle, dt, a_ex21, a_im21, a_im22, nu, vin, vo, _ptr(psi), tol, maxit,
+                               ctypes.byref(info)), info)
+    return info
 
 
 def dg_helmholtz_apply_host(m: Mesh, lam, nu, nu_const, u, out):

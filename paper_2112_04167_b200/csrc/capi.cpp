@@ -30,6 +30,8 @@ cudaError_t upload_tables()
     if ((e = upload_tables_vec()) != cudaSuccess) return e;
     if ((e = upload_tables_apply2()) != cudaSuccess) return e;
     if ((e = upload_tables_apply3()) != cudaSuccess) return e;
+    if ((e = upload_tables_stage()) != cudaSuccess) return e;
+    if ((e = upload_tables_stage_interp()) != cudaSuccess) return e;
     return upload_tables_convect();
 }
 
@@ -154,6 +156,8 @@ struct dg_mesh {
     ncclComm_t comm = nullptr;
     // host-variant staging
     double *st_a = nullptr, *st_b = nullptr, *st_c = nullptr;
+    // IMEX stage workspace (velocity mesh: F_c[0..dim), A v; pressure mesh: rhs)
+    double *sf[4] = {nullptr, nullptr, nullptr, nullptr};
     int *d_flag = nullptr;
     long long launches = 0;
 };
@@ -588,8 +592,9 @@ void dg_mesh_destroy(dg_mesh *m)
     if (!m) return;
     if (m->st) cudaStreamSynchronize(m->st);
     else cudaDeviceSynchronize();
-    double *bufs[] = {m->r, m->q, m->pa, m->pb, m->dinv, m->z, m->partial, m->sums, m->aux, m->mass_e, m->hist,
-                      m->h_lo, m->h_hi, m->hn_lo, m->hn_hi, m->st_a, m->st_b, m->st_c};
+    double *bufs[] = {m->r,    m->q,    m->pa,    m->pb,     m->dinv,   m->z,    m->partial,
+                      m->sums, m->aux,  m->mass_e, m->hist,  m->h_lo,   m->h_hi, m->hn_lo,
+                      m->hn_hi, m->st_a, m->st_b,  m->st_c,  m->sf[0], m->sf[1], m->sf[2], m->sf[3]};
     for (double *b : bufs)
         if (b) cudaFree(b);
     for (int c = 0; c < 3; ++c) {
@@ -720,6 +725,68 @@ dg_status dg_pcg_solve_host(dg_mesh *m, double lam, const double *nu_host, doubl
     CK(cudaMemcpyAsync(u_host, m->st_b, b, cudaMemcpyDeviceToHost, m->st));
     CK(cudaStreamSynchronize(m->st));
     return s;
+}
+
+dg_status dg_imex_stage(dg_mesh *mv, dg_mesh *mp, double dt, double a_ex21, double a_im21, double a_im22,
+                        double nu, const double *const v[3], double *const vout[3], double *psi, double tol,
+                        int maxit, dg_stage_info *info)
+{
+    if (!mv || !mp || !v || !vout || !psi) return set_error(DG_EINVAL, "null argument");
+    const Geom &g = mv->g, &gp = mp->g;
+    const int dim = g.dim;
+    if (gp.dim != dim || gp.P != g.P - 1 || mp->nranks != mv->nranks || mp->rank != mv->rank)
+        return set_error(DG_EINVAL, "pressure mesh must match the velocity mesh with degree P-1 (P:1036)");
+    for (int d = 0; d < 3; ++d)
+        if (gp.N[d] != g.N[d] || gp.h[d] != g.h[d]) return set_error(DG_EINVAL, "pressure mesh geometry differs");
+    if (g.P < 2) return set_error(DG_EINVAL, "stage needs P >= 2 (pressure degree P-1 >= 1)");
+    if (!(dt > 0.0) || !(a_im22 > 0.0) || !std::isfinite(a_ex21) || !std::isfinite(a_im21) ||
+        !(nu > 0.0 && std::isfinite(nu)))
+        return set_error(DG_EINVAL, "need dt > 0, a_im22 > 0, finite a_ex21/a_im21, nu > 0");
+    if (!(tol > 0.0) || maxit < 1) return set_error(DG_EINVAL, "need tol > 0 and maxit >= 1");
+    for (int c = 0; c < dim; ++c) {
+        if (!v[c] || !vout[c]) return set_error(DG_EINVAL, "null component pointer");
+        for (int c2 = 0; c2 < dim; ++c2)
+            if (vout[c] == v[c2]) return set_error(DG_EINVAL, "vout must not alias v");
+    }
+    cudaStream_t mp_stream = mp->st;
+    mp->st = mv->st;  // the whole stage runs on the velocity mesh's stream
+    struct Restore {
+        dg_mesh *m;
+        cudaStream_t s;
+        ~Restore() { m->st = s; }
+    } restore{mp, mp_stream};
+    const size_t bv = sizeof(double) * (size_t)mv->ndof, bp = sizeof(double) * (size_t)mp->ndof;
+    for (int c = 0; c <= dim; ++c) CKS(stage(mv, &mv->sf[c], bv));
+    CKS(stage(mp, &mp->sf[0], bp));
+    double *Fc[3] = {mv->sf[0], mv->sf[1], dim == 3 ? mv->sf[2] : nullptr};
+    double *Av = mv->sf[dim];
+    // line 4 (explicit part): F_c(v) (LLF DG) ...
+    CKS(dg_convect_rhs(mv, v, Fc));
+    const double lamH = 1.0 / (dt * a_im22);
+    for (int c = 0; c < dim; ++c) {
+        // ... and F_d1(v) = -M^-1 A_0 v; v' (line 4), and the Helmholtz rhs from g (line 8);
+        // Fc[c] is overwritten by f_H = lam g
+        CKS(apply_impl(mv, 0.0, nullptr, nu, v[c], Av));
+        CK(launch_stage_combine(g, mv->mass_e, dt * a_ex21, dt * (a_im21 - a_ex21), lamH, v[c], Fc[c], Av, vout[c],
+                                Fc[c], mv->st));
+        mv->launches += 1;
+    }
+    // line 5: pressure Poisson on the P-1 mesh, stand-in rhs -div(v')
+    CK(launch_div_interp(g, vout[0], vout[1], dim == 3 ? vout[2] : nullptr, mp->sf[0], mv->st));
+    mv->launches += 1;
+    CK(cudaMemsetAsync(psi, 0, bp, mv->st));
+    dg_solve_info ip{};
+    dg_status s = pcg_impl(mp, 0.0, nullptr, 1.0, mp->sf[0], tol, maxit, psi, &ip);
+    if (info) info->pressure = ip;
+    if (s != DG_OK) return s;
+    // line 9: v_i - dt a_ii div(nu grad v_i) = g_i per component, from the guess v'' = v'
+    for (int c = 0; c < dim; ++c) {
+        dg_solve_info iv{};
+        s = pcg_impl(mv, lamH, nullptr, nu, Fc[c], tol, maxit, vout[c], &iv);
+        if (info) info->velocity[c] = iv;
+        if (s != DG_OK) return s;
+    }
+    return DG_OK;
 }
 
 dg_status dg_gll_tables(int P, double *xi, double *w, double *D)

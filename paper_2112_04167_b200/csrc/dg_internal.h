@@ -129,6 +129,15 @@ cudaError_t upload_tables_vec();
 cudaError_t upload_tables_apply2();
 cudaError_t upload_tables_apply3();
 cudaError_t upload_tables_convect();
+cudaError_t upload_tables_stage();
+cudaError_t upload_tables_stage_interp();
+
+// stage.cu (config-4 IMEX-RK stage pieces)
+cudaError_t launch_stage_combine(const Geom &g, const double *mass_e, double a_ex, double c_g, double lamH,
+                                 const double *v, const double *Fc, const double *Av, double *vp, double *fH,
+                                 cudaStream_t st);
+cudaError_t launch_div_interp(const Geom &g, const double *v0, const double *v1, const double *v2, double *fp,
+                              cudaStream_t st);
 
 // PCG vector kernels -------------------------------------------------------
 struct PcgScal {                 // device-resident scalars of one solve

@@ -295,3 +295,43 @@ def test_convect_c4_sampled():
     for cc in range(3):
         tot = float((mass * do[cc]).sum())
         assert abs(tot) <= 1e-12 * float((mass * do[cc].abs()).sum())
+
+
+# ---------------------------------------------------------------------------
+# IMEX-RK stage: dg_imex_stage vs the oracle composition
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("dim,N,P", [(3, (2, 2, 4), 3), (3, (4, 2, 2), 4), (2, (4, 2), 5), (3, (2, 2, 2), 7)])
+def test_imex_stage_small(dim, N, P):
+    L = (TWO_PI,) * dim
+    mv = dg.dg_mesh_create(dim, N, L, P, stream=torch.cuda.current_stream())
+    mp = dg.dg_mesh_create(dim, N, L, P - 1, stream=torch.cuda.current_stream())
+    omv, omp = oracle.Mesh(dim, N, L, P), oracle.Mesh(dim, N, L, P - 1)
+    from workloads import node_coords
+
+    X = node_coords(dim, N, L, P)
+    rng = np.random.default_rng(40 + P)
+    if dim == 3:
+        base = [np.sin(X[0]) * np.cos(X[1]) * np.cos(X[2]), -np.cos(X[0]) * np.sin(X[1]) * np.cos(X[2]), 0 * X[0]]
+    else:
+        base = [np.sin(X[0]) * np.cos(X[1]), -np.cos(X[0]) * np.sin(X[1])]
+    v = [b + 1e-2 * rng.uniform(-1, 1, b.shape) for b in base]
+    dt, a, nu = 1e-2, 0.4358665, 1.0 / 1600.0
+    dv = [T(x) for x in v]
+    do = [torch.empty_like(dv[0]) for _ in range(dim)]
+    psi = torch.empty(omp.n_el, omp.npe, dtype=torch.float64, device=DEV)
+    info = dg.dg_imex_stage(mv, mp, dt, a, 0.0, a, nu, dv, do, psi, 1e-12, 20000)
+    ref, psi_ref, _ = oracle.imex_stage(omv, omp, dt, a, 0.0, a, nu, v, tol=1e-14)
+    for cc in range(dim):
+        assert rel(H(do[cc]), ref[cc]) <= 1e-9, (cc, info.as_dict())
+    assert rel(H(psi), psi_ref) <= 1e-9, info.as_dict()
+    assert info.pressure.iters > 0 and all(info.velocity[cc].iters > 0 for cc in range(dim))
+
+
+def test_imex_stage_rejects_mismatched_meshes():
+    mv = dg.dg_mesh_create(3, (2, 2, 2), (1.0, 1.0, 1.0), 4, stream=torch.cuda.current_stream())
+    mp = dg.dg_mesh_create(3, (2, 2, 2), (1.0, 1.0, 1.0), 4, stream=torch.cuda.current_stream())
+    z = torch.zeros(8, 125, dtype=torch.float64, device=DEV)
+    o = [torch.empty_like(z) for _ in range(3)]
+    with pytest.raises(dg.DGError) as e:
+        dg.dg_imex_stage(mv, mp, 1e-2, 0.5, 0.0, 0.5, 1e-3, [z, z, z], o, z, 1e-10, 100)
+    assert e.value.status == dg.DG_EINVAL
