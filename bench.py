@@ -38,6 +38,9 @@ from workloads import config as get_config  # noqa: E402
 
 WORKLOADS = {"c5": 5, "c4": 4, "c3": 3, "c2": 2, "c1": 1}
 BYTES_PER_DOF = {True: 24.0, False: 16.0}  # algorithmic bytes per DOF per apply (var / const nu)
+# bytes per DOF per fused PCG iteration: apply MODE 1 (read z, p_old, [nu];
+# write p, q) + update (read x, r, p, q, dinv; write x, r, z)
+PCG_BYTES_PER_DOF = {True: 104.0, False: 96.0}
 
 
 def measured_peaks():
@@ -65,7 +68,7 @@ class Clocks:
     def __enter__(self):
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.Q,
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                          "--format=csv,noheader,nounits", "-lms", "50"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -214,23 +217,24 @@ def run_product(args, rank, world, local_rank):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
-    # ---- device-timed apply steps
+    # ---- device-timed apply steps (clocks are sampled over the apply and PCG timed regions)
     for _ in range(args.warmup):
         dg.dg_helmholtz_apply(m, c.lam, nu, c.nu0, u, out)
     barrier()
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(2 * args.steps)]
+    clk = Clocks(local_rank).__enter__()
+    time.sleep(0.15)  # let the sampler start before the timed region
     l0 = dg.dg_mesh_launch_count(m)
-    with Clocks(local_rank) as clk:
-        barrier()
-        t_start = torch.cuda.Event(enable_timing=True)
-        t_end = torch.cuda.Event(enable_timing=True)
-        t_start.record(stream)
-        for k in range(args.steps):
-            ev[2 * k].record(stream)
-            dg.dg_helmholtz_apply(m, c.lam, nu, c.nu0, u, out)
-            ev[2 * k + 1].record(stream)
-        t_end.record(stream)
-        barrier()
+    barrier()
+    t_start = torch.cuda.Event(enable_timing=True)
+    t_end = torch.cuda.Event(enable_timing=True)
+    t_start.record(stream)
+    for k in range(args.steps):
+        ev[2 * k].record(stream)
+        dg.dg_helmholtz_apply(m, c.lam, nu, c.nu0, u, out)
+        ev[2 * k + 1].record(stream)
+    t_end.record(stream)
+    barrier()
     launches = dg.dg_mesh_launch_count(m) - l0
     total_ms = max_over_ranks(t_start.elapsed_time(t_end))
     per_launch_ms = statistics.mean(ev[2 * k].elapsed_time(ev[2 * k + 1]) for k in range(args.steps))
@@ -253,8 +257,16 @@ def run_product(args, rank, world, local_rank):
             solve_ms.append(max_over_ranks(a.elapsed_time(b)))
             iters.append(info.iters)
             infos.append(info.as_dict())
+    clk.__exit__(None, None, None)
     t_solve = statistics.mean(solve_ms)
     it = statistics.mean(iters)
+
+    # ---- one IMEX-RK stage of config 4: convect + F_d1 + Poisson (P-1)
+    #      + 3 Helmholtz solves, device-timed (1 GPU only: the c4 mesh shards, but the
+    #      stage leg is reported for the single-GPU run)
+    stage = None
+    if world == 1 and not args.no_stage:
+        stage = run_stage(dg, torch, stream, barrier)
 
     # ---- e2e through the host-buffer C-ABI call (rank-local slab)
     u_np = np.ascontiguousarray(u_h)
@@ -312,9 +324,12 @@ def run_product(args, rank, world, local_rank):
                    "bricks": None, "l2": "inputs larger than L2 (%.0f MB per field)" % (ndof_global * 8 / 1e6)},
         "pcg": {"iters_per_s": it / (t_solve * 1e-3), "iters": it, "ms_per_solve": t_solve, "tol": c.tol,
                 "solves": args.solves, "rel_res": infos[-1]["rel_res"], "kappa_est": infos[-1]["kappa_est"],
-                "gdof_iter_per_s": ndof_global * it / (t_solve * 1e-3) / 1e9},
+                "gdof_iter_per_s": ndof_global * it / (t_solve * 1e-3) / 1e9,
+                "bytes_per_dof_iter": PCG_BYTES_PER_DOF[varnu],
+                "achieved_gbs_incl_setup": ndof_global * it * PCG_BYTES_PER_DOF[varnu] / (t_solve * 1e-3) / 1e9},
+        "stage": stage,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": traffic, "kernel": "k_apply<3,%d,%s,false>" % (c.P, "true" if varnu else "false"),
+                     "traffic": traffic, "kernel": "v5::k_apply5<%d,%s,0>" % (c.P, "1" if varnu else "0"),
                      "bytes_per_dof": bpd, "peak_kind": peak_kind, "launch_ms": per_launch_ms},
         "e2e": {"value": ndof_global / e2e_s / 1e9, "unit": "GDOF/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "ms_per_step": e2e_s * 1e3},
@@ -325,16 +340,49 @@ def run_product(args, rank, world, local_rank):
     print(json.dumps(line), flush=True)
 
 
+def run_stage(dg, torch, stream, barrier, reps=2):
+    """One IMEX-RK stage (Alg. 3 lines 4-9) on config 4: 32^3 hexes, P = 7 velocity,
+    P_p = 6 pressure, TG velocity + 1e-3 noise, nu = 1/1600, dt = 1e-2, a_ex21 = a_im22 =
+    gamma, tol 1e-10."""
+    from workloads.inputs import GAMMA_SDIRK3
+
+    c4 = get_config(4)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    mv = dg.dg_mesh_create(3, c4.N, c4.L, c4.P, stream=stream)
+    mp = dg.dg_mesh_create(3, c4.N, c4.L, c4.P_p, stream=stream)
+    v = [torch.from_numpy(a).to(dev) for a in c4.tg_velocity()]
+    vo = [torch.empty_like(v[0]) for _ in range(3)]
+    psi = torch.empty(mp.n_el, mp.npe, dtype=torch.float64, device=dev)
+    g = GAMMA_SDIRK3
+    times, info = [], None
+    for k in range(reps + 1):
+        barrier()
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        info = dg.dg_imex_stage(mv, mp, 1e-2, g, 0.0, g, c4.nu0, v, vo, psi, c4.tol, 20000)
+        b.record(stream)
+        barrier()
+        if k > 0:
+            times.append(a.elapsed_time(b))
+    d = info.as_dict()
+    return {"workload": c4.name, "ms_per_stage": statistics.mean(times), "stages": reps,
+            "pressure_P": c4.P_p, "pressure_iters": d["pressure"]["iters"],
+            "velocity_iters": [x["iters"] for x in d["velocity"]], "tol": c4.tol,
+            "dofs": {"velocity_per_component": mv.ndof, "pressure": mp.ndof}}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--solves", type=int, default=3)
     ap.add_argument("--solve-warmup", type=int, default=1)
     ap.add_argument("--impl", default="product", choices=["product", "reference"])
     ap.add_argument("--workload", default="c5", choices=sorted(WORKLOADS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-stage", action="store_true", help="skip the config-4 IMEX stage leg")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
