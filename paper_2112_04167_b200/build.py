@@ -75,6 +75,7 @@ def _digest(paths, extra=""):
 def build(pset: str | None = None, jobs: int | None = None, force: bool = False, verbose: bool = False) -> str:
     os.makedirs(BUILD, exist_ok=True)
     defs = [] if pset is None else ["-DDG_PSET=%s" % pset]
+    defs += os.environ.get("DG_EXTRA_DEFS", "").split()  # development switches, e.g. -DDG_V5_DEBUG
     flags = ["-std=c++17", "-O3", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-Wall",
              "-I" + INC, "-I" + CSRC, "-I" + nccl_include()] + defs
     hdr = _digest(headers(), " ".join(flags))

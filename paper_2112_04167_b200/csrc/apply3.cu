@@ -15,3 +15,16 @@ cudaError_t launch_diag3(const Geom &g, double lam, const double *nu, double nuc
     return ApplyDispatch<3>::diag(g, lam, nu, nuc, h, d, st);
 }
 }  // namespace dg
+
+#ifdef DG_V5_DEBUG
+extern "C" int dg_debug_counters(unsigned long long *out, int reset)
+{
+    cudaDeviceSynchronize();
+    if (cudaMemcpyFromSymbol(out, dg::v5::g_dbg, sizeof(unsigned long long) * 16) != cudaSuccess) return 1;
+    if (reset) {
+        unsigned long long z[16] = {0};
+        cudaMemcpyToSymbol(dg::v5::g_dbg, z, sizeof(z));
+    }
+    return 0;
+}
+#endif

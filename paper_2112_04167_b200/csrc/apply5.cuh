@@ -32,6 +32,16 @@
 namespace dg {
 namespace v5 {
 
+#ifdef DG_V5_DEBUG
+// development instrumentation: per-role cycle counters (see dg_debug_counters in apply3.cu)
+__device__ unsigned long long g_dbg[16];
+#define V5_T0(var) const long long var = clock64()
+#define V5_ACC(idx, var) atomicAdd(&g_dbg[idx], (unsigned long long)(clock64() - (var)))
+#else
+#define V5_T0(var)
+#define V5_ACC(idx, var)
+#endif
+
 __device__ __forceinline__ unsigned su32(const void *p) { return static_cast<unsigned>(__cvta_generic_to_shared(p)); }
 
 __device__ __forceinline__ void mbar_init(uint64_t *b, unsigned count)
@@ -478,7 +488,10 @@ __global__ void __launch_bounds__((KC5<P, VARNU, MODE>::NT)) __maxnreg__((KC5<P,
             int e0[3] = {(col % nb0) * B, (col / nb0) * B, zs * seglen * B};
             for (int j = 0; j < seglen; ++j, ++it, e0[2] += B) {
                 const int buf = it & 1;
+                V5_T0(tw);
                 if (it >= 2) mbar_wait(&bar[2 + buf], ((it >> 1) - 1) & 1);
+                if (ptid == 0) V5_ACC(2, tw);
+                V5_T0(tt);
                 double *su = sm + K::OFF_U + buf * BRK;
                 double *snu = sm + K::OFF_NU + buf * BRK;
                 const long long eb = e0[0] + s1 * e0[1] + s2 * e0[2];
@@ -508,12 +521,18 @@ __global__ void __launch_bounds__((KC5<P, VARNU, MODE>::NT)) __maxnreg__((KC5<P,
                     }
                 }
                 double *tr = sm + K::OFF_TR + buf * K::TRB;
+                if (ptid == 0) V5_ACC(4, tt);
+                V5_T0(tx);
                 ptraces<K, 0>(a, T, tr, e0, ptid, beta, 3);
+                if (ptid == 0) V5_ACC(9, tx);
+                V5_T0(ty);
                 ptraces<K, 1>(a, T, tr, e0, ptid, beta, 3);
+                if (ptid == 0) V5_ACC(10, ty);
                 // z faces: from global memory only at segment ends; inside a segment the
                 // consumers carry the shared face from one brick to the next (ZCarry)
                 const int zm = (j == 0 ? 1 : 0) | (j == seglen - 1 ? 2 : 0);
                 if (zm) ptraces<K, 2>(a, T, tr, e0, ptid, beta, zm);
+                if (ptid == 0) V5_ACC(3, tx);
                 mbar_arrive(&bar[buf]);
             }
         }
@@ -534,15 +553,29 @@ __global__ void __launch_bounds__((KC5<P, VARNU, MODE>::NT)) __maxnreg__((KC5<P,
             const double *snu = sm + K::OFF_NU + buf * BRK;
             const double *tr = sm + K::OFF_TR + buf * K::TRB;
             const long long eb = e0[0] + s1 * e0[1] + s2 * e0[2];
+            V5_T0(tw);
             mbar_wait(&bar[buf], (it >> 1) & 1);
+            if (tid == 0) V5_ACC(0, tw);
+            V5_T0(tp);
             const bool zf = j == 0, zl = j == seglen - 1;
             cpass<K, 0, true, false>(a, T, su, snu, sacc, tr, eb, tid, epi0, epi1, zc, zf, zl);
+            if (tid == 0) V5_ACC(6, tp);
             named_sync(1, NC);
+            V5_T0(t1);
             cpass<K, 1, false, false>(a, T, su, snu, sacc, tr, eb, tid, epi0, epi1, zc, zf, zl);
+            if (tid == 0) V5_ACC(7, t1);
             named_sync(1, NC);
+            V5_T0(t2);
             cpass<K, 2, false, true>(a, T, su, snu, sacc, tr, eb, tid, epi0, epi1, zc, zf, zl);
+            if (tid == 0) V5_ACC(8, t2);
             mbar_arrive(&bar[2 + buf]);
             named_sync(1, NC);  // ACC is rewritten by the next brick's x pass
+            if (tid == 0) {
+                V5_ACC(1, tp);
+#ifdef DG_V5_DEBUG
+                atomicAdd(&g_dbg[5], 1ull);
+#endif
+            }
         }
     }
     if (MODE == 1) {
