@@ -245,7 +245,11 @@ struct ApplyDispatch {
             }
             long long gsz = (long long)nsm * std::min(occ, 4);
             const long long ncols = (long long)(a.g.Nl[0] / 2) * (a.g.Nl[1] / 2);
-            const int nbS = a.g.Nl[2] / 2;
+            if (a.zhi < 0) {
+                a.zlo = 0;
+                a.zhi = a.g.Nl[2];
+            }
+            const int nbS = (a.zhi - a.zlo) / 2;
             int nseg = 1;
             while (ncols * nseg < 3 * gsz && nbS % (2 * nseg) == 0) nseg *= 2;
             a.nseg = nseg;
@@ -267,6 +271,7 @@ struct ApplyDispatch {
         if (off || DIM != 3) return false;
         for (int d = 0; d < 3; ++d)
             if (a.g.Nl[d] % 2) return false;
+        if (a.zhi >= 0 && (a.zlo % 2 || a.zhi % 2 || a.zhi <= a.zlo || a.zhi > a.g.Nl[2])) return false;
         auto al = [](const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
         if (pcg) return al(a.pro.z) && al(a.pro.p_old) && al(a.pro.p_out) && (!a.nu || al(a.nu));
         return al(a.u) && (!a.nu || al(a.nu));
@@ -286,6 +291,7 @@ struct ApplyDispatch {
                 const cudaError_t e = go5<P, VARNU, MODE>(a, grid, st);
                 if (e != cudaErrorNotSupported) return e;
             }
+            if (a.zhi >= 0) return cudaErrorNotSupported;  // layer ranges need the v5 kernel
             if (N[0] % 2 == 0 && N[1] % 2 == 0 && N[2] % 2 == 0 && KC<3, P, VARNU, MODE, 2, 2, 2>::SMEM_BYTES <= budget)
                 return go<P, VARNU, MODE, 2, 2, 2>(a, grid, st);
             if (N[0] % 2 == 0 && N[1] % 2 == 0 && KC<3, P, VARNU, MODE, 2, 2, 1>::SMEM_BYTES <= budget)

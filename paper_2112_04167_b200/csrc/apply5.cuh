@@ -485,7 +485,7 @@ __global__ void __launch_bounds__((KC5<P, VARNU, MODE>::NT)) __maxnreg__((KC5<P,
         int it = 0;
         for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
             const int col = u % ncols, zs = u / ncols;
-            int e0[3] = {(col % nb0) * B, (col / nb0) * B, zs * seglen * B};
+            int e0[3] = {(col % nb0) * B, (col / nb0) * B, a.zlo + zs * seglen * B};
             for (int j = 0; j < seglen; ++j, ++it, e0[2] += B) {
                 const int buf = it & 1;
                 V5_T0(tw);
@@ -546,7 +546,7 @@ __global__ void __launch_bounds__((KC5<P, VARNU, MODE>::NT)) __maxnreg__((KC5<P,
     double *sacc = sm + K::OFF_ACC;
     for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
         const int col = u % ncols, zs = u / ncols;
-        int e0[3] = {(col % nb0) * B, (col / nb0) * B, zs * seglen * B};
+        int e0[3] = {(col % nb0) * B, (col / nb0) * B, a.zlo + zs * seglen * B};
         for (int j = 0; j < seglen; ++j, ++it, e0[2] += B) {
             const int buf = it & 1;
             const double *su = sm + K::OFF_U + buf * BRK;

@@ -156,6 +156,9 @@ struct dg_mesh {
     ncclComm_t comm = nullptr;
     // host-variant staging
     double *st_a = nullptr, *st_b = nullptr, *st_c = nullptr;
+    // pipelined host apply: copy streams and per-chunk events (created on first use)
+    cudaStream_t cs_in = nullptr, cs_out = nullptr;
+    std::vector<cudaEvent_t> ev;
     // IMEX stage workspace (velocity mesh: F_c[0..dim), A v; pressure mesh: rhs)
     double *sf[4] = {nullptr, nullptr, nullptr, nullptr};
     int *d_flag = nullptr;
@@ -273,7 +276,8 @@ dg_status check_common(dg_mesh *m, double lam, const double *nu, double nu_const
 }
 
 dg_status run_apply(dg_mesh *m, double lam, const double *nu, double nu_const, const double *u, double *out,
-                    const Halo &halo, const DotEpi &epi, const PProl &pro, int *grid_out = nullptr)
+                    const Halo &halo, const DotEpi &epi, const PProl &pro, int *grid_out = nullptr, int zlo = 0,
+                    int zhi = -1)
 {
     ApplyParams a{};
     a.g = m->g;
@@ -287,6 +291,8 @@ dg_status run_apply(dg_mesh *m, double lam, const double *nu, double nu_const, c
     a.pro = pro;
     a.b0 = 0;
     a.b1 = nbricks(a.g);
+    a.zlo = zlo;
+    a.zhi = zhi;
     const bool varnu = nu != nullptr;
     int grid = 0;
     const cudaError_t e = m->g.dim == 3 ? launch_apply3(a, varnu, pro.on, &grid, 0, m->st)
@@ -605,6 +611,9 @@ void dg_mesh_destroy(dg_mesh *m)
     if (m->d_flag) cudaFree(m->d_flag);
     if (m->hscal) cudaFreeHost(m->hscal);
     if (m->comm) nccl()->CommDestroy(m->comm);
+    for (cudaEvent_t e : m->ev) cudaEventDestroy(e);
+    if (m->cs_in) cudaStreamDestroy(m->cs_in);
+    if (m->cs_out) cudaStreamDestroy(m->cs_out);
     delete m;
 }
 
@@ -689,6 +698,11 @@ dg_status dg_convect_rhs(dg_mesh *m, const double *const v[3], double *const out
     return DG_OK;
 }
 
+// Host-buffer apply.  Single-rank 3-D meshes with even N (the v5 kernel) are pipelined over
+// C slabs of element layers: the H2D copies of u (and nu) run on one copy stream, the apply
+// of slab k starts as soon as slabs k-1, k, k+1 have landed (slab 0, which needs the last
+// slab across the periodic seam, goes last) and its result is copied back on a second copy
+// stream, so both PCIe directions and the kernel overlap.  Otherwise: copy, apply, copy.
 dg_status dg_helmholtz_apply_host(dg_mesh *m, double lam, const double *nu_host, double nu_const,
                                   const double *u_host, double *out_host)
 {
@@ -698,10 +712,57 @@ dg_status dg_helmholtz_apply_host(dg_mesh *m, double lam, const double *nu_host,
     CKS(stage(m, &m->st_a, b));
     CKS(stage(m, &m->st_b, b));
     if (nu_host) CKS(stage(m, &m->st_c, b));
-    CK(cudaMemcpyAsync(m->st_a, u_host, b, cudaMemcpyHostToDevice, m->st));
-    if (nu_host) CK(cudaMemcpyAsync(m->st_c, nu_host, b, cudaMemcpyHostToDevice, m->st));
-    CKS(apply_impl(m, lam, nu_host ? m->st_c : nullptr, nu_const, m->st_a, m->st_b));
-    CK(cudaMemcpyAsync(out_host, m->st_b, b, cudaMemcpyDeviceToHost, m->st));
+    const Geom &g = m->g;
+    int C = 0;
+    if (m->nranks == 1 && g.dim == 3 && g.Nl[0] % 2 == 0 && g.Nl[1] % 2 == 0 && g.Nl[2] % 2 == 0) {
+        const int nbz = g.Nl[2] / 2;
+        for (int c = 8; c >= 3; --c)
+            if (nbz % c == 0) {
+                C = c;
+                break;
+            }
+    }
+    if (C == 0) {
+        CK(cudaMemcpyAsync(m->st_a, u_host, b, cudaMemcpyHostToDevice, m->st));
+        if (nu_host) CK(cudaMemcpyAsync(m->st_c, nu_host, b, cudaMemcpyHostToDevice, m->st));
+        CKS(apply_impl(m, lam, nu_host ? m->st_c : nullptr, nu_const, m->st_a, m->st_b));
+        CK(cudaMemcpyAsync(out_host, m->st_b, b, cudaMemcpyDeviceToHost, m->st));
+        CK(cudaStreamSynchronize(m->st));
+        return DG_OK;
+    }
+    if (!m->cs_in) {
+        CK(cudaStreamCreateWithFlags(&m->cs_in, cudaStreamNonBlocking));
+        CK(cudaStreamCreateWithFlags(&m->cs_out, cudaStreamNonBlocking));
+    }
+    while ((int)m->ev.size() < 2 * C + 2) {
+        cudaEvent_t e;
+        CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        m->ev.push_back(e);
+    }
+    cudaEvent_t *ein = m->ev.data(), *ecmp = m->ev.data() + C, e0 = m->ev[2 * C], e1 = m->ev[2 * C + 1];
+    const int lay = g.Nl[2] / C;  // element layers per slab (even)
+    const size_t cb = b / C, cn = (size_t)m->ndof / C;
+    // staging buffers may still be read by earlier work on the mesh stream
+    CK(cudaEventRecord(e0, m->st));
+    CK(cudaStreamWaitEvent(m->cs_in, e0, 0));
+    CK(cudaStreamWaitEvent(m->cs_out, e0, 0));
+    for (int k = 0; k < C; ++k) {
+        CK(cudaMemcpyAsync(m->st_a + k * cn, u_host + k * cn, cb, cudaMemcpyHostToDevice, m->cs_in));
+        if (nu_host) CK(cudaMemcpyAsync(m->st_c + k * cn, nu_host + k * cn, cb, cudaMemcpyHostToDevice, m->cs_in));
+        CK(cudaEventRecord(ein[k], m->cs_in));
+    }
+    for (int q = 1; q <= C; ++q) {
+        const int k = q % C;                          // 1, 2, ..., C-1, then 0
+        CK(cudaStreamWaitEvent(m->st, ein[k == C - 1 ? 0 : (k + 1) % C], 0));
+        CK(cudaStreamWaitEvent(m->st, ein[k], 0));
+        CKS(run_apply(m, lam, nu_host ? m->st_c : nullptr, nu_const, m->st_a, m->st_b, Halo{}, DotEpi{}, PProl{},
+                      nullptr, k * lay, (k + 1) * lay));
+        CK(cudaEventRecord(ecmp[k], m->st));
+        CK(cudaStreamWaitEvent(m->cs_out, ecmp[k], 0));
+        CK(cudaMemcpyAsync(out_host + k * cn, m->st_b + k * cn, cb, cudaMemcpyDeviceToHost, m->cs_out));
+    }
+    CK(cudaEventRecord(e1, m->cs_out));
+    CK(cudaStreamWaitEvent(m->st, e1, 0));
     CK(cudaStreamSynchronize(m->st));
     return DG_OK;
 }

@@ -103,6 +103,8 @@ struct ApplyParams {
     PProl pro;
     long long b0, b1;   // brick range [b0, b1)
     int seglen = 1, nseg = 1;  // column segments along the slowest direction (apply kernel)
+    int zlo = 0, zhi = -1;     // element layers [zlo, zhi) of the slowest direction to apply
+                               // (3-D v5 kernel only; -1 = all), for the pipelined host call
 };
 
 struct ConvParams {
