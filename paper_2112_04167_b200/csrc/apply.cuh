@@ -86,6 +86,7 @@ __device__ __forceinline__ double end_flux(const DevTab &T, const double (&v)[P 
 
 #include "apply_kernel.cuh"
 #include "apply5.cuh"
+#include "apply6.cuh"
 
 namespace dg {
 
@@ -262,6 +263,64 @@ struct ApplyDispatch {
             return cudaGetLastError();
         }
     }
+    // v6 (3-D, n <= 6): one CTA per SM, 4x4x1 bricks, warpgroup-specialised (apply6.cuh)
+    template <int P, bool VARNU, int MODE>
+    static cudaError_t go6(ApplyParams a, int *grid, cudaStream_t st)
+    {
+        using K = v6::KC6<P, VARNU, MODE>;
+        if constexpr (K::n > 6 || K::SMEM_BYTES > 227 * 1024) {
+            return cudaErrorNotSupported;
+        } else {
+            auto kern = v6::k_apply6<P, VARNU, MODE>;
+            static int nsm = 0;
+            cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, K::SMEM_BYTES);
+            if (e != cudaSuccess) return e;
+            if (nsm == 0) {
+                int dev = 0;
+                cudaGetDevice(&dev);
+                cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+            }
+            long long gsz = nsm;
+            const long long ncols = (long long)(a.g.Nl[0] / 4) * (a.g.Nl[1] / 4);
+            if (a.zhi < 0) {
+                a.zlo = 0;
+                a.zhi = a.g.Nl[2];
+            }
+            const int nbS = a.zhi - a.zlo;  // one element layer per brick
+            int nseg = 1;
+            while (ncols * nseg < 3 * gsz && nbS % (2 * nseg) == 0 && nbS / (2 * nseg) >= 2) nseg *= 2;
+            a.nseg = nseg;
+            a.seglen = nbS / nseg;
+            const long long nunits = ncols * nseg;
+            if (gsz > nunits) gsz = nunits;
+            if (gsz < 1) gsz = 1;
+            *grid = (int)gsz;
+            kern<<<(int)gsz, K::NT, K::SMEM_BYTES, st>>>(a);
+            return cudaGetLastError();
+        }
+    }
+    static bool v6_ok(const ApplyParams &a, bool pcg)
+    {
+        static const bool off = [] {
+            const char *e = getenv("DG_APPLY_IMPL");
+            return e && e[0] == 'v' && (e[1] == '4' || e[1] == '5');
+        }();
+        // TMA copies single elements: n^3 doubles must be a multiple of 16 bytes (n even)
+        if (off || DIM != 3 || a.g.P > 5 || (a.g.P % 2) == 0) return false;
+        if (a.g.Nl[0] % 4 || a.g.Nl[1] % 4 || a.g.Nl[2] < 2) return false;
+        const int nz = a.zhi >= 0 ? a.zhi - a.zlo : a.g.Nl[2];
+        if (nz < 2) return false;
+        auto al = [](const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+        if (pcg) return al(a.pro.z) && al(a.pro.p_old) && al(a.pro.p_out) && (!a.nu || al(a.nu));
+        return al(a.u) && (!a.nu || al(a.nu));
+    }
+    // can this mesh be applied per range of slowest-direction layers (v5/v6 only)?
+    static bool ranges_ok(const Geom &g)
+    {
+        const char *e = getenv("DG_APPLY_IMPL");
+        if (e && e[0] == 'v' && e[1] == '4') return false;
+        return DIM == 3 && g.Nl[0] % 2 == 0 && g.Nl[1] % 2 == 0 && g.Nl[2] % 2 == 0;
+    }
     static bool v5_ok(const ApplyParams &a, bool pcg)
     {
         static const bool off = [] {
@@ -287,6 +346,10 @@ struct ApplyDispatch {
         }();
         const int *N = a.g.Nl;
         if constexpr (DIM == 3) {
+            if (MODE == 0 && v6_ok(a, false)) {  // the fused PCG operand stays on v5 (faster prologue)
+                const cudaError_t e = go6<P, VARNU, MODE>(a, grid, st);
+                if (e != cudaErrorNotSupported) return e;
+            }
             if (v5_ok(a, MODE == 1)) {
                 const cudaError_t e = go5<P, VARNU, MODE>(a, grid, st);
                 if (e != cudaErrorNotSupported) return e;

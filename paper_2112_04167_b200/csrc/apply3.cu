@@ -9,6 +9,7 @@ cudaError_t launch_apply3(const ApplyParams &a, bool varnu, bool pcg, int *grid,
 {
     return ApplyDispatch<3>::apply(a, varnu, pcg, grid, smem, st);
 }
+bool apply3_ranges_ok(const Geom &g) { return ApplyDispatch<3>::ranges_ok(g); }
 cudaError_t launch_diag3(const Geom &g, double lam, const double *nu, double nuc, const Halo &h, double *d,
                          cudaStream_t st)
 {

@@ -1,0 +1,589 @@
+// apply6.cuh -- 3-D SIP-DG apply, v6: one persistent CTA per SM, 4x4x1-element bricks,
+// warp-specialised producer / consumers, one element line per consumer thread with warp
+// shuffles across the in-brick faces.
+//
+// Same operator as apply.cuh / apply5.cuh (P:1039 interior penalty; Alg. 3 lines 5/9;
+// readings A1-A5).  What changes against v5 (DESIGN.md §6 "k_apply6"):
+//
+//   * bricks of 4x4x1 elements (a z-column segment is walked one element layer at a time):
+//     x/y brick faces per element halve against 2x2x2 (the producer's L2 trace work), and
+//     every z face is carried by the consumer that owns the z line in consecutive bricks;
+//   * 5 consumer warpgroups (one thread per element line: 16 n^2 lines per pass) and one
+//     producer warpgroup; the producer loads a brick's x/y neighbour lines in two memory
+//     rounds (at most 3 lines per thread in flight at 80 registers);
+//   * in the x and y passes the 4 elements of a brick row sit on 4 adjacent lanes: the
+//     in-brick faces exchange (u, nu (2/h) d_n u, nu) with __shfl_up/down, only the two
+//     brick-end lanes read the producer's trace table;
+//   * z pass: the bottom face comes from the thread's own carry (the previous brick's top
+//     line), the top face is deferred -- the element output is parked in shared memory and
+//     completed by the next brick (the v5 ZCarry, per element line);
+//   * staging: TMA bulk copies, one element per lane, into odd-chunk padded slots
+//     (conflict-free 16-byte x-line loads).
+#pragma once
+
+#include "apply5.cuh"
+
+namespace dg {
+namespace v6 {
+#ifdef DG_V5_DEBUG
+using v5::g_dbg;
+#endif
+
+using v5::eo;
+using v5::fence_proxy_async;
+using v5::l2_prefetch;
+using v5::mbar_arrive;
+using v5::mbar_expect_tx;
+using v5::mbar_init;
+using v5::mbar_wait;
+using v5::named_sync;
+using v5::rdot;
+using v5::tma_load;
+
+template <int P_, bool VARNU_, int MODE_>
+struct KC6 {
+    static constexpr int P = P_;
+    static constexpr bool VARNU = VARNU_;
+    static constexpr int MODE = MODE_;
+    static constexpr int n = P + 1;
+    static constexpr int NN = n * n;
+    static constexpr int NPE = n * n * n;
+    static constexpr int BX = 4, BY = 4, BE = 16;               // brick: 4 x 4 x 1 elements
+    static constexpr int SE = ((NPE + 1) / 2) * 2 + 4;          // padded element slot (doubles)
+    static constexpr int SY = 4 * SE + 4;                        // slot stride along y (bank spread)
+    static constexpr int NCL = BE * NN;                          // consumer lines per pass
+    static constexpr int NCW = ((NCL + 31) / 32 + 3) / 4 * 4;   // consumer warps (warpgroup-aligned)
+    static constexpr int NC = NCW * 32;
+    static constexpr int NP = 128;                               // producer warpgroup
+    static constexpr int NT = NC + NP;
+    static constexpr int NV = VARNU ? 3 : 2;                     // trace values: u, s (, nu)
+    static constexpr int LR = 4 * NN;                            // x / y brick-face lines per side
+    static constexpr int TRXY = 2 * 2 * NV * LR;                 // x/y trace table per buffer
+    static constexpr int NPT = NP - 32;                          // producer trace threads (warp 0: TMA)
+    static constexpr int KT = (4 * LR + NPT - 1) / NPT;          // producer x/y tasks per thread
+    static constexpr int BRK = 4 * SY;
+    static constexpr int OFF_U = 0;
+    static constexpr int OFF_NU = OFF_U + 2 * BRK;
+    static constexpr int OFF_ACC = OFF_NU + (VARNU ? 2 * BRK : 0);
+    static constexpr int OFF_TR = OFF_ACC + BRK;                 // [2][d][side][c][LR]
+    static constexpr int OFF_TZ = OFF_TR + 2 * TRXY;             // [side][c][NCL] (segment ends)
+    static constexpr int OFF_ZO = OFF_TZ + 2 * NV * NCL;         // parked z-pass outputs [n][NCL]
+    static constexpr int OFF_RED = OFF_ZO + n * NCL;
+    static constexpr int OFF_BAR = OFF_RED + 64;
+    static constexpr int SMEM_DOUBLES = OFF_BAR + 4;
+    static constexpr int SMEM_BYTES = SMEM_DOUBLES * 8;
+    static constexpr int REG_C = 65536 / NT / 8 * 8 > 80 ? 80 : 65536 / NT / 8 * 8;  // launch registers
+};
+
+// consumer z-line carry (the same thread owns the same z line in every brick of a column)
+struct ZC6 {
+    bool held = false;
+    double *po = nullptr;
+    double u, gP, nu;
+};
+
+// ---------------------------------------------------------------------------
+// consumer x / y pass: one element line per thread, 4 lanes per brick row
+// ---------------------------------------------------------------------------
+template <class K, int D, bool FIRST>
+__device__ __forceinline__ void cpass_xy(const ApplyParams &a, const DevTab &T, const double *su, const double *snu,
+                                         double *sacc, const double *tr, int t)
+{
+    constexpr int P = K::P, n = K::n, NN = K::NN, LR = K::LR, NV = K::NV, SE = K::SE;
+    constexpr int SSD = D == 0 ? 1 : n;
+    if ((t & ~31) >= K::NCL) return;  // fully idle warp (warp-uniform: no shuffle partners lost)
+    const bool act = t < K::NCL;
+    const int tt = act ? t : 0;
+    const int l = tt & 3, L = tt >> 2;  // position along D in the brick row, row index
+    const int ce = L / NN, tn = L - ce * NN;
+    const int ta = tn % n, tb = tn / n;
+    const int lx = D == 0 ? l : ce, ly = D == 0 ? ce : l;
+    const int base = lx * SE + ly * K::SY + (D == 0 ? ta * n + tb * NN : ta + tb * NN);
+    const Geom &g = a.g;
+    const double W = T.w[ta] * T.w[tb] * g.wfac[D];
+    const double sd = g.sd[D], htau = 0.5 * g.tau[D];
+
+    double v[n], nv[n];
+    if (D == 0 && (n % 2) == 0) {
+#pragma unroll
+        for (int i = 0; i < n; i += 2) {
+            const double2 x = *reinterpret_cast<const double2 *>(su + base + i);
+            v[i] = x.x;
+            v[i + 1] = x.y;
+            if (K::VARNU) {
+                const double2 y = *reinterpret_cast<const double2 *>(snu + base + i);
+                nv[i] = y.x;
+                nv[i + 1] = y.y;
+            }
+        }
+    } else {
+#pragma unroll
+        for (int i = 0; i < n; ++i) {
+            v[i] = su[base + i * SSD];
+            nv[i] = K::VARNU ? snu[base + i * SSD] : a.nu_const;
+        }
+    }
+    // brick-face traces (only the end lanes use them)
+    const double *trd = tr + D * 2 * NV * LR;
+    double uL = 0.0, sL = 0.0, nuL = a.nu_const, uR = 0.0, sR = 0.0, nuR = a.nu_const;
+    if (act && l == 0) {
+        uL = trd[L];
+        sL = trd[LR + L];
+        if (K::VARNU) nuL = trd[2 * LR + L];
+    }
+    if (act && l == 3) {
+        uR = trd[NV * LR + L];
+        sR = trd[(NV + 1) * LR + L];
+        if (K::VARNU) nuR = trd[(NV + 2) * LR + L];
+    }
+    double r[n];
+    if (K::VARNU) {
+        double gg[n];
+        eo<P, true>(T.eD, v, gg);
+        const double s0 = nv[0] * sd * gg[0], sP = nv[P] * sd * gg[P];
+        // in-brick faces: the left neighbour's right end arrives from lane - 1, the right
+        // neighbour's left end from lane + 1
+        const double xu = __shfl_up_sync(0xffffffffu, v[P], 1), xs = __shfl_up_sync(0xffffffffu, sP, 1),
+                     xn = __shfl_up_sync(0xffffffffu, nv[P], 1);
+        const double yu = __shfl_down_sync(0xffffffffu, v[0], 1), ys = __shfl_down_sync(0xffffffffu, s0, 1),
+                     yn = __shfl_down_sync(0xffffffffu, nv[0], 1);
+        if (l != 0) {
+            uL = xu;
+            sL = xs;
+            nuL = xn;
+        }
+        if (l != 3) {
+            uR = yu;
+            sR = ys;
+            nuR = yn;
+        }
+        const double JL = uL - v[0], JR = v[P] - uR;
+        const double FL = fma(htau * (nuL + nv[0]), JL, -0.5 * (sL + s0));
+        const double FR = fma(htau * (nv[P] + nuR), JR, -0.5 * (sP + sR));
+        double tv[n];
+#pragma unroll
+        for (int k = 0; k < n; ++k) tv[k] = g.wsd[D][k] * (nv[k] * gg[k]);
+        tv[P] = fma(-0.5 * sd * nv[P], JR, tv[P]);
+        tv[0] = fma(-0.5 * sd * nv[0], JL, tv[0]);
+        eo<P, true>(T.eE, tv, r);
+        r[P] += FR;
+        r[0] -= FL;
+    } else {
+        const double c = a.nu_const * sd, ck = c * (0.5 * (P + 1) * (P + 1));
+        const double d0 = rdot<P>(T, 0, v), dP = rdot<P>(T, P, v);
+        const double xu = __shfl_up_sync(0xffffffffu, v[P], 1), xs = __shfl_up_sync(0xffffffffu, c * dP, 1);
+        const double yu = __shfl_down_sync(0xffffffffu, v[0], 1), ys = __shfl_down_sync(0xffffffffu, c * d0, 1);
+        if (l != 0) {
+            uL = xu;
+            sL = xs;
+        }
+        if (l != 3) {
+            uR = yu;
+            sR = ys;
+        }
+        double kv[n];
+        eo<P, false>(T.eK, v, kv);
+        const double aR = 0.5 * c * uR, aL = -0.5 * c * uL;
+#pragma unroll
+        for (int i = 0; i < n; ++i) r[i] = fma(c, kv[i], fma(aR, T.D[P][i], aL * T.D[0][i]));
+        r[P] += fma(-ck, uR, -0.5 * sR);
+        r[0] += fma(-ck, uL, 0.5 * sL);
+    }
+    if (!act) return;
+    double *pa = sacc + base;
+#pragma unroll
+    for (int i = 0; i < n; ++i) pa[i * SSD] = FIRST ? W * r[i] : fma(W, r[i], pa[i * SSD]);
+}
+
+// ---------------------------------------------------------------------------
+// consumer z pass (last): carry, deferred top face, output
+// ---------------------------------------------------------------------------
+template <class K>
+__device__ __forceinline__ void cpass_z(const ApplyParams &a, const DevTab &T, const double *su, const double *snu,
+                                        const double *sacc, const double *tz, double *zo, long long eb, int t,
+                                        bool zfirst, bool zlast, ZC6 &zc, double &epi0, double &epi1)
+{
+    constexpr int P = K::P, n = K::n, NN = K::NN, NPE = K::NPE, NCL = K::NCL, NV = K::NV, SE = K::SE;
+    if (t >= NCL) return;
+    const Geom &g = a.g;
+    const int slot = t / NN, tn = t - slot * NN;
+    const int ta = tn % n, tb = tn / n;
+    const int base = (slot & 3) * SE + (slot >> 2) * K::SY + ta + tb * n;
+    const double W = T.w[ta] * T.w[tb] * g.wfac[2];
+    const double sd = g.sd[2], htau = 0.5 * g.tau[2];
+    double v[n], nv[n];
+#pragma unroll
+    for (int i = 0; i < n; ++i) {
+        v[i] = su[base + i * NN];
+        nv[i] = K::VARNU ? snu[base + i * NN] : a.nu_const;
+    }
+    double uL, sL, nuL, uR = 0.0, sR = 0.0, nuR = a.nu_const;
+    if (zfirst) {
+        uL = tz[t];
+        sL = tz[NCL + t];
+        nuL = K::VARNU ? tz[2 * NCL + t] : a.nu_const;
+    } else {
+        uL = zc.u;
+        nuL = K::VARNU ? zc.nu : a.nu_const;
+        sL = nuL * sd * zc.gP;
+    }
+    if (zlast) {
+        uR = tz[NV * NCL + t];
+        sR = tz[(NV + 1) * NCL + t];
+        nuR = K::VARNU ? tz[(NV + 2) * NCL + t] : a.nu_const;
+    }
+    // release the previous brick's parked output: its top-face terms
+    // dr_i = c D_{P,i} + [i == P] f0 with the face shared with our bottom
+    auto release = [&](double c, double f0) {
+        double s1 = 0.0;
+#pragma unroll
+        for (int i = 0; i < n; ++i) {
+            const double d = W * fma(c, T.D[P][i], i == P ? f0 : 0.0);
+            zc.po[i * NN] = zo[i * NCL + t] + d;
+            s1 += d;
+        }
+        if (K::MODE == 1) {
+            epi0 = fma(W, fma(c, zc.gP, f0 * zc.u), epi0);
+            epi1 += s1;
+        }
+        zc.held = false;
+    };
+    double r[n], gP;
+    if (K::VARNU) {
+        double gg[n];
+        eo<P, true>(T.eD, v, gg);
+        const double s0 = nv[0] * sd * gg[0], sP = nv[P] * sd * gg[P];
+        const double JL = uL - v[0];
+        const double FL = fma(htau * (nuL + nv[0]), JL, -0.5 * (sL + s0));
+        double JR = 0.0, FR = 0.0;
+        if (zlast) {
+            JR = v[P] - uR;
+            FR = fma(htau * (nv[P] + nuR), JR, -0.5 * (sP + sR));
+        }
+        if (!zfirst && zc.held) release(-0.5 * sd * zc.nu * JL, FL);
+        double tv[n];
+#pragma unroll
+        for (int k = 0; k < n; ++k) tv[k] = g.wsd[2][k] * (nv[k] * gg[k]);
+        tv[P] = fma(-0.5 * sd * nv[P], JR, tv[P]);
+        tv[0] = fma(-0.5 * sd * nv[0], JL, tv[0]);
+        eo<P, true>(T.eE, tv, r);
+        r[P] += FR;
+        r[0] -= FL;
+        gP = gg[P];
+    } else {
+        const double c = a.nu_const * sd, ck = c * (0.5 * (P + 1) * (P + 1));
+        const double d0 = rdot<P>(T, 0, v), dP = rdot<P>(T, P, v);
+        if (!zfirst && zc.held) release(0.5 * c * v[0], fma(-ck, v[0], -0.5 * c * d0));
+        double kv[n];
+        eo<P, false>(T.eK, v, kv);
+        const double aR = 0.5 * c * uR, aL = -0.5 * c * uL;
+#pragma unroll
+        for (int i = 0; i < n; ++i) r[i] = fma(c, kv[i], fma(aR, T.D[P][i], aL * T.D[0][i]));
+        r[P] += fma(-ck, uR, -0.5 * sR);
+        r[0] += fma(-ck, uL, 0.5 * sL);
+        gP = dP;
+    }
+    // output: element (slot % 4, slot / 4) of the brick layer
+    const long long ge = eb + (slot & 3) + (long long)g.Nl[0] * (slot >> 2);
+    double *po = a.out + ge * NPE + ta + tb * n;
+    const double lw = a.lam * W * (0.5 * g.h[2]);
+    const double *pa = sacc + base;
+#pragma unroll
+    for (int i = 0; i < n; ++i) {
+        const double o = fma(lw * T.w[i], v[i], fma(W, r[i], pa[i * NN]));
+        if (zlast) po[i * NN] = o;
+        else zo[i * NCL + t] = o;
+        if (K::MODE == 1) {
+            epi0 = fma(v[i], o, epi0);
+            epi1 += o;
+        }
+    }
+    if (!zlast) {
+        zc.held = true;
+        zc.po = po;
+        zc.u = v[P];
+        zc.gP = gP;
+        zc.nu = nv[P];
+    }
+}
+
+// ---------------------------------------------------------------------------
+// producer: x and y brick-face traces, one memory round (KT lines per thread in flight)
+// ---------------------------------------------------------------------------
+template <class K, int K0, int K1>
+__device__ __forceinline__ void ptraces_xy(const ApplyParams &a, const DevTab &T, double *tr, const int (&e0)[3],
+                                           long long eb, int ptid, double beta)
+{
+    constexpr int P = K::P, n = K::n, NN = K::NN, NPE = K::NPE, LR = K::LR, NV = K::NV, KT = K1 - K0;
+    const Geom &g = a.g;
+    const long long lay = (long long)g.Nl[0] * g.Nl[1];
+    const double *fu = K::MODE == 1 ? a.pro.z : a.u;
+    double v[KT][n], nuf[KT];
+    int meta[KT];
+#pragma unroll
+    for (int k = 0; k < KT; ++k) {
+        const int tk = ptid + (K0 + k) * K::NPT;
+        meta[k] = -1;
+        if (tk >= 4 * LR) continue;
+        const int D = tk / (2 * LR), side = (tk / LR) & 1, L = tk % LR;
+        const int ce = L / NN, tn = L - ce * NN;
+        const int ta = tn % n, tb = tn / n;
+        // neighbour element (local coordinates) and the face node of its line
+        int cx, cy;
+        int off, step;
+        if (D == 0) {
+            cx = side ? e0[0] + 4 : e0[0] - 1;
+            cx = cx < 0 ? cx + g.Nl[0] : (cx >= g.Nl[0] ? cx - g.Nl[0] : cx);
+            cy = e0[1] + ce;
+            off = ta * n + tb * NN + (side ? 0 : P);
+            step = side ? 1 : -1;
+        } else {
+            cy = side ? e0[1] + 4 : e0[1] - 1;
+            cy = cy < 0 ? cy + g.Nl[1] : (cy >= g.Nl[1] ? cy - g.Nl[1] : cy);
+            cx = e0[0] + ce;
+            off = ta + tb * NN + (side ? 0 : P * n);
+            step = side ? n : -n;
+        }
+        const long long o = (cx + (long long)g.Nl[0] * cy + lay * e0[2]) * NPE + off;
+        if (K::MODE == 1) {
+#pragma unroll
+            for (int i = 0; i < n; ++i) v[k][i] = fma(beta, __ldg(a.pro.p_old + o + i * step), __ldg(fu + o + i * step));
+        } else {
+#pragma unroll
+            for (int i = 0; i < n; ++i) v[k][i] = __ldg(fu + o + i * step);
+        }
+        nuf[k] = K::VARNU ? __ldg(a.nu + o) : a.nu_const;
+        meta[k] = tk;
+    }
+    (void)eb;
+#pragma unroll
+    for (int k = 0; k < KT; ++k) {
+        const int tk = meta[k];
+        if (tk < 0) continue;
+        const int D = tk / (2 * LR), side = (tk / LR) & 1, L = tk % LR;
+        const double dd = rdot<P>(T, 0, v[k]);  // v[0] is the face node (see v5::ptraces)
+        double *trd = tr + D * 2 * NV * LR + side * NV * LR;
+        trd[L] = v[k][0];
+        trd[LR + L] = nuf[k] * g.sd[D] * (side ? dd : -dd);
+        if (K::VARNU) trd[2 * LR + L] = nuf[k];
+    }
+}
+
+// z traces at column-segment ends (global memory; halo layers for multi-rank slabs)
+template <class K>
+__device__ __noinline__ void ptraces_z(const ApplyParams &a, const DevTab &T, double *tz, const int (&e0)[3], int ptid,
+                                       double beta, int side)
+{
+    constexpr int P = K::P, n = K::n, NN = K::NN, NPE = K::NPE, NCL = K::NCL, NV = K::NV;
+    const Geom &g = a.g;
+    const double *fu = K::MODE == 1 ? a.pro.z : a.u;
+    for (int t = ptid; t < NCL; t += K::NP) {
+        const int slot = t / NN, tn = t - slot * NN;
+        const int ta = tn % n, tb = tn / n;
+        const int cz = side ? e0[2] + 1 : e0[2] - 1;
+        const int goff = ta + tb * n + (side ? 0 : P * NN);
+        const int step = side ? NN : -NN;
+        const double *pu = v5::nbr<2>(g, fu, K::MODE == 1 ? nullptr : a.halo.u_lo, K::MODE == 1 ? nullptr : a.halo.u_hi,
+                                      e0[0] + (slot & 3), e0[1] + (slot >> 2), cz, NPE) + goff;
+        double v[n];
+        if (K::MODE == 1) {
+            const double *pp = a.pro.p_old + (pu - fu);
+#pragma unroll
+            for (int i = 0; i < n; ++i) v[i] = fma(beta, __ldg(pp + i * step), __ldg(pu + i * step));
+        } else {
+#pragma unroll
+            for (int i = 0; i < n; ++i) v[i] = __ldg(pu + i * step);
+        }
+        const double nuf = K::VARNU ? __ldg(v5::nbr<2>(g, a.nu, a.halo.nu_lo, a.halo.nu_hi, e0[0] + (slot & 3),
+                                                       e0[1] + (slot >> 2), cz, NPE) + goff)
+                                    : a.nu_const;
+        const double dd = rdot<P>(T, 0, v);
+        double *t0 = tz + side * NV * NCL;
+        t0[t] = v[0];
+        t0[NCL + t] = nuf * g.sd[2] * (side ? dd : -dd);
+        if (K::VARNU) t0[2 * NCL + t] = nuf;
+    }
+}
+
+template <int P, bool VARNU, int MODE>
+__global__ void __launch_bounds__((KC6<P, VARNU, MODE>::NT)) __maxnreg__((KC6<P, VARNU, MODE>::REG_C))
+    k_apply6(const __grid_constant__ ApplyParams a)
+{
+    using K = KC6<P, VARNU, MODE>;
+    constexpr int NPE = K::NPE, SE = K::SE, BRK = K::BRK, NC = K::NC, NP = K::NP, NCL = K::NCL;
+    const Geom &g = a.g;
+    const DevTab &T = c_tab[P];
+    extern __shared__ __align__(16) double sm[];
+    uint64_t *bar = reinterpret_cast<uint64_t *>(sm + K::OFF_BAR);  // full[0..1], empty[0..1]
+    const int tid = threadIdx.x;
+    if (MODE == 1 && *a.pro.done) return;
+    const double beta = MODE == 1 ? *a.pro.beta : 0.0;
+    if (tid == 0) {
+        mbar_init(&bar[0], NP);
+        mbar_init(&bar[1], NP);
+        mbar_init(&bar[2], NC);
+        mbar_init(&bar[3], NC);
+        fence_proxy_async();
+    }
+    __syncthreads();
+
+    const int nb0 = g.Nl[0] / K::BX, nb1 = g.Nl[1] / K::BY;
+    const int ncols = nb0 * nb1;
+    const int nunits = ncols * a.nseg;
+    const int seglen = a.seglen;
+    const long long s1 = g.Nl[0], s2 = (long long)g.Nl[0] * g.Nl[1];
+
+    if (tid >= NC) {
+        // ------------------------------- producer -------------------------------
+        const int ptid = tid - NC, lane = ptid & 31;
+        int it = 0;
+        for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
+            const int col = u % ncols, zs = u / ncols;
+            int e0[3] = {(col % nb0) * K::BX, (col / nb0) * K::BY, a.zlo + zs * seglen};
+            for (int j = 0; j < seglen; ++j, ++it, ++e0[2]) {
+                const int buf = it & 1;
+                V5_T0(tw);
+                if (it >= 2) mbar_wait(&bar[2 + buf], ((it >> 1) - 1) & 1);
+                if (ptid == 0) V5_ACC(2, tw);
+                V5_T0(tt);
+                double *su = sm + K::OFF_U + buf * BRK;
+                double *snu = sm + K::OFF_NU + buf * BRK;
+                const long long eb = e0[0] + s1 * e0[1] + s2 * e0[2];
+                if (ptid < 32) {
+                    // TMA: one element per lane into its padded slot (u lanes 0-15, nu 16-31)
+                    constexpr unsigned EB = NPE * 8u;
+                    if (lane == 0) {
+                        const unsigned bytes = (MODE == 0 ? 16u * EB : 0u) + (VARNU ? 16u * EB : 0u);
+                        if (bytes) mbar_expect_tx(&bar[buf], bytes);
+                    }
+                    __syncwarp();
+                    const int el = lane & 15;
+                    const long long ge = eb + (el & 3) + s1 * (el >> 2);
+                    const int so = (el & 3) * SE + (el >> 2) * K::SY;
+                    if (lane < 16 && MODE == 0) tma_load(su + so, a.u + ge * NPE, EB, &bar[buf]);
+                    if (lane >= 16 && VARNU) tma_load(snu + so, a.nu + ge * NPE, EB, &bar[buf]);
+                    // warm L2 with the next brick's x / y neighbour elements (4 single elements
+                    // per x side, one contiguous x-row of 4 per y side)
+                    int n0[3] = {e0[0], e0[1], e0[2] + 1};
+                    bool ok = j + 1 < seglen;
+                    if (!ok && u + (int)gridDim.x < nunits) {
+                        const int u2 = u + gridDim.x, c2 = u2 % ncols, z2 = u2 / ncols;
+                        n0[0] = (c2 % nb0) * K::BX;
+                        n0[1] = (c2 / nb0) * K::BY;
+                        n0[2] = a.zlo + z2 * seglen;
+                        ok = true;
+                    }
+                    const int q = lane % 10, f = lane / 10;
+                    constexpr int NF = (MODE == 1 ? 2 : 1) + (VARNU ? 1 : 0);
+                    if (ok && f < NF) {
+                        const double *fb = MODE == 1 ? (f == 0 ? a.pro.z : (f == 1 ? a.pro.p_old : a.nu))
+                                                     : (f == 0 ? a.u : a.nu);
+                        int cx, cy, cnt;
+                        if (q < 8) {
+                            cx = (q >> 2) ? n0[0] + 4 : n0[0] - 1;
+                            cx = cx < 0 ? cx + g.Nl[0] : (cx >= g.Nl[0] ? cx - g.Nl[0] : cx);
+                            cy = n0[1] + (q & 3);
+                            cnt = 1;
+                        } else {
+                            cx = n0[0];
+                            cy = (q & 1) ? n0[1] + 4 : n0[1] - 1;
+                            cy = cy < 0 ? cy + g.Nl[1] : (cy >= g.Nl[1] ? cy - g.Nl[1] : cy);
+                            cnt = 4;
+                        }
+                        l2_prefetch(fb + (cx + s1 * cy + s2 * n0[2]) * NPE, (unsigned)(cnt * NPE * 8));
+                    }
+                }
+                if (MODE == 1) {  // p = z + beta p_old -> shared (operand) and p_out (fused CG prologue)
+                    for (int q = ptid; q < 16 * NPE; q += NP) {
+                        const int el = q / NPE, w = q - el * NPE;
+                        const long long go = (eb + (el & 3) + s1 * (el >> 2)) * NPE + w;
+                        const double p = fma(beta, __ldg(a.pro.p_old + go), __ldg(a.pro.z + go));
+                        su[(el & 3) * SE + (el >> 2) * K::SY + w] = p;
+                        a.pro.p_out[go] = p;
+                    }
+                }
+                double *tr = sm + K::OFF_TR + buf * K::TRXY;
+                if (ptid == 0) V5_ACC(4, tt);
+                V5_T0(tx);
+                // x/y traces (warps 1-3) in rounds of at most 3 lines per thread (register budget)
+                if (ptid >= 32) {
+                    ptraces_xy<K, 0, (K::KT < 3 ? K::KT : 3)>(a, T, tr, e0, eb, ptid - 32, beta);
+                    if (ptid == 32) V5_ACC(9, tx);
+                    V5_T0(ty);
+                    if constexpr (K::KT > 3) ptraces_xy<K, 3, K::KT>(a, T, tr, e0, eb, ptid - 32, beta);
+                    if (ptid == 32) V5_ACC(10, ty);
+                }
+                if (j == 0) ptraces_z<K>(a, T, sm + K::OFF_TZ, e0, ptid, beta, 0);
+                if (j == seglen - 1) ptraces_z<K>(a, T, sm + K::OFF_TZ, e0, ptid, beta, 1);
+                if (ptid == 0) V5_ACC(3, tx);
+                mbar_arrive(&bar[buf]);
+            }
+        }
+        return;
+    }
+
+    // ------------------------------- consumers -------------------------------
+    double epi0 = 0.0, epi1 = 0.0;
+    int it = 0;
+    ZC6 zc;
+    double *sacc = sm + K::OFF_ACC;
+    double *zo = sm + K::OFF_ZO;
+    const double *tz = sm + K::OFF_TZ;
+    for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
+        const int col = u % ncols, zs = u / ncols;
+        int e0[3] = {(col % nb0) * K::BX, (col / nb0) * K::BY, a.zlo + zs * seglen};
+        for (int j = 0; j < seglen; ++j, ++it, ++e0[2]) {
+            const int buf = it & 1;
+            const double *su = sm + K::OFF_U + buf * BRK;
+            const double *snu = sm + K::OFF_NU + buf * BRK;
+            const double *tr = sm + K::OFF_TR + buf * K::TRXY;
+            const long long eb = e0[0] + s1 * e0[1] + s2 * e0[2];
+            V5_T0(tw);
+            mbar_wait(&bar[buf], (it >> 1) & 1);
+            if (tid == 0) V5_ACC(0, tw);
+            V5_T0(tp);
+            cpass_xy<K, 0, true>(a, T, su, snu, sacc, tr, tid);
+            if (tid == 0) V5_ACC(6, tp);
+            named_sync(1, NC);
+            V5_T0(t1);
+            cpass_xy<K, 1, false>(a, T, su, snu, sacc, tr, tid);
+            if (tid == 0) V5_ACC(7, t1);
+            named_sync(1, NC);
+            V5_T0(t2);
+            cpass_z<K>(a, T, su, snu, sacc, tz, zo, eb, tid, j == 0, j == seglen - 1, zc, epi0, epi1);
+            if (tid == 0) V5_ACC(8, t2);
+            mbar_arrive(&bar[2 + buf]);
+            named_sync(1, NC);  // ACC and the parked outputs are rewritten by the next brick
+            if (tid == 0) {
+                V5_ACC(1, tp);
+#ifdef DG_V5_DEBUG
+                atomicAdd(&v5::g_dbg[5], 1ull);
+#endif
+            }
+        }
+    }
+    if (MODE == 1) {
+        double *red = sm + K::OFF_RED;
+        const int lane = tid & 31, wid = tid >> 5;
+        epi0 = warp_sum(epi0);
+        epi1 = warp_sum(epi1);
+        if (lane == 0) {
+            red[wid] = epi0;
+            red[32 + wid] = epi1;
+        }
+        named_sync(1, NC);
+        if (tid == 0) {
+            double s0 = 0.0, s1v = 0.0;
+            for (int w = 0; w < NC / 32; ++w) {
+                s0 += red[w];
+                s1v += red[32 + w];
+            }
+            a.epi.partial[2 * blockIdx.x + 0] = s0;
+            a.epi.partial[2 * blockIdx.x + 1] = s1v;
+        }
+    }
+    (void)NCL;
+}
+
+}  // namespace v6
+}  // namespace dg

@@ -714,7 +714,7 @@ dg_status dg_helmholtz_apply_host(dg_mesh *m, double lam, const double *nu_host,
     if (nu_host) CKS(stage(m, &m->st_c, b));
     const Geom &g = m->g;
     int C = 0;
-    if (m->nranks == 1 && g.dim == 3 && g.Nl[0] % 2 == 0 && g.Nl[1] % 2 == 0 && g.Nl[2] % 2 == 0) {
+    if (m->nranks == 1 && g.dim == 3 && apply3_ranges_ok(g)) {
         const int nbz = g.Nl[2] / 2;
         for (int c = 8; c >= 3; --c)
             if (nbz % c == 0) {

@@ -119,6 +119,7 @@ struct ConvParams {
 // grid: out, the number of CTAs launched (persistent; <= 148 x 8)
 cudaError_t launch_apply2(const ApplyParams &a, bool varnu, bool pcg, int *grid, int smem, cudaStream_t st);
 cudaError_t launch_apply3(const ApplyParams &a, bool varnu, bool pcg, int *grid, int smem, cudaStream_t st);
+bool apply3_ranges_ok(const Geom &g);  // layer-range applies available (pipelined host call)
 cudaError_t launch_diag2(const Geom &g, double lam, const double *nu, double nuc, const Halo &h, double *d,
                          cudaStream_t st);
 cudaError_t launch_diag3(const Geom &g, double lam, const double *nu, double nuc, const Halo &h, double *d,

@@ -65,6 +65,9 @@ SMALL = [
     (2, (4, 4), 4), (2, (3, 5), 3), (2, (1, 2), 2), (2, (6, 1), 8), (2, (5, 7), 1), (2, (2, 3), 10),
     (3, (2, 2, 2), 3), (3, (3, 2, 5), 4), (3, (1, 1, 1), 2), (3, (4, 1, 3), 5), (3, (2, 3, 2), 7),
     (3, (3, 3, 3), 6), (3, (2, 2, 1), 1), (3, (2, 1, 2), 9), (3, (1, 2, 2), 10),
+    # v6 kernel shapes (N_x, N_y multiples of 4, P <= 5): segments of 2..5 layers, 1..4 columns
+    (3, (4, 4, 2), 3), (3, (4, 8, 3), 5), (3, (8, 4, 4), 2), (3, (4, 4, 5), 4), (3, (8, 8, 6), 5),
+    (3, (4, 4, 7), 1),
 ]
 
 
@@ -255,6 +258,20 @@ def test_pcg_small_poisson_vs_oracle():
     u = torch.zeros(f.shape, dtype=torch.float64, device=DEV)
     dg.dg_pcg_solve(m, 0.0, None, 1.0 / 1600, T(f), 1e-11, 20000, u)
     ref, *_ = oracle.pcg_solve(om, 0.0, f, nu_const=1.0 / 1600, tol=1e-14)
+    assert rel(H(u), ref) <= 1e-9
+
+
+@pytest.mark.parametrize("P,lam", [(4, 5.0), (5, 0.0)])
+def test_pcg_v6_shapes(P, lam):
+    # 4x4xN_z meshes run the v6 apply (fused PCG prologue / epilogue, column carry)
+    dim, N, L = 3, (4, 4, 6), (1.0, 1.1, 1.2)
+    m, om = meshes(dim, N, L, P)
+    rng = np.random.default_rng(20 + P)
+    f = rng.uniform(-1, 1, (om.n_el, om.npe))
+    nu = 0.5 + rng.uniform(0, 1, (om.n_el, om.npe))
+    u = torch.zeros(f.shape, dtype=torch.float64, device=DEV)
+    dg.dg_pcg_solve(m, lam, T(nu), 0.0, T(f), 1e-11, 20000, u)
+    ref, *_ = oracle.pcg_solve(om, lam, f, nu=nu, tol=1e-14)
     assert rel(H(u), ref) <= 1e-9
 
 
