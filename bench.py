@@ -329,7 +329,7 @@ def run_product(args, rank, world, local_rank):
                 "achieved_gbs_incl_setup": ndof_global * it * PCG_BYTES_PER_DOF[varnu] / (t_solve * 1e-3) / 1e9},
         "stage": stage,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": traffic, "kernel": "v5::k_apply5<%d,%s,0>" % (c.P, "1" if varnu else "0"),
+                     "traffic": traffic, "kernel": ("v6::k_apply6<%d,%s,0>" if c.P <= 5 and c.P % 2 else "v5::k_apply5<%d,%s,0>") % (c.P, "1" if varnu else "0"),
                      "bytes_per_dof": bpd, "peak_kind": peak_kind, "launch_ms": per_launch_ms},
         "e2e": {"value": ndof_global / e2e_s / 1e9, "unit": "GDOF/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "ms_per_step": e2e_s * 1e3},
