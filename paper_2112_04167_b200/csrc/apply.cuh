@@ -346,7 +346,7 @@ struct ApplyDispatch {
         }();
         const int *N = a.g.Nl;
         if constexpr (DIM == 3) {
-            if (MODE == 0 && v6_ok(a, false)) {  // the fused PCG operand stays on v5 (faster prologue)
+            if (MODE == 0 && v6_ok(a, false)) {  // the fused PCG operand stays on v5 (measured faster)
                 const cudaError_t e = go6<P, VARNU, MODE>(a, grid, st);
                 if (e != cudaErrorNotSupported) return e;
             }

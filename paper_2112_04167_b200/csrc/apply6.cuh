@@ -494,12 +494,17 @@ __global__ void __launch_bounds__((KC6<P, VARNU, MODE>::NT)) __maxnreg__((KC6<P,
                     }
                 }
                 if (MODE == 1) {  // p = z + beta p_old -> shared (operand) and p_out (fused CG prologue)
-                    for (int q = ptid; q < 16 * NPE; q += NP) {
-                        const int el = q / NPE, w = q - el * NPE;
-                        const long long go = (eb + (el & 3) + s1 * (el >> 2)) * NPE + w;
-                        const double p = fma(beta, __ldg(a.pro.p_old + go), __ldg(a.pro.z + go));
-                        su[(el & 3) * SE + (el >> 2) * K::SY + w] = p;
-                        a.pro.p_out[go] = p;
+                    constexpr int H = NPE / 2;  // double2 per element (n even)
+                    for (int q = ptid; q < 16 * H; q += NP) {
+                        const int el = q / H, w = q - el * H;
+                        const long long go = (eb + (el & 3) + s1 * (el >> 2)) * NPE + 2 * w;
+                        const double2 z = __ldg(reinterpret_cast<const double2 *>(a.pro.z + go));
+                        const double2 po = __ldg(reinterpret_cast<const double2 *>(a.pro.p_old + go));
+                        double2 p;
+                        p.x = fma(beta, po.x, z.x);
+                        p.y = fma(beta, po.y, z.y);
+                        *reinterpret_cast<double2 *>(su + (el & 3) * SE + (el >> 2) * K::SY + 2 * w) = p;
+                        *reinterpret_cast<double2 *>(a.pro.p_out + go) = p;
                     }
                 }
                 double *tr = sm + K::OFF_TR + buf * K::TRXY;
@@ -507,10 +512,12 @@ __global__ void __launch_bounds__((KC6<P, VARNU, MODE>::NT)) __maxnreg__((KC6<P,
                 V5_T0(tx);
                 // x/y traces (warps 1-3) in rounds of at most 3 lines per thread (register budget)
                 if (ptid >= 32) {
-                    ptraces_xy<K, 0, (K::KT < 3 ? K::KT : 3)>(a, T, tr, e0, eb, ptid - 32, beta);
+                    constexpr int R = MODE == 1 ? 2 : 3;  // lines in flight per thread (two loads each in MODE 1)
+                    ptraces_xy<K, 0, (K::KT < R ? K::KT : R)>(a, T, tr, e0, eb, ptid - 32, beta);
                     if (ptid == 32) V5_ACC(9, tx);
                     V5_T0(ty);
-                    if constexpr (K::KT > 3) ptraces_xy<K, 3, K::KT>(a, T, tr, e0, eb, ptid - 32, beta);
+                    if constexpr (K::KT > R) ptraces_xy<K, R, (K::KT < 2 * R ? K::KT : 2 * R)>(a, T, tr, e0, eb, ptid - 32, beta);
+                    if constexpr (K::KT > 2 * R) ptraces_xy<K, 2 * R, K::KT>(a, T, tr, e0, eb, ptid - 32, beta);
                     if (ptid == 32) V5_ACC(10, ty);
                 }
                 if (j == 0) ptraces_z<K>(a, T, sm + K::OFF_TZ, e0, ptid, beta, 0);
