@@ -61,7 +61,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t *b, unsigned parity)
     asm volatile(
         "{\n\t.reg .pred p;\n"
         "WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, 1000000;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
         "@!p bra WAIT_%=;\n}\n" ::"r"(su32(b)),
         "r"(parity)
         : "memory");
@@ -511,42 +511,6 @@ __global__ void __launch_bounds__((KC5<P, VARNU, MODE>::NT)) __maxnreg__((KC5<P,
                         const long long ge = eb + (q & 1) * s1 + (q >> 1) * s2;
                         if (MODE == 0) tma_load(su + q * 2 * NPE, a.u + ge * NPE, CH, &bar[buf]);
                         if (VARNU) tma_load(snu + q * 2 * NPE, a.nu + ge * NPE, CH, &bar[buf]);
-                    }
-                }
-                if (ptid < 32) {  // warm L2 with the x/y neighbour elements of the NEXT brick
-                    int n0[3] = {e0[0], e0[1], e0[2] + B};
-                    bool ok = j + 1 < seglen;
-                    if (!ok && u + (int)gridDim.x < nunits) {
-                        const int u2 = u + gridDim.x, c2 = u2 % ncols, z2 = u2 / ncols;
-                        n0[0] = (c2 % nb0) * B;
-                        n0[1] = (c2 / nb0) * B;
-                        n0[2] = a.zlo + z2 * seglen * B;
-                        ok = true;
-                    }
-                    // 12 element groups: x sides (4 single elements each), y sides (2 x-pairs each)
-                    const int q = ptid % 12, f = ptid / 12;  // f: field (u|z, nu|p_old, nu)
-                    constexpr int NF = (MODE == 1 ? 2 : 1) + (VARNU ? 1 : 0);
-                    if (ok && f < NF) {
-                        const double *fb = MODE == 1 ? (f == 0 ? a.pro.z : (f == 1 ? a.pro.p_old : a.nu))
-                                                     : (f == 0 ? a.u : a.nu);
-                        int c0, c1, c2, cnt;
-                        if (q < 8) {  // x neighbours
-                            const int side = q >> 2;
-                            c0 = side ? n0[0] + B : n0[0] - 1;
-                            c0 = c0 < 0 ? c0 + g.Nl[0] : (c0 >= g.Nl[0] ? c0 - g.Nl[0] : c0);
-                            c1 = n0[1] + (q & 1);
-                            c2 = n0[2] + ((q >> 1) & 1);
-                            cnt = 1;
-                        } else {      // y neighbours (contiguous x-pairs)
-                            const int side = (q - 8) >> 1;
-                            c0 = n0[0];
-                            c1 = side ? n0[1] + B : n0[1] - 1;
-                            c1 = c1 < 0 ? c1 + g.Nl[1] : (c1 >= g.Nl[1] ? c1 - g.Nl[1] : c1);
-                            c2 = n0[2] + (q & 1);
-                            cnt = 2;
-                        }
-                        const long long e = c0 + s1 * c1 + s2 * c2;
-                        l2_prefetch(fb + e * NPE, (unsigned)(cnt * NPE * 8));
                     }
                 }
                 if (MODE == 1) {  // p = z + beta p_old -> shared (operand) and p_out (fused CG prologue)
