@@ -315,6 +315,15 @@ struct ApplyDispatch {
         return al(a.u) && (!a.nu || al(a.nu));
     }
     // can this mesh be applied per range of slowest-direction layers (v5/v6 only)?
+    static bool split_pcg_ok(const Geom &g, const double *nu)
+    {
+        ApplyParams a{};
+        a.g = g;
+        a.u = nu ? nu : reinterpret_cast<const double *>(256);  // alignment probe only
+        a.nu = nu;
+        a.zhi = -1;
+        return v6_ok(a, false);
+    }
     static bool ranges_ok(const Geom &g)
     {
         const char *e = getenv("DG_APPLY_IMPL");
@@ -369,12 +378,21 @@ struct ApplyDispatch {
         }
     }
     template <int P>
-    static cudaError_t go_p(const ApplyParams &a, bool varnu, bool pcg, int *grid, cudaStream_t st)
+    static cudaError_t go_p(const ApplyParams &a, bool varnu, int mode, int *grid, cudaStream_t st)
     {
+        if (mode == 2) {  // dot epilogue only: v6 meshes (split PCG path)
+            if constexpr (DIM == 3) {
+                if (!v6_ok(a, false)) return cudaErrorNotSupported;
+                return varnu ? go6<P, true, 2>(a, grid, st) : go6<P, false, 2>(a, grid, st);
+            } else {
+                return cudaErrorNotSupported;
+            }
+        }
+        const bool pcg = mode == 1;
         if (varnu) return pcg ? pick<P, true, 1>(a, grid, st) : pick<P, true, 0>(a, grid, st);
         return pcg ? pick<P, false, 1>(a, grid, st) : pick<P, false, 0>(a, grid, st);
     }
-    static cudaError_t apply(const ApplyParams &a, bool varnu, bool pcg, int *grid, int smem, cudaStream_t st)
+    static cudaError_t apply(const ApplyParams &a, bool varnu, int pcg, int *grid, int smem, cudaStream_t st)
     {
         (void)smem;
         switch (a.g.P) {

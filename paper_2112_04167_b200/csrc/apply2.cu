@@ -5,9 +5,9 @@ DG_DEFINE_CONST_TABLES(upload_tables_apply2)
 }
 #include "apply.cuh"
 namespace dg {
-cudaError_t launch_apply2(const ApplyParams &a, bool varnu, bool pcg, int *grid, int smem, cudaStream_t st)
+cudaError_t launch_apply2(const ApplyParams &a, bool varnu, int mode, int *grid, int smem, cudaStream_t st)
 {
-    return ApplyDispatch<2>::apply(a, varnu, pcg, grid, smem, st);
+    return ApplyDispatch<2>::apply(a, varnu, mode, grid, smem, st);
 }
 cudaError_t launch_diag2(const Geom &g, double lam, const double *nu, double nuc, const Halo &h, double *d,
                          cudaStream_t st)

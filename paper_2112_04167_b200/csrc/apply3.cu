@@ -5,11 +5,12 @@ DG_DEFINE_CONST_TABLES(upload_tables_apply3)
 }
 #include "apply.cuh"
 namespace dg {
-cudaError_t launch_apply3(const ApplyParams &a, bool varnu, bool pcg, int *grid, int smem, cudaStream_t st)
+cudaError_t launch_apply3(const ApplyParams &a, bool varnu, int mode, int *grid, int smem, cudaStream_t st)
 {
-    return ApplyDispatch<3>::apply(a, varnu, pcg, grid, smem, st);
+    return ApplyDispatch<3>::apply(a, varnu, mode, grid, smem, st);
 }
 bool apply3_ranges_ok(const Geom &g) { return ApplyDispatch<3>::ranges_ok(g); }
+bool apply3_split_pcg_ok(const Geom &g, const double *nu) { return ApplyDispatch<3>::split_pcg_ok(g, nu); }
 cudaError_t launch_diag3(const Geom &g, double lam, const double *nu, double nuc, const Halo &h, double *d,
                          cudaStream_t st)
 {

@@ -1,3 +1,6 @@
+// MODE: 0 plain apply; 1 fused PCG operand (prologue p = z + beta p_old, dot epilogue);
+// 2 apply with the dot epilogue only (the split PCG path: p formed by k_pcg_pupd).
+//
 // apply6.cuh -- 3-D SIP-DG apply, v6: one persistent CTA per SM, 4x4x1-element bricks,
 // warp-specialised producer / consumers, one element line per consumer thread with warp
 // shuffles across the in-brick faces.
@@ -242,7 +245,7 @@ __device__ __forceinline__ void cpass_z(const ApplyParams &a, const DevTab &T, c
             zc.po[i * NN] = zo[i * NCL + t] + d;
             s1 += d;
         }
-        if (K::MODE == 1) {
+        if (K::MODE >= 1) {
             epi0 = fma(W, fma(c, zc.gP, f0 * zc.u), epi0);
             epi1 += s1;
         }
@@ -293,7 +296,7 @@ __device__ __forceinline__ void cpass_z(const ApplyParams &a, const DevTab &T, c
         const double o = fma(lw * T.w[i], v[i], fma(W, r[i], pa[i * NN]));
         if (zlast) po[i * NN] = o;
         else zo[i * NCL + t] = o;
-        if (K::MODE == 1) {
+        if (K::MODE >= 1) {
             epi0 = fma(v[i], o, epi0);
             epi1 += o;
         }
@@ -416,7 +419,7 @@ __global__ void __launch_bounds__((KC6<P, VARNU, MODE>::NT)) __maxnreg__((KC6<P,
     extern __shared__ __align__(16) double sm[];
     uint64_t *bar = reinterpret_cast<uint64_t *>(sm + K::OFF_BAR);  // full[0..1], empty[0..1]
     const int tid = threadIdx.x;
-    if (MODE == 1 && *a.pro.done) return;
+    if (MODE >= 1 && *a.pro.done) return;  // PCG converged: nothing to do
     const double beta = MODE == 1 ? *a.pro.beta : 0.0;
     if (tid == 0) {
         mbar_init(&bar[0], NP);
@@ -453,14 +456,14 @@ __global__ void __launch_bounds__((KC6<P, VARNU, MODE>::NT)) __maxnreg__((KC6<P,
                     // TMA: one element per lane into its padded slot (u lanes 0-15, nu 16-31)
                     constexpr unsigned EB = NPE * 8u;
                     if (lane == 0) {
-                        const unsigned bytes = (MODE == 0 ? 16u * EB : 0u) + (VARNU ? 16u * EB : 0u);
+                        const unsigned bytes = (MODE != 1 ? 16u * EB : 0u) + (VARNU ? 16u * EB : 0u);
                         if (bytes) mbar_expect_tx(&bar[buf], bytes);
                     }
                     __syncwarp();
                     const int el = lane & 15;
                     const long long ge = eb + (el & 3) + s1 * (el >> 2);
                     const int so = (el & 3) * SE + (el >> 2) * K::SY;
-                    if (lane < 16 && MODE == 0) tma_load(su + so, a.u + ge * NPE, EB, &bar[buf]);
+                    if (lane < 16 && MODE != 1) tma_load(su + so, a.u + ge * NPE, EB, &bar[buf]);
                     if (lane >= 16 && VARNU) tma_load(snu + so, a.nu + ge * NPE, EB, &bar[buf]);
                     // warm L2 with the next brick's x / y neighbour elements (4 single elements
                     // per x side, one contiguous x-row of 4 per y side)
@@ -569,7 +572,7 @@ __global__ void __launch_bounds__((KC6<P, VARNU, MODE>::NT)) __maxnreg__((KC6<P,
             }
         }
     }
-    if (MODE == 1) {
+    if (MODE >= 1) {  // dot epilogue: block partials of u.out and sum(out)
         double *red = sm + K::OFF_RED;
         const int lane = tid & 31, wid = tid >> 5;
         epi0 = warp_sum(epi0);

@@ -295,8 +295,9 @@ dg_status run_apply(dg_mesh *m, double lam, const double *nu, double nu_const, c
     a.zhi = zhi;
     const bool varnu = nu != nullptr;
     int grid = 0;
-    const cudaError_t e = m->g.dim == 3 ? launch_apply3(a, varnu, pro.on, &grid, 0, m->st)
-                                        : launch_apply2(a, varnu, pro.on, &grid, 0, m->st);
+    const int mode = pro.on ? 1 : (epi.partial ? 2 : 0);
+    const cudaError_t e = m->g.dim == 3 ? launch_apply3(a, varnu, mode, &grid, 0, m->st)
+                                        : launch_apply2(a, varnu, mode, &grid, 0, m->st);
     CK(e);
     if (grid_out) *grid_out = grid;
     m->launches += 1;
@@ -392,13 +393,30 @@ dg_status pcg_impl(dg_mesh *m, double lam, const double *nu, double nu_const, co
     CK(cudaMemsetAsync(m->pa, 0, sizeof(double) * (size_t)m->ndof, m->st));
 
     double *p_old = m->pa, *p_new = m->pb;
+    // split PCG step (pupd kernel + apply with the dot epilogue) where the v6 apply runs:
+    // measured faster than the fused prologue of v5
+    const bool split = !multi && g.dim == 3 && apply3_split_pcg_ok(g, nu) && !getenv("DG_PCG_FUSED");
     int chunk = 4;
     for (;;) {
         CK(cudaMemcpyAsync(m->hscal, m->scal, sizeof(PcgScal), cudaMemcpyDeviceToHost, m->st));
         CK(cudaStreamSynchronize(m->st));
         if (m->hscal->done) break;
         for (int it = 0; it < chunk; ++it) {
-            if (!multi) {
+            if (split) {
+                // p = z + beta p (in place) ; q = A p with the dot epilogue (apply MODE 2)
+                CK(launch_pcg_pupd(g, p_old, m->z, m->scal, m->st));
+                m->launches += 1;
+                PProl pro;
+                pro.done = &m->scal->done;
+                DotEpi epi;
+                epi.partial = m->partial;
+                int grid = 0;
+                CKS(run_apply(m, lam, nu, nu_const, p_old, m->q, Halo{}, epi, pro, &grid));
+                CKS(reduce_fin(m, grid, FIN_ALPHA));
+                CK(launch_pcg_update(g, u, m->r, p_old, m->q, m->dinv, m->z, m->mass_e, m->scal, m->partial, m->st));
+                m->launches += 1;
+                CKS(reduce_fin(m, VG, FIN_BETA));
+            } else if (!multi) {
                 // q = A p with p = dinv r + beta p_old (prologue), partials p.q, sum q (epilogue)
                 PProl pro;
                 pro.on = true;

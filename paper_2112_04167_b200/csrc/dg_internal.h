@@ -117,9 +117,10 @@ struct ConvParams {
 
 // apply2.cu / apply3.cu / convect.cu
 // grid: out, the number of CTAs launched (persistent; <= 148 x 8)
-cudaError_t launch_apply2(const ApplyParams &a, bool varnu, bool pcg, int *grid, int smem, cudaStream_t st);
-cudaError_t launch_apply3(const ApplyParams &a, bool varnu, bool pcg, int *grid, int smem, cudaStream_t st);
+cudaError_t launch_apply2(const ApplyParams &a, bool varnu, int mode, int *grid, int smem, cudaStream_t st);
+cudaError_t launch_apply3(const ApplyParams &a, bool varnu, int mode, int *grid, int smem, cudaStream_t st);
 bool apply3_ranges_ok(const Geom &g);  // layer-range applies available (pipelined host call)
+bool apply3_split_pcg_ok(const Geom &g, const double *nu);  // apply MODE 2 (dot epilogue) available
 cudaError_t launch_diag2(const Geom &g, double lam, const double *nu, double nuc, const Halo &h, double *d,
                          cudaStream_t st);
 cudaError_t launch_diag3(const Geom &g, double lam, const double *nu, double nuc, const Halo &h, double *d,
