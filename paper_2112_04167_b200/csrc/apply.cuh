@@ -95,6 +95,68 @@ namespace dg {
 // line operator on the unit vector (the neighbour line is e_I itself when the element is
 // its own periodic neighbour, N_d = 1, else zero).  One thread per node.
 // ---------------------------------------------------------------------------
+// Closed-form Jacobi diagonal for meshes with N_d > 1 in every direction:
+// per direction d of node I (index i along d):
+//   W_perp [ (2/h) sum_k w_k nu_k D_ki^2  + [i == P] (-nu_P (2/h) D_PP + tau (nu_P + nu_R)/2)
+//                                         + [i == 0] ( nu_0 (2/h) D_00 + tau (nu_0 + nu_L)/2) ]
+// plus lam m_I.  One CTA per element (grid-stride), the element's nu and the 1-D tables in
+// shared memory (per-lane table indices would serialise constant-cache reads).
+// invert: write 1/diag (the Jacobi preconditioner of the PCG) instead of diag.
+template <int DIM, int P, bool VARNU>
+__global__ void __launch_bounds__(256) k_diag_cf(const Geom g, double lam, const double *nu, double nu_const,
+                                                 Halo halo, double *diag, int invert)
+{
+    using C = Cfg<DIM, P>;
+    constexpr int n = C::n, NPE = C::NPE;
+    const DevTab &T = c_tab[P];
+    __shared__ double swd2[n * n], sw[n], sdd[n], snu[VARNU ? NPE : 1];
+    for (int q = threadIdx.x; q < n * n; q += blockDim.x) {
+        const int k = q / n, i = q % n;
+        swd2[q] = T.w[k] * T.D[k][i] * T.D[k][i];
+        if (q < n) {
+            sw[q] = T.w[q];
+            sdd[q] = T.D[q][q];
+        }
+    }
+    for (long long e = blockIdx.x; e < g.nel; e += gridDim.x) {
+        __syncthreads();
+        if (VARNU)
+            for (int q = threadIdx.x; q < NPE; q += blockDim.x) snu[q] = nu[e * NPE + q];
+        __syncthreads();
+        const int ec[3] = {(int)(e % g.Nl[0]), (int)((e / g.Nl[0]) % g.Nl[1]),
+                           DIM == 3 ? (int)(e / ((long long)g.Nl[0] * g.Nl[1])) : 0};
+        for (int q = threadIdx.x; q < NPE; q += blockDim.x) {
+            const int qc[3] = {q % n, (q / n) % n, DIM == 3 ? q / (n * n) : 0};
+            double m = g.mfac;
+#pragma unroll
+            for (int d = 0; d < DIM; ++d) m *= sw[qc[d]];
+            double dg = lam * m;
+#pragma unroll
+            for (int D = 0; D < DIM; ++D) {
+                const int GS = D == 0 ? 1 : (D == 1 ? n : n * n);
+                const int i = qc[D];
+                const int goff = q - i * GS;
+                const double sd = g.sd[D];
+                double acc = 0.0;
+#pragma unroll
+                for (int k = 0; k < n; ++k) acc = fma(swd2[k * n + i], VARNU ? snu[goff + k * GS] : nu_const, acc);
+                acc *= sd;
+                if (i == P || i == 0) {
+                    int cn[3] = {ec[0], ec[1], ec[2]};
+                    cn[D] += (i == P) ? 1 : -1;
+                    const double nown = VARNU ? snu[q] : nu_const;
+                    const double nnb = VARNU ? __ldg(elem_ptr(g, nu, halo.nu_lo, halo.nu_hi, cn[0], cn[1], cn[2]) + goff +
+                                                      (i == P ? 0 : P * GS))
+                                             : nu_const;
+                    acc += (i == P ? -1.0 : 1.0) * nown * sd * sdd[i] + 0.5 * g.tau[D] * (nown + nnb);
+                }
+                dg += (m / (sw[i] * 0.5 * g.h[D])) * acc;  // W_perp = m / (w_i h_d / 2)
+            }
+            diag[e * NPE + q] = invert ? 1.0 / dg : dg;
+        }
+    }
+}
+
 template <int DIM, int P, bool VARNU>
 __global__ void __launch_bounds__(256) k_diag(const Geom g, double lam, const double *nu, double nu_const,
                                               Halo halo, double *diag)
@@ -411,9 +473,18 @@ struct ApplyDispatch {
     }
     template <int P>
     static cudaError_t diag_p(const Geom &g, double lam, const double *nu, double nuc, const Halo &h, double *d,
-                              cudaStream_t st)
+                              int invert, cudaStream_t st)
     {
         const long long tot = g.nel * Cfg<DIM, P>::NPE;
+        bool self = false;
+        for (int dd = 0; dd < DIM; ++dd) self = self || g.N[dd] == 1;
+        if (!self) {  // closed form, one CTA per element (grid-stride)
+            const long long blocks = g.nel < 148LL * 16 ? g.nel : 148LL * 16;
+            if (nu) k_diag_cf<DIM, P, true><<<(int)blocks, 256, 0, st>>>(g, lam, nu, nuc, h, d, invert);
+            else k_diag_cf<DIM, P, false><<<(int)blocks, 256, 0, st>>>(g, lam, nu, nuc, h, d, invert);
+            return cudaGetLastError();
+        }
+        if (invert) return cudaErrorInvalidValue;  // N_d = 1 meshes: caller inverts separately
         long long blocks = (tot + 255) / 256;
         if (blocks > 148 * 64) blocks = 148 * 64;
         if (nu) k_diag<DIM, P, true><<<(int)blocks, 256, 0, st>>>(g, lam, nu, nuc, h, d);
@@ -421,19 +492,19 @@ struct ApplyDispatch {
         return cudaGetLastError();
     }
     static cudaError_t diag(const Geom &g, double lam, const double *nu, double nuc, const Halo &h, double *d,
-                            cudaStream_t st)
+                            int invert, cudaStream_t st)
     {
         switch (g.P) {
-        case 1: if constexpr (DG_HAS_P(1)) return diag_p<1>(g, lam, nu, nuc, h, d, st); else return cudaErrorNotSupported;
-        case 2: if constexpr (DG_HAS_P(2)) return diag_p<2>(g, lam, nu, nuc, h, d, st); else return cudaErrorNotSupported;
-        case 3: if constexpr (DG_HAS_P(3)) return diag_p<3>(g, lam, nu, nuc, h, d, st); else return cudaErrorNotSupported;
-        case 4: if constexpr (DG_HAS_P(4)) return diag_p<4>(g, lam, nu, nuc, h, d, st); else return cudaErrorNotSupported;
-        case 5: if constexpr (DG_HAS_P(5)) return diag_p<5>(g, lam, nu, nuc, h, d, st); else return cudaErrorNotSupported;
-        case 6: if constexpr (DG_HAS_P(6)) return diag_p<6>(g, lam, nu, nuc, h, d, st); else return cudaErrorNotSupported;
-        case 7: if constexpr (DG_HAS_P(7)) return diag_p<7>(g, lam, nu, nuc, h, d, st); else return cudaErrorNotSupported;
-        case 8: if constexpr (DG_HAS_P(8)) return diag_p<8>(g, lam, nu, nuc, h, d, st); else return cudaErrorNotSupported;
-        case 9: if constexpr (DG_HAS_P(9)) return diag_p<9>(g, lam, nu, nuc, h, d, st); else return cudaErrorNotSupported;
-        case 10: if constexpr (DG_HAS_P(10)) return diag_p<10>(g, lam, nu, nuc, h, d, st); else return cudaErrorNotSupported;
+        case 1: if constexpr (DG_HAS_P(1)) return diag_p<1>(g, lam, nu, nuc, h, d, invert, st); else return cudaErrorNotSupported;
+        case 2: if constexpr (DG_HAS_P(2)) return diag_p<2>(g, lam, nu, nuc, h, d, invert, st); else return cudaErrorNotSupported;
+        case 3: if constexpr (DG_HAS_P(3)) return diag_p<3>(g, lam, nu, nuc, h, d, invert, st); else return cudaErrorNotSupported;
+        case 4: if constexpr (DG_HAS_P(4)) return diag_p<4>(g, lam, nu, nuc, h, d, invert, st); else return cudaErrorNotSupported;
+        case 5: if constexpr (DG_HAS_P(5)) return diag_p<5>(g, lam, nu, nuc, h, d, invert, st); else return cudaErrorNotSupported;
+        case 6: if constexpr (DG_HAS_P(6)) return diag_p<6>(g, lam, nu, nuc, h, d, invert, st); else return cudaErrorNotSupported;
+        case 7: if constexpr (DG_HAS_P(7)) return diag_p<7>(g, lam, nu, nuc, h, d, invert, st); else return cudaErrorNotSupported;
+        case 8: if constexpr (DG_HAS_P(8)) return diag_p<8>(g, lam, nu, nuc, h, d, invert, st); else return cudaErrorNotSupported;
+        case 9: if constexpr (DG_HAS_P(9)) return diag_p<9>(g, lam, nu, nuc, h, d, invert, st); else return cudaErrorNotSupported;
+        case 10: if constexpr (DG_HAS_P(10)) return diag_p<10>(g, lam, nu, nuc, h, d, invert, st); else return cudaErrorNotSupported;
         default: return cudaErrorInvalidValue;
         }
     }

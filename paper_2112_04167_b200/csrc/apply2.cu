@@ -10,8 +10,8 @@ cudaError_t launch_apply2(const ApplyParams &a, bool varnu, int mode, int *grid,
     return ApplyDispatch<2>::apply(a, varnu, mode, grid, smem, st);
 }
 cudaError_t launch_diag2(const Geom &g, double lam, const double *nu, double nuc, const Halo &h, double *d,
-                         cudaStream_t st)
+                         cudaStream_t st, int invert)
 {
-    return ApplyDispatch<2>::diag(g, lam, nu, nuc, h, d, st);
+    return ApplyDispatch<2>::diag(g, lam, nu, nuc, h, d, invert, st);
 }
 }  // namespace dg

@@ -12,9 +12,9 @@ cudaError_t launch_apply3(const ApplyParams &a, bool varnu, int mode, int *grid,
 bool apply3_ranges_ok(const Geom &g) { return ApplyDispatch<3>::ranges_ok(g); }
 bool apply3_split_pcg_ok(const Geom &g, const double *nu) { return ApplyDispatch<3>::split_pcg_ok(g, nu); }
 cudaError_t launch_diag3(const Geom &g, double lam, const double *nu, double nuc, const Halo &h, double *d,
-                         cudaStream_t st)
+                         cudaStream_t st, int invert)
 {
-    return ApplyDispatch<3>::diag(g, lam, nu, nuc, h, d, st);
+    return ApplyDispatch<3>::diag(g, lam, nu, nuc, h, d, invert, st);
 }
 }  // namespace dg
 

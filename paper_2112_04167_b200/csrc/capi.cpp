@@ -369,10 +369,25 @@ dg_status pcg_impl(dg_mesh *m, double lam, const double *nu, double nu_const, co
     s0.maxit = maxit;
     CK(cudaMemcpyAsync(m->scal, &s0, sizeof(s0), cudaMemcpyHostToDevice, m->st));
 
-    // Jacobi preconditioner
-    CKS(diag_impl(m, lam, nu, nu_const, m->q));
-    CK(launch_recip(g, m->q, m->dinv, m->st));
-    m->launches += 1;
+    // Jacobi preconditioner: D^-1 straight from the closed-form kernel where it applies
+    bool self = false;
+    for (int d = 0; d < g.dim; ++d) self = self || g.N[d] == 1;
+    if (!self) {
+        Halo hd;
+        if (multi && nu) {
+            CKS(ensure_halos(m, false));
+            CKS(exchange(m, nu, m->hn_lo, m->hn_hi));
+            hd.nu_lo = m->hn_lo;
+            hd.nu_hi = m->hn_hi;
+        }
+        CK(g.dim == 3 ? launch_diag3(g, lam, nu, nu_const, hd, m->dinv, m->st, 1)
+                      : launch_diag2(g, lam, nu, nu_const, hd, m->dinv, m->st, 1));
+        m->launches += 1;
+    } else {
+        CKS(diag_impl(m, lam, nu, nu_const, m->q));
+        CK(launch_recip(g, m->q, m->dinv, m->st));
+        m->launches += 1;
+    }
     Halo hnu;
     if (multi && nu) {  // diag_impl exchanged nu already
         hnu.nu_lo = m->hn_lo;

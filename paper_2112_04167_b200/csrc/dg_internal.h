@@ -121,10 +121,11 @@ cudaError_t launch_apply2(const ApplyParams &a, bool varnu, int mode, int *grid,
 cudaError_t launch_apply3(const ApplyParams &a, bool varnu, int mode, int *grid, int smem, cudaStream_t st);
 bool apply3_ranges_ok(const Geom &g);  // layer-range applies available (pipelined host call)
 bool apply3_split_pcg_ok(const Geom &g, const double *nu);  // apply MODE 2 (dot epilogue) available
+// invert != 0: write 1/diag (closed-form meshes only; cudaErrorInvalidValue otherwise)
 cudaError_t launch_diag2(const Geom &g, double lam, const double *nu, double nuc, const Halo &h, double *d,
-                         cudaStream_t st);
+                         cudaStream_t st, int invert = 0);
 cudaError_t launch_diag3(const Geom &g, double lam, const double *nu, double nuc, const Halo &h, double *d,
-                         cudaStream_t st);
+                         cudaStream_t st, int invert = 0);
 cudaError_t launch_convect_k(const ConvParams &a, cudaStream_t st);
 cudaError_t launch_coords(const Geom &g, long long el_offset, double *xyz, cudaStream_t st);
 cudaError_t launch_mass(const Geom &g, double *mass, cudaStream_t st);
