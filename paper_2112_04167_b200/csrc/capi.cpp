@@ -418,8 +418,9 @@ dg_status pcg_impl(dg_mesh *m, double lam, const double *nu, double nu_const, co
         if (m->hscal->done) break;
         for (int it = 0; it < chunk; ++it) {
             if (split) {
-                // p = z + beta p (in place) ; q = A p with the dot epilogue (apply MODE 2)
-                CK(launch_pcg_pupd(g, p_old, m->z, m->scal, m->st));
+                // x += alpha p, p = z + beta p (in place; x deferred by one iteration) ;
+                // q = A p with the dot epilogue (apply MODE 2) ; r, z update
+                CK(launch_pcg_pupd_x(g, u, p_old, m->z, m->scal, m->st));
                 m->launches += 1;
                 PProl pro;
                 pro.done = &m->scal->done;
@@ -428,7 +429,7 @@ dg_status pcg_impl(dg_mesh *m, double lam, const double *nu, double nu_const, co
                 int grid = 0;
                 CKS(run_apply(m, lam, nu, nu_const, p_old, m->q, Halo{}, epi, pro, &grid));
                 CKS(reduce_fin(m, grid, FIN_ALPHA));
-                CK(launch_pcg_update(g, u, m->r, p_old, m->q, m->dinv, m->z, m->mass_e, m->scal, m->partial, m->st));
+                CK(launch_pcg_update_nox(g, m->r, m->q, m->dinv, m->z, m->mass_e, m->scal, m->partial, m->st));
                 m->launches += 1;
                 CKS(reduce_fin(m, VG, FIN_BETA));
             } else if (!multi) {
@@ -468,6 +469,10 @@ dg_status pcg_impl(dg_mesh *m, double lam, const double *nu, double nu_const, co
             }
         }
         chunk = std::min(chunk * 2, 32);
+    }
+    if (split) {  // the deferred x update of the last iteration
+        CK(launch_pcg_xfinal(g, u, p_old, m->scal, m->st));
+        m->launches += 1;
     }
     // lam == 0: zero mass-weighted mean of u
     if (lam == 0.0) {

@@ -178,6 +178,11 @@ cudaError_t launch_reduce_s(const double *partial, int G, int K, double *sums, c
 cudaError_t launch_reduce_fin(const double *partial, int G, int K, double *sums, int mode, PcgScal *s, double *hist,
                               double *aux, cudaStream_t st);
 cudaError_t launch_pcg_pupd(const Geom &g, double *p, const double *z, const PcgScal *s, cudaStream_t st);
+// split step with the x update deferred by one iteration (single rank)
+cudaError_t launch_pcg_pupd_x(const Geom &g, double *x, double *p, const double *z, const PcgScal *s, cudaStream_t st);
+cudaError_t launch_pcg_update_nox(const Geom &g, double *r, const double *q, const double *dinv, double *z,
+                                  const double *mass_e, const PcgScal *s, double *partial, cudaStream_t st);
+cudaError_t launch_pcg_xfinal(const Geom &g, double *x, const double *p, const PcgScal *s, cudaStream_t st);
 cudaError_t launch_dot_pq(const Geom &g, const double *p, const double *q, const PcgScal *s, double *partial,
                           cudaStream_t st);
 cudaError_t launch_recip(const Geom &g, const double *d, double *dinv, cudaStream_t st);

@@ -95,6 +95,50 @@ __global__ void k_pcg_update(long long ndof, int npe, double *__restrict__ x, do
     write_partials<2>(v, partial);
 }
 
+// split single-rank step, x update deferred by one iteration (saves a read and a write of
+// p and x in the update pass): x += alpha_{k-1} p_{k-1}, then p_k = z_k + beta_{k-1} p_{k-1}
+__global__ void k_pcg_pupd_x(long long ndof, double *__restrict__ x, double *__restrict__ p,
+                             const double *__restrict__ z, const PcgScal *s)
+{
+    if (s->done) return;
+    const double alpha = s->alpha, beta = s->beta;  // alpha = 0 before the first iteration
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < ndof; i += (long long)gridDim.x * blockDim.x) {
+        const double pi = p[i];
+        x[i] = fma(alpha, pi, x[i]);
+        p[i] = fma(beta, pi, z[i]);
+    }
+}
+
+// r -= alpha (q - qmean) ; z = dinv r ; partials r.z, sum (r/m)^2   (x deferred, see above)
+__global__ void k_pcg_update_nox(long long ndof, int npe, double *__restrict__ r, const double *__restrict__ q,
+                                 const double *__restrict__ dinv, double *__restrict__ z,
+                                 const double *__restrict__ me, const PcgScal *s, double *partial)
+{
+    if (s->done) return;
+    const double alpha = s->alpha, qmean = s->qmean;
+    double v[2] = {0.0, 0.0};
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < ndof; i += (long long)gridDim.x * blockDim.x) {
+        const double m = __ldg(me + (int)(i % npe));
+        const double ri = fma(-alpha, q[i] - qmean, r[i]);
+        r[i] = ri;
+        const double zi = dinv[i] * ri;
+        z[i] = zi;
+        v[0] = fma(ri, zi, v[0]);
+        const double rm = ri / m;
+        v[1] = fma(rm, rm, v[1]);
+    }
+    write_partials<2>(v, partial);
+}
+
+// the deferred last x update: x += alpha_k p_k once the loop stopped after an update pass
+__global__ void k_pcg_xfinal(long long ndof, double *__restrict__ x, const double *__restrict__ p, const PcgScal *s)
+{
+    if (s->iter < 1 || (s->status != PCG_ST_CONV && s->status != PCG_ST_MAXIT)) return;
+    const double alpha = s->alpha;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < ndof; i += (long long)gridDim.x * blockDim.x)
+        x[i] = fma(alpha, p[i], x[i]);
+}
+
 // p = z + beta p (multi-rank path, where the apply prologue is not used)
 __global__ void k_pcg_pupd(long long ndof, double *__restrict__ p, const double *__restrict__ z, const PcgScal *s)
 {
@@ -303,6 +347,25 @@ cudaError_t launch_pcg_update(const Geom &g, double *x, double *r, const double 
 cudaError_t launch_pcg_pupd(const Geom &g, double *p, const double *z, const PcgScal *s, cudaStream_t st)
 {
     k_pcg_pupd<<<vec_grid(), 256, 0, st>>>(nd(g), p, z, s);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_pcg_pupd_x(const Geom &g, double *x, double *p, const double *z, const PcgScal *s, cudaStream_t st)
+{
+    k_pcg_pupd_x<<<vec_grid(), 256, 0, st>>>(nd(g), x, p, z, s);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_pcg_update_nox(const Geom &g, double *r, const double *q, const double *dinv, double *z,
+                                  const double *mass_e, const PcgScal *s, double *partial, cudaStream_t st)
+{
+    k_pcg_update_nox<<<vec_grid(), 256, 0, st>>>(nd(g), g.npe, r, q, dinv, z, mass_e, s, partial);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_pcg_xfinal(const Geom &g, double *x, const double *p, const PcgScal *s, cudaStream_t st)
+{
+    k_pcg_xfinal<<<vec_grid(), 256, 0, st>>>(nd(g), x, p, s);
     return cudaGetLastError();
 }
 

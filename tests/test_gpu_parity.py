@@ -275,6 +275,23 @@ def test_pcg_v6_shapes(P, lam):
     assert rel(H(u), ref) <= 1e-9
 
 
+def test_pcg_v6_maxit_iterate():
+    # split path with the deferred x update: a run stopped by maxit must return the k-th
+    # CG iterate (compared with the oracle's Jacobi-PCG stopped after the same k)
+    dim, N, L, P = 3, (4, 4, 4), (1.0, 1.1, 1.2), 5
+    m, om = meshes(dim, N, L, P)
+    rng = np.random.default_rng(31)
+    f = rng.uniform(-1, 1, (om.n_el, om.npe))
+    nu = 0.5 + rng.uniform(0, 1, (om.n_el, om.npe))
+    for k in (1, 3, 6):
+        u = torch.zeros(f.shape, dtype=torch.float64, device=DEV)
+        info = dg.dg_pcg_solve(m, 2.0, T(nu), 0.0, T(f), 1e-14, k, u, raise_on_notconv=False)
+        assert info.iters == k
+        ref, it, *_ = oracle.pcg_solve(om, 2.0, f, nu=nu, tol=1e-30, maxit=k)
+        assert it == k
+        assert rel(H(u), ref) <= 1e-10, (k, rel(H(u), ref))
+
+
 def test_pcg_notconv_and_einval():
     c = config(1)
     m, om = cfg_mesh(c)
