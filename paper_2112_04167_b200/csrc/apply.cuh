@@ -384,7 +384,7 @@ struct ApplyDispatch {
         a.u = nu ? nu : reinterpret_cast<const double *>(256);  // alignment probe only
         a.nu = nu;
         a.zhi = -1;
-        return v6_ok(a, false);
+        return v6_ok(a, false) || v5_ok(a, false);
     }
     static bool ranges_ok(const Geom &g)
     {
@@ -442,10 +442,11 @@ struct ApplyDispatch {
     template <int P>
     static cudaError_t go_p(const ApplyParams &a, bool varnu, int mode, int *grid, cudaStream_t st)
     {
-        if (mode == 2) {  // dot epilogue only: v6 meshes (split PCG path)
+        if (mode == 2) {  // dot epilogue only (split PCG path): 3-D meshes the v6 or v5 kernel runs
             if constexpr (DIM == 3) {
-                if (!v6_ok(a, false)) return cudaErrorNotSupported;
-                return varnu ? go6<P, true, 2>(a, grid, st) : go6<P, false, 2>(a, grid, st);
+                if (v6_ok(a, false)) return varnu ? go6<P, true, 2>(a, grid, st) : go6<P, false, 2>(a, grid, st);
+                if (v5_ok(a, false)) return varnu ? go5<P, true, 2>(a, grid, st) : go5<P, false, 2>(a, grid, st);
+                return cudaErrorNotSupported;
             } else {
                 return cudaErrorNotSupported;
             }

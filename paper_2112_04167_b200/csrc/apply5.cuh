@@ -263,7 +263,7 @@ __device__ __forceinline__ void cpass(const ApplyParams &a, const DevTab &T, con
             zc.po[i * SS[D]] = zc.o[i] + d;
             s1 += d;
         }
-        if (K::MODE == 1) {
+        if (K::MODE >= 1) {
             epi0 = fma(W, fma(c, zc.gP, f0 * zc.u), epi0);  // sum_i v_i dr_i W
             epi1 += s1;
         }
@@ -293,7 +293,7 @@ __device__ __forceinline__ void cpass(const ApplyParams &a, const DevTab &T, con
                 const double o = fma(lw * T.w[i], ui, fma(W, r[i], pa[i * SS[D]]));
                 if (ZC && hold) zc.o[i] = o;
                 else po[i * SS[D]] = o;
-                if (K::MODE == 1) {
+                if (K::MODE >= 1) {
                     epi0 = fma(ui, o, epi0);
                     epi1 += o;
                 }
@@ -469,7 +469,7 @@ __global__ void __launch_bounds__((KC5<P, VARNU, MODE>::NT)) __maxnreg__((KC5<P,
     // full[0..1] (producers + TMA bytes), empty[0..1] (consumers)
     uint64_t *bar = reinterpret_cast<uint64_t *>(sm + K::OFF_BAR);
     const int tid = threadIdx.x;
-    if (MODE == 1 && *a.pro.done) return;
+    if (MODE >= 1 && *a.pro.done) return;  // PCG converged: nothing to do
     const double beta = MODE == 1 ? *a.pro.beta : 0.0;
     if (tid == 0) {
         mbar_init(&bar[0], NP);
@@ -504,12 +504,12 @@ __global__ void __launch_bounds__((KC5<P, VARNU, MODE>::NT)) __maxnreg__((KC5<P,
                 const long long eb = e0[0] + s1 * e0[1] + s2 * e0[2];
                 constexpr unsigned CH = 2u * NPE * 8u;  // bytes of one x-pair of elements
                 if (ptid == 0) {
-                    const unsigned bytes = (MODE == 0 ? 4u * CH : 0u) + (VARNU ? 4u * CH : 0u);
+                    const unsigned bytes = (MODE != 1 ? 4u * CH : 0u) + (VARNU ? 4u * CH : 0u);
                     if (bytes) mbar_expect_tx(&bar[buf], bytes);
 #pragma unroll
                     for (int q = 0; q < 4; ++q) {  // (y, z) rows of the brick; x pairs contiguous
                         const long long ge = eb + (q & 1) * s1 + (q >> 1) * s2;
-                        if (MODE == 0) tma_load(su + q * 2 * NPE, a.u + ge * NPE, CH, &bar[buf]);
+                        if (MODE != 1) tma_load(su + q * 2 * NPE, a.u + ge * NPE, CH, &bar[buf]);
                         if (VARNU) tma_load(snu + q * 2 * NPE, a.nu + ge * NPE, CH, &bar[buf]);
                     }
                 }
@@ -585,7 +585,7 @@ __global__ void __launch_bounds__((KC5<P, VARNU, MODE>::NT)) __maxnreg__((KC5<P,
             }
         }
     }
-    if (MODE == 1) {
+    if (MODE >= 1) {  // dot epilogue: block partials of u.out and sum(out)
         double *red = sm + K::OFF_RED;
         const int lane = tid & 31, wid = tid >> 5;
         epi0 = warp_sum(epi0);
