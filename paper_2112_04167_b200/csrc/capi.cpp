@@ -754,7 +754,7 @@ dg_status dg_helmholtz_apply_host(dg_mesh *m, double lam, const double *nu_host,
     int C = 0;
     if (m->nranks == 1 && g.dim == 3 && apply3_ranges_ok(g)) {
         const int nbz = g.Nl[2] / 2;
-        for (int c = 8; c >= 3; --c)
+        for (int c = 16; c >= 3; --c)
             if (nbz % c == 0) {
                 C = c;
                 break;
