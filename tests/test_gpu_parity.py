@@ -153,6 +153,26 @@ def test_apply_configs_sampled(cid):
     assert np.abs(o - c.lam * ms).max() <= 1e-12 * np.abs(c.lam * ms).max()
 
 
+def test_pcg_c5_full_size_residual():
+    # BASELINE configs[4] at full size in the bench's launch configuration (split PCG,
+    # v6 apply): the solution's residual, recomputed on sampled elements with the ORACLE's
+    # operator, meets the tolerance (reading A7; SURVEY Q14 residual cross-check)
+    c = config(5)
+    m, om = cfg_mesh(c)
+    f = c.rhs(0)
+    nu = c.nu()
+    u = torch.zeros(f.shape, dtype=torch.float64, device=DEV)
+    info = dg.dg_pcg_solve(m, c.lam, T(nu), c.nu0, T(f), c.tol, 2000, u)
+    assert info.rel_res <= c.tol and 10 <= info.iters <= 40
+    uh = H(u)
+    el = sample_elements(c.N, 3, 64, 55)
+    au = oracle.sip_apply(om, c.lam, uh, nu=nu, elems=el)
+    mass = oracle.mass(om)[el]
+    res = (mass * f[el] - au) / mass  # M^-1 (M f - A u) on the sampled rows
+    # per-row RMS ratio within a small factor of the global stopping test
+    assert np.linalg.norm(res) / np.linalg.norm(f[el]) <= 20 * c.tol
+
+
 def test_apply_deterministic_and_host_variant():
     c = config(3)
     m, om = cfg_mesh(c)
