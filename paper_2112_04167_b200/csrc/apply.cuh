@@ -150,7 +150,11 @@ __global__ void __launch_bounds__(256) k_diag_cf(const Geom g, double lam, const
                                              : nu_const;
                     acc += (i == P ? -1.0 : 1.0) * nown * sd * sdd[i] + 0.5 * g.tau[D] * (nown + nnb);
                 }
-                dg += (m / (sw[i] * 0.5 * g.h[D])) * acc;  // W_perp = m / (w_i h_d / 2)
+                double W = g.wfac[D];  // W_perp = prod_{d != D} w_{q_d} h_d / 2 (no division)
+#pragma unroll
+                for (int d = 0; d < DIM; ++d)
+                    if (d != D) W *= sw[qc[d]];
+                dg += W * acc;
             }
             diag[e * NPE + q] = invert ? 1.0 / dg : dg;
         }
