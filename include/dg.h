@@ -116,23 +116,42 @@ dg_status dg_pcg_solve(dg_mesh *m, double lam, const double *nu, double nu_const
  * out must not alias v. */
 dg_status dg_convect_rhs(dg_mesh *m, const double *const v[3], double *const out[3]);
 
+/* DG divergence / gradient pair of the projection step (Alg. 3 lines 5-6; SURVEY
+ * NEXT-1).  mv: velocity mesh (degree P >= 2), mp: pressure mesh with the same dim, N, L,
+ * rank/nranks and degree P-1.  Integrals on the velocity GLL grid (exact for these
+ * integrands), central fluxes {.} = (minus + plus)/2, [.] = minus - plus, n from the minus to
+ * the plus element:
+ *   dg_divergence: div_weak_a = -sum_K sum_q W_q v(x_q).grad phi^p_a(x_q)
+ *                               + sum_F sum_q W^F_q ({v}.n)[phi^p_a]        (pressure layout)
+ *   dg_gradient:   grad_weak_{c,i} = -sum_K sum_q W_q psi_h(x_q) d_c phi^v_i(x_q)
+ *                               + sum_F sum_q W^F_q {psi_h} n_c [phi^v_i]   (velocity layout)
+ * with psi_h the pressure interpolant at the velocity nodes.  -grad is the transpose of div;
+ * both are exact (= the weak forms of div v and grad psi) for continuous polynomial fields of
+ * degree <= P-1.  Weak vectors: nodal values are M^-1 times them.  DEVICE arrays; the call
+ * runs on mv's stream; collective for multi-rank meshes (face halos over NCCL).  The
+ * div/mass-flux stabilisation of P:1040 is not part of the pair (its formula is not in the
+ * paper). */
+dg_status dg_divergence(dg_mesh *mv, dg_mesh *mp, const double *const v[3], double *div_weak);
+dg_status dg_gradient(dg_mesh *mp, dg_mesh *mv, const double *psi, double *const grad_weak[3]);
+
 /* One IMEX-RK stage i = 2 of Alg. 3 for constant viscosity nu, F_s = 0 and
  * periodic boundaries (the config-4 composition):
  *   line 4: v' = v + dt a_ex21 (F_c(v) + F_d1(v)),  F_c by dg_convect_rhs (LLF),
  *           F_d1 = -M^-1 A_0 v (the SIP operator at lam = 0, P:693 F_d1 = div nu grad v);
  *           the grad-div terms F_d2 + F_d3 (they cancel the divergence part) are not formed;
- *   line 5: -lap psi = -div v' on the pressure mesh mp (degree P-1; reading A9) with
- *           the STAND-IN rhs of SURVEY a8: the broken (element-local collocation) divergence of
- *           v' interpolated to the pressure GLL nodes; solved by dg_pcg_solve (lam = 0: mean
- *           projection, reading A8) from psi = 0;
- *   line 6: v'' = v' (the DG gradient projection is SURVEY NEXT-1, not built);
+ *   line 5: -lap psi = -div v' on the pressure mesh mp (degree P-1; reading A9):
+ *           SIP Poisson with the weak DG divergence of v' as rhs (b = -D v'), solved
+ *           by dg_pcg_solve (lam = 0: mean projection, reading A8) from psi = 0;
+ *   line 6: v'' = v' - M^-1 G psi with the weak DG gradient G (dg_gradient);
  *   line 8: g = v'' + dt (a_im21 - a_ex21) F_d1(v);
  *   line 9: per component, solve v - dt a_im22 nu lap v = g, i.e. lam = 1/(dt a_im22),
  *           f = lam g (reading A4), by dg_pcg_solve from the initial guess v''.
+ * The projection is approximate (the SIP pressure operator is not -D M^-1 G), as in the
+ * paper's splitting; the final projection (lines 12-15) is skipped for constant nu.
  * mv: velocity mesh (degree P >= 2); mp: pressure mesh with the same dim, N, L, rank/nranks
  * and degree P-1.  v[c], vout[c] (c < dim): DEVICE [local_ndof of mv], vout must not alias
  * v; psi: DEVICE [local_ndof of mp].  Runs on mv's stream; synchronous (it contains solves).
- * The stage workspace (dim+1 velocity fields, one pressure field) is allocated on first use
+ * The stage workspace (2 dim velocity fields, one pressure field) is allocated on first use
  * and owned by the meshes.  Errors: DG_EINVAL for mismatched meshes or non-positive dt,
  * a_im22, nu, tol or maxit; solver errors as dg_pcg_solve (info holds every solve). */
 typedef struct {

@@ -210,53 +210,160 @@ def mass(mesh: Mesh):
 # ---------------------------------------------------------------------------
 # IMEX-RK stage -- plain numpy composition of the functions above.
 # ---------------------------------------------------------------------------
-def _lagrange_matrix(P, xi, pts):
-    """B[a, j] = l_j(pts[a]), dB[a, j] = l_j'(pts[a]) on the nodes xi (product formula)."""
-    B = np.zeros((len(pts), P + 1))
-    dB = np.zeros((len(pts), P + 1))
-    for a, x in enumerate(pts):
-        B[a], dB[a] = lagrange(P, xi, x)
-    return B, dB
-
-
-def broken_divergence_p1(mesh: Mesh, v):
-    """Element-local (broken) collocation divergence of the nodal velocity v at the GLL
-    nodes of degree P, interpolated to the GLL nodes of degree P-1, returned as
-    [N_el, P^d] (pressure-mesh layout).  The stand-in Poisson rhs of SURVEY §8(a) a8:
-    div v (x_q) = sum_d (2/h_d) sum_j l_j'(xi_{q_d}) v_d(.., x_j, ..) at the velocity nodes,
-    then the degree-P interpolant evaluated at the degree-(P-1) nodes."""
-    P, dim, n = mesh.P, mesh.dim, mesh.P + 1
-    xi, _ = gll(P)
-    xp, _ = gll(P - 1)
-    _, Dm = _lagrange_matrix(P, xi, xi)        # Dm[i, j] = l_j'(xi_i)
-    Ip, _ = _lagrange_matrix(P, xi, xp)        # Ip[a, j] = l_j(xp_a)
-    shp = (mesh.n_el,) + (n,) * dim            # node axes (k, j, i): x last
-    div = np.zeros(shp)
-    for d in range(dim):
-        vd = np.asarray(v[d], dtype=np.float64).reshape(shp)
-        ax = dim - d                            # array axis of direction d
-        div += (2.0 * mesh.N[d] / mesh.L[d]) * np.moveaxis(np.tensordot(Dm, vd, axes=([1], [ax])), 0, ax)
-    for d in range(dim):
-        ax = dim - d
-        div = np.moveaxis(np.tensordot(Ip, div, axes=([1], [ax])), 0, ax)
-    return div.reshape(mesh.n_el, P ** dim)
-
-
 def imex_stage(mv: Mesh, mp: Mesh, dt, a_ex21, a_im21, a_im22, nu, v, tol=1e-14):
     """Alg. 3 stage i = 2, constant nu, F_s = 0, under the readings of
-    include/dg.h dg_imex_stage: returns (vout[dim], psi, v').  Exact discrete solves
+    include/dg.h dg_imex_stage: returns (vout[dim], psi, v'').  Exact discrete solves
     (oracle PCG to tol)."""
     dim = mv.dim
     m = mass(mv)
     Fc = convect(mv, v)                                                     # F_c(v)   (P:693)
     Fd = [-sip_apply(mv, 0.0, v[c], nu_const=nu) / m for c in range(dim)]  # F_d1(v) = -M^-1 A_0 v
     vp = [np.asarray(v[c]) + dt * a_ex21 * (Fc[c] + Fd[c]) for c in range(dim)]         # line 4
-    fp = -broken_divergence_p1(mv, vp)                                       # line 5 rhs: -div v'
+    fp = -dg_divergence_weak(mv, vp) / mass(mp)                             # line 5 rhs: b = -D v'
     psi, *_ = pcg_solve(mp, 0.0, fp, nu_const=1.0, tol=tol)                 # line 5 (lam = 0)
+    gw = dg_gradient_weak(mp, psi)
+    vpp = [vp[c] - gw[c] / m for c in range(dim)]                           # line 6
     lam = 1.0 / (dt * a_im22)
     out = []
     for c in range(dim):
-        g = vp[c] + dt * (a_im21 - a_ex21) * Fd[c]                          # line 8 (v'' = v')
+        g = vpp[c] + dt * (a_im21 - a_ex21) * Fd[c]                         # line 8
         u, *_ = pcg_solve(mv, lam, lam * g, nu_const=nu, tol=tol)           # line 9
         out.append(u)
-    return out, psi, vp
+    return out, psi, vpp
+
+
+# ---------------------------------------------------------------------------
+# DG divergence / gradient pair of the projection step (SURVEY §8(f) NEXT-1; Alg. 3 lines
+# 5-6, P:829-840): velocity degree P, pressure degree P-1 (P:1036), central fluxes,
+# integrals on the velocity GLL grid (exact for these integrands: degree <= 2P-1 per
+# direction).  Plain numpy; element loops, library tensor contractions as steps.
+# ---------------------------------------------------------------------------
+def _pv_tables(P):
+    """GLL nodes of P and P-1, velocity weights w, pressure basis at velocity nodes E[i, a]
+    and its derivative Ed[i, a], velocity derivative matrix Dv[i, j] (product formula)."""
+    xv, wv = gll(P)
+    xp, _ = gll(P - 1)
+    E = np.zeros((P + 1, P))
+    Ed = np.zeros((P + 1, P))
+    Dv = np.zeros((P + 1, P + 1))
+    for i, x in enumerate(xv):
+        E[i], Ed[i] = lagrange(P - 1, xp, x)
+        _, Dv[i] = lagrange(P, xv, x)
+    return xv, wv, E, Ed, Dv
+
+
+def _elem_coords(mesh, e):
+    N = mesh.N
+    return [e % N[0], (e // N[0]) % N[1], e // (N[0] * N[1])][: mesh.dim]
+
+
+def _elem_index(mesh, c):
+    N = mesh.N
+    c = [c[d] % N[d] for d in range(mesh.dim)]
+    return c[0] + N[0] * (c[1] + (N[1] * c[2] if mesh.dim == 3 else 0))
+
+
+def _apply_1d(M, arr, axis):
+    """Contract matrix M[out, in] with array axis `axis`."""
+    return np.moveaxis(np.tensordot(M, arr, axes=([1], [axis])), 0, axis)
+
+
+def dg_divergence_weak(mv: Mesh, v):
+    """d_a = -sum_K sum_q W_q v(x_q).grad phi^p_a(x_q) + sum_F sum_q W^F_q ({v}.n)[phi^p_a],
+    the weak DG divergence of the nodal velocity v (dim arrays [N_el, (P+1)^d]) tested with
+    the degree-(P-1) pressure basis; returns [N_el, P^d] (pressure-mesh layout)."""
+    P, dim = mv.P, mv.dim
+    n, m = P + 1, P
+    _, wv, E, Ed, _ = _pv_tables(P)
+    h = [mv.L[d] / mv.N[d] for d in range(dim)]
+    vs = [np.asarray(v[c], dtype=np.float64).reshape((mv.n_el,) + (n,) * dim) for c in range(dim)]
+    out = np.zeros((mv.n_el,) + (m,) * dim)
+    # array axes of an element block: (k, j, i) -> direction d sits at axis dim-1-d
+    ax = lambda d: dim - 1 - d
+    Wq = np.ones((n,) * dim)
+    for d in range(dim):
+        shp = [1] * dim
+        shp[ax(d)] = n
+        Wq = Wq * (wv * 0.5 * h[d]).reshape(shp)
+    for e in range(mv.n_el):
+        acc = np.zeros((m,) * dim)
+        for c in range(dim):  # volume: -(v_c, d_c phi^p)
+            t = Wq * vs[c][e]
+            for d in range(dim):
+                t = _apply_1d((Ed * (2.0 / h[d])).T if d == c else E.T, t, ax(d))
+            acc -= t
+        ec = _elem_coords(mv, e)
+        for d in range(dim):  # faces normal to d; n = +e_d from the - side to the + side
+            Wf = np.ones((n,) * (dim - 1))
+            tdirs = [dd for dd in range(dim) if dd != d]
+            for k, dd in enumerate(tdirs):
+                shp = [1] * (dim - 1)
+                shp[dim - 2 - k] = n
+                Wf = Wf * (wv * 0.5 * h[dd]).reshape(shp)
+            for side in (0, 1):
+                cn = list(ec)
+                cn[d] += 1 if side else -1
+                en = _elem_index(mv, cn)
+                own = np.take(vs[d][e], P if side else 0, axis=ax(d))     # own face trace v_d
+                nbr = np.take(vs[d][en], 0 if side else P, axis=ax(d))    # neighbour's trace
+                flux = Wf * 0.5 * (own + nbr)                              # W^F {v}.e_d
+                # own test functions on the face: [phi] = +phi (own is '-', side 1) or -phi
+                t = flux
+                for k, dd in enumerate(tdirs):
+                    t = _apply_1d(E.T, t, dim - 2 - k)
+                layer = np.zeros(m)
+                layer[m - 1 if side else 0] = 1.0
+                shp = [1] * dim
+                shp[ax(d)] = m
+                acc += (1.0 if side else -1.0) * np.expand_dims(t, ax(d)) * layer.reshape(shp)
+        out[e] = acc
+    return out.reshape(mv.n_el, m ** dim)
+
+
+def dg_gradient_weak(mp: Mesh, psi):
+    """g_{c,i} = -sum_K sum_q W_q psi_h(x_q) d_c phi^v_i(x_q) + sum_F sum_q W^F_q {psi_h} n_c [phi^v_i]
+    for the degree-(P-1) pressure psi ([N_el, P^d] on mesh mp, P = mp.P + 1); returns dim
+    arrays [N_el, (P+1)^d] (velocity layout).  -g is the adjoint of dg_divergence_weak."""
+    P, dim = mp.P + 1, mp.dim
+    n, m = P + 1, P
+    _, wv, E, _, Dv = _pv_tables(P)
+    h = [mp.L[d] / mp.N[d] for d in range(dim)]
+    ps = np.asarray(psi, dtype=np.float64).reshape((mp.n_el,) + (m,) * dim)
+    ax = lambda d: dim - 1 - d
+    Wq = np.ones((n,) * dim)
+    for d in range(dim):
+        shp = [1] * dim
+        shp[ax(d)] = n
+        Wq = Wq * (wv * 0.5 * h[d]).reshape(shp)
+
+    def interp(a):  # pressure nodes -> velocity nodes (all directions)
+        for d in range(dim):
+            a = _apply_1d(E, a, ax(d))
+        return a
+
+    outs = [np.zeros((mp.n_el,) + (n,) * dim) for _ in range(dim)]
+    for e in range(mp.n_el):
+        ph = interp(ps[e])
+        ec = _elem_coords(mp, e)
+        for c in range(dim):
+            # volume: -(psi_h, d_c phi^v_i) = -(2/h_c) sum_q D[q_c][i_c] W_q psi_h(q)
+            outs[c][e] -= _apply_1d((Dv * (2.0 / h[c])).T, Wq * ph, ax(c))
+            # faces normal to c
+            d = c
+            tdirs = [dd for dd in range(dim) if dd != d]
+            Wf = np.ones((n,) * (dim - 1))
+            for k, dd in enumerate(tdirs):
+                shp = [1] * (dim - 1)
+                shp[dim - 2 - k] = n
+                Wf = Wf * (wv * 0.5 * h[dd]).reshape(shp)
+            for side in (0, 1):
+                cn = list(ec)
+                cn[d] += 1 if side else -1
+                en = _elem_index(mp, cn)
+                own = np.take(ph, P if side else 0, axis=ax(d))
+                nbr = np.take(interp(ps[en]), 0 if side else P, axis=ax(d))
+                val = (1.0 if side else -1.0) * Wf * 0.5 * (own + nbr)   # W^F {psi} n_c [phi_i]
+                idx = [slice(None)] * dim
+                idx[ax(d)] = P if side else 0
+                outs[c][e][tuple(idx)] += val
+    return [o.reshape(mp.n_el, n ** dim) for o in outs]

@@ -22,6 +22,8 @@ from ._capi import (  # noqa: F401
     StageInfo,
     dg_check_field,
     dg_convect_rhs,
+    dg_divergence,
+    dg_gradient,
     dg_gll_tables,
     dg_helmholtz_apply,
     dg_helmholtz_apply_host,

@@ -66,6 +66,8 @@ _c = {
     "dg_helmholtz_diag": _sig("dg_helmholtz_diag", _i, [_vp, _d, _vp, _d, _vp]),
     "dg_pcg_solve": _sig("dg_pcg_solve", _i, [_vp, _d, _vp, _d, _vp, _d, _i, _vp, ctypes.POINTER(SolveInfo)]),
     "dg_convect_rhs": _sig("dg_convect_rhs", _i, [_vp, ctypes.POINTER(_vp), ctypes.POINTER(_vp)]),
+    "dg_divergence": _sig("dg_divergence", _i, [_vp, _vp, ctypes.POINTER(_vp), _vp]),
+    "dg_gradient": _sig("dg_gradient", _i, [_vp, _vp, _vp, ctypes.POINTER(_vp)]),
     "dg_imex_stage": _sig("dg_imex_stage", _i, [_vp, _vp, _d, _d, _d, _d, _d, ctypes.POINTER(_vp),
                                                 ctypes.POINTER(_vp), _vp, _d, _i, ctypes.POINTER(StageInfo)]),
     "dg_helmholtz_apply_host": _sig("dg_helmholtz_apply_host", _i, [_vp, _d, _vp, _d, _vp, _vp]),
@@ -250,6 +252,18 @@ def dg_convect_rhs(m: Mesh, v, out):
     vin = (_vp * 3)(*([_ptr(x) for x in v] + [None] * (3 - len(v))))
     vout = (_vp * 3)(*([_ptr(x) for x in out] + [None] * (3 - len(out))))
     _check(_c["dg_convect_rhs"](m.handle, vin, vout))
+
+
+def dg_divergence(mv: Mesh, mp: Mesh, v, div_weak):
+    """Weak DG divergence of v (velocity mesh) tested with the pressure basis -- include/dg.h."""
+    vin = (_vp * 3)(*([_ptr(x) for x in v] + [None] * (3 - len(v))))
+    _check(_c["dg_divergence"](mv.handle, mp.handle, vin, _ptr(div_weak)))
+
+
+def dg_gradient(mp: Mesh, mv: Mesh, psi, grad_weak):
+    """Weak DG gradient of psi (pressure mesh) tested with the velocity basis -- include/dg.h."""
+    go = (_vp * 3)(*([_ptr(x) for x in grad_weak] + [None] * (3 - len(grad_weak))))
+    _check(_c["dg_gradient"](mp.handle, mv.handle, _ptr(psi), go))
 
 
 def dg_imex_stage(mv: Mesh, mp: Mesh, dt, a_ex21, a_im21, a_im22, nu, v, vout, psi, tol, maxit) -> StageInfo:

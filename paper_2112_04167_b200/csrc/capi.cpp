@@ -160,7 +160,7 @@ struct dg_mesh {
     cudaStream_t cs_in = nullptr, cs_out = nullptr;
     std::vector<cudaEvent_t> ev;
     // IMEX stage workspace (velocity mesh: F_c[0..dim), A v; pressure mesh: rhs)
-    double *sf[4] = {nullptr, nullptr, nullptr, nullptr};
+    double *sf[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
     int *d_flag = nullptr;
     long long launches = 0;
 };
@@ -510,6 +510,57 @@ dg_status stage(dg_mesh *m, double **buf, size_t bytes)
     return alloc((void **)buf, bytes);
 }
 
+dg_status check_pair(const dg_mesh *mv, const dg_mesh *mp)
+{
+    const Geom &g = mv->g, &gp = mp->g;
+    if (gp.dim != g.dim || gp.P != g.P - 1 || mp->nranks != mv->nranks || mp->rank != mv->rank)
+        return set_error(DG_EINVAL, "pressure mesh must match the velocity mesh with degree P-1 (P:1036)");
+    for (int d = 0; d < 3; ++d)
+        if (gp.N[d] != g.N[d] || gp.h[d] != g.h[d]) return set_error(DG_EINVAL, "pressure mesh geometry differs");
+    if (g.P < 2) return set_error(DG_EINVAL, "the velocity degree must be >= 2 (pressure degree P-1 >= 1)");
+    return DG_OK;
+}
+
+// weak DG divergence of v (velocity mesh) into div (pressure mesh), on mv's stream
+dg_status div_impl(dg_mesh *mv, const double *const v[3], double *div)
+{
+    DivGradParams a;
+    for (int c = 0; c < mv->g.dim; ++c) a.v[c] = v[c];
+    if (mv->nranks > 1) {
+        CKS(ensure_halos(mv, true));
+        for (int c = 0; c < mv->g.dim; ++c) {
+            CKS(exchange(mv, v[c], mv->hv_lo[c], mv->hv_hi[c]));
+            a.vlo[c] = mv->hv_lo[c];
+            a.vhi[c] = mv->hv_hi[c];
+        }
+    }
+    a.out = div;
+    CK(launch_dg_div(mv->g, a, mv->st));
+    mv->launches += 1;
+    return DG_OK;
+}
+
+// weak DG gradient of psi (pressure mesh) into grad[c] (velocity mesh), on mv's stream
+dg_status grad_impl(dg_mesh *mp, dg_mesh *mv, const double *psi, double *const grad[3])
+{
+    DivGradParams a;
+    a.psi = psi;
+    if (mp->nranks > 1) {
+        cudaStream_t s0 = mp->st;
+        mp->st = mv->st;
+        dg_status s = ensure_halos(mp, false);
+        if (s == DG_OK) s = exchange(mp, psi, mp->h_lo, mp->h_hi);
+        mp->st = s0;
+        if (s != DG_OK) return s;
+        a.plo = mp->h_lo;
+        a.phi = mp->h_hi;
+    }
+    for (int c = 0; c < mv->g.dim; ++c) a.gout[c] = grad[c];
+    CK(launch_dg_grad(mv->g, a, mv->st));
+    mv->launches += 1;
+    return DG_OK;
+}
+
 }  // namespace
 
 // ---------------------------------------------------------------------------
@@ -638,7 +689,8 @@ void dg_mesh_destroy(dg_mesh *m)
     else cudaDeviceSynchronize();
     double *bufs[] = {m->r,    m->q,    m->pa,    m->pb,     m->dinv,   m->z,    m->partial,
                       m->sums, m->aux,  m->mass_e, m->hist,  m->h_lo,   m->h_hi, m->hn_lo,
-                      m->hn_hi, m->st_a, m->st_b,  m->st_c,  m->sf[0], m->sf[1], m->sf[2], m->sf[3]};
+                      m->hn_hi, m->st_a, m->st_b,  m->st_c,  m->sf[0], m->sf[1], m->sf[2], m->sf[3],
+                      m->sf[4], m->sf[5]};
     for (double *b : bufs)
         if (b) cudaFree(b);
     for (int c = 0; c < 3; ++c) {
@@ -833,11 +885,7 @@ dg_status dg_imex_stage(dg_mesh *mv, dg_mesh *mp, double dt, double a_ex21, doub
     if (!mv || !mp || !v || !vout || !psi) return set_error(DG_EINVAL, "null argument");
     const Geom &g = mv->g, &gp = mp->g;
     const int dim = g.dim;
-    if (gp.dim != dim || gp.P != g.P - 1 || mp->nranks != mv->nranks || mp->rank != mv->rank)
-        return set_error(DG_EINVAL, "pressure mesh must match the velocity mesh with degree P-1 (P:1036)");
-    for (int d = 0; d < 3; ++d)
-        if (gp.N[d] != g.N[d] || gp.h[d] != g.h[d]) return set_error(DG_EINVAL, "pressure mesh geometry differs");
-    if (g.P < 2) return set_error(DG_EINVAL, "stage needs P >= 2 (pressure degree P-1 >= 1)");
+    CKS(check_pair(mv, mp));
     if (!(dt > 0.0) || !(a_im22 > 0.0) || !std::isfinite(a_ex21) || !std::isfinite(a_im21) ||
         !(nu > 0.0 && std::isfinite(nu)))
         return set_error(DG_EINVAL, "need dt > 0, a_im22 > 0, finite a_ex21/a_im21, nu > 0");
@@ -856,6 +904,7 @@ dg_status dg_imex_stage(dg_mesh *mv, dg_mesh *mp, double dt, double a_ex21, doub
     } restore{mp, mp_stream};
     const size_t bv = sizeof(double) * (size_t)mv->ndof, bp = sizeof(double) * (size_t)mp->ndof;
     for (int c = 0; c <= dim; ++c) CKS(stage(mv, &mv->sf[c], bv));
+    for (int c = 4; c < 4 + dim - 1; ++c) CKS(stage(mv, &mv->sf[c], bv));
     CKS(stage(mp, &mp->sf[0], bp));
     double *Fc[3] = {mv->sf[0], mv->sf[1], dim == 3 ? mv->sf[2] : nullptr};
     double *Av = mv->sf[dim];
@@ -870,15 +919,23 @@ dg_status dg_imex_stage(dg_mesh *mv, dg_mesh *mp, double dt, double a_ex21, doub
                                 Fc[c], mv->st));
         mv->launches += 1;
     }
-    // line 5: pressure Poisson on the P-1 mesh, stand-in rhs -div(v')
-    CK(launch_div_interp(g, vout[0], vout[1], dim == 3 ? vout[2] : nullptr, mp->sf[0], mv->st));
+    // line 5: -lap psi = -div v' on the P-1 mesh: b = -D v' (weak DG divergence), f = M_p^-1 b
+    CKS(div_impl(mv, vout, mp->sf[0]));
+    CK(launch_scale_minv(gp, mp->mass_e, -1.0, mp->sf[0], mp->sf[0], mv->st));
     mv->launches += 1;
     CK(cudaMemsetAsync(psi, 0, bp, mv->st));
     dg_solve_info ip{};
     dg_status s = pcg_impl(mp, 0.0, nullptr, 1.0, mp->sf[0], tol, maxit, psi, &ip);
     if (info) info->pressure = ip;
     if (s != DG_OK) return s;
-    // line 9: v_i - dt a_ii div(nu grad v_i) = g_i per component, from the guess v'' = v'
+    // line 6: v'' = v' - M^-1 G psi (weak DG gradient), and line 8's rhs follows (f_H -= lam M^-1 G psi)
+    double *gw[3] = {Av, mv->sf[4], mv->sf[5]};
+    CKS(grad_impl(mp, mv, psi, gw));
+    for (int c = 0; c < dim; ++c) {
+        CK(launch_stage_project(g, mv->mass_e, lamH, gw[c], vout[c], Fc[c], mv->st));
+        mv->launches += 1;
+    }
+    // line 9: v_i - dt a_ii div(nu grad v_i) = g_i per component, from the guess v''
     for (int c = 0; c < dim; ++c) {
         dg_solve_info iv{};
         s = pcg_impl(mv, lamH, nullptr, nu, Fc[c], tol, maxit, vout[c], &iv);
@@ -886,6 +943,24 @@ dg_status dg_imex_stage(dg_mesh *mv, dg_mesh *mp, double dt, double a_ex21, doub
         if (s != DG_OK) return s;
     }
     return DG_OK;
+}
+
+dg_status dg_divergence(dg_mesh *mv, dg_mesh *mp, const double *const v[3], double *div_weak)
+{
+    if (!mv || !mp || !v || !div_weak) return set_error(DG_EINVAL, "null argument");
+    CKS(check_pair(mv, mp));
+    for (int c = 0; c < mv->g.dim; ++c)
+        if (!v[c]) return set_error(DG_EINVAL, "null component pointer");
+    return div_impl(mv, v, div_weak);
+}
+
+dg_status dg_gradient(dg_mesh *mp, dg_mesh *mv, const double *psi, double *const grad_weak[3])
+{
+    if (!mv || !mp || !psi || !grad_weak) return set_error(DG_EINVAL, "null argument");
+    CKS(check_pair(mv, mp));
+    for (int c = 0; c < mv->g.dim; ++c)
+        if (!grad_weak[c] || grad_weak[c] == psi) return set_error(DG_EINVAL, "null or aliased component pointer");
+    return grad_impl(mp, mv, psi, grad_weak);
 }
 
 dg_status dg_gll_tables(int P, double *xi, double *w, double *D)

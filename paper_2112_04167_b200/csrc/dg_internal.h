@@ -141,8 +141,19 @@ cudaError_t upload_tables_stage_interp();
 cudaError_t launch_stage_combine(const Geom &g, const double *mass_e, double a_ex, double c_g, double lamH,
                                  const double *v, const double *Fc, const double *Av, double *vp, double *fH,
                                  cudaStream_t st);
-cudaError_t launch_div_interp(const Geom &g, const double *v0, const double *v1, const double *v2, double *fp,
+struct DivGradParams {  // geometry: the velocity mesh's (degree P); pressure degree P-1
+    const double *v[3] = {nullptr, nullptr, nullptr};     // div: velocity components
+    const double *vlo[3] = {nullptr, nullptr, nullptr}, *vhi[3] = {nullptr, nullptr, nullptr};
+    double *out = nullptr;                               // div: weak divergence (pressure layout)
+    const double *psi = nullptr, *plo = nullptr, *phi = nullptr;  // grad: pressure (+ halos)
+    double *gout[3] = {nullptr, nullptr, nullptr};      // grad: weak gradient (velocity layout)
+};
+cudaError_t launch_dg_div(const Geom &gv, const DivGradParams &a, cudaStream_t st);
+cudaError_t launch_scale_minv(const Geom &g, const double *mass_e, double c, const double *in, double *out,
                               cudaStream_t st);
+cudaError_t launch_stage_project(const Geom &g, const double *mass_e, double lamH, const double *gw, double *vp,
+                                 double *fH, cudaStream_t st);
+cudaError_t launch_dg_grad(const Geom &gv, const DivGradParams &a, cudaStream_t st);
 
 // PCG vector kernels -------------------------------------------------------
 struct PcgScal {                 // device-resident scalars of one solve

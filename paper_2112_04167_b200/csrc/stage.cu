@@ -5,21 +5,22 @@
 //                     v'   = v + dt a^ex_21 (F_c + F_d1)            (Alg. 3 line 4, F_s = 0)
 //                     g    = v' + dt (a^im_21 - a^ex_21) F_d1       (Alg. 3 line 8, v'' = v')
 //                     f_H  = g / (dt a^im_22)                       (reading A4: f = lam g)
-//   k_div_interp    : the stand-in pressure rhs of Alg. 3 line 5 until the DG divergence
-//                      lands: the broken (element-local collocation) divergence
-//                     of v' at the velocity GLL nodes, interpolated to the GLL nodes of the
-//                     pressure degree P-1, sign-flipped for the positive operator
-//                     (-lap psi = -div v').  The mass weighting and mean projection are done
-//                     by dg_pcg_solve (reading A8).
+//   k_dg_div        : weak DG divergence of v' tested with the degree-(P-1) pressure basis
+//                     (the rhs of the pressure Poisson problem, Alg. 3 line 5);
+//   k_dg_grad       : weak DG gradient of psi tested with the velocity basis (Alg. 3 line 6,
+//                     v'' = v' - M^-1 G psi).  -G is the transpose of D.
 #include "dev_common.cuh"
 
 namespace dg {
-DG_DEFINE_CONST_TABLES(upload_tables_stage)
+cudaError_t upload_tables_stage() { return cudaSuccess; }  // tables: upload_tables_stage_interp
 
-// interpolation from the degree-P GLL nodes to the degree-(P-1) GLL nodes:
-// I[a][i] = l_i(xi'_a), barycentric form in long double
+// pressure basis (degree P-1 GLL Lagrange) at the velocity GLL nodes of degree P:
+// E[i][a] = l^{P-1}_a(xi^P_i), Ed[i][a] = l^{P-1}_a'(xi^P_i) (barycentric, long double)
 struct StTab {
-    double I[NMAX][NMAX];
+    double w[NMAX];             // velocity GLL weights
+    double D[NMAX][NMAX];       // velocity differentiation matrix
+    double E[NMAX][NMAX - 1];
+    double Ed[NMAX][NMAX - 1];
 };
 static __constant__ StTab c_stab[PMAX + 1];
 
@@ -28,25 +29,35 @@ cudaError_t upload_tables_stage_interp()
     static StTab h[PMAX + 1];
     for (int P = 2; P <= PMAX; ++P) {
         const Tab &t = host_tab(P), &tp = host_tab(P - 1);
-        const int n = P + 1;
+        const int m = P;  // pressure nodes per direction
         long double bw[NMAX];
-        for (int j = 0; j < n; ++j) {
+        for (int a = 0; a < m; ++a) {
             long double b = 1.0L;
-            for (int m = 0; m < n; ++m)
-                if (m != j) b *= (long double)t.xi[j] - (long double)t.xi[m];
-            bw[j] = 1.0L / b;
+            for (int c = 0; c < m; ++c)
+                if (c != a) b *= (long double)tp.xi[a] - (long double)tp.xi[c];
+            bw[a] = 1.0L / b;
         }
-        for (int a = 0; a < P; ++a) {
-            const long double x = tp.xi[a];
-            int hit = -1;
-            for (int j = 0; j < n; ++j)
-                if (x == (long double)t.xi[j]) hit = j;
-            long double den = 0.0L, num[NMAX];
-            for (int j = 0; j < n; ++j) {
-                num[j] = hit >= 0 ? (j == hit ? 1.0L : 0.0L) : bw[j] / (x - (long double)t.xi[j]);
-                den += num[j];
+        for (int i = 0; i <= P; ++i) {
+            const long double x = t.xi[i];
+            // l_a(x) = prod_{c != a} (x - xp_c) bw_a ;  l_a'(x) = l_a(x) sum_{c != a} 1/(x - xp_c)
+            // (evaluated directly; velocity and pressure nodes coincide only at +-1)
+            for (int a = 0; a < m; ++a) {
+                long double la = bw[a], dla = 0.0L;
+                for (int c = 0; c < m; ++c) {
+                    if (c == a) continue;
+                    long double prod = bw[a];
+                    for (int c2 = 0; c2 < m; ++c2)
+                        if (c2 != a && c2 != c) prod *= x - (long double)tp.xi[c2];
+                    dla += prod;
+                    la *= x - (long double)tp.xi[c];
+                }
+                h[P].E[i][a] = (double)la;
+                h[P].Ed[i][a] = (double)dla;
             }
-            for (int j = 0; j < n; ++j) h[P].I[a][j] = hit >= 0 ? (double)num[j] : (double)(num[j] / den);
+        }
+        for (int i = 0; i <= P; ++i) {
+            h[P].w[i] = t.w[i];
+            for (int j = 0; j <= P; ++j) h[P].D[i][j] = t.D[i][j];
         }
     }
     return cudaMemcpyToSymbol(c_stab, h, sizeof(h));
@@ -65,84 +76,255 @@ __global__ void k_stage_combine(long long ndof, int npe, const double *mass_e, d
     }
 }
 
-// one CTA per element: div at the velocity nodes in shared memory, then three (two)
-// interpolation passes P -> P-1
-template <int DIM, int P>
-__global__ void __launch_bounds__(256) k_div_interp(const Geom g, const double *v0, const double *v1, const double *v2,
-                                                     double *fp)
+// out = c * in / m (nodal value of a weak vector; m = GLL-lumped mass of the node)
+__global__ void k_scale_minv(long long ndof, int npe, const double *mass_e, double c, const double *in, double *out)
 {
-    constexpr int n = P + 1, m = P;  // velocity / pressure nodes per direction
-    constexpr int NPE = DIM == 3 ? n * n * n : n * n;
-    constexpr int MPE = DIM == 3 ? m * m * m : m * m;
-    const DevTab &T = c_tab[P];
-    const StTab &S = c_stab[P];
-    __shared__ double sv[3][NPE];
-    __shared__ double sa[NPE], sb[NPE];
-    for (long long e = blockIdx.x; e < g.nel; e += gridDim.x) {
-        for (int q = threadIdx.x; q < NPE; q += blockDim.x) {
-            sv[0][q] = v0[e * NPE + q];
-            sv[1][q] = v1[e * NPE + q];
-            if (DIM == 3) sv[2][q] = v2[e * NPE + q];
-        }
-        __syncthreads();
-        for (int q = threadIdx.x; q < NPE; q += blockDim.x) {
-            const int i = q % n, j = (q / n) % n, k = DIM == 3 ? q / (n * n) : 0;
-            double d0 = 0.0, d1 = 0.0, d2 = 0.0;
-#pragma unroll
-            for (int r = 0; r < n; ++r) {
-                d0 = fma(T.D[i][r], sv[0][q + (r - i)], d0);
-                d1 = fma(T.D[j][r], sv[1][q + (r - j) * n], d1);
-                if (DIM == 3) d2 = fma(T.D[k][r], sv[2][q + (r - k) * n * n], d2);
-            }
-            sa[q] = g.sd[0] * d0 + g.sd[1] * d1 + (DIM == 3 ? g.sd[2] * d2 : 0.0);
-        }
-        __syncthreads();
-        // x: sa[k][j][i] -> sb[k][j][a]
-        for (int q = threadIdx.x; q < (DIM == 3 ? n * n * m : n * m); q += blockDim.x) {
-            const int a = q % m, r = q / m;  // r = j + n k
-            double s = 0.0;
-#pragma unroll
-            for (int i = 0; i < n; ++i) s = fma(S.I[a][i], sa[r * n + i], s);
-            sb[r * m + a] = s;
-        }
-        __syncthreads();
-        // y: sb[k][j][a] -> sa[k][b][a]
-        for (int q = threadIdx.x; q < (DIM == 3 ? n * m * m : m * m); q += blockDim.x) {
-            const int a = q % m, b = (q / m) % m, k = q / (m * m);
-            double s = 0.0;
-#pragma unroll
-            for (int j = 0; j < n; ++j) s = fma(S.I[b][j], sb[(k * n + j) * m + a], s);
-            sa[(k * m + b) * m + a] = s;
-        }
-        __syncthreads();
-        if (DIM == 3) {  // z: sa[k][b][a] -> out[c][b][a]
-            for (int q = threadIdx.x; q < MPE; q += blockDim.x) {
-                const int ab = q % (m * m), c = q / (m * m);
-                double s = 0.0;
-#pragma unroll
-                for (int k = 0; k < n; ++k) s = fma(S.I[c][k], sa[k * m * m + ab], s);
-                fp[e * MPE + q] = -s;
-            }
-        } else {
-            for (int q = threadIdx.x; q < MPE; q += blockDim.x) fp[e * MPE + q] = -sa[q];
-        }
-        __syncthreads();
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < ndof; t += (long long)gridDim.x * blockDim.x)
+        out[t] = c * in[t] / mass_e[t % npe];
+}
+
+// projection (Alg. 3 line 6) and its effect on the Helmholtz rhs (line 8):
+// v'' = v' - M^-1 G psi ;  f_H -= lam M^-1 G psi
+__global__ void k_stage_project(long long ndof, int npe, const double *mass_e, double lamH, const double *gw,
+                                double *vp, double *fH)
+{
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < ndof; t += (long long)gridDim.x * blockDim.x) {
+        const double gn = gw[t] / mass_e[t % npe];
+        vp[t] -= gn;
+        fH[t] = fma(-lamH, gn, fH[t]);
     }
 }
 
-template <int DIM>
-cudaError_t div_dispatch(const Geom &g, const double *v0, const double *v1, const double *v2, double *fp,
-                         cudaStream_t st)
+// ---------------------------------------------------------------------------
+// DG divergence / gradient pair (Alg. 3 lines 5-6).  One CTA per element
+// (grid-stride), element data in shared memory, sum-factorised 1-D contractions with the
+// pressure basis at the velocity GLL nodes (E, E') or the velocity derivative matrix (D),
+// face traces of the neighbours read from global memory (rank halos in the slowest
+// direction).  Integrals on the velocity GLL grid; central fluxes; see include/dg.h.
+// ---------------------------------------------------------------------------
+// out = M (contracted along axis ax) in; element arrays with x fastest, extents ext[0..2]
+// (ext[ax] = ni on input, no on output); M is [no][ni] row-major in shared memory.
+__device__ __forceinline__ void contract(const double *in, double *out, const double *M, const int (&ext)[3], int ax,
+                                         int ni, int no)
+{
+    int eo[3] = {ext[0], ext[1], ext[2]};
+    eo[ax] = no;
+    const int tot = eo[0] * eo[1] * eo[2];
+    const int st = ax == 0 ? 1 : (ax == 1 ? ext[0] : ext[0] * ext[1]);  // input stride along ax
+    for (int q = threadIdx.x; q < tot; q += blockDim.x) {
+        const int c0 = q % eo[0], c1 = (q / eo[0]) % eo[1], c2 = q / (eo[0] * eo[1]);
+        int ci[3] = {c0, c1, c2};
+        const int o = ci[ax];
+        ci[ax] = 0;
+        const int base = ci[0] + ext[0] * (ci[1] + ext[1] * ci[2]);
+        double s = 0.0;
+        for (int i = 0; i < ni; ++i) s = fma(M[o * ni + i], in[base + i * st], s);
+        out[q] = s;
+    }
+}
+
+template <int DIM, int P>
+struct PV {
+    static constexpr int n = P + 1, m = P;
+    static constexpr int NV = DIM == 3 ? n * n * n : n * n;   // velocity nodes per element
+    static constexpr int NPp = DIM == 3 ? m * m * m : m * m;  // pressure nodes per element
+};
+
+// shared tables: ET[a][i] = E[i][a] (m x n), EdT (m x n), Em = E (n x m), DT[j][i] = D[i][j] (n x n), w (n)
+template <int P>
+__device__ __forceinline__ void load_pv_tables(double *ET, double *EdT, double *Em, double *DT, double *sw)
+{
+    constexpr int n = P + 1, m = P;
+    const StTab &S = c_stab[P];
+    const StTab &T = S;
+    for (int t = threadIdx.x; t < m * n; t += blockDim.x) {
+        const int a = t / n, i = t % n;
+        ET[t] = S.E[i][a];
+        EdT[t] = S.Ed[i][a];
+        Em[i * m + a] = S.E[i][a];
+    }
+    for (int t = threadIdx.x; t < n * n; t += blockDim.x) DT[t] = T.D[t % n][t / n];
+    for (int t = threadIdx.x; t < n; t += blockDim.x) sw[t] = T.w[t];
+}
+
+// weak divergence d_a = -sum_q W_q v.grad phi^p_a + sum_F W^F {v}.n [phi^p_a]
+template <int DIM, int P>
+__global__ void __launch_bounds__(256) k_dg_div(const Geom g, DivGradParams a)
+{
+    using C = PV<DIM, P>;
+    constexpr int n = C::n, m = C::m, NV = C::NV, NPp = C::NPp;
+    __shared__ double ET[m * n], EdT[m * n], Em[n * m], DT[n * n], sw[n];
+    __shared__ double sv[NV], b1[NV], b2[NV], acc[NPp], fc[DIM == 3 ? n * n : n], fo[DIM == 3 ? n * m : m];
+    load_pv_tables<P>(ET, EdT, Em, DT, sw);
+    for (long long e = blockIdx.x; e < g.nel; e += gridDim.x) {
+        __syncthreads();
+        for (int q = threadIdx.x; q < NPp; q += blockDim.x) acc[q] = 0.0;
+        const int ec[3] = {(int)(e % g.Nl[0]), (int)((e / g.Nl[0]) % g.Nl[1]),
+                           DIM == 3 ? (int)(e / ((long long)g.Nl[0] * g.Nl[1])) : 0};
+        for (int c = 0; c < DIM; ++c) {
+            __syncthreads();
+            for (int q = threadIdx.x; q < NV; q += blockDim.x) {
+                const int i = q % n, j = (q / n) % n, k = DIM == 3 ? q / (n * n) : 0;
+                double W = sw[i] * sw[j] * g.mfac;
+                if (DIM == 3) W *= sw[k];
+                sv[q] = W * a.v[c][e * NV + q];
+            }
+            __syncthreads();
+            // volume: contract x, y (, z) with E^T, the direction c with (2/h_c) E'^T
+            int ext[3] = {n, n, DIM == 3 ? n : 1};
+            const double *src = sv;
+            double *bufs[2] = {b1, b2};
+            for (int d = 0; d < DIM; ++d) {
+                double *dst = bufs[d & 1];
+                contract(src, dst, d == c ? EdT : ET, ext, d, n, m);
+                __syncthreads();
+                ext[d] = m;
+                src = dst;
+            }
+            const double sdc = g.sd[c];
+            for (int q = threadIdx.x; q < NPp; q += blockDim.x) acc[q] -= sdc * src[q];
+        }
+        // faces normal to d: own side 1 is '-' ([phi] = +phi), side 0 is '+' ([phi] = -phi)
+        for (int d = 0; d < DIM; ++d) {
+            const int o1 = d == 0 ? 1 : 0, o2 = d == 2 ? 1 : 2;
+            const int GS[3] = {1, n, n * n};
+            const int nt = DIM == 3 ? n * n : n;
+            for (int side = 0; side < 2; ++side) {
+                __syncthreads();
+                int cn[3] = {ec[0], ec[1], ec[2]};
+                cn[d] += side ? 1 : -1;
+                const double *nb = elem_ptr(g, a.v[d], a.vlo[d], a.vhi[d], cn[0], cn[1], cn[2]);
+                const double *ow = a.v[d] + e * NV;
+                for (int t = threadIdx.x; t < nt; t += blockDim.x) {
+                    const int ta = t % n, tb = DIM == 3 ? t / n : 0;
+                    const int off = ta * GS[o1] + (DIM == 3 ? tb * GS[o2] : 0);
+                    double Wf = sw[ta] * g.wfac[d];
+                    if (DIM == 3) Wf *= sw[tb];
+                    fc[t] = Wf * 0.5 * (ow[off + (side ? P : 0) * GS[d]] + nb[off + (side ? 0 : P) * GS[d]]);
+                }
+                __syncthreads();
+                // transverse contractions with E^T: (n [, n]) -> (m [, m]); face array axes (o1, o2)
+                int ext[3] = {n, DIM == 3 ? n : 1, 1};
+                contract(fc, fo, ET, ext, 0, n, m);
+                __syncthreads();
+                const double *fr = fo;
+                if (DIM == 3) {
+                    ext[0] = m;
+                    contract(fo, fc, ET, ext, 1, n, m);
+                    __syncthreads();
+                    fr = fc;
+                }
+                const int PS[3] = {1, m, m * m};
+                const int lay = side ? m - 1 : 0;
+                for (int t = threadIdx.x; t < (DIM == 3 ? m * m : m); t += blockDim.x) {
+                    const int ta = t % m, tb = DIM == 3 ? t / m : 0;
+                    acc[ta * PS[o1] + (DIM == 3 ? tb * PS[o2] : 0) + lay * PS[d]] += (side ? 1.0 : -1.0) * fr[t];
+                }
+            }
+        }
+        __syncthreads();
+        for (int q = threadIdx.x; q < NPp; q += blockDim.x) a.out[e * NPp + q] = acc[q];
+    }
+}
+
+// weak gradient g_{c,i} = -sum_q W_q psi_h d_c phi^v_i + sum_F W^F {psi_h} n_c [phi^v_i]
+template <int DIM, int P>
+__global__ void __launch_bounds__(256) k_dg_grad(const Geom g, DivGradParams a)
+{
+    using C = PV<DIM, P>;
+    constexpr int n = C::n, m = C::m, NV = C::NV, NPp = C::NPp;
+    __shared__ double ET[m * n], EdT[m * n], Em[n * m], DT[n * n], sw[n];
+    __shared__ double sp[NV], b1[NV], b2[NV], fc[DIM == 3 ? n * n : n], fo[DIM == 3 ? n * n : n];
+    load_pv_tables<P>(ET, EdT, Em, DT, sw);
+    for (long long e = blockIdx.x; e < g.nel; e += gridDim.x) {
+        __syncthreads();
+        for (int q = threadIdx.x; q < NPp; q += blockDim.x) sp[q] = a.psi[e * NPp + q];
+        __syncthreads();
+        const int ec[3] = {(int)(e % g.Nl[0]), (int)((e / g.Nl[0]) % g.Nl[1]),
+                           DIM == 3 ? (int)(e / ((long long)g.Nl[0] * g.Nl[1])) : 0};
+        // psi_h at the velocity nodes (b1 or b2)
+        int ext[3] = {m, m, DIM == 3 ? m : 1};
+        const double *src = sp;
+        double *bufs[2] = {b1, b2};
+        for (int d = 0; d < DIM; ++d) {
+            double *dst = bufs[d & 1];
+            contract(src, dst, Em, ext, d, m, n);
+            __syncthreads();
+            ext[d] = n;
+            src = dst;
+        }
+        double *ph = const_cast<double *>(src);         // psi_h
+        double *wph = (ph == b1) ? b2 : b1;             // W psi_h
+        for (int q = threadIdx.x; q < NV; q += blockDim.x) {
+            const int i = q % n, j = (q / n) % n, k = DIM == 3 ? q / (n * n) : 0;
+            double W = sw[i] * sw[j] * g.mfac;
+            if (DIM == 3) W *= sw[k];
+            wph[q] = W * ph[q];
+        }
+        __syncthreads();
+        for (int c = 0; c < DIM; ++c) {
+            // volume: -(2/h_c) D^T along c of W psi_h -> written straight to out[c]
+            const int GS[3] = {1, n, n * n};
+            const double sdc = g.sd[c];
+            for (int q = threadIdx.x; q < NV; q += blockDim.x) {
+                const int qc[3] = {q % n, (q / n) % n, DIM == 3 ? q / (n * n) : 0};
+                const int i = qc[c], base = q - i * GS[c];
+                double s = 0.0;
+                for (int r = 0; r < n; ++r) s = fma(DT[i * n + r], wph[base + r * GS[c]], s);
+                a.gout[c][e * NV + q] = -sdc * s;
+            }
+            // faces normal to c
+            const int d = c, o1 = d == 0 ? 1 : 0, o2 = d == 2 ? 1 : 2;
+            const int PS[3] = {1, m, m * m};
+            const int nt = DIM == 3 ? n * n : n, mt = DIM == 3 ? m * m : m;
+            for (int side = 0; side < 2; ++side) {
+                int cn[3] = {ec[0], ec[1], ec[2]};
+                cn[d] += side ? 1 : -1;
+                Geom gp = g;  // pressure-mesh element stride
+                gp.npe = NPp;
+                const double *nb = elem_ptr(gp, a.psi, a.plo, a.phi, cn[0], cn[1], cn[2]);
+                __syncthreads();
+                // the neighbour's pressure face layer, then its transverse interpolation
+                for (int t = threadIdx.x; t < mt; t += blockDim.x) {
+                    const int ta = t % m, tb = DIM == 3 ? t / m : 0;
+                    fo[t] = nb[ta * PS[o1] + (DIM == 3 ? tb * PS[o2] : 0) + (side ? 0 : m - 1) * PS[d]];
+                }
+                __syncthreads();
+                int ext2[3] = {m, DIM == 3 ? m : 1, 1};
+                contract(fo, fc, Em, ext2, 0, m, n);
+                __syncthreads();
+                const double *fr = fc;
+                if (DIM == 3) {
+                    ext2[0] = n;
+                    contract(fc, fo, Em, ext2, 1, m, n);
+                    __syncthreads();
+                    fr = fo;
+                }
+                for (int t = threadIdx.x; t < nt; t += blockDim.x) {
+                    const int ta = t % n, tb = DIM == 3 ? t / n : 0;
+                    const int off = ta * GS[o1] + (DIM == 3 ? tb * GS[o2] : 0) + (side ? P : 0) * GS[d];
+                    double Wf = sw[ta] * g.wfac[d];
+                    if (DIM == 3) Wf *= sw[tb];
+                    a.gout[c][e * NV + off] += (side ? 1.0 : -1.0) * Wf * 0.5 * (ph[off] + fr[t]);
+                }
+            }
+        }
+    }
+}
+
+template <int DIM, bool DIV>
+cudaError_t dg_dispatch(const Geom &g, const DivGradParams &a, cudaStream_t st)
 {
     const long long blocks = g.nel < 148LL * 16 ? g.nel : 148LL * 16;
-    switch (g.P) {
-#define DG_CASE(p)                                                                          \
-    case p:                                                                                 \
-        if constexpr (DG_HAS_P(p) && (DIM == 2 || 5 * (p + 1) * (p + 1) * (p + 1) * 8 <= 48 * 1024)) { \
-            k_div_interp<DIM, p><<<(int)blocks, 256, 0, st>>>(g, v0, v1, v2, fp);           \
-            return cudaGetLastError();                                                      \
-        } else {                                                                            \
-            return cudaErrorNotSupported;                                                   \
+    switch (g.P) {  // g: the VELOCITY geometry (degree P >= 2)
+#define DG_CASE(p)                                                                                         \
+    case p:                                                                                                \
+        if constexpr (DG_HAS_P(p) && (DIM == 2 || 3 * (p + 1) * (p + 1) * (p + 1) * 8 <= 40 * 1024)) {     \
+            if (DIV) k_dg_div<DIM, p><<<(int)blocks, 256, 0, st>>>(g, a);                                 \
+            else k_dg_grad<DIM, p><<<(int)blocks, 256, 0, st>>>(g, a);                                    \
+            return cudaGetLastError();                                                                     \
+        } else {                                                                                           \
+            return cudaErrorNotSupported;                                                                  \
         }
         DG_CASE(2) DG_CASE(3) DG_CASE(4) DG_CASE(5) DG_CASE(6) DG_CASE(7) DG_CASE(8) DG_CASE(9) DG_CASE(10)
 #undef DG_CASE
@@ -163,10 +345,32 @@ cudaError_t launch_stage_combine(const Geom &g, const double *mass_e, double a_e
     return cudaGetLastError();
 }
 
-cudaError_t launch_div_interp(const Geom &g, const double *v0, const double *v1, const double *v2, double *fp,
+static int vblocks(long long nd) { return (int)((nd + 255) / 256 < 148LL * 16 ? (nd + 255) / 256 : 148LL * 16); }
+
+cudaError_t launch_scale_minv(const Geom &g, const double *mass_e, double c, const double *in, double *out,
                               cudaStream_t st)
 {
-    return g.dim == 3 ? div_dispatch<3>(g, v0, v1, v2, fp, st) : div_dispatch<2>(g, v0, v1, v2, fp, st);
+    const long long nd = g.nel * g.npe;
+    k_scale_minv<<<vblocks(nd), 256, 0, st>>>(nd, g.npe, mass_e, c, in, out);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_stage_project(const Geom &g, const double *mass_e, double lamH, const double *gw, double *vp,
+                                 double *fH, cudaStream_t st)
+{
+    const long long nd = g.nel * g.npe;
+    k_stage_project<<<vblocks(nd), 256, 0, st>>>(nd, g.npe, mass_e, lamH, gw, vp, fH);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_dg_div(const Geom &gv, const DivGradParams &a, cudaStream_t st)
+{
+    return gv.dim == 3 ? dg_dispatch<3, true>(gv, a, st) : dg_dispatch<2, true>(gv, a, st);
+}
+
+cudaError_t launch_dg_grad(const Geom &gv, const DivGradParams &a, cudaStream_t st)
+{
+    return gv.dim == 3 ? dg_dispatch<3, false>(gv, a, st) : dg_dispatch<2, false>(gv, a, st);
 }
 
 }  // namespace dg

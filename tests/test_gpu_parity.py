@@ -372,6 +372,26 @@ def test_convect_c4_sampled():
 # ---------------------------------------------------------------------------
 # IMEX-RK stage: dg_imex_stage vs the oracle composition
 # ---------------------------------------------------------------------------
+@pytest.mark.parametrize("dim,N,P", [(3, (2, 3, 2), 3), (3, (3, 2, 4), 5), (2, (4, 3), 4), (2, (1, 2), 2),
+                                     (3, (2, 2, 2), 7), (3, (1, 1, 2), 6)])
+def test_dg_divergence_gradient_small(dim, N, P):
+    L = (1.0, 1.4, 0.8)[:dim]
+    mv = dg.dg_mesh_create(dim, N, L, P, stream=torch.cuda.current_stream())
+    mp = dg.dg_mesh_create(dim, N, L, P - 1, stream=torch.cuda.current_stream())
+    omv, omp = oracle.Mesh(dim, N, L, P), oracle.Mesh(dim, N, L, P - 1)
+    rng = np.random.default_rng(70 + P)
+    v = [rng.uniform(-1, 1, (omv.n_el, omv.npe)) for _ in range(dim)]
+    q = rng.uniform(-1, 1, (omp.n_el, omp.npe))
+    d = torch.empty(omp.n_el, omp.npe, dtype=torch.float64, device=DEV)
+    dg.dg_divergence(mv, mp, [T(x) for x in v], d)
+    assert rel(H(d), oracle.dg_divergence_weak(omv, v)) <= 1e-12
+    gw = [torch.empty(omv.n_el, omv.npe, dtype=torch.float64, device=DEV) for _ in range(dim)]
+    dg.dg_gradient(mp, mv, T(q), gw)
+    ref = oracle.dg_gradient_weak(omp, q)
+    for cc in range(dim):
+        assert rel(H(gw[cc]), ref[cc]) <= 1e-12
+
+
 @pytest.mark.parametrize("dim,N,P", [(3, (2, 2, 4), 3), (3, (4, 2, 2), 4), (2, (4, 2), 5), (3, (2, 2, 2), 7)])
 def test_imex_stage_small(dim, N, P):
     L = (TWO_PI,) * dim

@@ -1,4 +1,5 @@
-"""Pins of the oracle's IMEX-RK stage pieces (Alg. 3 lines 4-9)."""
+"""Pins of the oracle's IMEX-RK stage pieces (Alg. 3 lines 4-9,
+P:818-861): the DG divergence / gradient pair of the projection step and the stage."""
 import numpy as np
 import pytest
 
@@ -15,24 +16,81 @@ def _poly(dim, X):
     return v, div
 
 
-@pytest.mark.parametrize("dim,N,P", [(2, (3, 2), 3), (3, (2, 2, 3), 3), (3, (2, 1, 2), 4), (2, (2, 2), 6)])
-def test_broken_divergence_exact_for_polynomials(dim, N, P):
-    """Collocation derivatives are exact for degree <= P and the interpolation to the P-1
-    nodes is exact for degree <= P-1: the result equals the analytic divergence there."""
+def _interior(mesh):
+    """Elements whose closure avoids the periodic seam (global polynomials are continuous there)."""
+    out = []
+    for e in range(mesh.n_el):
+        ec = oracle._elem_coords(mesh, e)
+        if all(0 < c < mesh.N[k] - 1 for k, c in enumerate(ec)):
+            out.append(e)
+    return out
+
+
+@pytest.mark.parametrize("dim,N,P", [(2, (3, 2), 3), (3, (2, 2, 3), 3), (2, (2, 3), 5), (3, (1, 2, 2), 2)])
+def test_dg_divergence_gradient_adjoint(dim, N, P):
+    """q . D v = -v . G q for all v, q (central fluxes, exact GLL_P quadrature): -G = D^T."""
     L = (1.0, 1.3, 0.8)[:dim]
-    om = oracle.Mesh(dim, N, L, P)
-    v, _ = _poly(dim, node_coords(dim, N, L, P))
-    _, dv = _poly(dim, node_coords(dim, N, L, P - 1))
-    got = oracle.broken_divergence_p1(om, v)
-    assert np.abs(got - dv).max() <= 1e-13 * np.abs(dv).max()
+    mv, mp = oracle.Mesh(dim, N, L, P), oracle.Mesh(dim, N, L, P - 1)
+    rng = np.random.default_rng(P)
+    v = [rng.uniform(-1, 1, (mv.n_el, mv.npe)) for _ in range(dim)]
+    q = rng.uniform(-1, 1, (mp.n_el, mp.npe))
+    d = oracle.dg_divergence_weak(mv, v)
+    g = oracle.dg_gradient_weak(mp, q)
+    lhs = float(np.sum(q * d))
+    rhs = -sum(float(np.sum(v[c] * g[c])) for c in range(dim))
+    assert abs(lhs - rhs) <= 1e-13 * (np.abs(q * d).sum() + 1.0)
 
 
-def test_broken_divergence_detects_transposed_direction():
-    dim, N, P, L = 2, (2, 2), 3, (1.0, 1.3)
-    om = oracle.Mesh(dim, N, L, P)
+@pytest.mark.parametrize("dim,N,P", [(2, (4, 3), 3), (3, (3, 3, 4), 3), (2, (3, 4), 5), (3, (3, 3, 3), 2)])
+def test_dg_divergence_gradient_polynomial_exactness(dim, N, P):
+    """For continuous polynomial fields of degree <= P-1 the pair is exact on interior elements:
+    D v = (phi^p, div v) evaluated with GLL_P quadrature, M^-1 G psi = grad psi at the nodes."""
+    L = (1.0, 1.3, 0.8)[:dim]
+    mv, mp = oracle.Mesh(dim, N, L, P), oracle.Mesh(dim, N, L, P - 1)
     X = node_coords(dim, N, L, P)
-    v = [X[1] ** 2, 0.0 * X[0]]          # div = 0 exactly; a swapped axis would give 2y
-    assert np.abs(oracle.broken_divergence_p1(om, v)).max() < 1e-13
+    x, y = X[0], X[1]
+    z = X[2] if dim == 3 else 0.0 * x
+    if P >= 3:
+        v = [x ** 2 * y + 0.3 * z, x * y ** 2 - z ** 2 * x, x * y * z + z ** 2][:dim]
+        divv = 4.0 * x * y + ((x * y + 2.0 * z) if dim == 3 else 0.0)
+    else:
+        v = [x * y + z, y * z + x, x * z + y][:dim]
+        divv = y + z + (x if dim == 3 else 0.0)
+    d = oracle.dg_divergence_weak(mv, v)
+    _, wv, E, _, _ = oracle._pv_tables(P)
+    n = P + 1
+    h = [L[k] / N[k] for k in range(dim)]
+    W = np.ones((n,) * dim)
+    for k in range(dim):
+        shp = [1] * dim
+        shp[dim - 1 - k] = n
+        W = W * (wv * 0.5 * h[k]).reshape(shp)
+    Xp = node_coords(dim, N, L, P - 1)
+    xp, yp = Xp[0], Xp[1]
+    zp = Xp[2] if dim == 3 else 0.0 * xp
+    psi = (xp ** 2 * yp + (zp * xp if dim == 3 else 0.0)) if P >= 3 else xp * yp + (zp if dim == 3 else 0.0)
+    gexact = ([2 * x * y + (z if dim == 3 else 0.0), x ** 2, x][:dim] if P >= 3 else [y, x + 0.0 * x, 1.0 + 0.0 * x][:dim])
+    g = oracle.dg_gradient_weak(mp, psi)
+    m = oracle.mass(mv)
+    inner = _interior(mv)
+    assert inner
+    for e in inner:
+        t = W * divv[e].reshape((n,) * dim)
+        for k in range(dim):
+            t = oracle._apply_1d(E.T, t, dim - 1 - k)
+        assert np.abs(d[e] - t.reshape(-1)).max() <= 1e-12 * max(np.abs(t).max(), 1e-300)
+        for c in range(dim):
+            assert np.abs(g[c][e] / m[e] - gexact[c][e]).max() <= 1e-12 * max(np.abs(gexact[c]).max(), 1.0)
+
+
+def test_dg_divergence_gradient_constants():
+    """Constant fields on a periodic mesh: D v = 0 and G psi = 0."""
+    dim, N, L, P = 3, (2, 3, 2), (1.0, 1.3, 0.8), 3
+    mv, mp = oracle.Mesh(dim, N, L, P), oracle.Mesh(dim, N, L, P - 1)
+    v = [np.full((mv.n_el, mv.npe), c) for c in (0.7, -0.2, 0.4)]
+    assert np.abs(oracle.dg_divergence_weak(mv, v)).max() < 1e-14
+    g = oracle.dg_gradient_weak(mp, np.full((mp.n_el, mp.npe), 2.5))
+    assert max(np.abs(x).max() for x in g) < 1e-13
 
 
 @pytest.mark.parametrize("dim,N,P", [(2, (3, 2), 3), (3, (2, 2, 2), 3)])
