@@ -366,7 +366,24 @@ def run_stage(dg, torch, stream, barrier, reps=2):
         if k > 0:
             times.append(a.elapsed_time(b))
     d = info.as_dict()
-    return {"workload": c4.name, "ms_per_stage": statistics.mean(times), "stages": reps,
+    # the explicit LLF convection alone, FP64-bound: algorithmic flops per element
+    # of the sum-factorised Gauss evaluation over the CUDA-event time
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    for _ in range(2):
+        dg.dg_convect_rhs(mv, v, vo)
+    barrier()
+    ev0.record(stream)
+    for _ in range(5):
+        dg.dg_convect_rhs(mv, v, vo)
+    ev1.record(stream)
+    barrier()
+    conv_ms = ev0.elapsed_time(ev1) / 5
+    n, Q = c4.P + 1, (3 * c4.P) // 2 + 1
+    interp = n ** 3 * Q + n * n * Q * Q + n * Q ** 3                  # GLL -> Gauss, per component
+    flops_el = 2 * (3 * interp + 9 * interp + 6 * Q ** 3) + 6 * 2 * (2 * 3 * (n * n * Q + n * Q * Q) + 3 * (Q * Q * n + Q * n * n) + 10 * Q * Q)
+    conv = {"ms": conv_ms, "flop_per_launch": flops_el * mv.n_el,
+            "tflops": flops_el * mv.n_el / (conv_ms * 1e-3) / 1e12}
+    return {"workload": c4.name, "ms_per_stage": statistics.mean(times), "stages": reps, "convect": conv,
             "pressure_P": c4.P_p, "pressure_iters": d["pressure"]["iters"],
             "velocity_iters": [x["iters"] for x in d["velocity"]], "tol": c4.tol,
             "dofs": {"velocity_per_component": mv.ndof, "pressure": mp.ndof}}
