@@ -136,14 +136,15 @@ dg_status dg_gradient(dg_mesh *mp, dg_mesh *mv, const double *psi, double *const
 
 /* One IMEX-RK stage i = 2 of Alg. 3 for constant viscosity nu, F_s = 0 and
  * periodic boundaries (the config-4 composition):
- *   line 4: v' = v + dt a_ex21 (F_c(v) + F_d1(v)),  F_c by dg_convect_rhs (LLF),
- *           F_d1 = -M^-1 A_0 v (the SIP operator at lam = 0, P:693 F_d1 = div nu grad v);
- *           the grad-div terms F_d2 + F_d3 (they cancel the divergence part) are not formed;
+ *   line 4: v' = v + dt a_ex21 (F_c + F_d + F_d3)(v),  F_c by dg_convect_rhs (LLF),
+ *           F_d1 = -M^-1 A_0 v (the SIP operator at lam = 0, P:693 F_d1 = div nu grad v) and,
+ *           for constant nu, F_d2 = -F_d3 = nu grad div v = nu M^-1 G M_p^-1 D v with the DG
+ *           pair below (F_d + F_d3 = F_d1 - nu grad div v: the rotational form);
  *   line 5: -lap psi = -div v' on the pressure mesh mp (degree P-1; reading A9):
  *           SIP Poisson with the weak DG divergence of v' as rhs (b = -D v'), solved
  *           by dg_pcg_solve (lam = 0: mean projection, reading A8) from psi = 0;
  *   line 6: v'' = v' - M^-1 G psi with the weak DG gradient G (dg_gradient);
- *   line 8: g = v'' + dt (a_im21 - a_ex21) F_d1(v);
+ *   line 8: g = v'' + dt [(a_im21 - a_ex21) F_d1(v) - a_ex21 F_d3(v)];
  *   line 9: per component, solve v - dt a_im22 nu lap v = g, i.e. lam = 1/(dt a_im22),
  *           f = lam g (reading A4), by dg_pcg_solve from the initial guess v''.
  * The projection is approximate (the SIP pressure operator is not -D M^-1 G), as in the
@@ -162,6 +163,42 @@ typedef struct {
 dg_status dg_imex_stage(dg_mesh *mv, dg_mesh *mp, double dt, double a_ex21, double a_im21, double a_im22,
                         double nu, const double *const v[3], double *const vout[3], double *psi, double tol,
                         int maxit, dg_stage_info *info);
+
+/* One step of an IMEX Runge-Kutta method (Alg. 3) for constant nu,
+ * F_s = 0, periodic boundaries, with the CK-type tableaux of the paper's appendix
+ * (implicit DIRK with a_im[0][0] = 0 and a strictly lower explicit tableau, equal
+ * nodes c).  With constant nu, F_d2 = -F_d3 = nu grad(div u), formed with the DG
+ * pair as nu M^-1 G M_p^-1 D u, so that the explicit viscous part of line 4 is the rotational,
+ * divergence-free form F_d + F_d3 = F_d1 - nu grad div u.  Stage 1: v_1 = v.
+ * Stages i = 2..s: line 4 v'_i = v + dt sum_j a_ex[i][j] (F_c + F_d1 - nu grad div u)_j,
+ * lines 5-6 (projection with the DG divergence/gradient pair and the SIP Poisson solve on
+ * mp), line 8 g_i = v''_i + dt sum_j [(a_im - a_ex)[i][j] F_d1,j + a_ex[i][j] nu grad div u_j],
+ * line 9 (Helmholtz solves, lam = 1/(dt a_im[i][i]), from the guess v''_i; a stage with
+ * a_im[i][i] = 0 takes v_i = g_i); line 11: v = v_s + dt sum_i [(b_ex - a_ex[s])_i F_c,i +
+ * (b_im - a_im[s])_i F_d1,i] (F_d2 + F_d3 = 0).  The final projection (lines 12-15) is
+ * skipped for constant nu.
+ * v[c] (c < dim): DEVICE velocity, in: v^n, out: v^{n+1}; psi: DEVICE pressure workspace (the
+ * last stage's psi'' on exit).  Workspace (3 s + 2) dim velocity fields, owned by mv.
+ * Synchronous.  DG_EINVAL for a malformed tableau (s outside [2, 8], a non-explicit first
+ * stage, upper-triangular entries) or bad scalars; solver errors as dg_pcg_solve. */
+#define DG_RK_MAX_STAGES 8
+typedef struct {
+    int s;
+    double c[DG_RK_MAX_STAGES];
+    double a_im[DG_RK_MAX_STAGES][DG_RK_MAX_STAGES];
+    double a_ex[DG_RK_MAX_STAGES][DG_RK_MAX_STAGES];
+    double b_im[DG_RK_MAX_STAGES];
+    double b_ex[DG_RK_MAX_STAGES];
+} dg_tableau;
+
+typedef struct {
+    int stages;          /* implicit stages performed (s - 1)                 */
+    int pressure_iters;  /* CG iterations summed over the Poisson solves     */
+    int velocity_iters;  /* CG iterations summed over the Helmholtz solves   */
+} dg_step_info;
+
+dg_status dg_imex_rk_step(dg_mesh *mv, dg_mesh *mp, const dg_tableau *tab, double dt, double nu,
+                          double *const v[3], double *psi, double tol, int maxit, dg_step_info *info);
 
 /* Host-buffer variants: same operations on HOST arrays; H2D and D2H copies through
  * mesh-owned device staging buffers are part of the call (allocated on first use). */

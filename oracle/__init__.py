@@ -218,7 +218,9 @@ def imex_stage(mv: Mesh, mp: Mesh, dt, a_ex21, a_im21, a_im22, nu, v, tol=1e-14)
     m = mass(mv)
     Fc = convect(mv, v)                                                     # F_c(v)
     Fd = [-sip_apply(mv, 0.0, v[c], nu_const=nu) / m for c in range(dim)]  # F_d1(v) = -M^-1 A_0 v
-    vp = [np.asarray(v[c]) + dt * a_ex21 * (Fc[c] + Fd[c]) for c in range(dim)]         # line 4
+    gd = dg_gradient_weak(mp, dg_divergence_weak(mv, v) / mass(mp))        # grad div v
+    Fg = [nu * gd[c] / m for c in range(dim)]                               # = F_d2 = -F_d3
+    vp = [np.asarray(v[c]) + dt * a_ex21 * (Fc[c] + Fd[c] - Fg[c]) for c in range(dim)]  # line 4
     fp = -dg_divergence_weak(mv, vp) / mass(mp)                             # line 5 rhs: b = -D v'
     psi, *_ = pcg_solve(mp, 0.0, fp, nu_const=1.0, tol=tol)                 # line 5 (lam = 0)
     gw = dg_gradient_weak(mp, psi)
@@ -226,7 +228,7 @@ def imex_stage(mv: Mesh, mp: Mesh, dt, a_ex21, a_im21, a_im22, nu, v, tol=1e-14)
     lam = 1.0 / (dt * a_im22)
     out = []
     for c in range(dim):
-        g = vpp[c] + dt * (a_im21 - a_ex21) * Fd[c]                         # line 8
+        g = vpp[c] + dt * ((a_im21 - a_ex21) * Fd[c] + a_ex21 * Fg[c])      # line 8
         u, *_ = pcg_solve(mv, lam, lam * g, nu_const=nu, tol=tol)           # line 9
         out.append(u)
     return out, psi, vpp
@@ -367,3 +369,63 @@ def dg_gradient_weak(mp: Mesh, psi):
                 idx[ax(d)] = P if side else 0
                 outs[c][e][tuple(idx)] += val
     return [o.reshape(mp.n_el, n ** dim) for o in outs]
+
+
+# ---------------------------------------------------------------------------
+# IMEX Runge-Kutta step (Alg. 3) composed from the oracle pieces.
+# Tableaux typed from the paper's appendix, independently of the product's.
+# ---------------------------------------------------------------------------
+ORACLE_TABLEAUX = {
+    "RK-CB3e": dict(  # implicit (left), explicit (right)
+        a_im=[[0, 0, 0, 0], [0, 1 / 3, 0, 0], [0, 1 / 2, 1 / 2, 0], [0, 3 / 4, -1 / 4, 1 / 2]],
+        a_ex=[[0, 0, 0, 0], [1 / 3, 0, 0, 0], [0, 1, 0, 0], [0, 3 / 4, 1 / 4, 0]],
+        b_im=[0, 3 / 4, -1 / 4, 1 / 2], b_ex=[0, 3 / 4, -1 / 4, 1 / 2]),
+    "RK-ARS3": dict(
+        a_im=[[0, 0, 0, 0, 0], [0, 1 / 2, 0, 0, 0], [0, 1 / 6, 1 / 2, 0, 0], [0, -1 / 2, 1 / 2, 1 / 2, 0],
+              [0, 3 / 2, -3 / 2, 1 / 2, 1 / 2]],
+        a_ex=[[0, 0, 0, 0, 0], [1 / 2, 0, 0, 0, 0], [11 / 18, 1 / 18, 0, 0, 0], [5 / 6, -5 / 6, 1 / 2, 0, 0],
+              [1 / 4, 7 / 4, 3 / 4, -7 / 4, 0]],
+        b_im=[0, 3 / 2, -3 / 2, 1 / 2, 1 / 2], b_ex=[1 / 4, 7 / 4, 3 / 4, -7 / 4, 0]),
+}
+
+
+def imex_rk_step(mv: Mesh, mp: Mesh, tab, dt, nu, v, tol=1e-14):
+    """One step of Alg. 3 under the readings of include/dg.h dg_imex_rk_step (constant nu,
+    F_s = 0, F_d2 = -F_d3 = nu grad div u with the DG pair, final projection skipped):
+    returns v^{n+1} (dim arrays)."""
+    dim = mv.dim
+    m, mpm = mass(mv), mass(mp)
+    A_im, A_ex = np.asarray(tab["a_im"], float), np.asarray(tab["a_ex"], float)
+    s = A_im.shape[0]
+
+    def forces(u):
+        gd = dg_gradient_weak(mp, dg_divergence_weak(mv, u) / mpm)                   # grad div u
+        return (convect(mv, u), [-sip_apply(mv, 0.0, u[c], nu_const=nu) / m for c in range(dim)],
+                [nu * gd[c] / m for c in range(dim)])
+
+    Fc, Fd, Fg = [None] * s, [None] * s, [None] * s
+    Fc[0], Fd[0], Fg[0] = forces([np.asarray(x, float) for x in v])
+    u = None
+    for i in range(1, s):
+        # line 4 with F_d + F_d3 = F_d1 - nu grad div u (constant nu; rotational form)
+        vp = [np.asarray(v[c], float) + dt * sum(A_ex[i, j] * (Fc[j][c] + Fd[j][c] - Fg[j][c]) for j in range(i))
+              for c in range(dim)]
+        psi, *_ = pcg_solve(mp, 0.0, -dg_divergence_weak(mv, vp) / mpm, nu_const=1.0, tol=tol)  # line 5
+        gw = dg_gradient_weak(mp, psi)
+        vpp = [vp[c] - gw[c] / m for c in range(dim)]                                   # line 6
+        u = []
+        for c in range(dim):
+            g = vpp[c] + dt * sum((A_im[i, j] - A_ex[i, j]) * Fd[j][c] + A_ex[i, j] * Fg[j][c]
+                                  for j in range(i))                                    # line 8
+            if A_im[i, i] > 0:
+                lam = 1.0 / (dt * A_im[i, i])
+                x, *_ = pcg_solve(mv, lam, lam * g, nu_const=nu, tol=tol)                # line 9
+                u.append(x)
+            else:
+                u.append(g)
+        Fc[i], Fd[i], Fg[i] = forces(u)
+    out = []
+    for c in range(dim):                                                                # line 11
+        out.append(u[c] + dt * sum((tab["b_ex"][j] - A_ex[s - 1, j]) * Fc[j][c]
+                                   + (tab["b_im"][j] - A_im[s - 1, j]) * Fd[j][c] for j in range(s)))
+    return out

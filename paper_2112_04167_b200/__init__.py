@@ -20,6 +20,8 @@ from ._capi import (  # noqa: F401
     Mesh,
     SolveInfo,
     StageInfo,
+    StepInfo,
+    Tableau,
     dg_check_field,
     dg_convect_rhs,
     dg_divergence,
@@ -28,6 +30,7 @@ from ._capi import (  # noqa: F401
     dg_helmholtz_apply,
     dg_helmholtz_apply_host,
     dg_helmholtz_diag,
+    dg_imex_rk_step,
     dg_imex_stage,
     dg_last_error,
     dg_mesh_create,
@@ -45,3 +48,4 @@ from ._capi import (  # noqa: F401
     dg_version,
     library_path,
 )
+from .tableaux import TABLEAUX  # noqa: F401,E402

@@ -43,6 +43,35 @@ class StageInfo(ctypes.Structure):
         return {"pressure": self.pressure.as_dict(), "velocity": [x.as_dict() for x in self.velocity]}
 
 
+RK_MAX = 8
+
+
+class Tableau(ctypes.Structure):
+    _fields_ = [("s", _i), ("c", _d * RK_MAX), ("a_im", (_d * RK_MAX) * RK_MAX), ("a_ex", (_d * RK_MAX) * RK_MAX),
+                ("b_im", _d * RK_MAX), ("b_ex", _d * RK_MAX)]
+
+    @classmethod
+    def from_dict(cls, t):
+        tab = cls()
+        s = len(t["c"])
+        tab.s = s
+        for i in range(s):
+            tab.c[i] = float(t["c"][i])
+            tab.b_im[i] = float(t["b_im"][i])
+            tab.b_ex[i] = float(t["b_ex"][i])
+            for j in range(s):
+                tab.a_im[i][j] = float(t["a_im"][i][j])
+                tab.a_ex[i][j] = float(t["a_ex"][i][j])
+        return tab
+
+
+class StepInfo(ctypes.Structure):
+    _fields_ = [("stages", _i), ("pressure_iters", _i), ("velocity_iters", _i)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
 def _sig(name, res, args):
     f = getattr(_lib, name)
     f.restype = res
@@ -66,6 +95,8 @@ _c = {
     "dg_helmholtz_diag": _sig("dg_helmholtz_diag", _i, [_vp, _d, _vp, _d, _vp]),
     "dg_pcg_solve": _sig("dg_pcg_solve", _i, [_vp, _d, _vp, _d, _vp, _d, _i, _vp, ctypes.POINTER(SolveInfo)]),
     "dg_convect_rhs": _sig("dg_convect_rhs", _i, [_vp, ctypes.POINTER(_vp), ctypes.POINTER(_vp)]),
+    "dg_imex_rk_step": _sig("dg_imex_rk_step", _i, [_vp, _vp, ctypes.POINTER(Tableau), _d, _d, ctypes.POINTER(_vp),
+                                                    _vp, _d, _i, ctypes.POINTER(StepInfo)]),
     "dg_divergence": _sig("dg_divergence", _i, [_vp, _vp, ctypes.POINTER(_vp), _vp]),
     "dg_gradient": _sig("dg_gradient", _i, [_vp, _vp, _vp, ctypes.POINTER(_vp)]),
     "dg_imex_stage": _sig("dg_imex_stage", _i, [_vp, _vp, _d, _d, _d, _d, _d, ctypes.POINTER(_vp),
@@ -252,6 +283,16 @@ def dg_convect_rhs(m: Mesh, v, out):
     vin = (_vp * 3)(*([_ptr(x) for x in v] + [None] * (3 - len(v))))
     vout = (_vp * 3)(*([_ptr(x) for x in out] + [None] * (3 - len(out))))
     _check(_c["dg_convect_rhs"](m.handle, vin, vout))
+
+
+def dg_imex_rk_step(mv: Mesh, mp: Mesh, tableau, dt, nu, v, psi, tol, maxit) -> StepInfo:
+    """One IMEX-RK step (Alg. 3) in place on v -- include/dg.h.  tableau: dict (tableaux.py) or Tableau."""
+    tab = tableau if isinstance(tableau, Tableau) else Tableau.from_dict(tableau)
+    vv = (_vp * 3)(*([_ptr(x) for x in v] + [None] * (3 - len(v))))
+    info = StepInfo()
+    _check(_c["dg_imex_rk_step"](mv.handle, mp.handle, ctypes.byref(tab), dt, nu, vv, _ptr(psi), tol, maxit,
+                                 ctypes.byref(info)), info)
+    return info
 
 
 def dg_divergence(mv: Mesh, mp: Mesh, v, div_weak):

@@ -161,6 +161,7 @@ struct dg_mesh {
     std::vector<cudaEvent_t> ev;
     // IMEX stage workspace (velocity mesh: F_c[0..dim), A v; pressure mesh: rhs)
     double *sf[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+    std::vector<double *> rk;  // IMEX-RK step workspace (velocity fields)
     int *d_flag = nullptr;
     long long launches = 0;
 };
@@ -702,6 +703,7 @@ void dg_mesh_destroy(dg_mesh *m)
     if (m->hscal) cudaFreeHost(m->hscal);
     if (m->comm) nccl()->CommDestroy(m->comm);
     for (cudaEvent_t e : m->ev) cudaEventDestroy(e);
+    for (double *b : m->rk) cudaFree(b);
     if (m->cs_in) cudaStreamDestroy(m->cs_in);
     if (m->cs_out) cudaStreamDestroy(m->cs_out);
     delete m;
@@ -919,6 +921,26 @@ dg_status dg_imex_stage(dg_mesh *mv, dg_mesh *mp, double dt, double a_ex21, doub
                                 Fc[c], mv->st));
         mv->launches += 1;
     }
+    // line 4's explicit viscous part in rotational form (constant nu):
+    // F_d + F_d3 = F_d1 - nu grad div v  ->  v' -= dt a_ex21 nu M^-1 G M_p^-1 D v.  In line 8
+    // the -a_ex21 F_d3 term adds it back, so f_H = lam g is unchanged.
+    double *gw[3] = {Av, mv->sf[4], mv->sf[5]};
+    {
+        const double *vin[3] = {v[0], v[1], dim == 3 ? v[2] : nullptr};
+        CKS(div_impl(mv, vin, mp->sf[0]));
+        CK(launch_scale_minv(gp, mp->mass_e, 1.0, mp->sf[0], mp->sf[0], mv->st));
+        mv->launches += 1;
+        CKS(grad_impl(mp, mv, mp->sf[0], gw));
+        for (int c = 0; c < dim; ++c) {
+            LinComb lc;
+            lc.x0 = vout[c];
+            lc.c0 = 1.0;
+            lc.w = gw[c];
+            lc.cm = -dt * a_ex21 * nu;
+            CK(launch_lincomb(g, lc, mv->mass_e, vout[c], mv->st));
+            mv->launches += 1;
+        }
+    }
     // line 5: -lap psi = -div v' on the P-1 mesh: b = -D v' (weak DG divergence), f = M_p^-1 b
     CKS(div_impl(mv, vout, mp->sf[0]));
     CK(launch_scale_minv(gp, mp->mass_e, -1.0, mp->sf[0], mp->sf[0], mv->st));
@@ -929,7 +951,6 @@ dg_status dg_imex_stage(dg_mesh *mv, dg_mesh *mp, double dt, double a_ex21, doub
     if (info) info->pressure = ip;
     if (s != DG_OK) return s;
     // line 6: v'' = v' - M^-1 G psi (weak DG gradient), and line 8's rhs follows (f_H -= lam M^-1 G psi)
-    double *gw[3] = {Av, mv->sf[4], mv->sf[5]};
     CKS(grad_impl(mp, mv, psi, gw));
     for (int c = 0; c < dim; ++c) {
         CK(launch_stage_project(g, mv->mass_e, lamH, gw[c], vout[c], Fc[c], mv->st));
@@ -942,6 +963,179 @@ dg_status dg_imex_stage(dg_mesh *mv, dg_mesh *mp, double dt, double a_ex21, doub
         if (info) info->velocity[c] = iv;
         if (s != DG_OK) return s;
     }
+    return DG_OK;
+}
+
+dg_status dg_imex_rk_step(dg_mesh *mv, dg_mesh *mp, const dg_tableau *tab, double dt, double nu,
+                          double *const v[3], double *psi, double tol, int maxit, dg_step_info *info)
+{
+    if (!mv || !mp || !tab || !v || !psi) return set_error(DG_EINVAL, "null argument");
+    CKS(check_pair(mv, mp));
+    const int S = tab->s, dim = mv->g.dim;
+    if (S < 2 || S > DG_RK_MAX_STAGES) return set_error(DG_EINVAL, "tableau: 2 <= s <= DG_RK_MAX_STAGES");
+    if (tab->a_im[0][0] != 0.0 || tab->c[0] != 0.0)
+        return set_error(DG_EINVAL, "tableau: the first stage must be explicit (a_im[0][0] = c[0] = 0)");
+    for (int i = 0; i < S; ++i) {
+        if (!(tab->a_im[i][i] >= 0.0)) return set_error(DG_EINVAL, "tableau: a_im[i][i] must be >= 0");
+        for (int j = i; j < S; ++j)
+            if (tab->a_ex[i][j] != 0.0 || (j > i && tab->a_im[i][j] != 0.0))
+                return set_error(DG_EINVAL, "tableau: a_ex strictly lower, a_im lower triangular");
+    }
+    if (!(dt > 0.0) || !(nu > 0.0 && std::isfinite(nu)) || !(tol > 0.0) || maxit < 1)
+        return set_error(DG_EINVAL, "need dt > 0, nu > 0, tol > 0, maxit >= 1");
+    for (int c = 0; c < dim; ++c)
+        if (!v[c]) return set_error(DG_EINVAL, "null component pointer");
+    cudaStream_t mp_stream = mp->st;
+    mp->st = mv->st;
+    struct Restore {
+        dg_mesh *m;
+        cudaStream_t s;
+        ~Restore() { m->st = s; }
+    } restore{mp, mp_stream};
+    const Geom &g = mv->g, &gp = mp->g;
+    const size_t bv = sizeof(double) * (size_t)mv->ndof;
+    const int need = (3 * S + 2) * dim;
+    while ((int)mv->rk.size() < need) {
+        double *b = nullptr;
+        CKS(alloc((void **)&b, bv));
+        mv->rk.push_back(b);
+    }
+    CKS(stage(mp, &mp->sf[0], sizeof(double) * (size_t)mp->ndof));
+    auto Fc = [&](int i, int c) { return mv->rk[(i * dim + c)]; };
+    auto Fd = [&](int i, int c) { return mv->rk[(S + i) * dim + c]; };
+    auto Fg = [&](int i, int c) { return mv->rk[(2 * S + i) * dim + c]; };  // nu grad(div u_i)
+    auto VP = [&](int c) { return mv->rk[3 * S * dim + c]; };
+    auto TM = [&](int c) { return mv->rk[(3 * S + 1) * dim + c]; };
+    dg_step_info inf{};
+    // stage forces: F_c, F_d1 = -M^-1 A_0 u and the grad-div term nu grad(div u)
+    // = nu M^-1 G M_p^-1 D u with the DG pair (constant nu: F_d2 = -F_d3 = nu grad div u)
+    auto forces = [&](int i, double *const *u) -> dg_status {
+        double *out[3] = {Fc(i, 0), Fc(i, 1), dim == 3 ? Fc(i, 2) : nullptr};
+        const double *uin[3] = {u[0], u[1], dim == 3 ? u[2] : nullptr};
+        CKS(dg_convect_rhs(mv, uin, out));
+        for (int c = 0; c < dim; ++c) {
+            CKS(apply_impl(mv, 0.0, nullptr, nu, u[c], TM(c)));
+            LinComb lc;
+            lc.w = TM(c);
+            lc.cm = -1.0;
+            CK(launch_lincomb(g, lc, mv->mass_e, Fd(i, c), mv->st));
+            mv->launches += 1;
+        }
+        double *tmg[3] = {TM(0), TM(1), dim == 3 ? TM(2) : nullptr};
+        CKS(div_impl(mv, uin, mp->sf[0]));
+        CK(launch_scale_minv(gp, mp->mass_e, 1.0, mp->sf[0], mp->sf[0], mv->st));
+        mv->launches += 1;
+        CKS(grad_impl(mp, mv, mp->sf[0], tmg));
+        for (int c = 0; c < dim; ++c) {
+            LinComb lc;
+            lc.w = TM(c);
+            lc.cm = nu;
+            CK(launch_lincomb(g, lc, mv->mass_e, Fg(i, c), mv->st));
+            mv->launches += 1;
+        }
+        return DG_OK;
+    };
+    CKS(forces(0, v));  // stage 1: v_1 = v
+    double *vp[3] = {VP(0), VP(1), dim == 3 ? VP(2) : nullptr};
+    double *tm[3] = {TM(0), TM(1), dim == 3 ? TM(2) : nullptr};
+    for (int i = 1; i < S; ++i) {
+        // line 4: v'_i = v + dt sum_j a_ex[i][j] (F_c + F_d + F_d3)_j, with (constant nu)
+        // F_d + F_d3 = F_d1 - nu grad div u_j: the rotational, divergence-free form
+        for (int c = 0; c < dim; ++c) {
+            LinComb lc;
+            lc.x0 = v[c];
+            lc.c0 = 1.0;
+            for (int j = 0; j < i; ++j) {
+                if (tab->a_ex[i][j] == 0.0) continue;
+                lc.c[lc.n] = dt * tab->a_ex[i][j];
+                lc.y[lc.n++] = Fc(j, c);
+                lc.c[lc.n] = dt * tab->a_ex[i][j];
+                lc.y[lc.n++] = Fd(j, c);
+                lc.c[lc.n] = -dt * tab->a_ex[i][j];
+                lc.y[lc.n++] = Fg(j, c);
+            }
+            CK(launch_lincomb(g, lc, mv->mass_e, vp[c], mv->st));
+            mv->launches += 1;
+        }
+        // lines 5-6: pressure Poisson with the weak DG divergence, v'' = v' - M^-1 G psi
+        CKS(div_impl(mv, vp, mp->sf[0]));
+        CK(launch_scale_minv(gp, mp->mass_e, -1.0, mp->sf[0], mp->sf[0], mv->st));
+        mv->launches += 1;
+        CK(cudaMemsetAsync(psi, 0, sizeof(double) * (size_t)mp->ndof, mv->st));
+        dg_solve_info ip{};
+        dg_status st = pcg_impl(mp, 0.0, nullptr, 1.0, mp->sf[0], tol, maxit, psi, &ip);
+        inf.pressure_iters += ip.iters;
+        if (st != DG_OK) {
+            if (info) *info = inf;
+            return st;
+        }
+        CKS(grad_impl(mp, mv, psi, tm));
+        for (int c = 0; c < dim; ++c) {
+            LinComb lc;
+            lc.x0 = vp[c];
+            lc.c0 = 1.0;
+            lc.w = tm[c];
+            lc.cm = -1.0;
+            CK(launch_lincomb(g, lc, mv->mass_e, vp[c], mv->st));
+            mv->launches += 1;
+        }
+        // lines 8-9: g_i = v'' + dt sum_j [(a_im - a_ex)[i][j] F_d1,j - a_ex[i][j] F_d3,j],
+        // F_d3,j = -nu grad div u_j ;  v_i - dt a_ii nu lap v_i = g_i
+        const double aii = tab->a_im[i][i];
+        const double lam = aii > 0.0 ? 1.0 / (dt * aii) : 1.0;
+        for (int c = 0; c < dim; ++c) {
+            LinComb lc;
+            lc.x0 = vp[c];
+            lc.c0 = lam;
+            for (int j = 0; j < i; ++j) {
+                const double cj = tab->a_im[i][j] - tab->a_ex[i][j];
+                if (cj != 0.0) {
+                    lc.c[lc.n] = lam * dt * cj;
+                    lc.y[lc.n++] = Fd(j, c);
+                }
+                if (tab->a_ex[i][j] != 0.0) {
+                    lc.c[lc.n] = lam * dt * tab->a_ex[i][j];
+                    lc.y[lc.n++] = Fg(j, c);
+                }
+            }
+            CK(launch_lincomb(g, lc, mv->mass_e, tm[c], mv->st));  // f = lam g_i
+            mv->launches += 1;
+            if (aii > 0.0) {
+                dg_solve_info iv{};
+                st = pcg_impl(mv, lam, nullptr, nu, tm[c], tol, maxit, vp[c], &iv);
+                inf.velocity_iters += iv.iters;
+                if (st != DG_OK) {
+                    if (info) *info = inf;
+                    return st;
+                }
+            } else {
+                CK(cudaMemcpyAsync(vp[c], tm[c], bv, cudaMemcpyDeviceToDevice, mv->st));
+            }
+        }
+        CKS(forces(i, vp));
+        inf.stages += 1;
+    }
+    // line 11: v = v_s + dt sum_i [(b_ex - a_ex[s])_i F_c,i + (b_im - a_im[s])_i F_d1,i]
+    for (int c = 0; c < dim; ++c) {
+        LinComb lc;
+        lc.x0 = vp[c];
+        lc.c0 = 1.0;
+        for (int j = 0; j < S; ++j) {
+            const double ce = tab->b_ex[j] - tab->a_ex[S - 1][j], ci = tab->b_im[j] - tab->a_im[S - 1][j];
+            if (ce != 0.0) {
+                lc.c[lc.n] = dt * ce;
+                lc.y[lc.n++] = Fc(j, c);
+            }
+            if (ci != 0.0) {
+                lc.c[lc.n] = dt * ci;
+                lc.y[lc.n++] = Fd(j, c);
+            }
+        }
+        CK(launch_lincomb(g, lc, mv->mass_e, v[c], mv->st));
+        mv->launches += 1;
+    }
+    CK(cudaStreamSynchronize(mv->st));
+    if (info) *info = inf;
     return DG_OK;
 }
 

@@ -149,6 +149,17 @@ struct DivGradParams {  // geometry: the velocity mesh's (degree P); pressure de
     double *gout[3] = {nullptr, nullptr, nullptr};      // grad: weak gradient (velocity layout)
 };
 cudaError_t launch_dg_div(const Geom &gv, const DivGradParams &a, cudaStream_t st);
+struct LinComb {  // out = c0 x0 + sum_k c[k] y[k] (+ cm w / m)
+    static constexpr int MAXT = 16;
+    const double *x0 = nullptr;
+    double c0 = 0.0;
+    int n = 0;
+    double c[MAXT];
+    const double *y[MAXT];
+    const double *w = nullptr;
+    double cm = 0.0;
+};
+cudaError_t launch_lincomb(const Geom &g, const LinComb &lc, const double *mass_e, double *out, cudaStream_t st);
 cudaError_t launch_scale_minv(const Geom &g, const double *mass_e, double c, const double *in, double *out,
                               cudaStream_t st);
 cudaError_t launch_stage_project(const Geom &g, const double *mass_e, double lamH, const double *gw, double *vp,

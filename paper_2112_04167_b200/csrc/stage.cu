@@ -83,6 +83,18 @@ __global__ void k_scale_minv(long long ndof, int npe, const double *mass_e, doub
         out[t] = c * in[t] / mass_e[t % npe];
 }
 
+// out = c0 x0 + sum_k c_k y_k  (+ cm * w / m when w != null) -- the stage combinations of the
+// IMEX-RK step driver (Alg. 3 lines 4, 6, 8, 11)
+__global__ void k_lincomb(long long ndof, int npe, LinComb lc, const double *mass_e, double *out)
+{
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < ndof; t += (long long)gridDim.x * blockDim.x) {
+        double s = lc.x0 ? lc.c0 * lc.x0[t] : 0.0;
+        for (int k = 0; k < lc.n; ++k) s = fma(lc.c[k], lc.y[k][t], s);
+        if (lc.w) s = fma(lc.cm, lc.w[t] / mass_e[t % npe], s);
+        out[t] = s;
+    }
+}
+
 // projection (Alg. 3 line 6) and its effect on the Helmholtz rhs (line 8):
 // v'' = v' - M^-1 G psi ;  f_H -= lam M^-1 G psi
 __global__ void k_stage_project(long long ndof, int npe, const double *mass_e, double lamH, const double *gw,
@@ -352,6 +364,13 @@ cudaError_t launch_scale_minv(const Geom &g, const double *mass_e, double c, con
 {
     const long long nd = g.nel * g.npe;
     k_scale_minv<<<vblocks(nd), 256, 0, st>>>(nd, g.npe, mass_e, c, in, out);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_lincomb(const Geom &g, const LinComb &lc, const double *mass_e, double *out, cudaStream_t st)
+{
+    const long long nd = g.nel * g.npe;
+    k_lincomb<<<vblocks(nd), 256, 0, st>>>(nd, g.npe, lc, mass_e, out);
     return cudaGetLastError();
 }
 

@@ -123,3 +123,58 @@ def test_stage_viscous_decay_of_a_shear_mode():
     assert np.abs(out[0] - expect).max() < 1e-5
     assert np.abs(out[1]).max() < 1e-9
     assert np.abs(psi).max() < 1e-6
+
+
+@pytest.mark.parametrize("name", ["RK-CB3e", "RK-ARS3"])
+def test_oracle_tableaux_consistency(name):
+    """Row sums of both tableaux give the same nodes c (CK structure, P:279-281); b sums to 1;
+    the explicit part is strictly lower triangular and a_im[0][0] = 0."""
+    t = oracle.ORACLE_TABLEAUX[name]
+    A_im, A_ex = np.array(t["a_im"]), np.array(t["a_ex"])
+    assert np.allclose(A_im.sum(1), A_ex.sum(1), atol=1e-15)
+    assert abs(sum(t["b_im"]) - 1) < 1e-15 and abs(sum(t["b_ex"]) - 1) < 1e-15
+    assert np.allclose(np.triu(A_ex), 0) and A_im[0, 0] == 0 and np.allclose(np.triu(A_im, 1), 0)
+
+
+@pytest.mark.parametrize("name", ["RK-CB3e", "RK-ARS3"])
+def test_rk_step_keeps_a_uniform_flow(name):
+    """v = const is an exact steady solution: every stage force vanishes, the step returns v."""
+    dim, N, L, P = 2, (3, 2), (1.0, 1.3), 3
+    mv, mp = oracle.Mesh(dim, N, L, P), oracle.Mesh(dim, N, L, P - 1)
+    v = [np.full((mv.n_el, mv.npe), c) for c in (0.7, -0.2)]
+    out = oracle.imex_rk_step(mv, mp, oracle.ORACLE_TABLEAUX[name], 0.05, 0.02, v)
+    for c in range(dim):
+        assert np.abs(out[c] - v[c]).max() < 1e-12
+
+
+@pytest.mark.parametrize("name,z", [("RK-CB3e", -0.3), ("RK-ARS3", -0.7)])
+def test_rk_step_shear_mode_is_the_dirk_stability_function(name, z):
+    """v = (sin(2 pi y / L_y) mode of the discrete operator, 0): F_c = 0, div v = 0, so one step
+    is the implicit (DIRK) tableau applied to u' = mu u on the mode's discrete eigenvalue mu:
+    u^{n+1} = R(dt mu) u^n with R(z) = 1 + z b^T (I - z A)^{-1} 1 (Alg. 3 lines 4, 8, 9, 11)."""
+    dim, N, L, P = 2, (2, 4), (1.0, 1.0), 5
+    mv, mp = oracle.Mesh(dim, N, L, P), oracle.Mesh(dim, N, L, P - 1)
+    # the discrete y-mode: eigenvector of M^-1 A_0 restricted to fields constant in x
+    X = node_coords(dim, N, L, P)
+    u0 = np.sin(2 * np.pi * X[1])
+    nu = 0.02
+    A = oracle.sip_dense(mv, 0.0, nu_const=nu)
+    m = oracle.mass(mv).reshape(-1)
+    w, V = np.linalg.eigh(A / np.sqrt(np.outer(m, m)))
+    # component of u0 along its dominant eigenvector (symmetric scaling M^-1/2 A M^-1/2)
+    y = np.sqrt(m) * u0.reshape(-1)
+    k = int(np.argmax(np.abs(V.T @ y)))
+    sel = np.abs(w - w[k]) <= 1e-9 * w[k]  # the eigenvalue is degenerate (x and y modes, sin and cos)
+    ev = V[:, sel] @ (V[:, sel].T @ y) / np.sqrt(m)   # u0's component in the eigenspace of M^-1 A
+    mu = -w[k]
+    ev = ev.reshape(mv.n_el, mv.npe) / np.abs(ev).max()
+    dt = z / mu
+    t = oracle.ORACLE_TABLEAUX[name]
+    A_im = np.array(t["a_im"])
+    s = A_im.shape[0]
+    R = 1 + z * np.array(t["b_im"]) @ np.linalg.solve(np.eye(s) - z * A_im, np.ones(s))
+    out = oracle.imex_rk_step(mv, mp, t, dt, nu, [ev, np.zeros_like(ev)])
+    # 1e-7: the eigen-projected mode carries ~1e-8 x-mode impurities (degenerate eigenspace);
+    # a wrong tableau entry or sign moves the result by O(|z| 1e-1)
+    assert np.abs(out[0] - R * ev).max() <= 1e-7
+    assert np.abs(out[1]).max() <= 1e-7
