@@ -64,7 +64,8 @@ typedef struct {
                             collocation points; reading A7)             */
     double removed_mean; /* lam == 0: mass-weighted mean removed from f (A8)    */
     double f_norm;       /* ||f||_2 after the lam == 0 projection               */
-    double kappa_est;    /* Lanczos estimate of cond(D^-1 A) from CG alpha/beta */
+    double kappa_est;    /* Lanczos estimate of cond(B A) from CG alpha/beta (B = the
+                            mesh's preconditioner, dg_mesh_set_precond)        */
 } dg_solve_info;
 
 /* NCCL unique id for multi-rank meshes (call on rank 0, broadcast the 128 bytes with
@@ -100,7 +101,8 @@ dg_status dg_helmholtz_apply(dg_mesh *m, double lam, const double *nu, double nu
 /* diag = diag(A) (the Jacobi preconditioner of the north star). */
 dg_status dg_helmholtz_diag(dg_mesh *m, double lam, const double *nu, double nu_const, double *diag);
 
-/* Solve A u = M f (M = GLL-lumped mass, reading A6) by Jacobi-preconditioned CG.
+/* Solve A u = M f (M = GLL-lumped mass, reading A6) by preconditioned CG (Jacobi unless
+ * dg_mesh_set_precond chose the two-level Schwarz preconditioner).
  * f: DEVICE nodal rhs.  u: DEVICE, initial guess on entry, solution on exit.
  * Stops when ||M^-1 r||_2 <= tol ||f||_2 (reading A7) -> DG_OK, or after maxit
  * iterations -> DG_ENOTCONV (u and info hold the last iterate).  lam == 0 (pressure
@@ -109,6 +111,28 @@ dg_status dg_helmholtz_diag(dg_mesh *m, double lam, const double *nu, double nu_
  * mean (reading A8).  info may be NULL.  Collective for multi-rank meshes. */
 dg_status dg_pcg_solve(dg_mesh *m, double lam, const double *nu, double nu_const, const double *f,
                        double tol, int maxit, double *u, dg_solve_info *info);
+
+/* Preconditioner of every later dg_pcg_solve on this mesh (including the solves inside
+ * dg_imex_stage / dg_imex_rk_step).  DG_PC_JACOBI (default): diag(A)^-1 (the north star).
+ * DG_PC_SCHWARZ2: two-level additive Schwarz (the paper solves with
+ * "Krylov-accelerated Schwarz/multigrid methods", formula not given; reading in
+ * DESIGN.md §9):
+ *     B r = sum_K R_K^T A_KK^-1 R_K r + P_1 A_c^+ P_1^T r,   A_c = P_1^T A P_1,
+ * non-overlapping element blocks (exact, by fast diagonalisation of the Kronecker-sum block)
+ * plus the continuous vertex-based Q1 space on the same mesh as coarse space (exact solve by
+ * a real Fourier diagonalisation; pseudo-inverse on the constants for lam = 0).  Needs a
+ * constant viscosity (solves with a nu field return DG_EUNSUPPORTED), 2 <= N_d <= 64 and
+ * P >= 2 (else DG_EUNSUPPORTED here).  Multi-rank: the coarse residual is all-reduced
+ * (NV = prod N_d doubles per iteration) and every rank solves the coarse problem. */
+#define DG_PC_JACOBI 0
+#define DG_PC_SCHWARZ2 1
+dg_status dg_mesh_set_precond(dg_mesh *m, int precond);
+int dg_mesh_get_precond(const dg_mesh *m);
+
+/* z = B r with the DG_PC_SCHWARZ2 preconditioner above for (lam, nu_const) (independent of
+ * the mesh's setting; for tests and for use as a smoother).  r, z: DEVICE [local_ndof], no
+ * aliasing.  Collective for multi-rank meshes. */
+dg_status dg_schwarz_apply(dg_mesh *m, double lam, double nu_const, const double *r, double *z);
 
 /* Explicit convective tendency F_c = -div(v v) with LLF fluxes, nodal (M^-1 applied,
  * GLL-lumped), Gauss quadrature with Q = floor(3P/2)+1 points per direction

@@ -429,3 +429,108 @@ def imex_rk_step(mv: Mesh, mp: Mesh, tab, dt, nu, v, tol=1e-14):
         out.append(u[c] + dt * sum((tab["b_ex"][j] - A_ex[s - 1, j]) * Fc[j][c]
                                    + (tab["b_im"][j] - A_im[s - 1, j]) * Fd[j][c] for j in range(s)))
     return out
+
+
+# ---------------------------------------------------------------------------
+# Two-level additive Schwarz preconditioner for the SIP system (
+# P:1045-1046 "Krylov-accelerated Schwarz/multigrid methods ... for solving the implicit
+# pressure and diffusion problems").  The paper gives no formula; DESIGN.md §9 states the
+# reading taken (both sides):
+#     B r = sum_K R_K^T A_KK^-1 R_K r  +  P_1 A_c^+ P_1^T r,   A_c = P_1^T A P_1,
+# with R_K the restriction to the nodes of element K (non-overlapping subdomains = elements,
+# A_KK the diagonal block of the assembled SIP matrix) and P_1 the prolongation of the
+# continuous vertex-based Q1 space on the same mesh to the DG nodes (trilinear hats
+# (1 -/+ xi)/2 evaluated at the GLL nodes, periodic vertex numbering).  A_c^+ is the
+# pseudo-inverse (lam = 0: the constant null space, reading A8).  Definitions written out:
+# A_KK and A_c by applying the oracle's own operator to unit / hat vectors, dense numpy
+# linear algebra (library routines) for the inverses.  Small meshes only.
+# ---------------------------------------------------------------------------
+def q1_prolongation(mesh: Mesh):
+    """Dense P_1 [ndof, NV]: column v = the periodic Q1 hat of vertex v at every DG node.
+    Vertex index v = vx + Nx (vy + Ny vz), vertex (vx, vy, vz) at x = vx h (periodic)."""
+    dim, N, n = mesh.dim, mesh.N, mesh.n
+    xi, _ = gll(mesh.P)
+    hat = [(1.0 - xi) / 2.0, (1.0 + xi) / 2.0]  # corner 0 (left), corner 1 (right)
+    NV = mesh.n_el
+    Pm = np.zeros((mesh.n_el, mesh.npe, NV))
+    for e in range(mesh.n_el):
+        ec = _elem_coords(mesh, e)
+        for corner in range(2 ** dim):
+            a = [(corner >> d) & 1 for d in range(dim)]
+            v = _elem_index(mesh, [ec[d] + a[d] for d in range(dim)])
+            if dim == 2:
+                val = np.outer(hat[a[1]], hat[a[0]])
+            else:
+                val = hat[a[2]][:, None, None] * hat[a[1]][None, :, None] * hat[a[0]][None, None, :]
+            Pm[e, :, v] += val.reshape(-1)  # += : with N_d = 1 two corners are one vertex
+    return Pm.reshape(mesh.ndof, NV)
+
+
+def q1_coarse_operator(mesh: Mesh, lam, nu_const=1.0):
+    """A_c = P_1^T A P_1 (dense [NV, NV]), the oracle's operator applied to every hat."""
+    Pm = q1_prolongation(mesh)
+    Ac = np.zeros((Pm.shape[1], Pm.shape[1]))
+    for v in range(Pm.shape[1]):
+        Ac[:, v] = Pm.T @ sip_apply(mesh, lam, Pm[:, v], nu_const=nu_const).reshape(-1)
+    return Ac, Pm
+
+
+def element_block(mesh: Mesh, lam, e, nu_const=1.0):
+    """A_KK [npe, npe]: rows and columns of element e of the assembled SIP matrix."""
+    B = np.zeros((mesh.npe, mesh.npe))
+    for j in range(mesh.npe):
+        u = np.zeros(mesh.ndof)
+        u[e * mesh.npe + j] = 1.0
+        B[:, j] = sip_apply(mesh, lam, u, nu_const=nu_const, elems=[e]).reshape(-1)
+    return B
+
+
+class Schwarz2:
+    """B = sum_K R_K^T A_KK^-1 R_K + P_1 A_c^+ P_1^T (see above); constant nu."""
+
+    def __init__(self, mesh: Mesh, lam, nu_const=1.0, coarse=True):
+        self.mesh = mesh
+        self.binv = [np.linalg.inv(element_block(mesh, lam, e, nu_const)) for e in range(mesh.n_el)]
+        self.coarse = coarse
+        if coarse:
+            Ac, self.Pm = q1_coarse_operator(mesh, lam, nu_const)
+            self.Acp = np.linalg.pinv(Ac, rcond=1e-13) if lam == 0.0 else np.linalg.inv(Ac)
+
+    def __call__(self, r):
+        r = np.asarray(r, dtype=np.float64).reshape(self.mesh.n_el, self.mesh.npe)
+        z = np.stack([self.binv[e] @ r[e] for e in range(self.mesh.n_el)])
+        if self.coarse:
+            z = z + (self.Pm @ (self.Acp @ (self.Pm.T @ r.reshape(-1)))).reshape(z.shape)
+        return z
+
+
+def pcg_precond(mesh: Mesh, lam, f, B, nu_const=1.0, tol=1e-12, maxit=10000):
+    """Preconditioned CG for A u = M f with preconditioner z = B(r) (plain numpy loop; the
+    stopping rule of reading A7, lam = 0 handled as reading A8).  Returns (u, iters)."""
+    m = mass(mesh).reshape(-1)
+    f = np.asarray(f, dtype=np.float64).reshape(-1)
+    if lam == 0.0:
+        f = f - (m @ f) / m.sum()
+    fn = np.linalg.norm(f)
+    A = lambda x: sip_apply(mesh, lam, x, nu_const=nu_const).reshape(-1)
+    u = np.zeros_like(f)
+    r = m * f
+    z = B(r).reshape(-1)
+    p = z.copy()
+    rz = r @ z
+    for it in range(1, maxit + 1):
+        q = A(p)
+        a = rz / (p @ q)
+        u += a * p
+        r -= a * q
+        if lam == 0.0:
+            r -= r.mean()
+        if np.linalg.norm(r / m) <= tol * fn:
+            break
+        z = B(r).reshape(-1)
+        rz2 = r @ z
+        p = z + (rz2 / rz) * p
+        rz = rz2
+    if lam == 0.0:
+        u -= (m @ u) / m.sum()
+    return u.reshape(mesh.n_el, mesh.npe), it

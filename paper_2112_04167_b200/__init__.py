@@ -16,6 +16,8 @@ from ._capi import (  # noqa: F401
     DG_ENOTCONV,
     DG_EUNSUPPORTED,
     DG_OK,
+    DG_PC_JACOBI,
+    DG_PC_SCHWARZ2,
     DGError,
     Mesh,
     SolveInfo,
@@ -41,7 +43,10 @@ from ._capi import (  # noqa: F401
     dg_mesh_local_ndof,
     dg_mesh_mass,
     dg_mesh_node_coords,
+    dg_mesh_get_precond,
+    dg_mesh_set_precond,
     dg_mesh_set_stream,
+    dg_schwarz_apply,
     dg_nccl_unique_id,
     dg_pcg_solve,
     dg_pcg_solve_host,

@@ -95,6 +95,9 @@ _c = {
     "dg_helmholtz_diag": _sig("dg_helmholtz_diag", _i, [_vp, _d, _vp, _d, _vp]),
     "dg_pcg_solve": _sig("dg_pcg_solve", _i, [_vp, _d, _vp, _d, _vp, _d, _i, _vp, ctypes.POINTER(SolveInfo)]),
     "dg_convect_rhs": _sig("dg_convect_rhs", _i, [_vp, ctypes.POINTER(_vp), ctypes.POINTER(_vp)]),
+    "dg_mesh_set_precond": _sig("dg_mesh_set_precond", _i, [_vp, _i]),
+    "dg_mesh_get_precond": _sig("dg_mesh_get_precond", _i, [_vp]),
+    "dg_schwarz_apply": _sig("dg_schwarz_apply", _i, [_vp, _d, _d, _vp, _vp]),
     "dg_imex_rk_step": _sig("dg_imex_rk_step", _i, [_vp, _vp, ctypes.POINTER(Tableau), _d, _d, ctypes.POINTER(_vp),
                                                     _vp, _d, _i, ctypes.POINTER(StepInfo)]),
     "dg_divergence": _sig("dg_divergence", _i, [_vp, _vp, ctypes.POINTER(_vp), _vp]),
@@ -277,6 +280,24 @@ def dg_pcg_solve(m: Mesh, lam, nu, nu_const, f, tol, maxit, u, raise_on_notconv=
                             _ptr(u), ctypes.byref(info))
     _check(st, info, allow=() if raise_on_notconv else (DG_ENOTCONV,))
     return info
+
+
+DG_PC_JACOBI = 0
+DG_PC_SCHWARZ2 = 1
+
+
+def dg_mesh_set_precond(m: Mesh, precond):
+    """Preconditioner of later dg_pcg_solve calls on m: DG_PC_JACOBI or DG_PC_SCHWARZ2 -- include/dg.h."""
+    _check(_c["dg_mesh_set_precond"](m.handle, int(precond)))
+
+
+def dg_mesh_get_precond(m: Mesh) -> int:
+    return int(_c["dg_mesh_get_precond"](m.handle))
+
+
+def dg_schwarz_apply(m: Mesh, lam, nu_const, r, z):
+    """z = B r, the two-level additive Schwarz preconditioner -- include/dg.h."""
+    _check(_c["dg_schwarz_apply"](m.handle, float(lam), float(nu_const), _ptr(r), _ptr(z)))
 
 
 def dg_convect_rhs(m: Mesh, v, out):

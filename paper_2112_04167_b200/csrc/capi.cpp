@@ -164,6 +164,12 @@ struct dg_mesh {
     std::vector<double *> rk;  // IMEX-RK step workspace (velocity fields)
     int *d_flag = nullptr;
     long long launches = 0;
+    // two-level Schwarz preconditioner (schwarz.cu): tables for sw_nu, coarse workspace
+    int pc = DG_PC_JACOBI;
+    SwTab *d_sw = nullptr;
+    SwTab h_sw{};
+    double *d_swF = nullptr, *rc_el = nullptr, *chat = nullptr, *xc = nullptr, *rc = nullptr;
+    double sw_nu = -1.0;
 };
 
 #define CK(call)                                                                                         \
@@ -353,6 +359,127 @@ dg_status reduce_fin(dg_mesh *m, int G, int mode)
     return DG_OK;
 }
 
+// ---------------------------------------------------------------------------
+// two-level Schwarz preconditioner (schwarz.cu)
+// ---------------------------------------------------------------------------
+dg_status sw_check(const dg_mesh *m, const double *nu)
+{
+    if (nu) return set_error(DG_EUNSUPPORTED, "the Schwarz preconditioner needs a constant viscosity (nu == NULL)");
+    const char *why = nullptr;
+    if (!schwarz_supported(m->g, &why)) return set_error(DG_EUNSUPPORTED, why);
+    return DG_OK;
+}
+
+dg_status ensure_sw(dg_mesh *m, double nu_const)
+{
+    const Geom &g = m->g;
+    const long long NV = (long long)g.N[0] * g.N[1] * (g.dim == 3 ? g.N[2] : 1);
+    if (!m->d_sw) {
+        CKS(alloc((void **)&m->d_sw, sizeof(SwTab)));
+        CKS(alloc((void **)&m->d_swF, sizeof(double) * 3 * SW_NCMAX * SW_NCMAX));
+        CKS(alloc((void **)&m->rc_el, sizeof(double) * (size_t)g.nel * (g.dim == 3 ? 8 : 4)));
+        CKS(alloc((void **)&m->chat, sizeof(double) * (size_t)NV));
+        CKS(alloc((void **)&m->xc, sizeof(double) * (size_t)NV));
+        if (m->nranks > 1) CKS(alloc((void **)&m->rc, sizeof(double) * (size_t)NV));
+    }
+    if (m->sw_nu != nu_const) {
+        std::vector<double> F;
+        build_sw_tab(g, nu_const, &m->h_sw, F);
+        CK(cudaMemcpyAsync(m->d_sw, &m->h_sw, sizeof(SwTab), cudaMemcpyHostToDevice, m->st));
+        CK(cudaMemcpyAsync(m->d_swF, F.data(), sizeof(double) * F.size(), cudaMemcpyHostToDevice, m->st));
+        CK(cudaStreamSynchronize(m->st));  // F is a host temporary
+        m->sw_nu = nu_const;
+    }
+    return DG_OK;
+}
+
+// coarse part: x_c = A_c^+ P_1^T r from the element moments rc_el; r_c.x_c partials written
+// to partial[pslot + b] (b < sw_cz_grid) when `partial` is set
+dg_status sw_coarse(dg_mesh *m, double lam, double *partial, int pslot)
+{
+    const Geom &g = m->g;
+    SwCoarseParams c;
+    c.T = m->d_sw;
+    c.F = m->d_swF;
+    c.dim = g.dim;
+    c.lam = lam;
+    c.chat = m->chat;
+    c.xc = m->xc;
+    c.partial = partial;
+    c.pslot = pslot;
+    c.count_dot = m->rank == 0;
+    c.nel = g.nel;
+    if (m->nranks == 1) {
+        c.rc_el = m->rc_el;
+    } else {
+        const long long NV = (long long)g.N[0] * g.N[1] * (g.dim == 3 ? g.N[2] : 1);
+        CK(cudaMemsetAsync(m->rc, 0, sizeof(double) * (size_t)NV, m->st));
+        SwCoarseParams gl = c;
+        gl.rc_el = m->rc_el;
+        gl.rc = m->rc;
+        const int S = g.dim - 1;
+        const long long lay_el = S == 2 ? (long long)g.N[0] * g.N[1] : (long long)g.N[0];
+        CK(launch_sw_gather_local(gl, S, (int)(m->el_off / lay_el), g.Nl[S], m->st));
+        m->launches += 1;
+        CKS(allreduce(m, m->rc, (int)NV));
+        c.rc = m->rc;
+    }
+    for (int stage = 0; stage < 3; ++stage) CK(launch_sw_coarse(c, m->h_sw, stage, m->st));
+    m->launches += 3;
+    return DG_OK;
+}
+
+// z = B r (block part into z, rc_el moments; then the coarse solve and z += P_1 x_c)
+dg_status sw_apply_impl(dg_mesh *m, double lam, const double *r, double *z)
+{
+    SwBlockParams b;
+    b.T = m->d_sw;
+    b.lam = lam;
+    b.mode = SW_APPLY;
+    b.nel = m->g.nel;
+    b.rin = r;
+    b.z = z;
+    b.rc_el = m->rc_el;
+    b.mass_e = m->mass_e;
+    int grid = 0;
+    CK(launch_sw_block(m->g, m->h_sw, b, m->st, &grid));
+    m->launches += 1;
+    CKS(sw_coarse(m, lam, nullptr, 0));
+    SwPupdParams p;
+    p.T = m->d_sw;
+    p.nel = m->g.nel;
+    p.el_off = m->el_off;
+    p.zb = z;
+    p.xc = m->xc;
+    p.p = z;
+    CK(launch_sw_pupd(m->g, m->h_sw, p, m->st));
+    m->launches += 1;
+    return DG_OK;
+}
+
+// PCG preconditioner step (mode SW_INIT or SW_UPDATE): r update, z_b, moments, coarse solve,
+// r.z and residual partials -> reduce_fin(fin)
+dg_status sw_pcg_step(dg_mesh *m, double lam, int mode, int fin)
+{
+    SwBlockParams b;
+    b.T = m->d_sw;
+    b.lam = lam;
+    b.mode = mode;
+    b.nel = m->g.nel;
+    b.r = m->r;
+    b.q = m->q;
+    b.z = m->z;
+    b.rc_el = m->rc_el;
+    b.mass_e = m->mass_e;
+    b.s = m->scal;
+    b.partial = m->partial;
+    int grid = 0;
+    CK(launch_sw_block(m->g, m->h_sw, b, m->st, &grid));
+    m->launches += 1;
+    CKS(sw_coarse(m, lam, m->partial, grid));
+    return reduce_fin(m, grid + sw_cz_grid(m->h_sw), fin);
+}
+
 dg_status pcg_impl(dg_mesh *m, double lam, const double *nu, double nu_const, const double *f, double tol,
                    int maxit, double *u, dg_solve_info *info)
 {
@@ -370,10 +497,17 @@ dg_status pcg_impl(dg_mesh *m, double lam, const double *nu, double nu_const, co
     s0.maxit = maxit;
     CK(cudaMemcpyAsync(m->scal, &s0, sizeof(s0), cudaMemcpyHostToDevice, m->st));
 
+    // preconditioner: two-level Schwarz (dg_mesh_set_precond) or Jacobi
+    const bool sw = m->pc == DG_PC_SCHWARZ2;
+    if (sw) {
+        CKS(sw_check(m, nu));
+        CKS(ensure_sw(m, nu_const));
+    }
     // Jacobi preconditioner: D^-1 straight from the closed-form kernel where it applies
     bool self = false;
     for (int d = 0; d < g.dim; ++d) self = self || g.N[d] == 1;
-    if (!self) {
+    if (sw) {
+    } else if (!self) {
         Halo hd;
         if (multi && nu) {
             CKS(ensure_halos(m, false));
@@ -403,22 +537,63 @@ dg_status pcg_impl(dg_mesh *m, double lam, const double *nu, double nu_const, co
     CK(launch_pcg_init(g, f, m->q, m->r, m->mass_e, m->scal, m->partial, m->st));
     m->launches += 1;
     CKS(reduce_fin(m, VG, FIN_INIT));
-    CK(launch_pcg_init2(g, m->r, m->dinv, m->z, m->mass_e, m->scal, m->partial, m->st));
-    m->launches += 1;
-    CKS(reduce_fin(m, VG, FIN_INIT2));
+    if (sw) {
+        CKS(sw_pcg_step(m, lam, SW_INIT, FIN_INIT2));
+    } else {
+        CK(launch_pcg_init2(g, m->r, m->dinv, m->z, m->mass_e, m->scal, m->partial, m->st));
+        m->launches += 1;
+        CKS(reduce_fin(m, VG, FIN_INIT2));
+    }
     CK(cudaMemsetAsync(m->pa, 0, sizeof(double) * (size_t)m->ndof, m->st));
 
     double *p_old = m->pa, *p_new = m->pb;
     // split PCG step (pupd kernel + apply with the dot epilogue) where the v6 apply runs:
     // measured faster than the fused prologue of v5
-    const bool split = !multi && g.dim == 3 && apply3_split_pcg_ok(g, nu) && !getenv("DG_PCG_FUSED");
+    const bool split_ok = !multi && g.dim == 3 && apply3_split_pcg_ok(g, nu);
+    const bool split = !sw && split_ok && !getenv("DG_PCG_FUSED");
     int chunk = 4;
     for (;;) {
         CK(cudaMemcpyAsync(m->hscal, m->scal, sizeof(PcgScal), cudaMemcpyDeviceToHost, m->st));
         CK(cudaStreamSynchronize(m->st));
         if (m->hscal->done) break;
         for (int it = 0; it < chunk; ++it) {
-            if (split) {
+            if (sw) {
+                // x += alpha p, p = z_b + P_1 x_c + beta p (in place) ; q = A p ; Schwarz step
+                SwPupdParams pp;
+                pp.T = m->d_sw;
+                pp.nel = g.nel;
+                pp.el_off = m->el_off;
+                pp.zb = m->z;
+                pp.xc = m->xc;
+                pp.p_old = p_old;
+                pp.p = p_old;
+                pp.x = u;
+                pp.s = m->scal;
+                CK(launch_sw_pupd(g, m->h_sw, pp, m->st));
+                m->launches += 1;
+                if (split_ok) {
+                    PProl pro;
+                    pro.done = &m->scal->done;
+                    DotEpi epi;
+                    epi.partial = m->partial;
+                    int grid = 0;
+                    CKS(run_apply(m, lam, nu, nu_const, p_old, m->q, Halo{}, epi, pro, &grid));
+                    CKS(reduce_fin(m, grid, FIN_ALPHA));
+                } else {
+                    Halo h;
+                    if (multi) {
+                        CKS(ensure_halos(m, false));
+                        CKS(exchange(m, p_old, m->h_lo, m->h_hi));
+                        h.u_lo = m->h_lo;
+                        h.u_hi = m->h_hi;
+                    }
+                    CKS(run_apply(m, lam, nu, nu_const, p_old, m->q, h, DotEpi{}, PProl{}));
+                    CK(launch_dot_pq(g, p_old, m->q, m->scal, m->partial, m->st));
+                    m->launches += 1;
+                    CKS(reduce_fin(m, VG, FIN_ALPHA));
+                }
+                CKS(sw_pcg_step(m, lam, SW_UPDATE, FIN_BETA));
+            } else if (split) {
                 // x += alpha p, p = z + beta p (in place; x deferred by one iteration) ;
                 // q = A p with the dot epilogue (apply MODE 2) ; r, z update
                 CK(launch_pcg_pupd_x(g, u, p_old, m->z, m->scal, m->st));
@@ -471,7 +646,7 @@ dg_status pcg_impl(dg_mesh *m, double lam, const double *nu, double nu_const, co
         }
         chunk = std::min(chunk * 2, 32);
     }
-    if (split) {  // the deferred x update of the last iteration
+    if (split || sw) {  // the deferred x update of the last iteration
         CK(launch_pcg_xfinal(g, u, p_old, m->scal, m->st));
         m->launches += 1;
     }
@@ -652,7 +827,7 @@ dg_status dg_mesh_create(int dim, const int N[3], const double L[3], int P, int 
             done.push_back(m->device);
         }
     }
-    const int pcap = 2 * std::max(APPLY_GRID_MAX, vec_grid()) + 64;
+    const int pcap = 2 * (std::max(APPLY_GRID_MAX, std::max(vec_grid(), 148 * 12)) + SW_NCMAX * SW_NCMAX / 32) + 64;
     dg_status s;
     if ((s = alloc((void **)&m->partial, sizeof(double) * pcap)) != DG_OK) return fail(s);
     m->partial_cap = pcap;
@@ -691,7 +866,7 @@ void dg_mesh_destroy(dg_mesh *m)
     double *bufs[] = {m->r,    m->q,    m->pa,    m->pb,     m->dinv,   m->z,    m->partial,
                       m->sums, m->aux,  m->mass_e, m->hist,  m->h_lo,   m->h_hi, m->hn_lo,
                       m->hn_hi, m->st_a, m->st_b,  m->st_c,  m->sf[0], m->sf[1], m->sf[2], m->sf[3],
-                      m->sf[4], m->sf[5]};
+                      m->sf[4], m->sf[5], m->d_swF, m->rc_el, m->chat, m->xc, m->rc};
     for (double *b : bufs)
         if (b) cudaFree(b);
     for (int c = 0; c < 3; ++c) {
@@ -699,6 +874,7 @@ void dg_mesh_destroy(dg_mesh *m)
         if (m->hv_hi[c]) cudaFree(m->hv_hi[c]);
     }
     if (m->scal) cudaFree(m->scal);
+    if (m->d_sw) cudaFree(m->d_sw);
     if (m->d_flag) cudaFree(m->d_flag);
     if (m->hscal) cudaFreeHost(m->hscal);
     if (m->comm) nccl()->CommDestroy(m->comm);
@@ -760,6 +936,30 @@ dg_status dg_pcg_solve(dg_mesh *m, double lam, const double *nu, double nu_const
     if (!(tol > 0.0)) return set_error(DG_EINVAL, "tol must be > 0");
     if (maxit < 1) return set_error(DG_EINVAL, "maxit must be >= 1");
     return pcg_impl(m, lam, nu, nu_const, f, tol, maxit, u, info);
+}
+
+dg_status dg_mesh_set_precond(dg_mesh *m, int precond)
+{
+    if (!m) return set_error(DG_EINVAL, "null mesh");
+    if (precond != DG_PC_JACOBI && precond != DG_PC_SCHWARZ2) return set_error(DG_EINVAL, "unknown preconditioner");
+    if (precond == DG_PC_SCHWARZ2) {
+        const char *why = nullptr;
+        if (!schwarz_supported(m->g, &why)) return set_error(DG_EUNSUPPORTED, why);
+    }
+    m->pc = precond;
+    return DG_OK;
+}
+
+int dg_mesh_get_precond(const dg_mesh *m) { return m ? m->pc : -1; }
+
+dg_status dg_schwarz_apply(dg_mesh *m, double lam, double nu_const, const double *r, double *z)
+{
+    CKS(check_common(m, lam, nullptr, nu_const));
+    if (!r || !z) return set_error(DG_EINVAL, "null field pointer");
+    if (r == z) return set_error(DG_EINVAL, "r and z must not alias");
+    CKS(sw_check(m, nullptr));
+    CKS(ensure_sw(m, nu_const));
+    return sw_apply_impl(m, lam, r, z);
 }
 
 dg_status dg_convect_rhs(dg_mesh *m, const double *const v[3], double *const out[3])

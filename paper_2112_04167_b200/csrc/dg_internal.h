@@ -5,6 +5,7 @@
 
 #include <cstdint>
 #include <string>
+#include <vector>
 
 #include "dg.h"
 
@@ -209,5 +210,60 @@ cudaError_t launch_dot_pq(const Geom &g, const double *p, const double *q, const
                           cudaStream_t st);
 cudaError_t launch_recip(const Geom &g, const double *d, double *dinv, cudaStream_t st);
 cudaError_t launch_check_field(long long n, const double *x, int positive, int *bad, cudaStream_t st);
+
+// schwarz.cu -- two-level additive Schwarz preconditioner
+constexpr int SW_NCMAX = 64;     // coarse (vertex) grid: N_d <= 64 per direction
+struct SwTab {                   // device-resident tables of one (mesh, nu)
+    int Nc[3];                   // vertices per direction (= N_d; 1 for an absent direction)
+    double nu;
+    double S[3][NMAX * NMAX];    // S_d[i*n + k]: M-orthonormal eigenvectors of the 1-D block
+    double Lam[3][NMAX];         // its eigenvalues (K_d S = M_d S Lam)
+    double hat[2][NMAX];         // Q1 hats (1 - xi)/2, (1 + xi)/2 at the GLL nodes
+    double eK[3][SW_NCMAX], eM[3][SW_NCMAX];  // 1-D coarse circulant symbols per Fourier column
+};
+enum { SW_APPLY = 0, SW_INIT = 1, SW_UPDATE = 2 };
+struct SwBlockParams {
+    const SwTab *T = nullptr;
+    double lam = 0.0;
+    int mode = SW_APPLY;
+    long long nel = 0;
+    double *r = nullptr;            // INIT/UPDATE: residual, updated in place
+    const double *rin = nullptr;    // APPLY: input
+    const double *q = nullptr;      // UPDATE: A p
+    double *z = nullptr;            // out: block part z_b
+    double *rc_el = nullptr;        // out: [2^dim][nel] hat moments of r
+    const double *mass_e = nullptr; // element mass table [npe]
+    const PcgScal *s = nullptr;
+    double *partial = nullptr;      // [grid][2]: r.z_b, sum (r/m)^2
+};
+struct SwCoarseParams {
+    const SwTab *T = nullptr;
+    const double *F = nullptr;      // [3][SW_NCMAX^2] Fourier bases F_d[j*N + col]
+    int dim = 3;
+    double lam = 0.0;
+    const double *rc_el = nullptr;  // element moments [2^dim][nel] (single rank: gathered directly)
+    long long nel = 0;              // local elements
+    double *rc = nullptr;           // multi-rank: the all-reduced vertex vector (cfwd input)
+    double *chat = nullptr;         // spectral workspace [NV]
+    double *xc = nullptr;           // out: coarse solution [NV]
+    double *partial = nullptr;
+    int pslot = 0;                  // first partial slot of the column kernel
+    int count_dot = 1;              // multi-rank: only rank 0 contributes r_c.x_c
+};
+struct SwPupdParams {
+    const SwTab *T = nullptr;
+    long long nel = 0, el_off = 0;
+    const double *zb = nullptr, *xc = nullptr;
+    const double *p_old = nullptr;  // null: p = z_b + P_1 x_c (preconditioner apply)
+    double *p = nullptr, *x = nullptr;
+    const PcgScal *s = nullptr;     // alpha, beta, done (null: beta = 0)
+};
+bool schwarz_supported(const Geom &g, const char **why);
+void build_sw_tab(const Geom &g, double nu, SwTab *t, std::vector<double> &F);
+cudaError_t launch_sw_block(const Geom &g, const SwTab &h, const SwBlockParams &a, cudaStream_t st, int *grid);
+cudaError_t launch_sw_pupd(const Geom &g, const SwTab &h, const SwPupdParams &a, cudaStream_t st);
+cudaError_t launch_sw_coarse(const SwCoarseParams &a, const SwTab &h, int stage, cudaStream_t st);
+cudaError_t launch_sw_gather_local(const SwCoarseParams &a, int S, int off, int nl, cudaStream_t st);
+int sw_cz_grid(const SwTab &h);
 
 }  // namespace dg
