@@ -254,7 +254,7 @@ struct SwPupdParams {
     const SwTab *T = nullptr;
     long long nel = 0, el_off = 0;
     const double *zb = nullptr, *xc = nullptr;
-    const double *p_old = nullptr;  // null: p = z_b + P_1 x_c (preconditioner apply)
+    const double *p_old = nullptr;  // null: p = z_b + P_1 x_c (preconditioner apply); else == p (in place)
     double *p = nullptr, *x = nullptr;
     const PcgScal *s = nullptr;     // alpha, beta, done (null: beta = 0)
 };

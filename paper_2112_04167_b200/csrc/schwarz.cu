@@ -185,9 +185,9 @@ struct SwCfg {
     static constexpr int NPE = DIM == 3 ? n * n * n : n * n;
     static constexpr int NL = DIM == 3 ? n * n : n;  // lines per element per direction
     static constexpr int NT = 256;
-    // elements per CTA tile: <= 32 and the static shared memory (2 tiles, 2 node tables,
-    // x moments) within 46 KB
-    static constexpr int epc(int e) { return (e > 1 && (2 * e * NPE + 2 * NPE + 2 * e * NL) * 8 > 46000) ? epc(e - 1) : e; }
+    // elements per CTA tile: <= 32 and the block kernel's dynamic shared memory (3 tiles,
+    // 2 node tables, x moments) within 110 KB (two CTAs per SM at the largest degrees)
+    static constexpr int epc(int e) { return (e > 1 && (3 * e * NPE + 2 * NPE + 2 * e * NL) * 8 > 110000) ? epc(e - 1) : e; }
     static constexpr int EPC = epc(NT / NL > 32 ? 32 : (NT / NL < 1 ? 1 : NT / NL));
     static constexpr int NC = 1 << DIM;
 };
@@ -206,18 +206,42 @@ __device__ __forceinline__ void line_xform(const double (&S)[n * n], const doubl
 }
 
 template <int DIM, int n>
+struct SwBlkSmem {  // dynamic shared memory layout of k_sw_block (doubles)
+    using C = SwCfg<DIM, n>;
+    static constexpr int T = C::EPC * C::NPE;
+    static constexpr int R = 0, Q = T, A = 2 * T, INV = 3 * T, MI = INV + C::NPE, X = MI + C::NPE;
+    static constexpr int TOTAL = X + 2 * C::EPC * C::NL;
+    static constexpr int BYTES = TOTAL * 8;
+};
+
+__device__ __forceinline__ void cp_async8(double *dst, const double *src)
+{
+    const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
+
+// Per tile: [wait for the tile's r (, q) in sR (, sQ)] -> r update in place (+ global store,
+// stopping-rule partial) -> x forward (sR -> sA) and x hat moments -> [sR, sQ free: the next
+// tile's cp.async prefetch is issued] -> corner moments, y forward, z forward / scale / backward
+// (r.z_b = sum t^2 / (lam + L) in the same thread), y backward, x backward -> store z.
+template <int DIM, int n>
 __global__ void __launch_bounds__(256) k_sw_block(SwBlockParams a, const __grid_constant__ SwLine<n> L)
 {
     using C = SwCfg<DIM, n>;
+    using SM = SwBlkSmem<DIM, n>;
     constexpr int NPE = C::NPE, NL = C::NL, NT = C::NT, EPC = C::EPC, NC = C::NC;
-    __shared__ double sr[EPC * NPE], sa[EPC * NPE], sInv[NPE], sm[NPE], sx[EPC * NL * 2];
+    extern __shared__ double smem[];
+    double *sR = smem + SM::R, *sQ = smem + SM::Q, *sA = smem + SM::A, *sInv = smem + SM::INV,
+           *sMi = smem + SM::MI, *sx = smem + SM::X;
     __shared__ double red[8][2];
     for (int t = threadIdx.x; t < NPE; t += NT) {
         const int i = t % n, j = (t / n) % n, k = DIM == 3 ? t / (n * n) : 0;
         double den = a.lam + L.L[0][i] + L.L[1][j];
         if (DIM == 3) den += L.L[2][k];
         sInv[t] = 1.0 / den;
-        sm[t] = a.mass_e[t];
+        sMi[t] = 1.0 / a.mass_e[t];
     }
     const PcgScal *s = a.s;
     if (a.mode == SW_UPDATE && s->done) return;
@@ -228,28 +252,37 @@ __global__ void __launch_bounds__(256) k_sw_block(SwBlockParams a, const __grid_
     } else if (a.mode == SW_INIT) {
         shift = s->qmean;  // FIN_INIT stores the mean of r here (lam == 0), else 0
     }
+    const double *__restrict__ rsrc = a.mode == SW_APPLY ? a.rin : a.r;
+    auto prefetch = [&](long long e0n) {
+        const long long g0 = e0n * NPE;
+        const int cnt = (int)((a.nel - e0n < EPC ? a.nel - e0n : EPC) * NPE);
+        for (int t = threadIdx.x; t < cnt; t += NT) {
+            cp_async8(sR + t, rsrc + g0 + t);
+            if (a.mode == SW_UPDATE) cp_async8(sQ + t, a.q + g0 + t);
+        }
+        cp_async_commit();
+    };
     double acc_rz = 0.0, acc_res = 0.0;
     const int le = threadIdx.x / NL, ln = threadIdx.x % NL;
-    for (long long e0 = (long long)blockIdx.x * EPC; e0 < a.nel; e0 += (long long)gridDim.x * EPC) {
+    const long long stride = (long long)gridDim.x * EPC;
+    if ((long long)blockIdx.x * EPC < a.nel) prefetch((long long)blockIdx.x * EPC);
+    for (long long e0 = (long long)blockIdx.x * EPC; e0 < a.nel; e0 += stride) {
         const int ne = a.nel - e0 < EPC ? (int)(a.nel - e0) : EPC;
         const bool act = le < ne;
-        __syncthreads();  // previous tile's readers are done
+        cp_async_wait_all();
+        __syncthreads();  // the tile has landed; the previous tile's sA readers are done
         {
             const long long g0 = e0 * NPE;
             int tn = threadIdx.x % NPE;
             for (int t = threadIdx.x; t < ne * NPE; t += NT) {
-                double ri;
-                if (a.mode == SW_UPDATE) {
-                    ri = fma(-alpha, a.q[g0 + t] - shift, a.r[g0 + t]);
+                double ri = sR[t];
+                if (a.mode == SW_UPDATE) ri = fma(-alpha, sQ[t] - shift, ri);
+                else if (a.mode == SW_INIT) ri -= shift;
+                if (a.mode != SW_APPLY) {
                     a.r[g0 + t] = ri;
-                } else if (a.mode == SW_INIT) {
-                    ri = a.r[g0 + t] - shift;
-                    a.r[g0 + t] = ri;
-                } else {
-                    ri = a.rin[g0 + t];
+                    sR[t] = ri;
                 }
-                sr[t] = ri;
-                const double rm = ri / sm[tn];
+                const double rm = ri * sMi[tn];
                 acc_res = fma(rm, rm, acc_res);
                 tn += NT % NPE;
                 if (tn >= NPE) tn -= NPE;
@@ -261,7 +294,7 @@ __global__ void __launch_bounds__(256) k_sw_block(SwBlockParams a, const __grid_
         if (act) {
             const int b = le * NPE + ln * n;
 #pragma unroll
-            for (int m = 0; m < n; ++m) v[m] = sr[b + m];
+            for (int m = 0; m < n; ++m) v[m] = sR[b + m];
             double h0 = 0.0, h1 = 0.0;
 #pragma unroll
             for (int m = 0; m < n; ++m) {
@@ -272,18 +305,21 @@ __global__ void __launch_bounds__(256) k_sw_block(SwBlockParams a, const __grid_
             sx[(le * NL + ln) * 2 + 1] = h1;
             line_xform<n, true>(L.S[0], v, o);
 #pragma unroll
-            for (int m = 0; m < n; ++m) sa[b + m] = o[m];
+            for (int m = 0; m < n; ++m) sA[b + m] = o[m];
         }
         __syncthreads();
+        if (e0 + stride < a.nel) prefetch(e0 + stride);  // sR, sQ are free now
         // corner moments rc_el[c][e] = sum_{j,k} hat_cy(j) hat_cz(k) xmoment_cx(j,k)
         if (threadIdx.x < ne * NC) {
             const int el = threadIdx.x / NC, c = threadIdx.x % NC;
+            const double *xm = sx + el * NL * 2 + (c & 1);
             double acc = 0.0;
-            for (int l = 0; l < NL; ++l) {
-                const int j = l % n, k = DIM == 3 ? l / n : 0;
-                double hv = L.hat[(c >> 1) & 1][j];
-                if (DIM == 3) hv *= L.hat[(c >> 2) & 1][k];
-                acc = fma(hv, sx[(el * NL + l) * 2 + (c & 1)], acc);
+#pragma unroll
+            for (int k = 0; k < (DIM == 3 ? n : 1); ++k) {
+                double accj = 0.0;
+#pragma unroll
+                for (int j = 0; j < n; ++j) accj = fma(L.hat[(c >> 1) & 1][j], xm[2 * (j + n * k)], accj);
+                acc = DIM == 3 ? fma(L.hat[(c >> 2) & 1][k], accj, acc) : accj;
             }
             a.rc_el[(long long)c * a.nel + e0 + el] = acc;
         }
@@ -292,33 +328,37 @@ __global__ void __launch_bounds__(256) k_sw_block(SwBlockParams a, const __grid_
             if (act) {
                 const int i = ln % n, k = ln / n, b = le * NPE + i + n * n * k;
 #pragma unroll
-                for (int m = 0; m < n; ++m) v[m] = sa[b + m * n];
+                for (int m = 0; m < n; ++m) v[m] = sA[b + m * n];
                 line_xform<n, true>(L.S[1], v, o);
 #pragma unroll
-                for (int m = 0; m < n; ++m) sa[b + m * n] = o[m];
+                for (int m = 0; m < n; ++m) sA[b + m * n] = o[m];
             }
             __syncthreads();
-            // z forward, scale, z backward (line i,j)
+            // z forward, scale, z backward (line i,j); r.z_b = sum t^2 / (lam + L)
             if (act) {
                 const int b = le * NPE + ln;
 #pragma unroll
-                for (int m = 0; m < n; ++m) v[m] = sa[b + m * n * n];
+                for (int m = 0; m < n; ++m) v[m] = sA[b + m * n * n];
                 line_xform<n, true>(L.S[2], v, o);
 #pragma unroll
-                for (int m = 0; m < n; ++m) o[m] *= sInv[ln + m * n * n];
+                for (int m = 0; m < n; ++m) {
+                    const double oi = o[m] * sInv[ln + m * n * n];
+                    acc_rz = fma(oi, o[m], acc_rz);
+                    o[m] = oi;
+                }
                 line_xform<n, false>(L.S[2], o, v);
 #pragma unroll
-                for (int m = 0; m < n; ++m) sa[b + m * n * n] = v[m];
+                for (int m = 0; m < n; ++m) sA[b + m * n * n] = v[m];
             }
             __syncthreads();
             // y backward
             if (act) {
                 const int i = ln % n, k = ln / n, b = le * NPE + i + n * n * k;
 #pragma unroll
-                for (int m = 0; m < n; ++m) v[m] = sa[b + m * n];
+                for (int m = 0; m < n; ++m) v[m] = sA[b + m * n];
                 line_xform<n, false>(L.S[1], v, o);
 #pragma unroll
-                for (int m = 0; m < n; ++m) sa[b + m * n] = o[m];
+                for (int m = 0; m < n; ++m) sA[b + m * n] = o[m];
             }
             __syncthreads();
         } else {
@@ -326,13 +366,17 @@ __global__ void __launch_bounds__(256) k_sw_block(SwBlockParams a, const __grid_
             if (act) {
                 const int b = le * NPE + ln;
 #pragma unroll
-                for (int m = 0; m < n; ++m) v[m] = sa[b + m * n];
+                for (int m = 0; m < n; ++m) v[m] = sA[b + m * n];
                 line_xform<n, true>(L.S[1], v, o);
 #pragma unroll
-                for (int m = 0; m < n; ++m) o[m] *= sInv[ln + m * n];
+                for (int m = 0; m < n; ++m) {
+                    const double oi = o[m] * sInv[ln + m * n];
+                    acc_rz = fma(oi, o[m], acc_rz);
+                    o[m] = oi;
+                }
                 line_xform<n, false>(L.S[1], o, v);
 #pragma unroll
-                for (int m = 0; m < n; ++m) sa[b + m * n] = v[m];
+                for (int m = 0; m < n; ++m) sA[b + m * n] = v[m];
             }
             __syncthreads();
         }
@@ -340,21 +384,18 @@ __global__ void __launch_bounds__(256) k_sw_block(SwBlockParams a, const __grid_
         if (act) {
             const int b = le * NPE + ln * n;
 #pragma unroll
-            for (int m = 0; m < n; ++m) v[m] = sa[b + m];
+            for (int m = 0; m < n; ++m) v[m] = sA[b + m];
             line_xform<n, false>(L.S[0], v, o);
 #pragma unroll
-            for (int m = 0; m < n; ++m) sa[b + m] = o[m];
+            for (int m = 0; m < n; ++m) sA[b + m] = o[m];
         }
         __syncthreads();
         {
             const long long g0 = e0 * NPE;
-            for (int t = threadIdx.x; t < ne * NPE; t += NT) {
-                const double zi = sa[t];
-                a.z[g0 + t] = zi;
-                acc_rz = fma(sr[t], zi, acc_rz);
-            }
+            for (int t = threadIdx.x; t < ne * NPE; t += NT) a.z[g0 + t] = sA[t];
         }
     }
+    cp_async_wait_all();
     // partials: r.z_b, sum (r/m)^2 (fixed-order CTA reduction)
     acc_rz = warp_sum(acc_rz);
     acc_res = warp_sum(acc_res);
@@ -550,6 +591,11 @@ __global__ void __launch_bounds__(256) k_sw_pupd(SwPupdParams a, const __grid_co
         beta = a.s->beta;
     }
     const int N0 = T->Nc[0], N1 = T->Nc[1], N2 = T->Nc[2];
+    // p is updated in place (a.p_old == a.p or null): distinct streams z_b, p, x
+    const bool upd = a.p_old != nullptr;
+    const double *__restrict__ zb = a.zb;
+    double *__restrict__ p = a.p;
+    double *__restrict__ x = a.x;
     for (long long e0 = (long long)blockIdx.x * EPC; e0 < a.nel; e0 += (long long)gridDim.x * EPC) {
         const int ne = a.nel - e0 < EPC ? (int)(a.nel - e0) : EPC;
         __syncthreads();
@@ -564,32 +610,42 @@ __global__ void __launch_bounds__(256) k_sw_pupd(SwPupdParams a, const __grid_co
             sxv[el][c] = a.xc[(long long)vx + (long long)N0 * (vy + (long long)N1 * vz)];
         }
         __syncthreads();
+        // all loads of the tile first (up to 3 PER doubles in flight per thread), then the
+        // interpolation and the stores
         const long long g0 = e0 * NPE;
-        int tn = threadIdx.x % NPE, el = threadIdx.x / NPE;
-        for (int t = threadIdx.x; t < ne * NPE; t += NT) {
-            // trilinear (bilinear) interpolation of the element's vertex values at node tn
-            const int i = tn % n, j = (tn / n) % n;
-            const double hx0 = sh[0][i], hx1 = sh[1][i], hy0 = sh[0][j], hy1 = sh[1][j];
-            const double *xv = sxv[el];
-            double zc = hy0 * fma(hx1, xv[1], hx0 * xv[0]) + hy1 * fma(hx1, xv[3], hx0 * xv[2]);
-            if (DIM == 3) {
-                const int k = tn / (n * n);
-                const double zc1 = hy0 * fma(hx1, xv[5], hx0 * xv[4]) + hy1 * fma(hx1, xv[7], hx0 * xv[6]);
-                zc = fma(sh[1][k], zc1, sh[0][k] * zc);
+        const int cnt = ne * NPE;
+        constexpr int PER = (EPC * NPE + NT - 1) / NT;
+        double rz[PER], rp[PER], rx[PER];
+#pragma unroll
+        for (int q = 0; q < PER; ++q) {
+            const int t = threadIdx.x + q * NT;
+            if (t < cnt) {
+                rz[q] = zb[g0 + t];
+                rp[q] = upd ? p[g0 + t] : 0.0;
+                rx[q] = (upd && x) ? x[g0 + t] : 0.0;
             }
-            const double zb = a.zb[g0 + t];
-            if (a.p_old) {
-                const double po = a.p_old[g0 + t];
-                if (a.x) a.x[g0 + t] = fma(alpha, po, a.x[g0 + t]);
-                a.p[g0 + t] = fma(beta, po, zb + zc);
-            } else {
-                a.p[g0 + t] = zb + zc;
-            }
-            tn += NT % NPE;
-            el += NT / NPE;
-            if (tn >= NPE) {
-                tn -= NPE;
-                el += 1;
+        }
+#pragma unroll
+        for (int q = 0; q < PER; ++q) {
+            const int t = threadIdx.x + q * NT;
+            if (t < cnt) {
+                const int el = t / NPE, tn = t - el * NPE;
+                // trilinear (bilinear) interpolation of the element's vertex values at node tn
+                const int i = tn % n, j = (tn / n) % n;
+                const double hx0 = sh[0][i], hx1 = sh[1][i], hy0 = sh[0][j], hy1 = sh[1][j];
+                const double *xv = sxv[el];
+                double zc = hy0 * fma(hx1, xv[1], hx0 * xv[0]) + hy1 * fma(hx1, xv[3], hx0 * xv[2]);
+                if (DIM == 3) {
+                    const int k = tn / (n * n);
+                    const double zc1 = hy0 * fma(hx1, xv[5], hx0 * xv[4]) + hy1 * fma(hx1, xv[7], hx0 * xv[6]);
+                    zc = fma(sh[1][k], zc1, sh[0][k] * zc);
+                }
+                if (upd) {
+                    if (x) x[g0 + t] = fma(alpha, rp[q], rx[q]);
+                    p[g0 + t] = fma(beta, rp[q], rz[q] + zc);
+                } else {
+                    p[g0 + t] = rz[q] + zc;
+                }
             }
         }
     }
@@ -620,7 +676,13 @@ struct SwDispatch {
         if (g > 148LL * 6) g = 148LL * 6;
         if (g < 1) g = 1;
         *grid = (int)g;
-        k_sw_block<DIM, P + 1><<<(int)g, 256, 0, st>>>(a, make_line<P + 1>(h));
+        constexpr int smem = SwBlkSmem<DIM, P + 1>::BYTES;
+        static bool attr = false;
+        if (!attr) {
+            cudaFuncSetAttribute(k_sw_block<DIM, P + 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+            attr = true;
+        }
+        k_sw_block<DIM, P + 1><<<(int)g, 256, smem, st>>>(a, make_line<P + 1>(h));
         return cudaGetLastError();
     }
     template <int P>
