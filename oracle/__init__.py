@@ -534,3 +534,120 @@ def pcg_precond(mesh: Mesh, lam, f, B, nu_const=1.0, tol=1e-12, maxit=10000):
     if lam == 0.0:
         u -= (m @ u) / m.sum()
     return u.reshape(mesh.n_el, mesh.npe), it
+
+
+# ---------------------------------------------------------------------------
+# Variable viscosity: Alg. 3 line 7 nu_i = nu(v''_i) with the model of
+# P:1218-1224, the explicit viscous parts F_d2 = div(nu grad(v)^T) and F_d3 = -grad(nu div v)
+# (P:693-703), line 11 and the final projection (lines 12-15).  Readings (DESIGN.md
+# §9): the derivatives in F_d2 / F_d3 are the velocity-level central-flux DG derivative
+#     (Dc u)_i = m_i^-1 [ -sum_K sum_q W_q u(x_q) d_c phi_i(x_q) + sum_F sum_q W^F_q {u} n_c [phi_i] ]
+# (GLL_P quadrature), so F_d2,c = sum_e D_e(nu D_c v_e), F_d3,c = -D_c(nu sum_e D_e v_e); the
+# stage forces of stage i use nu_i (the viscosity of its implicit solve).
+# ---------------------------------------------------------------------------
+def dg_derivative(mesh: Mesh, u):
+    """Nodal central-flux DG derivatives [D_0 u, ..., D_{dim-1} u] of the degree-P field u
+    ([N_el, (P+1)^d]); each [N_el, (P+1)^d]."""
+    P, dim, n = mesh.P, mesh.dim, mesh.n
+    xv, wv = gll(P)
+    Dv = np.zeros((n, n))
+    for i, x in enumerate(xv):
+        _, Dv[i] = lagrange(P, xv, x)
+    h = [mesh.L[d] / mesh.N[d] for d in range(dim)]
+    us = np.asarray(u, dtype=np.float64).reshape((mesh.n_el,) + (n,) * dim)
+    ax = lambda d: dim - 1 - d
+    Wq = np.ones((n,) * dim)
+    for d in range(dim):
+        shp = [1] * dim
+        shp[ax(d)] = n
+        Wq = Wq * (wv * 0.5 * h[d]).reshape(shp)
+    outs = [np.zeros((mesh.n_el,) + (n,) * dim) for _ in range(dim)]
+    for e in range(mesh.n_el):
+        ec = _elem_coords(mesh, e)
+        for c in range(dim):
+            # volume: -(u, d_c phi_i) = -(2/h_c) sum_q D[q_c][i_c] W_q u(q)
+            outs[c][e] -= _apply_1d((Dv * (2.0 / h[c])).T, Wq * us[e], ax(c))
+            tdirs = [dd for dd in range(dim) if dd != c]
+            Wf = np.ones((n,) * (dim - 1))
+            for k, dd in enumerate(tdirs):
+                shp = [1] * (dim - 1)
+                shp[dim - 2 - k] = n
+                Wf = Wf * (wv * 0.5 * h[dd]).reshape(shp)
+            for side in (0, 1):
+                cn = list(ec)
+                cn[c] += 1 if side else -1
+                en = _elem_index(mesh, cn)
+                own = np.take(us[e], P if side else 0, axis=ax(c))
+                nbr = np.take(us[en], 0 if side else P, axis=ax(c))
+                idx = [slice(None)] * dim
+                idx[ax(c)] = P if side else 0
+                outs[c][e][tuple(idx)] += (1.0 if side else -1.0) * Wf * 0.5 * (own + nbr)  # W^F {u} n_c [phi_i]
+    m = mass(mesh)
+    return [o.reshape(mesh.n_el, mesh.npe) / m for o in outs]
+
+
+def visc_model(v, nu0, nu1, vmax):
+    """nu(v) = nu0 + nu1 (|v| / v_max)^2, pointwise at the nodes."""
+    return nu0 + nu1 * sum(np.asarray(x, float) ** 2 for x in v) / vmax ** 2
+
+
+def viscous_explicit(mv: Mesh, v, nu):
+    """(F_d3, F_d2 + F_d3) of the nodal velocity v with the nodal viscosity field nu."""
+    dim = mv.dim
+    Dv = [dg_derivative(mv, v[e]) for e in range(dim)]            # Dv[e][c] = D_c v_e
+    div = sum(Dv[e][e] for e in range(dim))
+    Fd3 = [-g for g in dg_derivative(mv, nu * div)]
+    Fd2 = [sum(dg_derivative(mv, nu * Dv[e][c])[e] for e in range(dim)) for c in range(dim)]
+    return Fd3, [Fd2[c] + Fd3[c] for c in range(dim)]
+
+
+def imex_rk_step_vv(mv: Mesh, mp: Mesh, tab, dt, visc, v, fs=None, final_projection=True, tol=1e-14):
+    """One step of Alg. 3 with the solution-dependent viscosity nu(v) =
+    nu0 + nu1 (|v|/v_max)^2 (visc = (nu0, nu1, vmax)) and forcing fs[j][c] (nodal, at
+    t + c_j dt; None = 0), under the readings of include/dg.h dg_imex_rk_step_vv."""
+    dim = mv.dim
+    m, mpm = mass(mv), mass(mp)
+    A_im, A_ex = np.asarray(tab["a_im"], float), np.asarray(tab["a_ex"], float)
+    s = A_im.shape[0]
+    nu0, nu1, vmax = visc
+    F = (lambda j, c: 0.0) if fs is None else (lambda j, c: np.asarray(fs[j][c], float))
+
+    def forces(u, nu):
+        Fd3, Fd23 = viscous_explicit(mv, u, nu)
+        Fd1 = [-sip_apply(mv, 0.0, u[c], nu=nu) / m for c in range(dim)]         # F_d1 = div nu grad u
+        return convect(mv, u), Fd1, Fd3, Fd23
+
+    def project(w):  # lines 5-6 / 13-14: solve lap psi = div w, w - grad psi
+        psi, *_ = pcg_solve(mp, 0.0, -dg_divergence_weak(mv, w) / mpm, nu_const=1.0, tol=tol)
+        gw = dg_gradient_weak(mp, psi)
+        return [w[c] - gw[c] / m for c in range(dim)]
+
+    v0 = [np.asarray(x, float) for x in v]
+    Fc, Fd1, Fd3, Fd23 = [None] * s, [None] * s, [None] * s, [None] * s
+    Fc[0], Fd1[0], Fd3[0], Fd23[0] = forces(v0, visc_model(v0, nu0, nu1, vmax))
+    u = v0
+    for i in range(1, s):
+        vp = [v0[c] + dt * (sum(A_ex[i, j] * (Fc[j][c] + Fd1[j][c] + Fd23[j][c] + Fd3[j][c]) for j in range(i))
+                            + sum(A_im[i, j] * F(j, c) for j in range(i + 1)))
+              for c in range(dim)]                                                   # line 4
+        vpp = project(vp)                                                            # lines 5-6
+        nu_i = visc_model(vpp, nu0, nu1, vmax)                                       # line 7
+        u = []
+        for c in range(dim):
+            g = vpp[c] + dt * sum((A_im[i, j] - A_ex[i, j]) * Fd1[j][c] - A_ex[i, j] * Fd3[j][c]
+                                  for j in range(i))                                 # line 8
+            if A_im[i, i] > 0:
+                lam = 1.0 / (dt * A_im[i, i])
+                x, *_ = pcg_solve(mv, lam, lam * g, nu=nu_i, tol=tol)                 # line 9
+                u.append(x)
+            else:
+                u.append(g)
+        Fc[i], Fd1[i], Fd3[i], Fd23[i] = forces(u, nu_i)
+    out = []
+    for c in range(dim):                                                             # line 11
+        out.append(u[c] + dt * sum((tab["b_ex"][j] - A_ex[s - 1, j]) * (Fc[j][c] + Fd23[j][c])
+                                   + (tab["b_im"][j] - A_im[s - 1, j]) * (Fd1[j][c] + F(j, c))
+                                   for j in range(s)))
+    if final_projection:
+        out = project(out)                                                           # lines 12-15
+    return out

@@ -206,3 +206,47 @@ CONFIGS = {
 
 def config(cid: int) -> Config:
     return CONFIGS[cid]
+
+
+# ---------------------------------------------------------------------------
+# 3-D vortex with solution-dependent viscosity, case VVP: the paper's
+# closed-form exact solution, viscosity model and manufactured forcing, sampled at nodes.
+# (Input data of the convergence experiment; none of the method's discrete arithmetic.)
+# ---------------------------------------------------------------------------
+VVP_VMAX = 2.0  # v^ex_max
+
+
+def vvp_exact(X, t):
+    """(v^ex, p^ex) of eq. var-visc-test at coordinates X = (x, y, z)."""
+    k = 2.0 * math.pi
+    A, B, C = k * (X[0] + t), k * (X[1] + t), k * (X[2] + t)
+    v = [(np.sin(A) + np.cos(B)) * np.sin(C),
+         (np.cos(A) + np.sin(B)) * np.sin(C),
+         (np.cos(A) + np.cos(B)) * np.cos(C)]
+    p = np.sin(A) * np.sin(B) * np.sin(C)
+    return v, p
+
+
+def vvp_forcing(X, t, nu0, nu1, vmax=VVP_VMAX):
+    """f = d_t v + div(v v) - div[nu(v) (grad v + grad v^T)] + grad p for the exact VVP solution
+    (PAPER.md:1229-1239), nu(v) = nu0 + nu1 (|v|/vmax)^2, in closed form:
+    with the phases A, B, C = 2 pi (x + t, y + t, z + t): div v = 0, lap v = -2 (2 pi)^2 v,
+    d_t = d_x + d_y + d_z, div(v v) = (v . grad) v, div[nu S] = nu lap v + S grad nu."""
+    k = 2.0 * math.pi
+    A, B, C = k * (X[0] + t), k * (X[1] + t), k * (X[2] + t)
+    sA, cA, sB, cB, sC, cC = np.sin(A), np.cos(A), np.sin(B), np.cos(B), np.sin(C), np.cos(C)
+    v, _ = vvp_exact(X, t)
+    # G[c][e] = d_e v_c
+    G = [[k * cA * sC, -k * sB * sC, k * (sA + cB) * cC],
+         [-k * sA * sC, k * cB * sC, k * (cA + sB) * cC],
+         [-k * sA * cC, -k * sB * cC, -k * (cA + cB) * sC]]
+    gp = [k * cA * sB * sC, k * sA * cB * sC, k * sA * sB * cC]
+    nu = nu0 + nu1 * (v[0] ** 2 + v[1] ** 2 + v[2] ** 2) / vmax ** 2
+    gnu = [2.0 * nu1 / vmax ** 2 * sum(v[c] * G[c][e] for c in range(3)) for e in range(3)]
+    f = []
+    for c in range(3):
+        dt_v = G[c][0] + G[c][1] + G[c][2]
+        conv = sum(v[e] * G[c][e] for e in range(3))
+        visc = nu * (-2.0 * k * k * v[c]) + sum(gnu[e] * (G[c][e] + G[e][c]) for e in range(3))
+        f.append(dt_v + conv - visc + gp[c])
+    return f
