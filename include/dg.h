@@ -224,6 +224,40 @@ typedef struct {
 dg_status dg_imex_rk_step(dg_mesh *mv, dg_mesh *mp, const dg_tableau *tab, double dt, double nu,
                           double *const v[3], double *psi, double tol, int maxit, dg_step_info *info);
 
+/* One step of Alg. 3 with the solution-dependent viscosity of P:1218-1224,
+ * nu(v) = nu0 + nu1 (|v| / vmax)^2, forcing F_s and the final projection:
+ *   stage 1: v_1 = v, nu_1 = nu(v);  stages i = 2..s:
+ *   line 4:  v'_i = v + dt [sum_{j<i} a_ex[i][j] (F_c + F_d1 + F_d2 + 2 F_d3)_j
+ *                          + sum_{j<=i} a_im[i][j] F_s,j]   (F_d + F_d3)
+ *   lines 5-6: projection with the DG pair and the SIP Poisson solve on mp (as dg_imex_rk_step);
+ *   line 7:  nu_i = nu(v''_i) at the nodes;
+ *   line 8:  g_i = v''_i + dt sum_{j<i} [(a_im - a_ex)[i][j] F_d1,j - a_ex[i][j] F_d3,j];
+ *   line 9:  v_i - dt a_im[i][i] div(nu_i grad v_i) = g_i  (variable-nu SIP Helmholtz, Jacobi-PCG);
+ *   line 11: v = v_s + dt sum_i [(b_ex - a_ex[s])_i (F_c + F_d2 + F_d3)_i
+ *                               + (b_im - a_im[s])_i (F_d1 + F_s)_i];
+ *   lines 12-15 (final_projection != 0): lap psi = div v, v <- v - grad psi.
+ * Stage forces of stage i use nu_i (the viscosity of its implicit solve; stage 1: nu(v)):
+ * F_c by dg_convect_rhs, F_d1 = -M^-1 A_0(nu_i) u (SIP, lam = 0, nodal nu field), and, with the
+ * velocity-level central-flux DG derivative (D_c u)_i = m_i^-1 [-sum_K (u, d_c phi_i)_GLL +
+ * sum_F ({u} n_c, [phi_i])_GLL]:  F_d2,c = sum_e D_e(nu D_c u_e),  F_d3,c = -D_c(nu sum_e D_e u_e)
+ * (readings in DESIGN.md §9; for constant nu F_d2 + F_d3 = 0 exactly, the D_c commute).
+ * fs: NULL (F_s = 0) or s*dim DEVICE pointers, fs[j*dim + c] = F_s,c at t + c_j dt (nodal).
+ * The Helmholtz solves need mv's preconditioner to be Jacobi (variable nu); mp may use
+ * DG_PC_SCHWARZ2.  Workspace (4 s + 2) dim + dim^2 + 2 velocity fields, owned by mv.
+ * Synchronous.  Errors as dg_imex_rk_step; DG_EINVAL for nu0 <= 0, nu1 < 0 or vmax <= 0. */
+typedef struct {
+    double nu0, nu1, vmax;
+} dg_visc_model;
+
+dg_status dg_imex_rk_step_vv(dg_mesh *mv, dg_mesh *mp, const dg_tableau *tab, double dt, const dg_visc_model *visc,
+                             const double *const *fs, int final_projection, double *const v[3], double *psi,
+                             double tol, int maxit, dg_step_info *info);
+
+/* Velocity-level central-flux DG derivatives out[c] = D_c u (c < dim; out[c] may be NULL to
+ * skip a direction), the operator of dg_imex_rk_step_vv's F_d2 / F_d3.  DEVICE arrays of m;
+ * no aliasing of u with out.  Collective for multi-rank meshes. */
+dg_status dg_derivative(dg_mesh *m, const double *u, double *const out[3]);
+
 /* Host-buffer variants: same operations on HOST arrays; H2D and D2H copies through
  * mesh-owned device staging buffers are part of the call (allocated on first use). */
 dg_status dg_helmholtz_apply_host(dg_mesh *m, double lam, const double *nu_host, double nu_const,

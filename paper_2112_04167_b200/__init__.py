@@ -26,6 +26,8 @@ from ._capi import (  # noqa: F401
     Tableau,
     dg_check_field,
     dg_convect_rhs,
+    ViscModel,
+    dg_derivative,
     dg_divergence,
     dg_gradient,
     dg_gll_tables,
@@ -33,6 +35,7 @@ from ._capi import (  # noqa: F401
     dg_helmholtz_apply_host,
     dg_helmholtz_diag,
     dg_imex_rk_step,
+    dg_imex_rk_step_vv,
     dg_imex_stage,
     dg_last_error,
     dg_mesh_create,

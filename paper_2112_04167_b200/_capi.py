@@ -72,6 +72,11 @@ class StepInfo(ctypes.Structure):
         return {k: getattr(self, k) for k, _ in self._fields_}
 
 
+class ViscModel(ctypes.Structure):
+    """nu(v) = nu0 + nu1 (|v| / vmax)^2 (P:1222)."""
+    _fields_ = [("nu0", _d), ("nu1", _d), ("vmax", _d)]
+
+
 def _sig(name, res, args):
     f = getattr(_lib, name)
     f.restype = res
@@ -95,6 +100,10 @@ _c = {
     "dg_helmholtz_diag": _sig("dg_helmholtz_diag", _i, [_vp, _d, _vp, _d, _vp]),
     "dg_pcg_solve": _sig("dg_pcg_solve", _i, [_vp, _d, _vp, _d, _vp, _d, _i, _vp, ctypes.POINTER(SolveInfo)]),
     "dg_convect_rhs": _sig("dg_convect_rhs", _i, [_vp, ctypes.POINTER(_vp), ctypes.POINTER(_vp)]),
+    "dg_derivative": _sig("dg_derivative", _i, [_vp, _vp, ctypes.POINTER(_vp)]),
+    "dg_imex_rk_step_vv": _sig("dg_imex_rk_step_vv", _i, [_vp, _vp, ctypes.POINTER(Tableau), _d,
+                                                          ctypes.POINTER(ViscModel), ctypes.POINTER(_vp), _i,
+                                                          ctypes.POINTER(_vp), _vp, _d, _i, ctypes.POINTER(StepInfo)]),
     "dg_mesh_set_precond": _sig("dg_mesh_set_precond", _i, [_vp, _i]),
     "dg_mesh_get_precond": _sig("dg_mesh_get_precond", _i, [_vp]),
     "dg_schwarz_apply": _sig("dg_schwarz_apply", _i, [_vp, _d, _d, _vp, _vp]),
@@ -313,6 +322,29 @@ def dg_imex_rk_step(mv: Mesh, mp: Mesh, tableau, dt, nu, v, psi, tol, maxit) -> 
     info = StepInfo()
     _check(_c["dg_imex_rk_step"](mv.handle, mp.handle, ctypes.byref(tab), dt, nu, vv, _ptr(psi), tol, maxit,
                                  ctypes.byref(info)), info)
+    return info
+
+
+def dg_derivative(m: Mesh, u, out):
+    """Velocity-level central-flux DG derivatives out[c] = D_c u (None skips c) -- include/dg.h."""
+    o = (_vp * 3)(*([_ptr(x) for x in out] + [None] * (3 - len(out))))
+    _check(_c["dg_derivative"](m.handle, _ptr(u), o))
+
+
+def dg_imex_rk_step_vv(mv: Mesh, mp: Mesh, tableau, dt, visc, v, psi, tol, maxit, fs=None, final_projection=True):
+    """One IMEX-RK step (Alg. 3) with nu(v) = nu0 + nu1 (|v|/vmax)^2, forcing fs[j][c] (device
+    tensors at t + c_j dt, or None) and the final projection, in place on v -- include/dg.h."""
+    tab = tableau if isinstance(tableau, Tableau) else Tableau.from_dict(tableau)
+    vm = ViscModel(*[float(x) for x in visc])
+    vv = (_vp * 3)(*([_ptr(x) for x in v] + [None] * (3 - len(v))))
+    fsp = None
+    if fs is not None:
+        flat = [_ptr(fs[j][c]) for j in range(len(fs)) for c in range(len(v))]
+        fsp = (_vp * len(flat))(*flat)
+    info = StepInfo()
+    _check(_c["dg_imex_rk_step_vv"](mv.handle, mp.handle, ctypes.byref(tab), float(dt), ctypes.byref(vm), fsp,
+                                    int(bool(final_projection)), vv, _ptr(psi), float(tol), int(maxit),
+                                    ctypes.byref(info)), info)
     return info
 
 

@@ -381,6 +381,30 @@ struct ApplyDispatch {
         return al(a.u) && (!a.nu || al(a.nu));
     }
     // can this mesh be applied per range of slowest-direction layers (v5/v6 only)?
+    template <int P, bool VARNU>
+    static constexpr bool mode2_fits6()
+    {
+        if constexpr (P <= 5 && P % 2 == 1) return v6::KC6<P, VARNU, 2>::SMEM_BYTES <= 227 * 1024;
+        else return false;
+    }
+    template <int P, bool VARNU>
+    static constexpr bool mode2_fits5() { return v5::KC5<P, VARNU, 2>::SMEM_BYTES <= 227 * 1024; }
+    static bool mode2_compiled(int P, bool varnu, bool six)
+    {
+        switch (P) {
+#define DG_M2(p)                                                                                           \
+    case p:                                                                                                \
+        if constexpr (DG_HAS_P(p) && DIM == 3)                                                             \
+            return six ? (varnu ? mode2_fits6<p, true>() : mode2_fits6<p, false>())                        \
+                       : (varnu ? mode2_fits5<p, true>() : mode2_fits5<p, false>());                       \
+        else                                                                                               \
+            return false;
+            DG_M2(1) DG_M2(2) DG_M2(3) DG_M2(4) DG_M2(5) DG_M2(6) DG_M2(7) DG_M2(8) DG_M2(9) DG_M2(10)
+#undef DG_M2
+        default:
+            return false;
+        }
+    }
     static bool split_pcg_ok(const Geom &g, const double *nu)
     {
         ApplyParams a{};
@@ -388,7 +412,9 @@ struct ApplyDispatch {
         a.u = nu ? nu : reinterpret_cast<const double *>(256);  // alignment probe only
         a.nu = nu;
         a.zhi = -1;
-        return v6_ok(a, false) || v5_ok(a, false);
+        // the MODE-2 (dot epilogue) kernel the apply dispatch would pick must exist for this P
+        if (v6_ok(a, false)) return mode2_compiled(g.P, nu != nullptr, true);
+        return v5_ok(a, false) && mode2_compiled(g.P, nu != nullptr, false);
     }
     static bool ranges_ok(const Geom &g)
     {

@@ -32,6 +32,7 @@ cudaError_t upload_tables()
     if ((e = upload_tables_apply3()) != cudaSuccess) return e;
     if ((e = upload_tables_stage()) != cudaSuccess) return e;
     if ((e = upload_tables_stage_interp()) != cudaSuccess) return e;
+    if ((e = upload_tables_visc()) != cudaSuccess) return e;
     return upload_tables_convect();
 }
 
@@ -1333,6 +1334,283 @@ dg_status dg_imex_rk_step(dg_mesh *mv, dg_mesh *mp, const dg_tableau *tab, doubl
         }
         CK(launch_lincomb(g, lc, mv->mass_e, v[c], mv->st));
         mv->launches += 1;
+    }
+    CK(cudaStreamSynchronize(mv->st));
+    if (info) *info = inf;
+    return DG_OK;
+}
+
+dg_status dg_derivative(dg_mesh *m, const double *u, double *const out[3])
+{
+    if (!m || !u || !out) return set_error(DG_EINVAL, "null argument");
+    DerivParams a;
+    a.u = u;
+    a.dirs = 0;
+    for (int c = 0; c < m->g.dim; ++c)
+        if (out[c]) {
+            if (out[c] == u) return set_error(DG_EINVAL, "out must not alias u");
+            a.out[c] = out[c];
+            a.dirs |= 1 << c;
+        }
+    if (m->nranks > 1) {
+        CKS(ensure_halos(m, true));
+        CKS(exchange(m, u, m->hv_lo[0], m->hv_hi[0]));
+        a.lo = m->hv_lo[0];
+        a.hi = m->hv_hi[0];
+    }
+    CK(launch_dg_deriv(m->g, a, m->st));
+    m->launches += 1;
+    return DG_OK;
+}
+
+dg_status dg_imex_rk_step_vv(dg_mesh *mv, dg_mesh *mp, const dg_tableau *tab, double dt, const dg_visc_model *visc,
+                             const double *const *fs, int final_projection, double *const v[3], double *psi,
+                             double tol, int maxit, dg_step_info *info)
+{
+    if (!mv || !mp || !tab || !visc || !v || !psi) return set_error(DG_EINVAL, "null argument");
+    CKS(check_pair(mv, mp));
+    const int S = tab->s, dim = mv->g.dim;
+    if (S < 2 || S > DG_RK_MAX_STAGES) return set_error(DG_EINVAL, "tableau: 2 <= s <= DG_RK_MAX_STAGES");
+    if (tab->a_im[0][0] != 0.0 || tab->c[0] != 0.0)
+        return set_error(DG_EINVAL, "tableau: the first stage must be explicit (a_im[0][0] = c[0] = 0)");
+    for (int i = 0; i < S; ++i) {
+        if (!(tab->a_im[i][i] >= 0.0)) return set_error(DG_EINVAL, "tableau: a_im[i][i] must be >= 0");
+        for (int j = i; j < S; ++j)
+            if (tab->a_ex[i][j] != 0.0 || (j > i && tab->a_im[i][j] != 0.0))
+                return set_error(DG_EINVAL, "tableau: a_ex strictly lower, a_im lower triangular");
+    }
+    if (!(dt > 0.0) || !(visc->nu0 > 0.0) || !(visc->nu1 >= 0.0) || !(visc->vmax > 0.0) || !std::isfinite(visc->nu0) ||
+        !std::isfinite(visc->nu1) || !(tol > 0.0) || maxit < 1)
+        return set_error(DG_EINVAL, "need dt > 0, nu0 > 0, nu1 >= 0, vmax > 0, tol > 0, maxit >= 1");
+    for (int c = 0; c < dim; ++c)
+        if (!v[c]) return set_error(DG_EINVAL, "null component pointer");
+    if (fs)
+        for (int k = 0; k < S * dim; ++k)
+            if (!fs[k]) return set_error(DG_EINVAL, "null forcing pointer");
+    cudaStream_t mp_stream = mp->st;
+    mp->st = mv->st;
+    struct Restore {
+        dg_mesh *m;
+        cudaStream_t s;
+        ~Restore() { m->st = s; }
+    } restore{mp, mp_stream};
+    const Geom &g = mv->g, &gp = mp->g;
+    const size_t bv = sizeof(double) * (size_t)mv->ndof;
+    const int need = 4 * S * dim + 2 * dim + 2 + dim * dim;
+    while ((int)mv->rk.size() < need) {
+        double *b = nullptr;
+        CKS(alloc((void **)&b, bv));
+        mv->rk.push_back(b);
+    }
+    CKS(stage(mp, &mp->sf[0], sizeof(double) * (size_t)mp->ndof));
+    auto Fc = [&](int i, int c) { return mv->rk[(i * dim + c)]; };
+    auto Fd1 = [&](int i, int c) { return mv->rk[(S + i) * dim + c]; };
+    auto Fd3 = [&](int i, int c) { return mv->rk[(2 * S + i) * dim + c]; };
+    auto Fd23 = [&](int i, int c) { return mv->rk[(3 * S + i) * dim + c]; };  // F_d2 + F_d3
+    auto VP = [&](int c) { return mv->rk[4 * S * dim + c]; };
+    auto TM = [&](int c) { return mv->rk[(4 * S + 1) * dim + c]; };
+    double *NU = mv->rk[(4 * S + 2) * dim], *WK = mv->rk[(4 * S + 2) * dim + 1];
+    auto DV = [&](int e, int c) { return mv->rk[(4 * S + 2) * dim + 2 + e * dim + c]; };  // D_c v_e
+    const bool multi = mv->nranks > 1;
+    if (multi) CKS(ensure_halos(mv, true));
+    dg_step_info inf{};
+    // D_c u for the selected directions (overwrite or accumulate scale * D_c u)
+    auto deriv = [&](const double *u, double *const *out, int dirs, int acc, double scale) -> dg_status {
+        DerivParams a;
+        a.u = u;
+        if (multi) {
+            CKS(exchange(mv, u, mv->hv_lo[0], mv->hv_hi[0]));
+            a.lo = mv->hv_lo[0];
+            a.hi = mv->hv_hi[0];
+        }
+        for (int c = 0; c < 3; ++c) a.out[c] = out[c];
+        a.dirs = dirs;
+        a.accumulate = acc;
+        a.scale = scale;
+        CK(launch_dg_deriv(g, a, mv->st));
+        mv->launches += 1;
+        return DG_OK;
+    };
+    // stage forces at (u, nu): F_c (LLF), F_d1 = -M^-1 A_0(nu) u (SIP, lam = 0),
+    // F_d3 = -D(nu div u), F_d2 + F_d3 = sum_e D_e(nu D_c u_e) + F_d3, div u = sum_e D_e u_e
+    auto forces = [&](int i, double *const *u, const double *nu) -> dg_status {
+        double *out[3] = {Fc(i, 0), Fc(i, 1), dim == 3 ? Fc(i, 2) : nullptr};
+        const double *uin[3] = {u[0], u[1], dim == 3 ? u[2] : nullptr};
+        CKS(dg_convect_rhs(mv, uin, out));
+        for (int c = 0; c < dim; ++c) {
+            CKS(apply_impl(mv, 0.0, nu, 0.0, u[c], TM(c)));
+            LinComb lc;
+            lc.w = TM(c);
+            lc.cm = -1.0;
+            CK(launch_lincomb(g, lc, mv->mass_e, Fd1(i, c), mv->st));
+            mv->launches += 1;
+        }
+        for (int e = 0; e < dim; ++e) {
+            double *o[3] = {DV(e, 0), DV(e, 1), dim == 3 ? DV(e, 2) : nullptr};
+            CKS(deriv(u[e], o, (1 << dim) - 1, 0, 1.0));
+        }
+        LinComb ld;
+        for (int e = 0; e < dim; ++e) {
+            ld.c[ld.n] = 1.0;
+            ld.y[ld.n++] = DV(e, e);
+        }
+        CK(launch_lincomb(g, ld, mv->mass_e, WK, mv->st));  // div u
+        CK(launch_nu_mul(g, nu, WK, nullptr, WK, mv->st));   // nu div u
+        mv->launches += 2;
+        double *f3[3] = {Fd3(i, 0), Fd3(i, 1), dim == 3 ? Fd3(i, 2) : nullptr};
+        CKS(deriv(WK, f3, (1 << dim) - 1, 0, -1.0));
+        for (int c = 0; c < dim; ++c) {
+            LinComb lc;
+            lc.x0 = Fd3(i, c);
+            lc.c0 = 1.0;
+            CK(launch_lincomb(g, lc, mv->mass_e, Fd23(i, c), mv->st));
+            mv->launches += 1;
+            for (int e = 0; e < dim; ++e) {
+                CK(launch_nu_mul(g, nu, DV(e, c), nullptr, WK, mv->st));  // nu D_c u_e
+                mv->launches += 1;
+                double *o[3] = {nullptr, nullptr, nullptr};
+                o[e] = Fd23(i, c);
+                CKS(deriv(WK, o, 1 << e, 1, 1.0));
+            }
+        }
+        return DG_OK;
+    };
+    // lines 5-6 (and 13-14): lap psi = div w (weak DG divergence, SIP Poisson on mp from psi = 0),
+    // w <- w - M^-1 G psi
+    auto project = [&](double *const *w) -> dg_status {
+        CKS(div_impl(mv, w, mp->sf[0]));
+        CK(launch_scale_minv(gp, mp->mass_e, -1.0, mp->sf[0], mp->sf[0], mv->st));
+        mv->launches += 1;
+        CK(cudaMemsetAsync(psi, 0, sizeof(double) * (size_t)mp->ndof, mv->st));
+        dg_solve_info ip{};
+        const dg_status st = pcg_impl(mp, 0.0, nullptr, 1.0, mp->sf[0], tol, maxit, psi, &ip);
+        inf.pressure_iters += ip.iters;
+        if (st != DG_OK) return st;
+        double *tm[3] = {TM(0), TM(1), dim == 3 ? TM(2) : nullptr};
+        CKS(grad_impl(mp, mv, psi, tm));
+        for (int c = 0; c < dim; ++c) {
+            LinComb lc;
+            lc.x0 = w[c];
+            lc.c0 = 1.0;
+            lc.w = tm[c];
+            lc.cm = -1.0;
+            CK(launch_lincomb(g, lc, mv->mass_e, w[c], mv->st));
+            mv->launches += 1;
+        }
+        return DG_OK;
+    };
+    auto fsp = [&](int j, int c) { return fs ? fs[j * dim + c] : nullptr; };
+    auto fail = [&](dg_status st) {
+        if (info) *info = inf;
+        return st;
+    };
+    // stage 1: v_1 = v, nu_1 = nu(v)
+    {
+        const double *vv[3] = {v[0], v[1], dim == 3 ? v[2] : nullptr};
+        CK(launch_visc_model(g, vv, visc->nu0, visc->nu1, visc->vmax, NU, mv->st));
+        mv->launches += 1;
+        dg_status st = forces(0, v, NU);
+        if (st != DG_OK) return fail(st);
+    }
+    double *vp[3] = {VP(0), VP(1), dim == 3 ? VP(2) : nullptr};
+    double *tm[3] = {TM(0), TM(1), dim == 3 ? TM(2) : nullptr};
+    for (int i = 1; i < S; ++i) {
+        // line 4: v'_i = v + dt [sum_j a_ex[i][j] (F_c + F_d + F_d3)_j + sum_{j<=i} a_im[i][j] F_s,j],
+        // F_d + F_d3 = F_d1 + (F_d2 + F_d3) + F_d3
+        for (int c = 0; c < dim; ++c) {
+            LinComb lc;
+            lc.x0 = v[c];
+            lc.c0 = 1.0;
+            for (int j = 0; j < i; ++j) {
+                const double a = dt * tab->a_ex[i][j];
+                if (a == 0.0) continue;
+                const double *ys[4] = {Fc(j, c), Fd1(j, c), Fd23(j, c), Fd3(j, c)};
+                for (const double *y : ys) {
+                    lc.c[lc.n] = a;
+                    lc.y[lc.n++] = y;
+                }
+            }
+            for (int j = 0; j <= i && fs; ++j)
+                if (tab->a_im[i][j] != 0.0) {
+                    lc.c[lc.n] = dt * tab->a_im[i][j];
+                    lc.y[lc.n++] = fsp(j, c);
+                }
+            CK(launch_lincomb(g, lc, mv->mass_e, vp[c], mv->st));
+            mv->launches += 1;
+        }
+        dg_status st = project(vp);  // lines 5-6
+        if (st != DG_OK) return fail(st);
+        // line 7: nu_i = nu(v''_i)
+        {
+            const double *vv[3] = {vp[0], vp[1], dim == 3 ? vp[2] : nullptr};
+            CK(launch_visc_model(g, vv, visc->nu0, visc->nu1, visc->vmax, NU, mv->st));
+            mv->launches += 1;
+        }
+        // lines 8-9: g_i = v'' + dt sum_j [(a_im - a_ex)[i][j] F_d1,j - a_ex[i][j] F_d3,j];
+        // v_i - dt a_ii div(nu_i grad v_i) = g_i  (lam = 1/(dt a_ii), f = lam g_i; Jacobi-PCG
+        // with the nu_i field), from the guess v''_i
+        const double aii = tab->a_im[i][i];
+        const double lam = aii > 0.0 ? 1.0 / (dt * aii) : 1.0;
+        for (int c = 0; c < dim; ++c) {
+            LinComb lc;
+            lc.x0 = vp[c];
+            lc.c0 = lam;
+            for (int j = 0; j < i; ++j) {
+                const double cj = tab->a_im[i][j] - tab->a_ex[i][j];
+                if (cj != 0.0) {
+                    lc.c[lc.n] = lam * dt * cj;
+                    lc.y[lc.n++] = Fd1(j, c);
+                }
+                if (tab->a_ex[i][j] != 0.0) {
+                    lc.c[lc.n] = -lam * dt * tab->a_ex[i][j];
+                    lc.y[lc.n++] = Fd3(j, c);
+                }
+            }
+            CK(launch_lincomb(g, lc, mv->mass_e, tm[c], mv->st));
+            mv->launches += 1;
+            if (aii > 0.0) {
+                dg_solve_info iv{};
+                st = pcg_impl(mv, lam, NU, 0.0, tm[c], tol, maxit, vp[c], &iv);
+                inf.velocity_iters += iv.iters;
+                if (st != DG_OK) return fail(st);
+            } else {
+                CK(cudaMemcpyAsync(vp[c], tm[c], bv, cudaMemcpyDeviceToDevice, mv->st));
+            }
+        }
+        st = forces(i, vp, NU);
+        if (st != DG_OK) return fail(st);
+        inf.stages += 1;
+    }
+    // line 11: v = v_s + dt sum_i [(b_ex - a_ex[s])_i (F_c + F_d2 + F_d3)_i
+    //                              + (b_im - a_im[s])_i (F_d1 + F_s)_i]
+    for (int c = 0; c < dim; ++c) {
+        LinComb lc;
+        lc.x0 = vp[c];
+        lc.c0 = 1.0;
+        for (int j = 0; j < S; ++j) {
+            const double ce = tab->b_ex[j] - tab->a_ex[S - 1][j], ci = tab->b_im[j] - tab->a_im[S - 1][j];
+            if (ce != 0.0) {
+                lc.c[lc.n] = dt * ce;
+                lc.y[lc.n++] = Fc(j, c);
+                lc.c[lc.n] = dt * ce;
+                lc.y[lc.n++] = Fd23(j, c);
+            }
+            if (ci != 0.0) {
+                lc.c[lc.n] = dt * ci;
+                lc.y[lc.n++] = Fd1(j, c);
+                if (fs) {
+                    lc.c[lc.n] = dt * ci;
+                    lc.y[lc.n++] = fsp(j, c);
+                }
+            }
+        }
+        CK(launch_lincomb(g, lc, mv->mass_e, v[c], mv->st));
+        mv->launches += 1;
+    }
+    // lines 12-15: final projection
+    if (final_projection) {
+        const dg_status st = project(v);
+        if (st != DG_OK) return fail(st);
     }
     CK(cudaStreamSynchronize(mv->st));
     if (info) *info = inf;

@@ -151,7 +151,7 @@ struct DivGradParams {  // geometry: the velocity mesh's (degree P); pressure de
 };
 cudaError_t launch_dg_div(const Geom &gv, const DivGradParams &a, cudaStream_t st);
 struct LinComb {  // out = c0 x0 + sum_k c[k] y[k] (+ cm w / m)
-    static constexpr int MAXT = 16;
+    static constexpr int MAXT = 40;
     const double *x0 = nullptr;
     double c0 = 0.0;
     int n = 0;
@@ -265,5 +265,21 @@ cudaError_t launch_sw_pupd(const Geom &g, const SwTab &h, const SwPupdParams &a,
 cudaError_t launch_sw_coarse(const SwCoarseParams &a, const SwTab &h, int stage, cudaStream_t st);
 cudaError_t launch_sw_gather_local(const SwCoarseParams &a, int S, int off, int nl, cudaStream_t st);
 int sw_cz_grid(const SwTab &h);
+
+// visc.cu -- variable-viscosity step pieces
+struct DerivParams {
+    const double *u = nullptr;
+    const double *lo = nullptr, *hi = nullptr;  // neighbour slab layers (multi-rank)
+    double *out[3] = {nullptr, nullptr, nullptr};
+    int dirs = 7;           // bit c: compute D_c u into out[c]
+    int accumulate = 0;     // out += scale D_c u  (else out = scale D_c u)
+    double scale = 1.0;
+};
+cudaError_t launch_dg_deriv(const Geom &g, const DerivParams &a, cudaStream_t st);
+cudaError_t launch_visc_model(const Geom &g, const double *const v[3], double nu0, double nu1, double vmax, double *nu,
+                              cudaStream_t st);
+cudaError_t launch_nu_mul(const Geom &g, const double *nu, const double *x, const double *y, double *out,
+                          cudaStream_t st);
+cudaError_t upload_tables_visc();
 
 }  // namespace dg
