@@ -378,8 +378,6 @@ def run_stage(dg, torch, stream, barrier, reps=2):
     ms_j, dj = timed(0, 1)
     dg.dg_mesh_set_precond(mp, dg.DG_PC_SCHWARZ2)
     times = [ms_sw]
-    info = None
-    d = info.as_dict()
     # the explicit LLF convection alone, FP64-bound: algorithmic flops per element
     # of the sum-factorised Gauss evaluation over the CUDA-event time
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
