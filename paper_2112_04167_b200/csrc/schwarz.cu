@@ -26,6 +26,7 @@
 // * The prolongation P_1 x_c is never stored: the PCG direction update p = z_b + P_1 x_c +
 //   beta p evaluates the trilinear hats on the fly from the element's 2^dim vertex values
 //   (L2-resident), and r.z = r.z_b + r_c.x_c.
+#include <algorithm>
 #include <cmath>
 #include <vector>
 
@@ -426,6 +427,7 @@ __device__ __forceinline__ double gather_vertex(const double *rc_el, long long n
 {
     double acc = 0.0;
     const int NC = 1 << dim;
+#pragma unroll 8
     for (int c = 0; c < NC; ++c) {
         int ex = vx - (c & 1), ey = vy - ((c >> 1) & 1), ez = vz - ((c >> 2) & 1);
         if (ex < 0) ex += Nc[0];
@@ -474,14 +476,14 @@ __global__ void k_sw_cz(SwCoarseParams a)
     const SwTab *T = a.T;
     const int Nx = T->Nc[0], Ny = T->Nc[1], Nz = T->Nc[2], NP = Nx * Ny;
     double *col = sm, *hat = sm + 32 * Nz, *Fz = hat + 32 * Nz;
-    __shared__ double red[8];
-    for (int q = threadIdx.y * 32 + threadIdx.x; q < Nz * Nz; q += 256) Fz[q] = a.F[2 * SW_NCMAX * SW_NCMAX + q];
+    __shared__ double red[32];
+    for (int q = threadIdx.y * 32 + threadIdx.x; q < Nz * Nz; q += 32 * blockDim.y) Fz[q] = a.F[2 * SW_NCMAX * SW_NCMAX + q];
     const int p = blockIdx.x * 32 + threadIdx.x;  // plane index ky * Nx + kx
-    for (int vz = threadIdx.y; vz < Nz; vz += 8) col[vz * 32 + threadIdx.x] = p < NP ? a.chat[(long long)vz * NP + p] : 0.0;
+    for (int vz = threadIdx.y; vz < Nz; vz += blockDim.y) col[vz * 32 + threadIdx.x] = p < NP ? a.chat[(long long)vz * NP + p] : 0.0;
     __syncthreads();
     double dot = 0.0;
     const int kx = p % Nx, ky = p / Nx;
-    for (int kz = threadIdx.y; kz < Nz; kz += 8) {
+    for (int kz = threadIdx.y; kz < Nz; kz += blockDim.y) {
         double acc = 0.0;
         for (int j = 0; j < Nz; ++j) acc = fma(Fz[j * Nz + kz], col[j * 32 + threadIdx.x], acc);
         double inv = 0.0;
@@ -495,7 +497,7 @@ __global__ void k_sw_cz(SwCoarseParams a)
         hat[kz * 32 + threadIdx.x] = acc * inv;
     }
     __syncthreads();
-    for (int vz = threadIdx.y; vz < Nz; vz += 8) {
+    for (int vz = threadIdx.y; vz < Nz; vz += blockDim.y) {
         double acc = 0.0;
         for (int k = 0; k < Nz; ++k) acc = fma(Fz[vz * Nz + k], hat[k * 32 + threadIdx.x], acc);
         if (p < NP) a.chat[(long long)vz * NP + p] = acc;
@@ -506,7 +508,7 @@ __global__ void k_sw_cz(SwCoarseParams a)
     __syncthreads();
     if (threadIdx.x == 0 && threadIdx.y == 0 && a.partial) {
         double t = 0.0;
-        for (int w = 0; w < 8; ++w) t += red[w];
+        for (int w = 0; w < (int)blockDim.y; ++w) t += red[w];
         a.partial[(a.pslot + blockIdx.x) * 2 + 0] = a.count_dot ? t : 0.0;
         a.partial[(a.pslot + blockIdx.x) * 2 + 1] = 0.0;
     }
@@ -744,10 +746,13 @@ cudaError_t launch_sw_coarse(const SwCoarseParams &a, const SwTab &h, int stage,
         cudaFuncSetAttribute(k_sw_cinv, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
         attr = true;
     }
+    // one thread per plane entry (latency-bound small transforms), one per column entry
+    const int pt = std::min(1024, std::max(128, ((Nx * Ny + 31) / 32) * 32));
+    const int cy = std::min(32, Nz);
     switch (stage) {
-    case 0: k_sw_cfwd<<<Nz, 256, plane_smem, st>>>(a); break;
-    case 1: k_sw_cz<<<sw_cz_grid(h), dim3(32, 8), sizeof(double) * (64 * (size_t)Nz + (size_t)Nz * Nz), st>>>(a); break;
-    case 2: k_sw_cinv<<<Nz, 256, plane_smem, st>>>(a); break;
+    case 0: k_sw_cfwd<<<Nz, pt, plane_smem, st>>>(a); break;
+    case 1: k_sw_cz<<<sw_cz_grid(h), dim3(32, cy), sizeof(double) * (64 * (size_t)Nz + (size_t)Nz * Nz), st>>>(a); break;
+    case 2: k_sw_cinv<<<Nz, pt, plane_smem, st>>>(a); break;
     default: return cudaErrorInvalidValue;
     }
     return cudaGetLastError();

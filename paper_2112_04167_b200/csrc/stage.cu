@@ -9,6 +9,8 @@
 //                     (the rhs of the pressure Poisson problem, Alg. 3 line 5);
 //   k_dg_grad       : weak DG gradient of psi tested with the velocity basis (Alg. 3 line 6,
 //                     v'' = v' - M^-1 G psi).  -G is the transpose of D.
+#include <cstdlib>
+
 #include "dev_common.cuh"
 
 namespace dg {
@@ -324,6 +326,303 @@ __global__ void __launch_bounds__(256) k_dg_grad(const Geom g, DivGradParams a)
     }
 }
 
+// ---------------------------------------------------------------------------
+// Tiled versions (the ones dispatched): a CTA takes EPC consecutive elements, one thread per
+// element line; 1-D transforms with the tables of __constant__ c_stab (uniform operands in
+// fully unrolled loops), data exchanged through shared memory, coalesced global loads and
+// stores; the neighbours' face layers are gathered into shared memory once per tile.
+// ---------------------------------------------------------------------------
+template <int DIM, int P>
+struct DG2 {
+    static constexpr int n = P + 1, m = P;
+    static constexpr int NV = DIM == 3 ? n * n * n : n * n;
+    static constexpr int NPp = DIM == 3 ? m * m * m : m * m;
+    static constexpr int NL = DIM == 3 ? n * n : n;       // velocity lines per direction
+    static constexpr int FV = DIM == 3 ? n * n : n;       // velocity face nodes
+    static constexpr int FP = DIM == 3 ? m * m : m;       // pressure face nodes
+    static constexpr int NT = 256;
+    static constexpr int EPC = NT / NL > 16 ? 16 : (NT / NL < 1 ? 1 : NT / NL);
+};
+
+// strides of direction d in an element array with extents (e0, e1, e2), x fastest
+__device__ __forceinline__ int gstride(int d, int e0, int e1) { return d == 0 ? 1 : (d == 1 ? e0 : e0 * e1); }
+
+// weak gradient (velocity layout) of the pressure psi, see k_dg_grad
+template <int DIM, int P>
+__global__ void __launch_bounds__(256, 2) k_dg_grad2(const Geom g, DivGradParams a)
+{
+    using C = DG2<DIM, P>;
+    constexpr int n = C::n, m = C::m, NV = C::NV, NPp = C::NPp, NL = C::NL, FP = C::FP, NT = C::NT, EPC = C::EPC;
+    const StTab &S = c_stab[P];
+    extern __shared__ double dsm[];
+    double *sPs = dsm;                       // [EPC][NPp]
+    double *sX = sPs + EPC * NPp;            // [EPC][NV] (interpolation stages, output staging)
+    double *sH = sX + EPC * NV;              // [EPC][NV] psi_h
+    double *sF = sH + EPC * NV;              // [EPC][DIM][2][FP] neighbour pressure face layers
+    const int le = threadIdx.x / NL, ln = threadIdx.x % NL;
+    Geom gp = g;
+    gp.npe = NPp;
+    for (long long e0 = (long long)blockIdx.x * EPC; e0 < g.nel; e0 += (long long)gridDim.x * EPC) {
+        const int ne = g.nel - e0 < EPC ? (int)(g.nel - e0) : EPC;
+        const bool act = le < ne;
+        __syncthreads();
+        for (int t = threadIdx.x; t < ne * NPp; t += NT) sPs[t] = a.psi[e0 * NPp + t];
+        // neighbour face layers: element el, direction d, side s (s = 1: the +d neighbour's layer 0)
+        for (int t = threadIdx.x; t < ne * DIM * 2 * FP; t += NT) {
+            const int f = t % FP, r = t / FP, s = r % 2, d = (r / 2) % DIM, el = r / (2 * DIM);
+            const long long e = e0 + el;
+            int cn[3] = {(int)(e % g.Nl[0]), (int)((e / g.Nl[0]) % g.Nl[1]),
+                         DIM == 3 ? (int)(e / ((long long)g.Nl[0] * g.Nl[1])) : 0};
+            cn[d] += s ? 1 : -1;
+            const double *nb = elem_ptr(gp, a.psi, a.plo, a.phi, cn[0], cn[1], cn[2]);
+            const int o1 = d == 0 ? 1 : 0, o2 = d == 2 ? 1 : 2;
+            const int fa = f % m, fb = DIM == 3 ? f / m : 0;
+            sF[t] = nb[fa * gstride(o1, m, m) + (DIM == 3 ? fb * gstride(o2, m, m) : 0) + (s ? 0 : m - 1) * gstride(d, m, m)];
+        }
+        __syncthreads();
+        double v[n], o[n];
+        // psi_h = (E (x) E (x) E) psi: x (m^(d-1) lines), y, z
+        if (act && ln < (DIM == 3 ? m * m : m)) {
+            const int b = le * NPp + ln * m;
+#pragma unroll
+            for (int r = 0; r < m; ++r) v[r] = sPs[b + r];
+#pragma unroll
+            for (int i = 0; i < n; ++i) {
+                double s = 0.0;
+#pragma unroll
+                for (int r = 0; r < m; ++r) s = fma(S.E[i][r], v[r], s);
+                sX[le * NV + ln * n + i] = s;  // layout (i, b, c): extents (n, m, m)
+            }
+        }
+        __syncthreads();
+        if (DIM == 3) {
+            if (act && ln < n * m) {  // y lines (i, c) of the (n, m, m) array -> (n, n, m)
+                const int i = ln % n, c = ln / n;
+#pragma unroll
+                for (int r = 0; r < m; ++r) v[r] = sX[le * NV + i + n * (r + m * c)];
+#pragma unroll
+                for (int j = 0; j < n; ++j) {
+                    double s = 0.0;
+#pragma unroll
+                    for (int r = 0; r < m; ++r) s = fma(S.E[j][r], v[r], s);
+                    o[j] = s;
+                }
+            }
+            __syncthreads();
+            if (act && ln < n * m) {
+                const int i = ln % n, c = ln / n;
+#pragma unroll
+                for (int j = 0; j < n; ++j) sX[le * NV + i + n * (j + n * c)] = o[j];
+            }
+            __syncthreads();
+            if (act) {  // z lines (i, j) of (n, n, m) -> psi_h (n, n, n)
+#pragma unroll
+                for (int r = 0; r < m; ++r) v[r] = sX[le * NV + ln + n * n * r];
+#pragma unroll
+                for (int k = 0; k < n; ++k) {
+                    double s = 0.0;
+#pragma unroll
+                    for (int r = 0; r < m; ++r) s = fma(S.E[k][r], v[r], s);
+                    sH[le * NV + ln + n * n * k] = s;
+                }
+            }
+        } else {
+            if (act) {  // y lines (i) of (n, m) -> (n, n)
+#pragma unroll
+                for (int r = 0; r < m; ++r) v[r] = sX[le * NV + ln + n * r];
+#pragma unroll
+                for (int j = 0; j < n; ++j) {
+                    double s = 0.0;
+#pragma unroll
+                    for (int r = 0; r < m; ++r) s = fma(S.E[j][r], v[r], s);
+                    sH[le * NV + ln + n * j] = s;
+                }
+            }
+        }
+        __syncthreads();
+        // per direction d: line along d through transverse node (t1, t2) = ln
+        for (int d = 0; d < DIM; ++d) {
+            const int o1 = d == 0 ? 1 : 0, o2 = d == 2 ? 1 : 2;
+            const int t1 = ln % n, t2 = DIM == 3 ? ln / n : 0;
+            const int GS = gstride(d, n, n);
+            if (act) {
+                const int base = le * NV + t1 * gstride(o1, n, n) + (DIM == 3 ? t2 * gstride(o2, n, n) : 0);
+                double Wt = S.w[t1] * g.wfac[d];  // transverse weight W^F
+                if (DIM == 3) Wt *= S.w[t2];
+#pragma unroll
+                for (int r = 0; r < n; ++r) v[r] = sH[base + r * GS];
+                // neighbour psi_h on the two faces at (t1, t2): (E (x) E) of the face layers
+                double nb[2];
+#pragma unroll
+                for (int s = 0; s < 2; ++s) {
+                    const double *F = sF + ((le * DIM + d) * 2 + s) * FP;
+                    double acc = 0.0;
+                    if (DIM == 3) {
+#pragma unroll
+                        for (int fb = 0; fb < m; ++fb) {
+                            double ra = 0.0;
+#pragma unroll
+                            for (int fa = 0; fa < m; ++fa) ra = fma(S.E[t1][fa], F[fa + m * fb], ra);
+                            acc = fma(S.E[t2][fb], ra, acc);
+                        }
+                    } else {
+#pragma unroll
+                        for (int fa = 0; fa < m; ++fa) acc = fma(S.E[t1][fa], F[fa], acc);
+                    }
+                    nb[s] = acc;
+                }
+                const double sdc = g.sd[d] * g.h[d] * 0.5;  // (2/h) * (h/2): W = W^F w_r h/2
+#pragma unroll
+                for (int k = 0; k < n; ++k) {
+                    double s = 0.0;
+#pragma unroll
+                    for (int r = 0; r < n; ++r) s = fma(S.D[r][k] * S.w[r], v[r], s);
+                    o[k] = -sdc * Wt * s;
+                }
+                o[0] -= Wt * 0.5 * (v[0] + nb[0]);
+                o[P] += Wt * 0.5 * (v[P] + nb[1]);
+#pragma unroll
+                for (int k = 0; k < n; ++k) sX[base + k * GS] = o[k];
+            }
+            __syncthreads();
+            for (int t = threadIdx.x; t < ne * NV; t += NT) a.gout[d][e0 * NV + t] = sX[t];
+            __syncthreads();
+        }
+    }
+}
+
+// weak divergence (pressure layout) of the velocity v, see k_dg_div
+template <int DIM, int P>
+__global__ void __launch_bounds__(256, 2) k_dg_div2(const Geom g, DivGradParams a)
+{
+    using C = DG2<DIM, P>;
+    constexpr int n = C::n, m = C::m, NV = C::NV, NPp = C::NPp, NL = C::NL, FV = C::FV, NT = C::NT, EPC = C::EPC;
+    const StTab &S = c_stab[P];
+    extern __shared__ double dsm[];
+    double *sV = dsm;                        // [EPC][NV] one velocity component
+    double *sX = sV + EPC * NV;              // [EPC][NV] work
+    double *sY = sX + EPC * NV;              // [EPC][NV] work
+    double *sO = sY + EPC * NV;              // [EPC][NPp] accumulated divergence
+    double *sF = sO + EPC * NPp;             // [EPC][2][FV] neighbour velocity face layers
+    const int le = threadIdx.x / NL, ln = threadIdx.x % NL;
+    for (long long e0 = (long long)blockIdx.x * EPC; e0 < g.nel; e0 += (long long)gridDim.x * EPC) {
+        const int ne = g.nel - e0 < EPC ? (int)(g.nel - e0) : EPC;
+        const bool act = le < ne;
+        __syncthreads();
+        for (int t = threadIdx.x; t < ne * NPp; t += NT) sO[t] = 0.0;
+        for (int c = 0; c < DIM; ++c) {
+            const int o1 = c == 0 ? 1 : 0, o2 = c == 2 ? 1 : 2;
+            __syncthreads();
+            for (int t = threadIdx.x; t < ne * NV; t += NT) sV[t] = a.v[c][e0 * NV + t];
+            for (int t = threadIdx.x; t < ne * 2 * FV; t += NT) {
+                const int f = t % FV, s = (t / FV) % 2, el = t / (2 * FV);
+                const long long e = e0 + el;
+                int cn[3] = {(int)(e % g.Nl[0]), (int)((e / g.Nl[0]) % g.Nl[1]),
+                             DIM == 3 ? (int)(e / ((long long)g.Nl[0] * g.Nl[1])) : 0};
+                cn[c] += s ? 1 : -1;
+                const double *nb = elem_ptr(g, a.v[c], a.vlo[c], a.vhi[c], cn[0], cn[1], cn[2]);
+                const int fa = f % n, fb = DIM == 3 ? f / n : 0;
+                sF[t] = nb[fa * gstride(o1, n, n) + (DIM == 3 ? fb * gstride(o2, n, n) : 0) + (s ? 0 : P) * gstride(c, n, n)];
+            }
+            __syncthreads();
+            // c lines: -(2/h_c) E'^T (W v_c) plus the face fluxes at the end layers
+            const int t1 = ln % n, t2 = DIM == 3 ? ln / n : 0;
+            double v[n], o[n];
+            if (act) {
+                const int GS = gstride(c, n, n);
+                const int tb = t1 * gstride(o1, n, n) + (DIM == 3 ? t2 * gstride(o2, n, n) : 0);
+                double Wt = S.w[t1] * g.wfac[c];
+                if (DIM == 3) Wt *= S.w[t2];
+#pragma unroll
+                for (int r = 0; r < n; ++r) v[r] = sV[le * NV + tb + r * GS];
+                const double sdc = g.sd[c] * g.h[c] * 0.5;
+#pragma unroll
+                for (int q = 0; q < m; ++q) {
+                    double s = 0.0;
+#pragma unroll
+                    for (int r = 0; r < n; ++r) s = fma(S.Ed[r][q] * S.w[r], v[r], s);
+                    o[q] = -sdc * Wt * s;
+                }
+                const double *F0 = sF + (le * 2 + 0) * FV, *F1 = sF + (le * 2 + 1) * FV;
+                o[0] -= Wt * 0.5 * (v[0] + F0[ln]);
+                o[m - 1] += Wt * 0.5 * (v[P] + F1[ln]);
+                // result (q along c; transverse n x n) -> sX with the c extent m
+                int ex[3] = {n, n, n};
+                ex[c] = m;
+                const int ob = t1 * gstride(o1, ex[0], ex[1]) + (DIM == 3 ? t2 * gstride(o2, ex[0], ex[1]) : 0);
+#pragma unroll
+                for (int q = 0; q < m; ++q) sX[le * NV + ob + q * gstride(c, ex[0], ex[1])] = o[q];
+            }
+            __syncthreads();
+            // transverse projections with E^T along o1 (then o2): n -> m
+            {
+                int ex[3] = {n, n, DIM == 3 ? n : 1};
+                ex[c] = m;
+                // along o1: lines over the other two axes
+                const int nl1 = (DIM == 3 ? ex[c] * ex[o2] : ex[c]);
+                if (act && ln < nl1) {
+                    const int u0 = ln % ex[c], u1 = DIM == 3 ? ln / ex[c] : 0;
+                    int ey[3] = {ex[0], ex[1], ex[2]};
+                    ey[o1] = m;
+                    const int bi = u0 * gstride(c, ex[0], ex[1]) + (DIM == 3 ? u1 * gstride(o2, ex[0], ex[1]) : 0);
+                    const int bo = u0 * gstride(c, ey[0], ey[1]) + (DIM == 3 ? u1 * gstride(o2, ey[0], ey[1]) : 0);
+#pragma unroll
+                    for (int r = 0; r < n; ++r) v[r] = sX[le * NV + bi + r * gstride(o1, ex[0], ex[1])];
+#pragma unroll
+                    for (int q = 0; q < m; ++q) {
+                        double s = 0.0;
+#pragma unroll
+                        for (int r = 0; r < n; ++r) s = fma(S.E[r][q], v[r], s);
+                        if (DIM == 3) sY[le * NV + bo + q * gstride(o1, ey[0], ey[1])] = s;
+                        else sO[le * NPp + bo + q * gstride(o1, ey[0], ey[1])] += s;
+                    }
+                }
+                if (DIM == 3) {
+                    __syncthreads();
+                    ex[o1] = m;  // now (m along c, m along o1, n along o2)
+                    const int nl2 = ex[c] * ex[o1];
+                    if (act && ln < nl2) {
+                        const int u0 = ln % ex[c], u1 = ln / ex[c];
+                        const int bi = u0 * gstride(c, ex[0], ex[1]) + u1 * gstride(o1, ex[0], ex[1]);
+                        const int bo = u0 * gstride(c, m, m) + u1 * gstride(o1, m, m);
+#pragma unroll
+                        for (int r = 0; r < n; ++r) v[r] = sY[le * NV + bi + r * gstride(o2, ex[0], ex[1])];
+#pragma unroll
+                        for (int q = 0; q < m; ++q) {
+                            double s = 0.0;
+#pragma unroll
+                            for (int r = 0; r < n; ++r) s = fma(S.E[r][q], v[r], s);
+                            sO[le * NPp + bo + q * gstride(o2, m, m)] += s;
+                        }
+                    }
+                }
+            }
+        }
+        __syncthreads();
+        for (int t = threadIdx.x; t < ne * NPp; t += NT) a.out[e0 * NPp + t] = sO[t];
+    }
+}
+
+template <int DIM, bool DIV, int P>
+cudaError_t dg2_launch(const Geom &g, const DivGradParams &a, cudaStream_t st)
+{
+    using C = DG2<DIM, P>;
+    const int smem = DIV ? (int)sizeof(double) * (3 * C::EPC * C::NV + C::EPC * C::NPp + C::EPC * 2 * C::FV)
+                         : (int)sizeof(double) * (C::EPC * C::NPp + 2 * C::EPC * C::NV + C::EPC * DIM * 2 * C::FP);
+    if (smem > 227 * 1024) return cudaErrorNotSupported;
+    static bool attr = false;
+    if (!attr) {
+        if (DIV) cudaFuncSetAttribute(k_dg_div2<DIM, P>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        else cudaFuncSetAttribute(k_dg_grad2<DIM, P>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        attr = true;
+    }
+    long long blocks = (g.nel + C::EPC - 1) / C::EPC;
+    if (blocks > 148LL * 8) blocks = 148LL * 8;
+    if (DIV) k_dg_div2<DIM, P><<<(int)blocks, C::NT, smem, st>>>(g, a);
+    else k_dg_grad2<DIM, P><<<(int)blocks, C::NT, smem, st>>>(g, a);
+    return cudaGetLastError();
+}
+
 template <int DIM, bool DIV>
 cudaError_t dg_dispatch(const Geom &g, const DivGradParams &a, cudaStream_t st)
 {
@@ -332,6 +631,7 @@ cudaError_t dg_dispatch(const Geom &g, const DivGradParams &a, cudaStream_t st)
 #define DG_CASE(p)                                                                                         \
     case p:                                                                                                \
         if constexpr (DG_HAS_P(p) && (DIM == 2 || 3 * (p + 1) * (p + 1) * (p + 1) * 8 <= 40 * 1024)) {     \
+            if (!getenv("DG_DIVGRAD_V1")) return dg2_launch<DIM, DIV, p>(g, a, st);                        \
             if (DIV) k_dg_div<DIM, p><<<(int)blocks, 256, 0, st>>>(g, a);                                 \
             else k_dg_grad<DIM, p><<<(int)blocks, 256, 0, st>>>(g, a);                                    \
             return cudaGetLastError();                                                                     \
