@@ -15,6 +15,8 @@
 // (~400 flop per component-DOF at P=7), shared-memory resident.
 #pragma once
 
+#include <cstdlib>
+
 #include "dev_common.cuh"
 
 namespace dg {
@@ -299,11 +301,309 @@ __global__ void __launch_bounds__(256) k_convect(const ConvParams a)
     }
 }
 
+// ---------------------------------------------------------------------------
+// k_convect3 (3-D, the dispatched kernel): one thread per element line, the 1-D tables of
+// __constant__ c_ctab as uniform operands of fully unrolled contractions.
+//   interpolation GLL -> Gauss: x lines (n^2), y lines (Q n), z lines (Q^2; the Gauss column
+//   of all three components stays in the thread's registers);
+//   volume, per component c: fluxes W v_c v_e at the column's Gauss points, tested along z
+//   (B, B, G'), then y (lines (qx, k): B and G'), then x (lines (j, k): G' and B);
+//   faces: per direction d both sides at once: own (shared) and neighbour (global) traces
+//   interpolated to the face Gauss points along o1 then o2, the LLF flux, projected back.
+// Shared memory: nodal v, the accumulator, two work regions (the interpolation arrays, then
+// the test arrays, then the face arrays).
+// ---------------------------------------------------------------------------
+template <int P>
+struct C3Cfg {
+    static constexpr int n = P + 1, Q = (3 * P) / 2 + 1;
+    static constexpr int NPE = n * n * n;
+    static constexpr int NT = ((Q * Q + 31) / 32) * 32 < 128 ? 128 : ((Q * Q + 31) / 32) * 32;
+    static constexpr int W1 = 3 * n * n * Q;            // T1 / D region
+    static constexpr int W2 = 3 * n * Q * Q;            // T2 / A region
+    static constexpr int FACE1 = 2 * 3 * n * Q;         // per direction: F1 (both sides)
+    static constexpr int FACE2 = 2 * 3 * Q * Q;         // G (both sides)
+    static_assert(FACE1 <= W1 && FACE2 <= W2, "face arrays fit the work regions");
+    static constexpr int SMEM = (2 * 3 * NPE + W1 + W2) * 8;
+};
+
+template <int P>
+__global__ void __launch_bounds__(C3Cfg<P>::NT) k_convect3(const ConvParams a)
+{
+    using C = C3Cfg<P>;
+    constexpr int n = C::n, Q = C::Q, NPE = C::NPE, NT = C::NT;
+    const Geom &g = a.g;
+    const CvTab &T = c_ctab[P];
+    extern __shared__ double sm[];
+    double *sv = sm;                // [3][NPE] nodal v
+    double *sy = sv + 3 * NPE;      // [3][NPE] accumulator (weak form)
+    double *R1 = sy + 3 * NPE;      // W1 doubles
+    double *R2 = R1 + C::W1;        // W2 doubles
+    const int tid = threadIdx.x;
+    const double hx2 = 0.5 * g.h[0], hy2 = 0.5 * g.h[1], hz2 = 0.5 * g.h[2];
+    const double Wc = hx2 * hy2 * hz2;
+    const double sdx = 2.0 / g.h[0], sdy = 2.0 / g.h[1], sdz = 2.0 / g.h[2];
+    for (long long e = blockIdx.x; e < g.nel; e += gridDim.x) {
+        const int ec[3] = {(int)(e % g.Nl[0]), (int)((e / g.Nl[0]) % g.Nl[1]),
+                           (int)(e / ((long long)g.Nl[0] * g.Nl[1]))};
+        __syncthreads();
+        for (int t = tid; t < 3 * NPE; t += NT) {
+            const int c = t / NPE, q = t - c * NPE;
+            sv[t] = a.v[c][e * NPE + q];
+        }
+        __syncthreads();
+        // ---- interpolation x: lines (c, j, k) -> T1[c][(k n + j) Q + qx]
+        for (int l = tid; l < 3 * n * n; l += NT) {
+            const double *src = sv + l * n;
+            double v[n];
+#pragma unroll
+            for (int i = 0; i < n; ++i) v[i] = src[i];
+#pragma unroll
+            for (int q = 0; q < Q; ++q) {
+                double s = 0.0;
+#pragma unroll
+                for (int i = 0; i < n; ++i) s = fma(T.Bq[q][i], v[i], s);
+                R1[l * Q + q] = s;
+            }
+        }
+        __syncthreads();
+        // ---- y: lines (c, k, qx) over j -> T2[c][(k Q + qy) Q + qx]
+        for (int l = tid; l < 3 * n * Q; l += NT) {
+            const int qx = l % Q, ck = l / Q;  // ck = c n + k
+            double v[n];
+#pragma unroll
+            for (int j = 0; j < n; ++j) v[j] = R1[(ck * n + j) * Q + qx];
+#pragma unroll
+            for (int q = 0; q < Q; ++q) {
+                double s = 0.0;
+#pragma unroll
+                for (int j = 0; j < n; ++j) s = fma(T.Bq[q][j], v[j], s);
+                R2[(ck * Q + q) * Q + qx] = s;
+            }
+        }
+        __syncthreads();
+        // ---- z: column (qx, qy) of all three components, kept in registers
+        const bool col = tid < Q * Q;
+        const int qx = tid % Q, qy = tid / Q;
+        double vz[3][Q];
+        if (col) {
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                double v[n];
+#pragma unroll
+                for (int k = 0; k < n; ++k) v[k] = R2[((c * n + k) * Q + qy) * Q + qx];
+#pragma unroll
+                for (int q = 0; q < Q; ++q) {
+                    double s = 0.0;
+#pragma unroll
+                    for (int k = 0; k < n; ++k) s = fma(T.Bq[q][k], v[k], s);
+                    vz[c][q] = s;
+                }
+            }
+        }
+        // ---- volume, per component
+        for (int c = 0; c < 3; ++c) {
+            __syncthreads();  // R2 (T2 / previous A) and R1 (previous D) are free
+            if (col) {
+                const double wxy = T.wq[qx] * T.wq[qy] * Wc;
+                double ax[n], ay[n], az[n];
+#pragma unroll
+                for (int k = 0; k < n; ++k) ax[k] = ay[k] = az[k] = 0.0;
+#pragma unroll
+                for (int q = 0; q < Q; ++q) {
+                    const double w = wxy * T.wq[q] * vz[c][q];
+                    const double fx = w * vz[0][q], fy = w * vz[1][q], fz = w * vz[2][q];
+#pragma unroll
+                    for (int k = 0; k < n; ++k) {
+                        ax[k] = fma(T.Bq[q][k], fx, ax[k]);
+                        ay[k] = fma(T.Bq[q][k], fy, ay[k]);
+                        az[k] = fma(T.Gq[q][k], fz, az[k]);
+                    }
+                }
+                // A[t][(k Q + qy) Q + qx], t = x, y, z term
+#pragma unroll
+                for (int k = 0; k < n; ++k) {
+                    const int o = (k * Q + qy) * Q + qx;
+                    R2[o] = ax[k];
+                    R2[n * Q * Q + o] = ay[k];
+                    R2[2 * n * Q * Q + o] = az[k] * sdz;
+                }
+            }
+            __syncthreads();
+            // y: lines (k, qx): D1 = B_y A_x, D2 = (2/hy) G_y A_y + B_y A_z -> R1[t][(k n + j) Q + qx]
+            for (int l = tid; l < n * Q; l += NT) {
+                const int lqx = l % Q, k = l / Q;
+                double x1[Q], x2[Q], x3[Q];
+#pragma unroll
+                for (int q = 0; q < Q; ++q) {
+                    const int o = (k * Q + q) * Q + lqx;
+                    x1[q] = R2[o];
+                    x2[q] = R2[n * Q * Q + o];
+                    x3[q] = R2[2 * n * Q * Q + o];
+                }
+#pragma unroll
+                for (int j = 0; j < n; ++j) {
+                    double d1 = 0.0, d2 = 0.0, d3 = 0.0;
+#pragma unroll
+                    for (int q = 0; q < Q; ++q) {
+                        d1 = fma(T.Bq[q][j], x1[q], d1);
+                        d2 = fma(T.Gq[q][j], x2[q], d2);
+                        d3 = fma(T.Bq[q][j], x3[q], d3);
+                    }
+                    R1[(k * n + j) * Q + lqx] = d1;
+                    R1[n * n * Q + (k * n + j) * Q + lqx] = fma(d2, sdy, d3);
+                }
+            }
+            __syncthreads();
+            // x: lines (j, k): out_i = (2/hx) sum G D1 + sum B D2
+            for (int l = tid; l < n * n; l += NT) {
+                double x1[Q], x2[Q];
+#pragma unroll
+                for (int q = 0; q < Q; ++q) {
+                    x1[q] = R1[l * Q + q];
+                    x2[q] = R1[n * n * Q + l * Q + q];
+                }
+#pragma unroll
+                for (int i = 0; i < n; ++i) {
+                    double s1 = 0.0, s2 = 0.0;
+#pragma unroll
+                    for (int q = 0; q < Q; ++q) {
+                        s1 = fma(T.Gq[q][i], x1[q], s1);
+                        s2 = fma(T.Bq[q][i], x2[q], s2);
+                    }
+                    sy[c * NPE + l * n + i] = fma(s1, sdx, s2);
+                }
+            }
+        }
+        // ---- faces, per direction d (both sides): node of face index (fa along o1, fb along o2)
+        for (int d = 0; d < 3; ++d) {
+            const int o1 = d == 0 ? 1 : 0, o2 = d == 2 ? 1 : 2;
+            const int S[3] = {1, n, n * n};
+            const double ho1 = 0.5 * g.h[o1], ho2 = 0.5 * g.h[o2];
+            __syncthreads();  // R1 / R2 free
+            // F1[s][side2][c][fb][qa]: along o1, n -> Q; s = 0: face at node 0 (side -1), s = 1: node P
+            // side2 = 0: own trace, 1: neighbour trace
+            double *F1 = R1, *G2 = R2;
+            for (int l = tid; l < 2 * 2 * 3 * n; l += NT) {
+                const int fb = l % n, c = (l / n) % 3, side2 = (l / (3 * n)) % 2, s = l / (6 * n);
+                double v[n];
+                if (side2 == 0) {
+                    const int base = c * NPE + fb * S[o2] + (s ? P : 0) * S[d];
+#pragma unroll
+                    for (int fa = 0; fa < n; ++fa) v[fa] = sv[base + fa * S[o1]];
+                } else {
+                    int cn[3] = {ec[0], ec[1], ec[2]};
+                    cn[d] += s ? 1 : -1;
+                    const double *nb = elem_ptr(g, a.v[c], a.lo[c], a.hi[c], cn[0], cn[1], cn[2]) + fb * S[o2] +
+                                       (s ? 0 : P) * S[d];
+#pragma unroll
+                    for (int fa = 0; fa < n; ++fa) v[fa] = __ldg(nb + fa * S[o1]);
+                }
+#pragma unroll
+                for (int q = 0; q < Q; ++q) {
+                    double acc = 0.0;
+#pragma unroll
+                    for (int fa = 0; fa < n; ++fa) acc = fma(T.Bq[q][fa], v[fa], acc);
+                    F1[l * Q + q] = acc;
+                }
+            }
+            __syncthreads();
+            // G2[s][side2][c][qb][qa]: along o2, n -> Q
+            for (int l = tid; l < 2 * 2 * 3 * Q; l += NT) {
+                const int qa = l % Q, r = l / Q;  // r = (s 2 + side2) 3 + c
+                double v[n];
+#pragma unroll
+                for (int fb = 0; fb < n; ++fb) v[fb] = F1[(r * n + fb) * Q + qa];
+#pragma unroll
+                for (int q = 0; q < Q; ++q) {
+                    double acc = 0.0;
+#pragma unroll
+                    for (int fb = 0; fb < n; ++fb) acc = fma(T.Bq[q][fb], v[fb], acc);
+                    G2[(r * Q + q) * Q + qa] = acc;
+                }
+            }
+            __syncthreads();
+            // LLF flux at the face Gauss points -> H[s][c][qb][qa] (in F1's region)
+            double *H = F1;
+            for (int l = tid; l < 2 * Q * Q; l += NT) {
+                const int t = l % (Q * Q), s = l / (Q * Q);
+                const int qa = t % Q, qb = t / Q;
+                const double WF = T.wq[qa] * ho1 * T.wq[qb] * ho2;
+                // side s = 1 (node P): own is '-', neighbour '+'; s = 0: neighbour '-', own '+'
+                const double *own = G2 + (s * 2 + 0) * 3 * Q * Q, *nbr = G2 + (s * 2 + 1) * 3 * Q * Q;
+                const double *vm = s ? own : nbr, *vp = s ? nbr : own;
+                const double vnm = vm[d * Q * Q + t], vnp = vp[d * Q * Q + t];
+                const double Lam = 2.0 * fmax(fabs(vnm), fabs(vnp));
+                const double sgn = s ? 1.0 : -1.0;
+#pragma unroll
+                for (int c = 0; c < 3; ++c) {
+                    const double hc = 0.5 * (vnm * vm[c * Q * Q + t] + vnp * vp[c * Q * Q + t]) +
+                                      0.5 * Lam * (vm[c * Q * Q + t] - vp[c * Q * Q + t]);
+                    H[(s * 3 + c) * Q * Q + t] = sgn * WF * hc;
+                }
+            }
+            __syncthreads();
+            // back along o1: lines (s, c, qb): Q -> n  -> P1[s][c][qb][fa] (in G2's region)
+            double *P1 = G2;
+            for (int l = tid; l < 2 * 3 * Q; l += NT) {
+                double v[Q];
+#pragma unroll
+                for (int q = 0; q < Q; ++q) v[q] = H[l * Q + q];
+#pragma unroll
+                for (int fa = 0; fa < n; ++fa) {
+                    double acc = 0.0;
+#pragma unroll
+                    for (int q = 0; q < Q; ++q) acc = fma(T.Bq[q][fa], v[q], acc);
+                    P1[l * n + fa] = acc;
+                }
+            }
+            __syncthreads();
+            // back along o2: lines (s, c, fa): Q -> n, subtract at the face nodes
+            for (int l = tid; l < 2 * 3 * n; l += NT) {
+                const int fa = l % n, c = (l / n) % 3, s = l / (3 * n);
+                double v[Q];
+#pragma unroll
+                for (int q = 0; q < Q; ++q) v[q] = P1[((s * 3 + c) * Q + q) * n + fa];
+#pragma unroll
+                for (int fb = 0; fb < n; ++fb) {
+                    double acc = 0.0;
+#pragma unroll
+                    for (int q = 0; q < Q; ++q) acc = fma(T.Bq[q][fb], v[q], acc);
+                    sy[c * NPE + fa * S[o1] + fb * S[o2] + (s ? P : 0) * S[d]] -= acc;
+                }
+            }
+        }
+        __syncthreads();
+        // ---- M^-1 (GLL-lumped) and store
+        for (int t = tid; t < 3 * NPE; t += NT) {
+            const int c = t / NPE, q = t - c * NPE;
+            const int i = q % n, j = (q / n) % n, k = q / (n * n);
+            const double m = T.w[i] * hx2 * T.w[j] * hy2 * T.w[k] * hz2;
+            a.out[c][e * NPE + q] = sy[t] / m;
+        }
+    }
+}
+
 template <int DIM>
 struct ConvDispatch {
     template <int P>
     static cudaError_t go(const ConvParams &a, cudaStream_t st)
     {
+        if constexpr (DIM == 3 && C3Cfg<P>::SMEM <= 227 * 1024) {
+            static const bool v1 = getenv("DG_CONVECT_V1") != nullptr;
+            if (!v1) {
+                constexpr int smem3 = C3Cfg<P>::SMEM;
+                static bool attr = false;
+                if (!attr) {
+                    cudaError_t e = cudaFuncSetAttribute(k_convect3<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem3);
+                    if (e != cudaSuccess) return e;
+                    attr = true;
+                }
+                long long grid = a.g.nel;
+                if (grid > 148 * 16) grid = 148 * 16;
+                k_convect3<P><<<(int)grid, C3Cfg<P>::NT, smem3, st>>>(a);
+                return cudaGetLastError();
+            }
+        }
         constexpr int smem = CCfg<DIM, P>::SMEM;
         if constexpr (smem > 227 * 1024) {
             return cudaErrorNotSupported;  // shared-memory tile too large (3-D P=10)
