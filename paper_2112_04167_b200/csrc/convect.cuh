@@ -317,26 +317,28 @@ template <int P>
 struct C3Cfg {
     static constexpr int n = P + 1, Q = (3 * P) / 2 + 1;
     static constexpr int NPE = n * n * n;
+    static constexpr int NX = n % 2 == 0 ? n + 1 : n;   // padded x-line pitch of sv / sy (odd:
+    static constexpr int NPEP = NX * n * n;             //  conflict-free strided line access)
     static constexpr int NT = ((Q * Q + 31) / 32) * 32 < 128 ? 128 : ((Q * Q + 31) / 32) * 32;
     static constexpr int W1 = 3 * n * n * Q;            // T1 / D region
     static constexpr int W2 = 3 * n * Q * Q;            // T2 / A region
     static constexpr int FACE1 = 2 * 3 * n * Q;         // per direction: F1 (both sides)
     static constexpr int FACE2 = 2 * 3 * Q * Q;         // G (both sides)
-    static_assert(FACE1 <= W1 && FACE2 <= W2, "face arrays fit the work regions");
-    static constexpr int SMEM = (2 * 3 * NPE + W1 + W2) * 8;
+    static_assert(FACE1 <= W1 && FACE2 <= W2 && 2 * 3 * Q * (n + 1) <= W2, "face arrays fit the work regions");
+    static constexpr int SMEM = (2 * 3 * NPEP + W1 + W2) * 8;
 };
 
 template <int P>
 __global__ void __launch_bounds__(C3Cfg<P>::NT) k_convect3(const ConvParams a)
 {
     using C = C3Cfg<P>;
-    constexpr int n = C::n, Q = C::Q, NPE = C::NPE, NT = C::NT;
+    constexpr int n = C::n, Q = C::Q, NPE = C::NPE, NT = C::NT, NX = C::NX, NPEP = C::NPEP;
     const Geom &g = a.g;
     const CvTab &T = c_ctab[P];
     extern __shared__ double sm[];
-    double *sv = sm;                // [3][NPE] nodal v
-    double *sy = sv + 3 * NPE;      // [3][NPE] accumulator (weak form)
-    double *R1 = sy + 3 * NPE;      // W1 doubles
+    double *sv = sm;                // [3][NPEP] nodal v (x-line pitch NX)
+    double *sy = sv + 3 * NPEP;     // [3][NPEP] accumulator (weak form)
+    double *R1 = sy + 3 * NPEP;     // W1 doubles
     double *R2 = R1 + C::W1;        // W2 doubles
     const int tid = threadIdx.x;
     const double hx2 = 0.5 * g.h[0], hy2 = 0.5 * g.h[1], hz2 = 0.5 * g.h[2];
@@ -348,12 +350,12 @@ __global__ void __launch_bounds__(C3Cfg<P>::NT) k_convect3(const ConvParams a)
         __syncthreads();
         for (int t = tid; t < 3 * NPE; t += NT) {
             const int c = t / NPE, q = t - c * NPE;
-            sv[t] = a.v[c][e * NPE + q];
+            sv[c * NPEP + (q / n) * NX + q % n] = a.v[c][e * NPE + q];
         }
         __syncthreads();
         // ---- interpolation x: lines (c, j, k) -> T1[c][(k n + j) Q + qx]
         for (int l = tid; l < 3 * n * n; l += NT) {
-            const double *src = sv + l * n;
+            const double *src = sv + (l / (n * n)) * NPEP + (l % (n * n)) * NX;
             double v[n];
 #pragma unroll
             for (int i = 0; i < n; ++i) v[i] = src[i];
@@ -470,14 +472,14 @@ __global__ void __launch_bounds__(C3Cfg<P>::NT) k_convect3(const ConvParams a)
                         s1 = fma(T.Gq[q][i], x1[q], s1);
                         s2 = fma(T.Bq[q][i], x2[q], s2);
                     }
-                    sy[c * NPE + l * n + i] = fma(s1, sdx, s2);
+                    sy[c * NPEP + l * NX + i] = fma(s1, sdx, s2);
                 }
             }
         }
         // ---- faces, per direction d (both sides): node of face index (fa along o1, fb along o2)
         for (int d = 0; d < 3; ++d) {
             const int o1 = d == 0 ? 1 : 0, o2 = d == 2 ? 1 : 2;
-            const int S[3] = {1, n, n * n};
+            const int S[3] = {1, NX, NX * n};
             const double ho1 = 0.5 * g.h[o1], ho2 = 0.5 * g.h[o2];
             __syncthreads();  // R1 / R2 free
             // F1[s][side2][c][fb][qa]: along o1, n -> Q; s = 0: face at node 0 (side -1), s = 1: node P
@@ -487,16 +489,17 @@ __global__ void __launch_bounds__(C3Cfg<P>::NT) k_convect3(const ConvParams a)
                 const int fb = l % n, c = (l / n) % 3, side2 = (l / (3 * n)) % 2, s = l / (6 * n);
                 double v[n];
                 if (side2 == 0) {
-                    const int base = c * NPE + fb * S[o2] + (s ? P : 0) * S[d];
+                    const int base = c * NPEP + fb * S[o2] + (s ? P : 0) * S[d];
 #pragma unroll
                     for (int fa = 0; fa < n; ++fa) v[fa] = sv[base + fa * S[o1]];
                 } else {
                     int cn[3] = {ec[0], ec[1], ec[2]};
                     cn[d] += s ? 1 : -1;
-                    const double *nb = elem_ptr(g, a.v[c], a.lo[c], a.hi[c], cn[0], cn[1], cn[2]) + fb * S[o2] +
-                                       (s ? 0 : P) * S[d];
+                    const int G[3] = {1, n, n * n};  // global (unpadded) strides
+                    const double *nb = elem_ptr(g, a.v[c], a.lo[c], a.hi[c], cn[0], cn[1], cn[2]) + fb * G[o2] +
+                                       (s ? 0 : P) * G[d];
 #pragma unroll
-                    for (int fa = 0; fa < n; ++fa) v[fa] = __ldg(nb + fa * S[o1]);
+                    for (int fa = 0; fa < n; ++fa) v[fa] = __ldg(nb + fa * G[o1]);
                 }
 #pragma unroll
                 for (int q = 0; q < Q; ++q) {
@@ -553,7 +556,7 @@ __global__ void __launch_bounds__(C3Cfg<P>::NT) k_convect3(const ConvParams a)
                     double acc = 0.0;
 #pragma unroll
                     for (int q = 0; q < Q; ++q) acc = fma(T.Bq[q][fa], v[q], acc);
-                    P1[l * n + fa] = acc;
+                    P1[l * NX + fa] = acc;
                 }
             }
             __syncthreads();
@@ -562,13 +565,13 @@ __global__ void __launch_bounds__(C3Cfg<P>::NT) k_convect3(const ConvParams a)
                 const int fa = l % n, c = (l / n) % 3, s = l / (3 * n);
                 double v[Q];
 #pragma unroll
-                for (int q = 0; q < Q; ++q) v[q] = P1[((s * 3 + c) * Q + q) * n + fa];
+                for (int q = 0; q < Q; ++q) v[q] = P1[((s * 3 + c) * Q + q) * NX + fa];
 #pragma unroll
                 for (int fb = 0; fb < n; ++fb) {
                     double acc = 0.0;
 #pragma unroll
                     for (int q = 0; q < Q; ++q) acc = fma(T.Bq[q][fb], v[q], acc);
-                    sy[c * NPE + fa * S[o1] + fb * S[o2] + (s ? P : 0) * S[d]] -= acc;
+                    sy[c * NPEP + fa * S[o1] + fb * S[o2] + (s ? P : 0) * S[d]] -= acc;
                 }
             }
         }
@@ -578,7 +581,7 @@ __global__ void __launch_bounds__(C3Cfg<P>::NT) k_convect3(const ConvParams a)
             const int c = t / NPE, q = t - c * NPE;
             const int i = q % n, j = (q / n) % n, k = q / (n * n);
             const double m = T.w[i] * hx2 * T.w[j] * hy2 * T.w[k] * hz2;
-            a.out[c][e * NPE + q] = sy[t] / m;
+            a.out[c][e * NPE + q] = sy[c * NPEP + (q / n) * NX + i] / m;
         }
     }
 }
