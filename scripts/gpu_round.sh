@@ -4,4 +4,6 @@ timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -30 > gpurun_out/pyt
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1
 timeout 600 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err
 cat gpurun_out/pytest_gpu.log gpurun_out/smoke.log gpurun_out/bench.json
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches.csv python bench.py --steps 3 --warmup 3 --solves 1 --solve-warmup 0 --no-cpu-baseline > gpurun_out/ncu_launch.log 2>&1
+timeout 600 python bench.py --steps 3 --warmup 3 --solves 1 --solve-warmup 0 --no-cpu-baseline > gpurun_out/plain.log 2>&1 && \
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 3000 --csv --log-file gpurun_out/launches.csv python bench.py --steps 3 --warmup 3 --solves 1 --solve-warmup 0 --no-cpu-baseline > gpurun_out/ncu_launch.log 2>&1
+python tools/launch_summary.py gpurun_out/launches.csv > gpurun_out/launch_summary.txt; head -30 gpurun_out/launch_summary.txt
