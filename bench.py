@@ -267,6 +267,7 @@ def run_product(args, rank, world, local_rank):
     stage = None
     if world == 1 and not args.no_stage:
         stage = run_stage(dg, torch, stream, barrier)
+        stage["vv_step"] = run_vv_step(dg, torch, stream, barrier)
 
     # ---- e2e through the host-buffer C-ABI call (rank-local slab)
     u_np = np.ascontiguousarray(u_h)
@@ -338,6 +339,47 @@ def run_product(args, rank, world, local_rank):
         "cpu_baseline": cb,
     }
     print(json.dumps(line), flush=True)
+
+
+def run_vv_step(dg, torch, stream, barrier, N=16, P=7, reps=2):
+    """One IMEX-RK step with solution-dependent viscosity (Alg. 3 with nu(v),
+    F_d2/F_d3, forcing and the final projection) on the VVP manufactured solution (PAPER.md:
+    1189-1290, nu0 = nu1 = 0.01) on N^3 elements of the unit cube, P velocity / P-1 pressure
+    (Schwarz Poisson, Jacobi variable-nu Helmholtz: lam h^2 / nu ~ 67 here, where the mean-nu
+    Schwarz preconditioner saves only ~25 % of the iterations at ~1.4x their cost), RK-ARS3,
+    dt = 2^-7."""
+    from workloads import node_coords
+    from workloads.inputs import vvp_exact, vvp_forcing
+
+    dev = torch.device("cuda", torch.cuda.current_device())
+    L = (1.0, 1.0, 1.0)
+    mv = dg.dg_mesh_create(3, (N,) * 3, L, P, stream=stream)
+    mp = dg.dg_mesh_create(3, (N,) * 3, L, P - 1, stream=stream)
+    dg.dg_mesh_set_precond(mp, dg.DG_PC_SCHWARZ2)
+    X = node_coords(3, (N,) * 3, L, P)
+    tab = dg.TABLEAUX["RK-ARS3"]
+    dt, visc = 2.0 ** -7, (0.01, 0.01, 2.0)
+    fs = [[torch.from_numpy(np.ascontiguousarray(a)).to(dev) for a in vvp_forcing(X, c * dt, *visc[:2])]
+          for c in tab["c"]]
+    v0 = [torch.from_numpy(np.ascontiguousarray(a)).to(dev) for a in vvp_exact(X, 0.0)[0]]
+    psi = torch.zeros(mp.n_el, mp.npe, dtype=torch.float64, device=dev)
+    times, info = [], None
+    for k in range(reps + 1):
+        v = [x.clone() for x in v0]
+        barrier()
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        info = dg.dg_imex_rk_step_vv(mv, mp, tab, dt, visc, v, psi, 1e-10, 20000, fs=fs)
+        b.record(stream)
+        barrier()
+        if k > 0:
+            times.append(a.elapsed_time(b))
+    d = info.as_dict()
+    return {"workload": "VVP %d^3 P=%d (P_p=%d), RK-ARS3, dt=2^-7, nu0=nu1=0.01" % (N, P, P - 1),
+            "ms_per_step": statistics.mean(times), "steps": reps, "pressure_iters": d["pressure_iters"],
+            "velocity_iters": d["velocity_iters"], "implicit_stages": d["stages"],
+            "dofs_per_component": mv.ndof}
 
 
 def run_stage(dg, torch, stream, barrier, reps=2):

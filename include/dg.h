@@ -120,9 +120,13 @@ dg_status dg_pcg_solve(dg_mesh *m, double lam, const double *nu, double nu_const
  *     B r = sum_K R_K^T A_KK^-1 R_K r + P_1 A_c^+ P_1^T r,   A_c = P_1^T A P_1,
  * non-overlapping element blocks (exact, by fast diagonalisation of the Kronecker-sum block)
  * plus the continuous vertex-based Q1 space on the same mesh as coarse space (exact solve by
- * a real Fourier diagonalisation; pseudo-inverse on the constants for lam = 0).  Needs a
- * constant viscosity (solves with a nu field return DG_EUNSUPPORTED), 2 <= N_d <= 64 and
- * P >= 2 (else DG_EUNSUPPORTED here).  Multi-rank: the coarse residual is all-reduced
+ * a real Fourier diagonalisation; pseudo-inverse on the constants for lam = 0).  Exact
+ * blocks / coarse operator for a constant viscosity; for a nu field both are built with the
+ * mass-weighted mean viscosity (computed on the device per solve): a spectrally equivalent
+ * preconditioner (constant max nu / min nu).  In dg_pcg_solve the coarse term is used while
+ * diffusion dominates at the element scale, lam min_d h_d^2 <= 50 nu (above, the element
+ * blocks alone converge faster: measured); dg_schwarz_apply always applies the full B.
+ * Needs 2 <= N_d <= 64 and P >= 2 (else DG_EUNSUPPORTED here).  Multi-rank: the coarse residual is all-reduced
  * (NV = prod N_d doubles per iteration) and every rank solves the coarse problem. */
 #define DG_PC_JACOBI 0
 #define DG_PC_SCHWARZ2 1
@@ -242,8 +246,8 @@ dg_status dg_imex_rk_step(dg_mesh *mv, dg_mesh *mp, const dg_tableau *tab, doubl
  * sum_F ({u} n_c, [phi_i])_GLL]:  F_d2,c = sum_e D_e(nu D_c u_e),  F_d3,c = -D_c(nu sum_e D_e u_e)
  * (readings in DESIGN.md §9; for constant nu F_d2 + F_d3 = 0 exactly, the D_c commute).
  * fs: NULL (F_s = 0) or s*dim DEVICE pointers, fs[j*dim + c] = F_s,c at t + c_j dt (nodal).
- * The Helmholtz solves need mv's preconditioner to be Jacobi (variable nu); mp may use
- * DG_PC_SCHWARZ2.  Workspace (4 s + 2) dim + dim^2 + 2 velocity fields, owned by mv.
+ * The Helmholtz solves (variable nu) and the Poisson solves use the preconditioner set on mv
+ * and mp respectively (DG_PC_SCHWARZ2 uses the mean viscosity for the variable-nu solves).  Workspace (4 s + 2) dim + dim^2 + 2 velocity fields, owned by mv.
  * Synchronous.  Errors as dg_imex_rk_step; DG_EINVAL for nu0 <= 0, nu1 < 0 or vmax <= 0. */
 typedef struct {
     double nu0, nu1, vmax;

@@ -171,6 +171,7 @@ struct dg_mesh {
     SwTab h_sw{};
     double *d_swF = nullptr, *rc_el = nullptr, *chat = nullptr, *xc = nullptr, *rc = nullptr;
     double sw_nu = -1.0;
+    bool sw_coarse_on = true;
 };
 
 #define CK(call)                                                                                         \
@@ -365,7 +366,7 @@ dg_status reduce_fin(dg_mesh *m, int G, int mode)
 // ---------------------------------------------------------------------------
 dg_status sw_check(const dg_mesh *m, const double *nu)
 {
-    if (nu) return set_error(DG_EUNSUPPORTED, "the Schwarz preconditioner needs a constant viscosity (nu == NULL)");
+    (void)nu;  // variable nu: the preconditioner uses the mass-weighted mean viscosity
     const char *why = nullptr;
     if (!schwarz_supported(m->g, &why)) return set_error(DG_EUNSUPPORTED, why);
     return DG_OK;
@@ -383,23 +384,26 @@ dg_status ensure_sw(dg_mesh *m, double nu_const)
         CKS(alloc((void **)&m->xc, sizeof(double) * (size_t)NV));
         if (m->nranks > 1) CKS(alloc((void **)&m->rc, sizeof(double) * (size_t)NV));
     }
-    if (m->sw_nu != nu_const) {
+    (void)nu_const;  // the tables are built once for nu = 1 (nu scales eigenvalues / symbols only)
+    if (m->sw_nu != 1.0) {
         std::vector<double> F;
-        build_sw_tab(g, nu_const, &m->h_sw, F);
+        build_sw_tab(g, 1.0, &m->h_sw, F);
         CK(cudaMemcpyAsync(m->d_sw, &m->h_sw, sizeof(SwTab), cudaMemcpyHostToDevice, m->st));
         CK(cudaMemcpyAsync(m->d_swF, F.data(), sizeof(double) * F.size(), cudaMemcpyHostToDevice, m->st));
         CK(cudaStreamSynchronize(m->st));  // F is a host temporary
-        m->sw_nu = nu_const;
+        m->sw_nu = 1.0;
     }
     return DG_OK;
 }
 
 // coarse part: x_c = A_c^+ P_1^T r from the element moments rc_el; r_c.x_c partials written
 // to partial[pslot + b] (b < sw_cz_grid) when `partial` is set
-dg_status sw_coarse(dg_mesh *m, double lam, double *partial, int pslot)
+dg_status sw_coarse(dg_mesh *m, double lam, double nu, const double *nu_eff, double *partial, int pslot)
 {
     const Geom &g = m->g;
     SwCoarseParams c;
+    c.nu = nu;
+    c.nu_eff = nu_eff;
     c.T = m->d_sw;
     c.F = m->d_swF;
     c.dim = g.dim;
@@ -431,11 +435,12 @@ dg_status sw_coarse(dg_mesh *m, double lam, double *partial, int pslot)
 }
 
 // z = B r (block part into z, rc_el moments; then the coarse solve and z += P_1 x_c)
-dg_status sw_apply_impl(dg_mesh *m, double lam, const double *r, double *z)
+dg_status sw_apply_impl(dg_mesh *m, double lam, double nu, const double *r, double *z)
 {
     SwBlockParams b;
     b.T = m->d_sw;
     b.lam = lam;
+    b.nu = nu;
     b.mode = SW_APPLY;
     b.nel = m->g.nel;
     b.rin = r;
@@ -445,7 +450,7 @@ dg_status sw_apply_impl(dg_mesh *m, double lam, const double *r, double *z)
     int grid = 0;
     CK(launch_sw_block(m->g, m->h_sw, b, m->st, &grid));
     m->launches += 1;
-    CKS(sw_coarse(m, lam, nullptr, 0));
+    CKS(sw_coarse(m, lam, nu, nullptr, nullptr, 0));
     SwPupdParams p;
     p.T = m->d_sw;
     p.nel = m->g.nel;
@@ -465,6 +470,7 @@ dg_status sw_pcg_step(dg_mesh *m, double lam, int mode, int fin)
     SwBlockParams b;
     b.T = m->d_sw;
     b.lam = lam;
+    b.nu_eff = &m->scal->nu_eff;
     b.mode = mode;
     b.nel = m->g.nel;
     b.r = m->r;
@@ -477,7 +483,8 @@ dg_status sw_pcg_step(dg_mesh *m, double lam, int mode, int fin)
     int grid = 0;
     CK(launch_sw_block(m->g, m->h_sw, b, m->st, &grid));
     m->launches += 1;
-    CKS(sw_coarse(m, lam, m->partial, grid));
+    if (!m->sw_coarse_on) return reduce_fin(m, grid, fin);  // element blocks only (x_c = 0)
+    CKS(sw_coarse(m, lam, 1.0, &m->scal->nu_eff, m->partial, grid));
     return reduce_fin(m, grid + sw_cz_grid(m->h_sw), fin);
 }
 
@@ -496,6 +503,7 @@ dg_status pcg_impl(dg_mesh *m, double lam, const double *nu, double nu_const, co
     s0.tol2 = tol * tol;
     s0.ndof_global = m->ndof_global;
     s0.maxit = maxit;
+    s0.nu_eff = nu ? 1.0 : nu_const;
     CK(cudaMemcpyAsync(m->scal, &s0, sizeof(s0), cudaMemcpyHostToDevice, m->st));
 
     // preconditioner: two-level Schwarz (dg_mesh_set_precond) or Jacobi
@@ -503,6 +511,22 @@ dg_status pcg_impl(dg_mesh *m, double lam, const double *nu, double nu_const, co
     if (sw) {
         CKS(sw_check(m, nu));
         CKS(ensure_sw(m, nu_const));
+        double nu_bar = nu_const;
+        if (nu) {  // variable nu: blocks and coarse operator with the mass-weighted mean viscosity
+            CK(launch_mass_moments(g, nu, m->mass_e, m->partial, m->st));
+            m->launches += 1;
+            CKS(reduce_fin(m, VG, FIN_NUMEAN));
+            CK(cudaMemcpyAsync(m->hscal, m->scal, sizeof(PcgScal), cudaMemcpyDeviceToHost, m->st));
+            CK(cudaStreamSynchronize(m->st));
+            nu_bar = m->hscal->nu_eff;
+        }
+        // the Q1 coarse space pays while diffusion dominates at the element scale (measured:
+        // lam h^2 / nu <= ~50); above, the element blocks alone are better
+        double h2 = 1e300;
+        for (int d = 0; d < g.dim; ++d) h2 = std::min(h2, g.h[d] * g.h[d]);
+        m->sw_coarse_on = lam * h2 <= 50.0 * nu_bar;
+        if (!m->sw_coarse_on) CK(cudaMemsetAsync(m->xc, 0, sizeof(double) * (size_t)g.N[0] * g.N[1] *
+                                                              (g.dim == 3 ? g.N[2] : 1), m->st));
     }
     // Jacobi preconditioner: D^-1 straight from the closed-form kernel where it applies
     bool self = false;
@@ -960,7 +984,7 @@ dg_status dg_schwarz_apply(dg_mesh *m, double lam, double nu_const, const double
     if (r == z) return set_error(DG_EINVAL, "r and z must not alias");
     CKS(sw_check(m, nullptr));
     CKS(ensure_sw(m, nu_const));
-    return sw_apply_impl(m, lam, r, z);
+    return sw_apply_impl(m, lam, nu_const, r, z);
 }
 
 dg_status dg_convect_rhs(dg_mesh *m, const double *const v[3], double *const out[3])

@@ -321,7 +321,8 @@ struct C3Cfg {
     static constexpr int NPEP = NX * n * n;             //  conflict-free strided line access)
     static constexpr int NT = ((Q * Q + 31) / 32) * 32 < 128 ? 128 : ((Q * Q + 31) / 32) * 32;
     static constexpr int W1 = 3 * n * n * Q;            // T1 / D region
-    static constexpr int W2 = 3 * n * Q * Q;            // T2 / A region
+    static constexpr int W2a = 3 * n * Q * Q, W2b = 2 * 3 * Q * (n + 1);
+    static constexpr int W2 = W2a > W2b ? W2a : W2b;    // T2 / A / face G2, P1 region
     static constexpr int FACE1 = 2 * 3 * n * Q;         // per direction: F1 (both sides)
     static constexpr int FACE2 = 2 * 3 * Q * Q;         // G (both sides)
     static_assert(FACE1 <= W1 && FACE2 <= W2 && 2 * 3 * Q * (n + 1) <= W2, "face arrays fit the work regions");

@@ -170,6 +170,7 @@ cudaError_t launch_dg_grad(const Geom &gv, const DivGradParams &a, cudaStream_t 
 // PCG vector kernels -------------------------------------------------------
 struct PcgScal {                 // device-resident scalars of one solve
     double rz, pq, alpha, beta, qmean, res2, fnorm2, fmean, sum_m, tol2;
+    double nu_eff;                 // Schwarz preconditioner viscosity (mass-weighted mean of nu)
     double lam;
     long long ndof_global;
     int iter, done, status, maxit;
@@ -195,7 +196,7 @@ cudaError_t launch_shift(const Geom &g, double *x, const double *shift, cudaStre
 // deterministic reduction of partial[G][K] into sums[K] (single CTA, fixed order)
 cudaError_t launch_reduce(const double *partial, int G, int K, double *sums, cudaStream_t st);
 // scalar finalisation steps (single thread), mode-dependent
-enum FinMode { FIN_FMEAN = 0, FIN_INIT = 1, FIN_INIT2 = 2, FIN_ALPHA = 3, FIN_BETA = 4, FIN_UMEAN = 5 };
+enum FinMode { FIN_FMEAN = 0, FIN_INIT = 1, FIN_INIT2 = 2, FIN_ALPHA = 3, FIN_BETA = 4, FIN_UMEAN = 5, FIN_NUMEAN = 6 };
 cudaError_t launch_finalize(int mode, const double *sums, PcgScal *s, double *hist, double *aux, cudaStream_t st);
 cudaError_t launch_reduce_s(const double *partial, int G, int K, double *sums, const PcgScal *s, cudaStream_t st);
 cudaError_t launch_reduce_fin(const double *partial, int G, int K, double *sums, int mode, PcgScal *s, double *hist,
@@ -225,6 +226,8 @@ enum { SW_APPLY = 0, SW_INIT = 1, SW_UPDATE = 2 };
 struct SwBlockParams {
     const SwTab *T = nullptr;
     double lam = 0.0;
+    double nu = 1.0;                // viscosity of the blocks (tables are for nu = 1) ...
+    const double *nu_eff = nullptr; // ... or read from the device (PCG: PcgScal::nu_eff)
     int mode = SW_APPLY;
     long long nel = 0;
     double *r = nullptr;            // INIT/UPDATE: residual, updated in place
@@ -241,6 +244,8 @@ struct SwCoarseParams {
     const double *F = nullptr;      // [3][SW_NCMAX^2] Fourier bases F_d[j*N + col]
     int dim = 3;
     double lam = 0.0;
+    double nu = 1.0;
+    const double *nu_eff = nullptr;
     const double *rc_el = nullptr;  // element moments [2^dim][nel] (single rank: gathered directly)
     long long nel = 0;              // local elements
     double *rc = nullptr;           // multi-rank: the all-reduced vertex vector (cfwd input)

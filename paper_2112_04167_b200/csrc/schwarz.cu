@@ -237,10 +237,13 @@ __global__ void __launch_bounds__(256) k_sw_block(SwBlockParams a, const __grid_
     double *sR = smem + SM::R, *sQ = smem + SM::Q, *sA = smem + SM::A, *sInv = smem + SM::INV,
            *sMi = smem + SM::MI, *sx = smem + SM::X;
     __shared__ double red[8][2];
+    // tables are built for nu = 1: K = nu (2/h) Kref scales the eigenvalues only
+    const double nu_eff = a.nu_eff ? *a.nu_eff : a.nu;
     for (int t = threadIdx.x; t < NPE; t += NT) {
         const int i = t % n, j = (t / n) % n, k = DIM == 3 ? t / (n * n) : 0;
-        double den = a.lam + L.L[0][i] + L.L[1][j];
-        if (DIM == 3) den += L.L[2][k];
+        double ls = L.L[0][i] + L.L[1][j];
+        if (DIM == 3) ls += L.L[2][k];
+        const double den = fma(nu_eff, ls, a.lam);
         sInv[t] = 1.0 / den;
         sMi[t] = 1.0 / a.mass_e[t];
     }
@@ -479,6 +482,7 @@ __global__ void k_sw_cz(SwCoarseParams a)
     __shared__ double red[32];
     for (int q = threadIdx.y * 32 + threadIdx.x; q < Nz * Nz; q += 32 * blockDim.y) Fz[q] = a.F[2 * SW_NCMAX * SW_NCMAX + q];
     const int p = blockIdx.x * 32 + threadIdx.x;  // plane index ky * Nx + kx
+    const double nu_eff = a.nu_eff ? *a.nu_eff : a.nu;
     for (int vz = threadIdx.y; vz < Nz; vz += blockDim.y) col[vz * 32 + threadIdx.x] = p < NP ? a.chat[(long long)vz * NP + p] : 0.0;
     __syncthreads();
     double dot = 0.0;
@@ -490,7 +494,7 @@ __global__ void k_sw_cz(SwCoarseParams a)
         if (p < NP) {
             const double mx = T->eM[0][kx], my = T->eM[1][ky], mz = T->eM[2][kz];
             const double mu = a.lam * mx * my * mz +
-                              T->nu * (T->eK[0][kx] * my * mz + mx * T->eK[1][ky] * mz + mx * my * T->eK[2][kz]);
+                              nu_eff * (T->eK[0][kx] * my * mz + mx * T->eK[1][ky] * mz + mx * my * T->eK[2][kz]);
             inv = mu > 0.0 ? 1.0 / mu : 0.0;
         }
         dot = fma(acc * inv, acc, dot);

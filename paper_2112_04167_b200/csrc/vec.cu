@@ -246,6 +246,9 @@ __device__ void finalize(int mode, const double *sums, PcgScal *s, double *hist,
     case FIN_UMEAN:
         aux[0] = sums[0] / sums[1];
         break;
+    case FIN_NUMEAN:  // sum m nu / sum m
+        s->nu_eff = sums[0] / sums[1];
+        break;
     }
 }
 
