@@ -165,3 +165,22 @@ def test_schwarz_variable_nu_solve_matches_oracle(dim, N, P, lam):
         u2 = torch.zeros_like(u)
         info_j = dg.dg_pcg_solve(m2, lam, T(nu), 0.0, T(f), 1e-11, 5000, u2)
         assert info.iters < 0.6 * info_j.iters, (info.iters, info_j.iters)
+
+
+def test_schwarz_c3_poisson_full_size():
+    """Config-3 pressure Poisson (16^3, P_p = 6, lam = 0) with the Schwarz preconditioner at the
+    config tolerance, checked with the ORACLE's full operator: ||M^-1 (M f' - A u)|| / ||f'||."""
+    c = config(3)
+    m = dg.dg_mesh_create(3, c.N, c.L, c.P_p, stream=torch.cuda.current_stream())
+    om = oracle.Mesh(3, c.N, c.L, c.P_p)
+    dg.dg_mesh_set_precond(m, dg.DG_PC_SCHWARZ2)
+    f = c.poisson_rhs_raw()
+    u = torch.zeros(f.shape, dtype=torch.float64, device=DEV)
+    info = dg.dg_pcg_solve(m, 0.0, None, 1.0, T(f), c.tol, 2000, u)
+    mass = oracle.mass(om)
+    fp = f - (mass * f).sum() / mass.sum()
+    uh = H(u)
+    r = mass * fp - oracle.sip_apply(om, 0.0, uh, nu_const=1.0)
+    res = np.linalg.norm(r / mass) / np.linalg.norm(fp)
+    assert res <= 1.1 * c.tol, (res, info.as_dict())
+    assert info.iters <= 120, info.as_dict()
