@@ -859,7 +859,7 @@ dg_status dg_mesh_create(int dim, const int N[3], const double L[3], int P, int 
     if ((s = alloc((void **)&m->sums, sizeof(double) * 8)) != DG_OK) return fail(s);
     if ((s = alloc((void **)&m->aux, sizeof(double) * 8)) != DG_OK) return fail(s);
     if ((s = alloc((void **)&m->scal, sizeof(PcgScal))) != DG_OK) return fail(s);
-    if ((s = alloc((void **)&m->mass_e, sizeof(double) * g.npe)) != DG_OK) return fail(s);
+    if ((s = alloc((void **)&m->mass_e, sizeof(double) * 2 * g.npe)) != DG_OK) return fail(s);  // m, 1/m
     if ((s = alloc((void **)&m->d_flag, sizeof(int))) != DG_OK) return fail(s);
     if (cudaMallocHost((void **)&m->hscal, sizeof(PcgScal)) != cudaSuccess)
         return fail(set_error(DG_ENOMEM, "cudaMallocHost failed"));
@@ -868,8 +868,9 @@ dg_status dg_mesh_create(int dim, const int N[3], const double L[3], int P, int 
         Geom g1 = g;
         g1.nel = 1;
         cudaError_t e = launch_mass(g1, m->mass_e, m->st);
+        if (e == cudaSuccess) e = launch_recip(g1, m->mass_e, m->mass_e + g.npe, m->st);
         if (e != cudaSuccess) return fail(set_error(DG_ECUDA, cudaGetErrorString(e)));
-        m->launches += 1;
+        m->launches += 2;
     }
     if (nranks > 1) {
         NcclApi *nc = nccl();

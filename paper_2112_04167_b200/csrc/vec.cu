@@ -17,6 +17,20 @@ int vec_grid() { return 148 * 8; }
 
 namespace {
 
+// Grid-stride loops over the DOFs of a slab track the node index q = i mod npe incrementally
+// (no 64-bit division per DOF); the mesh's mass table holds m_q at [0, npe) and 1/m_q at
+// [npe, 2 npe) (no double division per DOF).
+struct NodeIdx {
+    int q, step, npe;
+    __device__ __forceinline__ NodeIdx(long long i0, long long stride, int npe_)
+        : q((int)(i0 % npe_)), step((int)(stride % npe_)), npe(npe_) {}
+    __device__ __forceinline__ void next()
+    {
+        q += step;
+        if (q >= npe) q -= npe;
+    }
+};
+
 template <int K>
 __device__ __forceinline__ void write_partials(double (&v)[K], double *partial)
 {
@@ -31,8 +45,10 @@ __global__ void k_mass_moments(long long ndof, int npe, const double *__restrict
                                const double *__restrict__ me, double *partial)
 {
     double v[2] = {0.0, 0.0};
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < ndof; i += (long long)gridDim.x * blockDim.x) {
-        const double m = __ldg(me + (int)(i % npe));
+    const long long i0 = blockIdx.x * (long long)blockDim.x + threadIdx.x, st = (long long)gridDim.x * blockDim.x;
+    NodeIdx nq(i0, st, npe);
+    for (long long i = i0; i < ndof; i += st, nq.next()) {
+        const double m = __ldg(me + nq.q);
         v[0] = fma(m, f[i], v[0]);
         v[1] += m;
     }
@@ -44,8 +60,10 @@ __global__ void k_pcg_init(long long ndof, int npe, const double *__restrict__ f
 {
     const double fmean = s->fmean;
     double v[2] = {0.0, 0.0};
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < ndof; i += (long long)gridDim.x * blockDim.x) {
-        const double m = __ldg(me + (int)(i % npe));
+    const long long i0 = blockIdx.x * (long long)blockDim.x + threadIdx.x, st = (long long)gridDim.x * blockDim.x;
+    NodeIdx nq(i0, st, npe);
+    for (long long i = i0; i < ndof; i += st, nq.next()) {
+        const double m = __ldg(me + nq.q);
         const double fp = f[i] - fmean;
         const double ri = fma(m, fp, -Ar[i]);
         r[i] = ri;
@@ -60,14 +78,15 @@ __global__ void k_pcg_init2(long long ndof, int npe, double *__restrict__ r, con
 {
     const double rmean = s->qmean;  // FIN_INIT stores the mean of r here (lam == 0), else 0
     double v[2] = {0.0, 0.0};
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < ndof; i += (long long)gridDim.x * blockDim.x) {
-        const double m = __ldg(me + (int)(i % npe));
+    const long long i0 = blockIdx.x * (long long)blockDim.x + threadIdx.x, st = (long long)gridDim.x * blockDim.x;
+    NodeIdx nq(i0, st, npe);
+    for (long long i = i0; i < ndof; i += st, nq.next()) {
         const double ri = r[i] - rmean;
         r[i] = ri;
         const double zi = dinv[i] * ri;
         z[i] = zi;
         v[0] = fma(ri, zi, v[0]);
-        const double rm = ri / m;
+        const double rm = ri * __ldg(me + npe + nq.q);
         v[1] = fma(rm, rm, v[1]);
     }
     write_partials<2>(v, partial);
@@ -81,15 +100,16 @@ __global__ void k_pcg_update(long long ndof, int npe, double *__restrict__ x, do
     if (s->done) return;
     const double alpha = s->alpha, qmean = s->qmean;
     double v[2] = {0.0, 0.0};
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < ndof; i += (long long)gridDim.x * blockDim.x) {
-        const double m = __ldg(me + (int)(i % npe));
+    const long long i0 = blockIdx.x * (long long)blockDim.x + threadIdx.x, st = (long long)gridDim.x * blockDim.x;
+    NodeIdx nq(i0, st, npe);
+    for (long long i = i0; i < ndof; i += st, nq.next()) {
         x[i] = fma(alpha, p[i], x[i]);
         const double ri = fma(-alpha, q[i] - qmean, r[i]);
         r[i] = ri;
         const double zi = dinv[i] * ri;
         z[i] = zi;
         v[0] = fma(ri, zi, v[0]);
-        const double rm = ri / m;
+        const double rm = ri * __ldg(me + npe + nq.q);
         v[1] = fma(rm, rm, v[1]);
     }
     write_partials<2>(v, partial);
@@ -117,14 +137,15 @@ __global__ void k_pcg_update_nox(long long ndof, int npe, double *__restrict__ r
     if (s->done) return;
     const double alpha = s->alpha, qmean = s->qmean;
     double v[2] = {0.0, 0.0};
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < ndof; i += (long long)gridDim.x * blockDim.x) {
-        const double m = __ldg(me + (int)(i % npe));
+    const long long i0 = blockIdx.x * (long long)blockDim.x + threadIdx.x, st = (long long)gridDim.x * blockDim.x;
+    NodeIdx nq(i0, st, npe);
+    for (long long i = i0; i < ndof; i += st, nq.next()) {
         const double ri = fma(-alpha, q[i] - qmean, r[i]);
         r[i] = ri;
         const double zi = dinv[i] * ri;
         z[i] = zi;
         v[0] = fma(ri, zi, v[0]);
-        const double rm = ri / m;
+        const double rm = ri * __ldg(me + npe + nq.q);
         v[1] = fma(rm, rm, v[1]);
     }
     write_partials<2>(v, partial);
