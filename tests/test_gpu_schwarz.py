@@ -184,3 +184,23 @@ def test_schwarz_c3_poisson_full_size():
     res = np.linalg.norm(r / mass) / np.linalg.norm(fp)
     assert res <= 1.1 * c.tol, (res, info.as_dict())
     assert info.iters <= 120, info.as_dict()
+
+
+def test_schwarz_max_coarse_grid_c5_mesh():
+    """The largest coarse grid (N_d = 64: config-5 mesh, 56.6 M DOF, P = 5) with constant nu:
+    Poisson to 1e-10, residual recomputed with the ORACLE's operator on sampled elements."""
+    c = config(5)
+    m = dg.dg_mesh_create(3, c.N, c.L, c.P, stream=torch.cuda.current_stream())
+    om = oracle.Mesh(3, c.N, c.L, c.P)
+    dg.dg_mesh_set_precond(m, dg.DG_PC_SCHWARZ2)
+    f = c.rhs(0)
+    u = torch.zeros(f.shape, dtype=torch.float64, device=DEV)
+    info = dg.dg_pcg_solve(m, 0.0, None, 1.0, T(f), 1e-10, 2000, u)
+    assert info.rel_res <= 1e-10 and info.iters <= 150, info.as_dict()
+    mass = oracle.mass(om)
+    fbar = (mass * f).sum() / mass.sum()
+    uh = H(u)
+    el = np.sort(np.random.default_rng(3).choice(om.n_el, 128, replace=False))
+    au = oracle.sip_apply(om, 0.0, uh, nu_const=1.0, elems=el)
+    res = (mass[el] * (f[el] - fbar) - au) / mass[el]
+    assert np.linalg.norm(res) / np.linalg.norm(f[el] - fbar) <= 20 * 1e-10
