@@ -748,6 +748,8 @@ cudaError_t launch_sw_coarse(const SwCoarseParams &a, const SwTab &h, int stage,
         const int mx = (int)(sizeof(double) * (2 * SW_NCMAX * SW_NCMAX + 2 * SW_NCMAX * SW_NCMAX));
         cudaFuncSetAttribute(k_sw_cfwd, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
         cudaFuncSetAttribute(k_sw_cinv, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+        cudaFuncSetAttribute(k_sw_cz, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)(sizeof(double) * (64 * SW_NCMAX + SW_NCMAX * SW_NCMAX)));
         attr = true;
     }
     // one thread per plane entry (latency-bound small transforms), one per column entry
