@@ -576,6 +576,9 @@ dg_status pcg_impl(dg_mesh *m, double lam, const double *nu, double nu_const, co
     // measured faster than the fused prologue of v5
     const bool split_ok = !multi && g.dim == 3 && apply3_split_pcg_ok(g, nu);
     const bool split = !sw && split_ok && !getenv("DG_PCG_FUSED");
+    // constant nu on the uniform periodic mesh (N_d >= 2: the closed-form diagonal): the first
+    // element's D^-1 serves every element
+    const bool table = split && !nu && !self && !getenv("DG_PCG_NOTABLE");
     int chunk = 4;
     for (;;) {
         CK(cudaMemcpyAsync(m->hscal, m->scal, sizeof(PcgScal), cudaMemcpyDeviceToHost, m->st));
@@ -620,8 +623,10 @@ dg_status pcg_impl(dg_mesh *m, double lam, const double *nu, double nu_const, co
                 CKS(sw_pcg_step(m, lam, SW_UPDATE, FIN_BETA));
             } else if (split) {
                 // x += alpha p, p = z + beta p (in place; x deferred by one iteration) ;
-                // q = A p with the dot epilogue (apply MODE 2) ; r, z update
-                CK(launch_pcg_pupd_x(g, u, p_old, m->z, m->scal, m->st));
+                // q = A p with the dot epilogue (apply MODE 2) ; r, z update.  Constant nu: z is
+                // never stored (the diagonal is one [npe] table, applied on the fly)
+                if (table) CK(launch_pcg_pupd_xt(g, u, p_old, m->r, m->dinv, m->scal, m->st));
+                else CK(launch_pcg_pupd_x(g, u, p_old, m->z, m->scal, m->st));
                 m->launches += 1;
                 PProl pro;
                 pro.done = &m->scal->done;
@@ -630,7 +635,8 @@ dg_status pcg_impl(dg_mesh *m, double lam, const double *nu, double nu_const, co
                 int grid = 0;
                 CKS(run_apply(m, lam, nu, nu_const, p_old, m->q, Halo{}, epi, pro, &grid));
                 CKS(reduce_fin(m, grid, FIN_ALPHA));
-                CK(launch_pcg_update_nox(g, m->r, m->q, m->dinv, m->z, m->mass_e, m->scal, m->partial, m->st));
+                if (table) CK(launch_pcg_update_t(g, m->r, m->q, m->dinv, m->mass_e, m->scal, m->partial, m->st));
+                else CK(launch_pcg_update_nox(g, m->r, m->q, m->dinv, m->z, m->mass_e, m->scal, m->partial, m->st));
                 m->launches += 1;
                 CKS(reduce_fin(m, VG, FIN_BETA));
             } else if (!multi) {

@@ -206,6 +206,11 @@ cudaError_t launch_pcg_pupd(const Geom &g, double *p, const double *z, const Pcg
 cudaError_t launch_pcg_pupd_x(const Geom &g, double *x, double *p, const double *z, const PcgScal *s, cudaStream_t st);
 cudaError_t launch_pcg_update_nox(const Geom &g, double *r, const double *q, const double *dinv, double *z,
                                   const double *mass_e, const PcgScal *s, double *partial, cudaStream_t st);
+// constant-nu uniform-mesh split step (dinv_t: the [npe] diagonal-inverse table)
+cudaError_t launch_pcg_update_t(const Geom &g, double *r, const double *q, const double *dinv_t,
+                                const double *mass_e, const PcgScal *s, double *partial, cudaStream_t st);
+cudaError_t launch_pcg_pupd_xt(const Geom &g, double *x, double *p, const double *r, const double *dinv_t,
+                               const PcgScal *s, cudaStream_t st);
 cudaError_t launch_pcg_xfinal(const Geom &g, double *x, const double *p, const PcgScal *s, cudaStream_t st);
 cudaError_t launch_dot_pq(const Geom &g, const double *p, const double *q, const PcgScal *s, double *partial,
                           cudaStream_t st);

@@ -151,6 +151,42 @@ __global__ void k_pcg_update_nox(long long ndof, int npe, double *__restrict__ r
     write_partials<2>(v, partial);
 }
 
+// constant-nu split step on a uniform periodic mesh: diag(A) is the same for every element, so
+// z = D^-1 r is never stored -- dinv_t[q] (the first element's diagonal inverse) is applied on
+// the fly: the update reads r, q and writes r (24 B/DOF), the p update reads x, p, r (40 B/DOF)
+__global__ void k_pcg_update_t(long long ndof, int npe, double *__restrict__ r, const double *__restrict__ q,
+                               const double *__restrict__ dinv_t, const double *__restrict__ me, const PcgScal *s,
+                               double *partial)
+{
+    if (s->done) return;
+    const double alpha = s->alpha, qmean = s->qmean;
+    double v[2] = {0.0, 0.0};
+    const long long i0 = blockIdx.x * (long long)blockDim.x + threadIdx.x, st = (long long)gridDim.x * blockDim.x;
+    NodeIdx nq(i0, st, npe);
+    for (long long i = i0; i < ndof; i += st, nq.next()) {
+        const double ri = fma(-alpha, q[i] - qmean, r[i]);
+        r[i] = ri;
+        v[0] = fma(ri * __ldg(dinv_t + nq.q), ri, v[0]);
+        const double rm = ri * __ldg(me + npe + nq.q);
+        v[1] = fma(rm, rm, v[1]);
+    }
+    write_partials<2>(v, partial);
+}
+
+__global__ void k_pcg_pupd_xt(long long ndof, int npe, double *__restrict__ x, double *__restrict__ p,
+                              const double *__restrict__ r, const double *__restrict__ dinv_t, const PcgScal *s)
+{
+    if (s->done) return;
+    const double alpha = s->alpha, beta = s->beta;
+    const long long i0 = blockIdx.x * (long long)blockDim.x + threadIdx.x, st = (long long)gridDim.x * blockDim.x;
+    NodeIdx nq(i0, st, npe);
+    for (long long i = i0; i < ndof; i += st, nq.next()) {
+        const double pi = p[i];
+        x[i] = fma(alpha, pi, x[i]);
+        p[i] = fma(beta, pi, r[i] * __ldg(dinv_t + nq.q));
+    }
+}
+
 // the deferred last x update: x += alpha_k p_k once the loop stopped after an update pass
 __global__ void k_pcg_xfinal(long long ndof, double *__restrict__ x, const double *__restrict__ p, const PcgScal *s)
 {
@@ -384,6 +420,20 @@ cudaError_t launch_pcg_update_nox(const Geom &g, double *r, const double *q, con
                                   const double *mass_e, const PcgScal *s, double *partial, cudaStream_t st)
 {
     k_pcg_update_nox<<<vec_grid(), 256, 0, st>>>(nd(g), g.npe, r, q, dinv, z, mass_e, s, partial);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_pcg_update_t(const Geom &g, double *r, const double *q, const double *dinv_t,
+                                const double *mass_e, const PcgScal *s, double *partial, cudaStream_t st)
+{
+    k_pcg_update_t<<<vec_grid(), 256, 0, st>>>(nd(g), g.npe, r, q, dinv_t, mass_e, s, partial);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_pcg_pupd_xt(const Geom &g, double *x, double *p, const double *r, const double *dinv_t,
+                               const PcgScal *s, cudaStream_t st)
+{
+    k_pcg_pupd_xt<<<vec_grid(), 256, 0, st>>>(nd(g), g.npe, x, p, r, dinv_t, s);
     return cudaGetLastError();
 }
 
