@@ -330,7 +330,7 @@ struct C3Cfg {
 };
 
 template <int P>
-__global__ void __launch_bounds__(C3Cfg<P>::NT) k_convect3(const ConvParams a)
+__global__ void __launch_bounds__(C3Cfg<P>::NT, P >= 7 ? 3 : 1) k_convect3(const ConvParams a)
 {
     using C = C3Cfg<P>;
     constexpr int n = C::n, Q = C::Q, NPE = C::NPE, NT = C::NT, NX = C::NX, NPEP = C::NPEP;
@@ -433,48 +433,47 @@ __global__ void __launch_bounds__(C3Cfg<P>::NT) k_convect3(const ConvParams a)
             }
             __syncthreads();
             // y: lines (k, qx): D1 = B_y A_x, D2 = (2/hy) G_y A_y + B_y A_z -> R1[t][(k n + j) Q + qx]
+            // (q-outer: the inputs stream through, 3 n accumulators stay in registers next to
+            // the Gauss column)
             for (int l = tid; l < n * Q; l += NT) {
                 const int lqx = l % Q, k = l / Q;
-                double x1[Q], x2[Q], x3[Q];
+                double d1[n], d2[n], d3[n];
+#pragma unroll
+                for (int j = 0; j < n; ++j) d1[j] = d2[j] = d3[j] = 0.0;
 #pragma unroll
                 for (int q = 0; q < Q; ++q) {
                     const int o = (k * Q + q) * Q + lqx;
-                    x1[q] = R2[o];
-                    x2[q] = R2[n * Q * Q + o];
-                    x3[q] = R2[2 * n * Q * Q + o];
+                    const double x1 = R2[o], x2 = R2[n * Q * Q + o], x3 = R2[2 * n * Q * Q + o];
+#pragma unroll
+                    for (int j = 0; j < n; ++j) {
+                        d1[j] = fma(T.Bq[q][j], x1, d1[j]);
+                        d2[j] = fma(T.Gq[q][j], x2, d2[j]);
+                        d3[j] = fma(T.Bq[q][j], x3, d3[j]);
+                    }
                 }
 #pragma unroll
                 for (int j = 0; j < n; ++j) {
-                    double d1 = 0.0, d2 = 0.0, d3 = 0.0;
-#pragma unroll
-                    for (int q = 0; q < Q; ++q) {
-                        d1 = fma(T.Bq[q][j], x1[q], d1);
-                        d2 = fma(T.Gq[q][j], x2[q], d2);
-                        d3 = fma(T.Bq[q][j], x3[q], d3);
-                    }
-                    R1[(k * n + j) * Q + lqx] = d1;
-                    R1[n * n * Q + (k * n + j) * Q + lqx] = fma(d2, sdy, d3);
+                    R1[(k * n + j) * Q + lqx] = d1[j];
+                    R1[n * n * Q + (k * n + j) * Q + lqx] = fma(d2[j], sdy, d3[j]);
                 }
             }
             __syncthreads();
-            // x: lines (j, k): out_i = (2/hx) sum G D1 + sum B D2
+            // x: lines (j, k): out_i = (2/hx) sum G D1 + sum B D2 (q-outer)
             for (int l = tid; l < n * n; l += NT) {
-                double x1[Q], x2[Q];
+                double s1[n], s2[n];
+#pragma unroll
+                for (int i = 0; i < n; ++i) s1[i] = s2[i] = 0.0;
 #pragma unroll
                 for (int q = 0; q < Q; ++q) {
-                    x1[q] = R1[l * Q + q];
-                    x2[q] = R1[n * n * Q + l * Q + q];
-                }
+                    const double x1 = R1[l * Q + q], x2 = R1[n * n * Q + l * Q + q];
 #pragma unroll
-                for (int i = 0; i < n; ++i) {
-                    double s1 = 0.0, s2 = 0.0;
-#pragma unroll
-                    for (int q = 0; q < Q; ++q) {
-                        s1 = fma(T.Gq[q][i], x1[q], s1);
-                        s2 = fma(T.Bq[q][i], x2[q], s2);
+                    for (int i = 0; i < n; ++i) {
+                        s1[i] = fma(T.Gq[q][i], x1, s1[i]);
+                        s2[i] = fma(T.Bq[q][i], x2, s2[i]);
                     }
-                    sy[c * NPEP + l * NX + i] = fma(s1, sdx, s2);
                 }
+#pragma unroll
+                for (int i = 0; i < n; ++i) sy[c * NPEP + l * NX + i] = fma(s1[i], sdx, s2[i]);
             }
         }
         // ---- faces, per direction d (both sides): node of face index (fa along o1, fb along o2)
