@@ -398,10 +398,12 @@ dg_status ensure_sw(dg_mesh *m, double nu_const)
 
 // coarse part: x_c = A_c^+ P_1^T r from the element moments rc_el; r_c.x_c partials written
 // to partial[pslot + b] (b < sw_cz_grid) when `partial` is set
-dg_status sw_coarse(dg_mesh *m, double lam, double nu, const double *nu_eff, double *partial, int pslot)
+dg_status sw_coarse(dg_mesh *m, double lam, double nu, const double *nu_eff, double *partial, int pslot,
+                    const int *done = nullptr)
 {
     const Geom &g = m->g;
     SwCoarseParams c;
+    c.done = done;
     c.nu = nu;
     c.nu_eff = nu_eff;
     c.T = m->d_sw;
@@ -484,7 +486,7 @@ dg_status sw_pcg_step(dg_mesh *m, double lam, int mode, int fin)
     CK(launch_sw_block(m->g, m->h_sw, b, m->st, &grid));
     m->launches += 1;
     if (!m->sw_coarse_on) return reduce_fin(m, grid, fin);  // element blocks only (x_c = 0)
-    CKS(sw_coarse(m, lam, 1.0, &m->scal->nu_eff, m->partial, grid));
+    CKS(sw_coarse(m, lam, 1.0, &m->scal->nu_eff, m->partial, grid, mode == SW_UPDATE ? &m->scal->done : nullptr));
     return reduce_fin(m, grid + sw_cz_grid(m->h_sw), fin);
 }
 

@@ -259,6 +259,7 @@ struct SwCoarseParams {
     double *partial = nullptr;
     int pslot = 0;                  // first partial slot of the column kernel
     int count_dot = 1;              // multi-rank: only rank 0 contributes r_c.x_c
+    const int *done = nullptr;      // PCG converged: skip (the host checks convergence per chunk)
 };
 struct SwPupdParams {
     const SwTab *T = nullptr;

@@ -445,6 +445,7 @@ __device__ __forceinline__ double gather_vertex(const double *rc_el, long long n
 // plane vz: gather (single rank) or read rc, then transform along x and y (forward, F^T)
 __global__ void k_sw_cfwd(SwCoarseParams a)
 {
+    if (a.done && *a.done) return;
     extern __shared__ double sm[];
     const SwTab *T = a.T;
     const int Nx = T->Nc[0], Ny = T->Nc[1];
@@ -475,6 +476,7 @@ __global__ void k_sw_cfwd(SwCoarseParams a)
 // 32 columns (ky, kx) per CTA (blockDim 32 x 8): z transform, 1/mu, Parseval partial, inverse z
 __global__ void k_sw_cz(SwCoarseParams a)
 {
+    if (a.done && *a.done) return;
     extern __shared__ double sm[];
     const SwTab *T = a.T;
     const int Nx = T->Nc[0], Ny = T->Nc[1], Nz = T->Nc[2], NP = Nx * Ny;
@@ -521,6 +523,7 @@ __global__ void k_sw_cz(SwCoarseParams a)
 // plane vz: inverse y then x transform -> x_c
 __global__ void k_sw_cinv(SwCoarseParams a)
 {
+    if (a.done && *a.done) return;
     extern __shared__ double sm[];
     const SwTab *T = a.T;
     const int Nx = T->Nc[0], Ny = T->Nc[1];
@@ -549,6 +552,7 @@ __global__ void k_sw_cinv(SwCoarseParams a)
 // vertex layers; the caller zeroes rc and all-reduces it)
 __global__ void k_sw_cgather_local(SwCoarseParams a, int S, int off, int nl)
 {
+    if (a.done && *a.done) return;
     const SwTab *T = a.T;
     const int *Nc = T->Nc;
     const int NC = 1 << a.dim;
