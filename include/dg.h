@@ -206,7 +206,8 @@ dg_status dg_imex_stage(dg_mesh *mv, dg_mesh *mp, double dt, double a_ex21, doub
  * (b_im - a_im[s])_i F_d1,i] (F_d2 + F_d3 = 0).  The final projection (lines 12-15) is
  * skipped for constant nu.
  * v[c] (c < dim): DEVICE velocity, in: v^n, out: v^{n+1}; psi: DEVICE pressure workspace (the
- * last stage's psi'' on exit).  Workspace (3 s + 2) dim velocity fields, owned by mv.
+ * last stage's psi'' on exit; the first implicit stage's Poisson solve starts from 0, later
+ * stages from the previous stage's psi'').  Workspace (3 s + 2) dim velocity fields, owned by mv.
  * Synchronous.  DG_EINVAL for a malformed tableau (s outside [2, 8], a non-explicit first
  * stage, upper-triangular entries) or bad scalars; solver errors as dg_pcg_solve. */
 #define DG_RK_MAX_STAGES 8

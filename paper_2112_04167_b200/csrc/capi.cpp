@@ -1295,7 +1295,9 @@ dg_status dg_imex_rk_step(dg_mesh *mv, dg_mesh *mp, const dg_tableau *tab, doubl
         CKS(div_impl(mv, vp, mp->sf[0]));
         CK(launch_scale_minv(gp, mp->mass_e, -1.0, mp->sf[0], mp->sf[0], mv->st));
         mv->launches += 1;
-        CK(cudaMemsetAsync(psi, 0, sizeof(double) * (size_t)mp->ndof, mv->st));
+        // first implicit stage from psi = 0, later stages from the previous stage's psi''
+        // (psi''_i ~ dt sum_j a_ij p_j changes smoothly from stage to stage)
+        if (i == 1) CK(cudaMemsetAsync(psi, 0, sizeof(double) * (size_t)mp->ndof, mv->st));
         dg_solve_info ip{};
         dg_status st = pcg_impl(mp, 0.0, nullptr, 1.0, mp->sf[0], tol, maxit, psi, &ip);
         inf.pressure_iters += ip.iters;
@@ -1510,11 +1512,13 @@ dg_status dg_imex_rk_step_vv(dg_mesh *mv, dg_mesh *mp, const dg_tableau *tab, do
     };
     // lines 5-6 (and 13-14): lap psi = div w (weak DG divergence, SIP Poisson on mp from psi = 0),
     // w <- w - M^-1 G psi
-    auto project = [&](double *const *w) -> dg_status {
+    auto project = [&](double *const *w, bool warm) -> dg_status {
         CKS(div_impl(mv, w, mp->sf[0]));
         CK(launch_scale_minv(gp, mp->mass_e, -1.0, mp->sf[0], mp->sf[0], mv->st));
         mv->launches += 1;
-        CK(cudaMemsetAsync(psi, 0, sizeof(double) * (size_t)mp->ndof, mv->st));
+        // stages i > 2 start from the previous stage's psi''; the first stage and the
+        // final projection (a small correction) from 0
+        if (!warm) CK(cudaMemsetAsync(psi, 0, sizeof(double) * (size_t)mp->ndof, mv->st));
         dg_solve_info ip{};
         const dg_status st = pcg_impl(mp, 0.0, nullptr, 1.0, mp->sf[0], tol, maxit, psi, &ip);
         inf.pressure_iters += ip.iters;
@@ -1571,7 +1575,7 @@ dg_status dg_imex_rk_step_vv(dg_mesh *mv, dg_mesh *mp, const dg_tableau *tab, do
             CK(launch_lincomb(g, lc, mv->mass_e, vp[c], mv->st));
             mv->launches += 1;
         }
-        dg_status st = project(vp);  // lines 5-6
+        dg_status st = project(vp, i > 1);  // lines 5-6
         if (st != DG_OK) return fail(st);
         // line 7: nu_i = nu(v''_i)
         {
@@ -1642,7 +1646,7 @@ dg_status dg_imex_rk_step_vv(dg_mesh *mv, dg_mesh *mp, const dg_tableau *tab, do
     }
     // lines 12-15: final projection
     if (final_projection) {
-        const dg_status st = project(v);
+        const dg_status st = project(v, false);
         if (st != DG_OK) return fail(st);
     }
     CK(cudaStreamSynchronize(mv->st));
