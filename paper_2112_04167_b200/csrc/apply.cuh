@@ -353,8 +353,26 @@ struct ApplyDispatch {
                 a.zhi = a.g.Nl[2];
             }
             const int nbS = a.zhi - a.zlo;  // one element layer per brick
+            // column segments per column: the persistent CTAs take ceil(units / grid) units of
+            // seglen bricks each plus a per-segment cost (segment-end z traces, pipeline fill)
+            // of ~3.3 bricks (fitted on c5: nseg = 2, 4, 8, 16 -> 0.576, 0.551, 0.633, 0.761 ms);
+            // pick the divisor of nbS (seglen >= 2) with the least modelled time
             int nseg = 1;
-            while (ncols * nseg < 3 * gsz && nbS % (2 * nseg) == 0 && nbS / (2 * nseg) >= 2) nseg *= 2;
+            double best = 1e300;
+            for (int ns = 1; ns <= nbS / 2; ++ns) {
+                if (nbS % ns) continue;
+                const long long units = ncols * ns;
+                const double cost = (double)((units + gsz - 1) / gsz) * (nbS / ns + 3.3);
+                if (cost <= best * 1.01) {  // near-ties: more units (finer balance; measured)
+                    best = cost < best ? cost : best;
+                    nseg = ns;
+                }
+            }
+            if (nbS < 2) nseg = 1;
+            if (const char *ev = getenv("DG_V6_NSEG")) {  // development override
+                const int want = atoi(ev);
+                if (want >= 1 && nbS % want == 0 && nbS / want >= 2) nseg = want;
+            }
             a.nseg = nseg;
             a.seglen = nbS / nseg;
             const long long nunits = ncols * nseg;
