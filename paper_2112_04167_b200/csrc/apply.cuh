@@ -317,8 +317,26 @@ struct ApplyDispatch {
                 a.zhi = a.g.Nl[2];
             }
             const int nbS = (a.zhi - a.zlo) / 2;
+            // segments per column by the same load-balance model as v6, with a per-segment cost
+            // of ~1.5 bricks (fitted on the c4 P = 6 / P = 7 applies: nseg = 1, 2, 4, 8, 16 ->
+            // Poisson 276, 284, 292, 298, 325 us per Jacobi-PCG iteration); near-ties: fewer
+            // segments (the z carry pays more than balance here)
             int nseg = 1;
-            while (ncols * nseg < 3 * gsz && nbS % (2 * nseg) == 0) nseg *= 2;
+            {
+                double best = 1e300;
+                for (int ns = 1; ns <= nbS; ++ns) {
+                    if (nbS % ns) continue;
+                    const double cost = (double)((ncols * ns + gsz - 1) / gsz) * (nbS / ns + 1.5);
+                    if (cost < best * 0.99) {
+                        best = cost;
+                        nseg = ns;
+                    }
+                }
+            }
+            if (const char *ev = getenv("DG_V5_NSEG")) {  // development override
+                const int want = atoi(ev);
+                if (want >= 1 && nbS % want == 0) nseg = want;
+            }
             a.nseg = nseg;
             a.seglen = nbS / nseg;
             const long long nunits = ncols * nseg;
