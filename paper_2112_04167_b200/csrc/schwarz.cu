@@ -676,22 +676,33 @@ SwLine<n> make_line(const SwTab &h)
     return L;
 }
 
+// CTAs of one full wave: SMs x resident CTAs per SM (at least one wave of 148)
+template <class F>
+int resident_ctas(F kern, int threads, int smem)
+{
+    int dev = 0, nsm = 148, occ = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem) != cudaSuccess || occ < 1) occ = 1;
+    return nsm * occ;
+}
+
 template <int DIM>
 struct SwDispatch {
     template <int P>
     static cudaError_t block_p(const SwBlockParams &a, const SwTab &h, cudaStream_t st, int *grid)
     {
         constexpr int EPC = SwCfg<DIM, P + 1>::EPC;
+        constexpr int smem = SwBlkSmem<DIM, P + 1>::BYTES;
+        static int resident = 0;  // one wave of persistent CTAs (a partial second wave would
+        if (!resident) {          // double the tail)
+            cudaFuncSetAttribute(k_sw_block<DIM, P + 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+            resident = resident_ctas(k_sw_block<DIM, P + 1>, 256, smem);
+        }
         long long g = (a.nel + EPC - 1) / EPC;
-        if (g > 148LL * 6) g = 148LL * 6;
+        if (g > resident) g = resident;
         if (g < 1) g = 1;
         *grid = (int)g;
-        constexpr int smem = SwBlkSmem<DIM, P + 1>::BYTES;
-        static bool attr = false;
-        if (!attr) {
-            cudaFuncSetAttribute(k_sw_block<DIM, P + 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-            attr = true;
-        }
         k_sw_block<DIM, P + 1><<<(int)g, 256, smem, st>>>(a, make_line<P + 1>(h));
         return cudaGetLastError();
     }
@@ -699,8 +710,10 @@ struct SwDispatch {
     static cudaError_t pupd_p(const SwPupdParams &a, const SwTab &h, cudaStream_t st)
     {
         constexpr int EPC = SwCfg<DIM, P + 1>::EPC;
+        static int resident = 0;
+        if (!resident) resident = resident_ctas(k_sw_pupd<DIM, P + 1>, 256, 0);
         long long g = (a.nel + EPC - 1) / EPC;
-        if (g > 148LL * 8) g = 148LL * 8;
+        if (g > resident) g = resident;
         if (g < 1) g = 1;
         k_sw_pupd<DIM, P + 1><<<(int)g, 256, 0, st>>>(a, make_line<P + 1>(h));
         return cudaGetLastError();
