@@ -595,14 +595,20 @@ struct ConvDispatch {
             static const bool v1 = getenv("DG_CONVECT_V1") != nullptr;
             if (!v1) {
                 constexpr int smem3 = C3Cfg<P>::SMEM;
-                static bool attr = false;
-                if (!attr) {
+                static int resident = 0;  // persistent: one full wave of CTAs
+                if (!resident) {
                     cudaError_t e = cudaFuncSetAttribute(k_convect3<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem3);
                     if (e != cudaSuccess) return e;
-                    attr = true;
+                    int dev = 0, nsm = 148, occ = 1;
+                    cudaGetDevice(&dev);
+                    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+                    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_convect3<P>, C3Cfg<P>::NT, smem3) !=
+                            cudaSuccess || occ < 1)
+                        occ = 1;
+                    resident = nsm * occ;
                 }
                 long long grid = a.g.nel;
-                if (grid > 148 * 16) grid = 148 * 16;
+                if (grid > resident) grid = resident;
                 k_convect3<P><<<(int)grid, C3Cfg<P>::NT, smem3, st>>>(a);
                 return cudaGetLastError();
             }

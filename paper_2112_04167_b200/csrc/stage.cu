@@ -610,14 +610,24 @@ cudaError_t dg2_launch(const Geom &g, const DivGradParams &a, cudaStream_t st)
     const int smem = DIV ? (int)sizeof(double) * (3 * C::EPC * C::NV + C::EPC * C::NPp + C::EPC * 2 * C::FV)
                          : (int)sizeof(double) * (C::EPC * C::NPp + 2 * C::EPC * C::NV + C::EPC * DIM * 2 * C::FP);
     if (smem > 227 * 1024) return cudaErrorNotSupported;
-    static bool attr = false;
-    if (!attr) {
-        if (DIV) cudaFuncSetAttribute(k_dg_div2<DIM, P>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        else cudaFuncSetAttribute(k_dg_grad2<DIM, P>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        attr = true;
+    static int resident = 0;  // persistent tiles: one full wave of CTAs
+    if (!resident) {
+        int dev = 0, nsm = 148, occ = 1;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+        cudaError_t e;
+        if (DIV) {
+            cudaFuncSetAttribute(k_dg_div2<DIM, P>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+            e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_dg_div2<DIM, P>, C::NT, smem);
+        } else {
+            cudaFuncSetAttribute(k_dg_grad2<DIM, P>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+            e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_dg_grad2<DIM, P>, C::NT, smem);
+        }
+        if (e != cudaSuccess || occ < 1) occ = 1;
+        resident = nsm * occ;
     }
     long long blocks = (g.nel + C::EPC - 1) / C::EPC;
-    if (blocks > 148LL * 8) blocks = 148LL * 8;
+    if (blocks > resident) blocks = resident;
     if (DIV) k_dg_div2<DIM, P><<<(int)blocks, C::NT, smem, st>>>(g, a);
     else k_dg_grad2<DIM, P><<<(int)blocks, C::NT, smem, st>>>(g, a);
     return cudaGetLastError();
