@@ -55,7 +55,7 @@ __global__ void k_mass_moments(long long ndof, int npe, const double *__restrict
     write_partials<2>(v, partial);
 }
 
-__global__ void k_pcg_init(long long ndof, int npe, const double *__restrict__ f, const double *__restrict__ Ar,
+__global__ void __launch_bounds__(256, 8) k_pcg_init(long long ndof, int npe, const double *__restrict__ f, const double *__restrict__ Ar,
                            double *__restrict__ r, const double *__restrict__ me, const PcgScal *s, double *partial)
 {
     const double fmean = s->fmean;
@@ -154,7 +154,7 @@ __global__ void k_pcg_update_nox(long long ndof, int npe, double *__restrict__ r
 // constant-nu split step on a uniform periodic mesh: diag(A) is the same for every element, so
 // z = D^-1 r is never stored -- dinv_t[q] (the first element's diagonal inverse) is applied on
 // the fly: the update reads r, q and writes r (24 B/DOF), the p update reads x, p, r (40 B/DOF)
-__global__ void k_pcg_update_t(long long ndof, int npe, double *__restrict__ r, const double *__restrict__ q,
+__global__ void __launch_bounds__(256, 8) k_pcg_update_t(long long ndof, int npe, double *__restrict__ r, const double *__restrict__ q,
                                const double *__restrict__ dinv_t, const double *__restrict__ me, const PcgScal *s,
                                double *partial)
 {
@@ -335,7 +335,7 @@ __global__ void k_finalize(int mode, const double *sums, PcgScal *s, double *his
     if (threadIdx.x == 0 && blockIdx.x == 0) finalize(mode, sums, s, hist, aux);
 }
 
-__global__ void k_coords(int dim, int n, int npe, int Nl0, int Nl1, long long nel, long long el_off0, int N0, int N1,
+__global__ void __launch_bounds__(256, 8) k_coords(int dim, int n, int npe, int Nl0, int Nl1, long long nel, long long el_off0, int N0, int N1,
                          double h0, double h1, double h2, long long ndof, double *xyz, int P)
 {
     const DevTab &T = c_tab[P];
