@@ -640,7 +640,7 @@ dg_status pcg_impl(dg_mesh *m, double lam, const double *nu, double nu_const, co
                 if (table) CK(launch_pcg_update_t(g, m->r, m->q, m->dinv, m->mass_e, m->scal, m->partial, m->st));
                 else CK(launch_pcg_update_nox(g, m->r, m->q, m->dinv, m->z, m->mass_e, m->scal, m->partial, m->st));
                 m->launches += 1;
-                CKS(reduce_fin(m, VG, FIN_BETA));
+                CKS(reduce_fin(m, table ? vec_grid_wide() : VG, FIN_BETA));
             } else if (!multi) {
                 // q = A p with p = dinv r + beta p_old (prologue), partials p.q, sum q (epilogue)
                 PProl pro;

@@ -177,7 +177,8 @@ struct PcgScal {                 // device-resident scalars of one solve
 };
 enum { PCG_ST_RUN = 0, PCG_ST_CONV = 1, PCG_ST_MAXIT = 2, PCG_ST_BREAKDOWN = 3 };
 
-int vec_grid();
+int vec_grid();       // grid (and partial count) of the reduction vector kernels
+int vec_grid_wide();  // grid of the streaming vector kernels (and of k_pcg_update_t's partials)
 // partial sums of m*f and m over the local slab -> partial[blk*2 + {0,1}]
 cudaError_t launch_mass_moments(const Geom &g, const double *f, const double *mass_e, double *partial,
                                 cudaStream_t st);

@@ -13,7 +13,10 @@ namespace dg {
 
 DG_DEFINE_CONST_TABLES(upload_tables_vec)
 
-int vec_grid() { return 148 * 8; }
+// one full wave of 256-thread CTAs: 6 per SM for the 40-register reduction kernels, 8 per SM
+// for the <= 32-register streams (a partial second wave costs up to the whole first one)
+int vec_grid() { return 148 * 6; }
+int vec_grid_wide() { return 148 * 8; }
 
 namespace {
 
@@ -406,13 +409,13 @@ cudaError_t launch_pcg_update(const Geom &g, double *x, double *r, const double 
 
 cudaError_t launch_pcg_pupd(const Geom &g, double *p, const double *z, const PcgScal *s, cudaStream_t st)
 {
-    k_pcg_pupd<<<vec_grid(), 256, 0, st>>>(nd(g), p, z, s);
+    k_pcg_pupd<<<vec_grid_wide(), 256, 0, st>>>(nd(g), p, z, s);
     return cudaGetLastError();
 }
 
 cudaError_t launch_pcg_pupd_x(const Geom &g, double *x, double *p, const double *z, const PcgScal *s, cudaStream_t st)
 {
-    k_pcg_pupd_x<<<vec_grid(), 256, 0, st>>>(nd(g), x, p, z, s);
+    k_pcg_pupd_x<<<vec_grid_wide(), 256, 0, st>>>(nd(g), x, p, z, s);
     return cudaGetLastError();
 }
 
@@ -426,20 +429,20 @@ cudaError_t launch_pcg_update_nox(const Geom &g, double *r, const double *q, con
 cudaError_t launch_pcg_update_t(const Geom &g, double *r, const double *q, const double *dinv_t,
                                 const double *mass_e, const PcgScal *s, double *partial, cudaStream_t st)
 {
-    k_pcg_update_t<<<vec_grid(), 256, 0, st>>>(nd(g), g.npe, r, q, dinv_t, mass_e, s, partial);
+    k_pcg_update_t<<<vec_grid_wide(), 256, 0, st>>>(nd(g), g.npe, r, q, dinv_t, mass_e, s, partial);
     return cudaGetLastError();
 }
 
 cudaError_t launch_pcg_pupd_xt(const Geom &g, double *x, double *p, const double *r, const double *dinv_t,
                                const PcgScal *s, cudaStream_t st)
 {
-    k_pcg_pupd_xt<<<vec_grid(), 256, 0, st>>>(nd(g), g.npe, x, p, r, dinv_t, s);
+    k_pcg_pupd_xt<<<vec_grid_wide(), 256, 0, st>>>(nd(g), g.npe, x, p, r, dinv_t, s);
     return cudaGetLastError();
 }
 
 cudaError_t launch_pcg_xfinal(const Geom &g, double *x, const double *p, const PcgScal *s, cudaStream_t st)
 {
-    k_pcg_xfinal<<<vec_grid(), 256, 0, st>>>(nd(g), x, p, s);
+    k_pcg_xfinal<<<vec_grid_wide(), 256, 0, st>>>(nd(g), x, p, s);
     return cudaGetLastError();
 }
 
@@ -452,13 +455,13 @@ cudaError_t launch_dot_pq(const Geom &g, const double *p, const double *q, const
 
 cudaError_t launch_shift(const Geom &g, double *x, const double *shift, cudaStream_t st)
 {
-    k_shift<<<vec_grid(), 256, 0, st>>>(nd(g), x, shift);
+    k_shift<<<vec_grid_wide(), 256, 0, st>>>(nd(g), x, shift);
     return cudaGetLastError();
 }
 
 cudaError_t launch_recip(const Geom &g, const double *d, double *dinv, cudaStream_t st)
 {
-    k_recip<<<vec_grid(), 256, 0, st>>>(nd(g), d, dinv);
+    k_recip<<<vec_grid_wide(), 256, 0, st>>>(nd(g), d, dinv);
     return cudaGetLastError();
 }
 
