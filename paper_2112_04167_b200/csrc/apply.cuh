@@ -161,6 +161,67 @@ __global__ void __launch_bounds__(256) k_diag_cf(const Geom g, double lam, const
     }
 }
 
+// Same closed form, one thread per node (grid-stride over the slab's nodes, no barriers): the
+// element's nu lines come through L1 (every element is read by its npe consecutive threads),
+// the w_k D_ki^2 table from shared memory.  The once-per-solve setup of the variable-nu PCG.
+template <int DIM, int P, bool VARNU>
+__global__ void __launch_bounds__(256) k_diag_cf2(const Geom g, double lam, const double *__restrict__ nu,
+                                                  double nu_const, Halo halo, double *__restrict__ diag, int invert)
+{
+    using C = Cfg<DIM, P>;
+    constexpr int n = C::n, NPE = C::NPE;
+    const DevTab &T = c_tab[P];
+    __shared__ double swd2[n * n], sw[n], sdd[n];
+    for (int q = threadIdx.x; q < n * n; q += blockDim.x) {
+        const int k = q / n, i = q % n;
+        swd2[q] = T.w[k] * T.D[k][i] * T.D[k][i];
+        if (q < n) {
+            sw[q] = T.w[q];
+            sdd[q] = T.D[q][q];
+        }
+    }
+    __syncthreads();
+    const long long tot = g.nel * NPE;
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < tot; t += (long long)gridDim.x * blockDim.x) {
+        const long long e = t / NPE;
+        const int q = (int)(t - e * NPE);
+        const int ec[3] = {(int)(e % g.Nl[0]), (int)((e / g.Nl[0]) % g.Nl[1]),
+                           DIM == 3 ? (int)(e / ((long long)g.Nl[0] * g.Nl[1])) : 0};
+        const int qc[3] = {q % n, (q / n) % n, DIM == 3 ? q / (n * n) : 0};
+        const double *ne = VARNU ? nu + e * NPE : nullptr;
+        double m = g.mfac;
+#pragma unroll
+        for (int d = 0; d < DIM; ++d) m *= sw[qc[d]];
+        double dg = lam * m;
+#pragma unroll
+        for (int D = 0; D < DIM; ++D) {
+            const int GS = D == 0 ? 1 : (D == 1 ? n : n * n);
+            const int i = qc[D];
+            const int goff = q - i * GS;
+            const double sd = g.sd[D];
+            double acc = 0.0;
+#pragma unroll
+            for (int k = 0; k < n; ++k) acc = fma(swd2[k * n + i], VARNU ? __ldg(ne + goff + k * GS) : nu_const, acc);
+            acc *= sd;
+            if (i == P || i == 0) {
+                int cn[3] = {ec[0], ec[1], ec[2]};
+                cn[D] += (i == P) ? 1 : -1;
+                const double nown = VARNU ? __ldg(ne + q) : nu_const;
+                const double nnb = VARNU ? __ldg(elem_ptr(g, nu, halo.nu_lo, halo.nu_hi, cn[0], cn[1], cn[2]) + goff +
+                                                  (i == P ? 0 : P * GS))
+                                         : nu_const;
+                acc += (i == P ? -1.0 : 1.0) * nown * sd * sdd[i] + 0.5 * g.tau[D] * (nown + nnb);
+            }
+            double W = g.wfac[D];
+#pragma unroll
+            for (int d = 0; d < DIM; ++d)
+                if (d != D) W *= sw[qc[d]];
+            dg += W * acc;
+        }
+        diag[t] = invert ? 1.0 / dg : dg;
+    }
+}
+
 template <int DIM, int P, bool VARNU>
 __global__ void __launch_bounds__(256) k_diag(const Geom g, double lam, const double *nu, double nu_const,
                                               Halo halo, double *diag)
@@ -546,6 +607,13 @@ struct ApplyDispatch {
         bool self = false;
         for (int dd = 0; dd < DIM; ++dd) self = self || g.N[dd] == 1;
         if (!self) {  // closed form, one CTA per element (grid-stride)
+            if (!getenv("DG_DIAG_V1")) {  // one thread per node (measured faster)
+                long long blocks = (tot + 255) / 256;
+                if (blocks > 148LL * 8) blocks = 148LL * 8;
+                if (nu) k_diag_cf2<DIM, P, true><<<(int)blocks, 256, 0, st>>>(g, lam, nu, nuc, h, d, invert);
+                else k_diag_cf2<DIM, P, false><<<(int)blocks, 256, 0, st>>>(g, lam, nu, nuc, h, d, invert);
+                return cudaGetLastError();
+            }
             const long long blocks = g.nel < 148LL * 16 ? g.nel : 148LL * 16;
             if (nu) k_diag_cf<DIM, P, true><<<(int)blocks, 256, 0, st>>>(g, lam, nu, nuc, h, d, invert);
             else k_diag_cf<DIM, P, false><<<(int)blocks, 256, 0, st>>>(g, lam, nu, nuc, h, d, invert);
