@@ -662,12 +662,13 @@ cudaError_t launch_stage_combine(const Geom &g, const double *mass_e, double a_e
                                  cudaStream_t st)
 {
     const long long nd = g.nel * g.npe;
-    const long long blocks = (nd + 255) / 256 < 148LL * 16 ? (nd + 255) / 256 : 148LL * 16;
+    const long long blocks = (nd + 255) / 256 < 148LL * 6 ? (nd + 255) / 256 : 148LL * 6;
     k_stage_combine<<<(int)blocks, 256, 0, st>>>(nd, g.npe, mass_e, a_ex, c_g, lamH, v, Fc, Av, vp, fH);
     return cudaGetLastError();
 }
 
-static int vblocks(long long nd) { return (int)((nd + 255) / 256 < 148LL * 16 ? (nd + 255) / 256 : 148LL * 16); }
+// one full wave of the 34-40-register streams (6 CTAs of 256 threads per SM)
+static int vblocks(long long nd) { return (int)((nd + 255) / 256 < 148LL * 6 ? (nd + 255) / 256 : 148LL * 6); }
 
 cudaError_t launch_scale_minv(const Geom &g, const double *mass_e, double c, const double *in, double *out,
                               cudaStream_t st)
