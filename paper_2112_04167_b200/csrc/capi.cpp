@@ -559,8 +559,17 @@ dg_status pcg_impl(dg_mesh *m, double lam, const double *nu, double nu_const, co
     CK(launch_mass_moments(g, f, m->mass_e, m->partial, m->st));
     m->launches += 1;
     CKS(reduce_fin(m, VG, FIN_FMEAN));
-    // r = M (f - fmean) - A u
-    CKS(apply_impl(m, lam, nu, nu_const, u, m->q));
+    // r = M (f - fmean) - A u; an all-zero guess (one reduction and a host read instead of an
+    // operator application) takes A u = 0
+    CK(launch_abssum(g, u, m->partial, m->st));
+    m->launches += 1;
+    CKS(reduce_fin(m, VG, FIN_ABSSUM));
+    double usum = 1.0;
+    CK(cudaMemcpyAsync(&m->hscal->rz, m->aux, sizeof(double), cudaMemcpyDeviceToHost, m->st));
+    CK(cudaStreamSynchronize(m->st));
+    usum = m->hscal->rz;
+    if (usum == 0.0) CK(cudaMemsetAsync(m->q, 0, sizeof(double) * (size_t)m->ndof, m->st));
+    else CKS(apply_impl(m, lam, nu, nu_const, u, m->q));
     CK(launch_pcg_init(g, f, m->q, m->r, m->mass_e, m->scal, m->partial, m->st));
     m->launches += 1;
     CKS(reduce_fin(m, VG, FIN_INIT));

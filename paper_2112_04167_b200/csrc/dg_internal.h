@@ -177,6 +177,7 @@ struct PcgScal {                 // device-resident scalars of one solve
 };
 enum { PCG_ST_RUN = 0, PCG_ST_CONV = 1, PCG_ST_MAXIT = 2, PCG_ST_BREAKDOWN = 3 };
 
+cudaError_t launch_abssum(const Geom &g, const double *u, double *partial, cudaStream_t st);
 int vec_grid();       // grid (and partial count) of the reduction vector kernels
 int vec_grid_wide();  // grid of the streaming vector kernels (and of k_pcg_update_t's partials)
 // partial sums of m*f and m over the local slab -> partial[blk*2 + {0,1}]
@@ -197,7 +198,7 @@ cudaError_t launch_shift(const Geom &g, double *x, const double *shift, cudaStre
 // deterministic reduction of partial[G][K] into sums[K] (single CTA, fixed order)
 cudaError_t launch_reduce(const double *partial, int G, int K, double *sums, cudaStream_t st);
 // scalar finalisation steps (single thread), mode-dependent
-enum FinMode { FIN_FMEAN = 0, FIN_INIT = 1, FIN_INIT2 = 2, FIN_ALPHA = 3, FIN_BETA = 4, FIN_UMEAN = 5, FIN_NUMEAN = 6 };
+enum FinMode { FIN_FMEAN = 0, FIN_INIT = 1, FIN_INIT2 = 2, FIN_ALPHA = 3, FIN_BETA = 4, FIN_UMEAN = 5, FIN_NUMEAN = 6, FIN_ABSSUM = 7 };
 cudaError_t launch_finalize(int mode, const double *sums, PcgScal *s, double *hist, double *aux, cudaStream_t st);
 cudaError_t launch_reduce_s(const double *partial, int G, int K, double *sums, const PcgScal *s, cudaStream_t st);
 cudaError_t launch_reduce_fin(const double *partial, int G, int K, double *sums, int mode, PcgScal *s, double *hist,

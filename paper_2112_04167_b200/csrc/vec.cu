@@ -58,6 +58,15 @@ __global__ void k_mass_moments(long long ndof, int npe, const double *__restrict
     write_partials<2>(v, partial);
 }
 
+// partials: sum |u| and 0 (an all-zero initial guess skips the initial-residual apply)
+__global__ void k_abssum(long long ndof, const double *__restrict__ u, double *partial)
+{
+    double v[2] = {0.0, 0.0};
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < ndof; i += (long long)gridDim.x * blockDim.x)
+        v[0] += fabs(u[i]);
+    write_partials<2>(v, partial);
+}
+
 __global__ void __launch_bounds__(256, 8) k_pcg_init(long long ndof, int npe, const double *__restrict__ f, const double *__restrict__ Ar,
                            double *__restrict__ r, const double *__restrict__ me, const PcgScal *s, double *partial)
 {
@@ -306,6 +315,9 @@ __device__ void finalize(int mode, const double *sums, PcgScal *s, double *hist,
     case FIN_UMEAN:
         aux[0] = sums[0] / sums[1];
         break;
+    case FIN_ABSSUM:
+        aux[0] = sums[0];
+        break;
     case FIN_NUMEAN:  // sum m nu / sum m
         s->nu_eff = sums[0] / sums[1];
         break;
@@ -382,6 +394,12 @@ inline long long nd(const Geom &g) { return g.nel * g.npe; }
 cudaError_t launch_mass_moments(const Geom &g, const double *f, const double *mass_e, double *partial, cudaStream_t st)
 {
     k_mass_moments<<<vec_grid(), 256, 0, st>>>(nd(g), g.npe, f, mass_e, partial);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_abssum(const Geom &g, const double *u, double *partial, cudaStream_t st)
+{
+    k_abssum<<<vec_grid(), 256, 0, st>>>(nd(g), u, partial);
     return cudaGetLastError();
 }
 
