@@ -590,11 +590,27 @@ dg_status pcg_impl(dg_mesh *m, double lam, const double *nu, double nu_const, co
     // constant nu on the uniform periodic mesh (N_d >= 2: the closed-form diagonal): the first
     // element's D^-1 serves every element
     const bool table = split && !nu && !self && !getenv("DG_PCG_NOTABLE");
-    int chunk = 4;
+    // iterations are enqueued in chunks between host convergence checks; after the first chunk
+    // the next one is sized from the observed residual reduction per iteration (launches past
+    // convergence exit at their first instruction but still cost a few microseconds each)
+    int chunk = 4, prev_iter = -1;
+    double prev_res2 = 0.0;
     for (;;) {
         CK(cudaMemcpyAsync(m->hscal, m->scal, sizeof(PcgScal), cudaMemcpyDeviceToHost, m->st));
         CK(cudaStreamSynchronize(m->st));
         if (m->hscal->done) break;
+        {
+            const PcgScal &hs = *m->hscal;
+            int next = std::min(chunk * 2, 32);
+            if (prev_iter >= 0 && hs.iter > prev_iter && hs.res2 > 0.0 && prev_res2 > hs.res2) {
+                const double rate = std::log(hs.res2 / prev_res2) / (hs.iter - prev_iter);  // < 0
+                const double need = std::log(hs.tol2 * hs.fnorm2 / hs.res2) / rate;
+                if (std::isfinite(need) && need > 0.0) next = std::max(2, std::min(64, (int)std::ceil(1.1 * need) + 1));
+            }
+            if (prev_iter >= 0) chunk = next;
+            prev_iter = hs.iter;
+            prev_res2 = hs.res2;
+        }
         for (int it = 0; it < chunk; ++it) {
             if (sw) {
                 // x += alpha p, p = z_b + P_1 x_c + beta p (in place) ; q = A p ; Schwarz step
@@ -686,7 +702,7 @@ dg_status pcg_impl(dg_mesh *m, double lam, const double *nu, double nu_const, co
                 CKS(reduce_fin(m, VG, FIN_BETA));
             }
         }
-        chunk = std::min(chunk * 2, 32);
+        (void)0;  // the next chunk is sized at the top of the loop
     }
     if (split || sw) {  // the deferred x update of the last iteration
         CK(launch_pcg_xfinal(g, u, p_old, m->scal, m->st));
