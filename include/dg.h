@@ -2,7 +2,7 @@
  * dg.h -- C-ABI of libdgsip.so, the B200-native (sm_100a) implicit-stage hot path of
  * arXiv 2112.04167 (Guesmi, Grotteschi, Stiller, "Assessment of high-order IMEX methods
  * for incompressible flow").  Citations "P:L" are lines of the paper text
- * (/root/reference/PAPER.md); readings A1..A21 are SURVEY.md §8(c), listed in DESIGN.md.
+ * (/root/reference/PAPER.md); readings A1..A21 are SURVEY.md §8(c), A22..A25 DESIGN.md's, all listed in DESIGN.md.
  *
  * What is computed.  Each IMEX-RK stage (Alg. 3) solves
  *   line 5:  a periodic pressure Poisson problem  -lap psi = rhs  (lam = 0)
@@ -10,7 +10,11 @@
  *                        i.e.  lam v - div(nu grad v) = f  with lam = 1/(dt a_ii), f = lam g
  * discretised by the symmetric interior-penalty DG method on tensor-product
  * GLL elements of degree P, plus the explicit DG convective term
- * F_c = -div(v v) with local Lax-Friedrichs fluxes.
+ * F_c = -div(v v) with local Lax-Friedrichs fluxes.  Built on these:
+ * the DG divergence/gradient pair of the projection (lines 5-6), whole IMEX-RK steps for
+ * constant viscosity and for the solution-dependent viscosity of P:1222 (with F_d2/F_d3,
+ * forcing and the final projection), and a two-level Schwarz preconditioner for the solves
+ * (readings A22-A25 in DESIGN.md).
  *
  * Mesh and data layout (all calls).  Periodic box [0,L0]x[0,L1](x[0,L2]) with N[d]
  * uniform elements per direction.  Global element index e = ex + N0*(ey + N1*ez);
