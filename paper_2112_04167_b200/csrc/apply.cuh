@@ -571,7 +571,11 @@ struct ApplyDispatch {
     {
         if (mode == 2) {  // dot epilogue only (split PCG path): 3-D meshes the v6 or v5 kernel runs
             if constexpr (DIM == 3) {
-                if (v6_ok(a, false)) return varnu ? go6<P, true, 2>(a, grid, st) : go6<P, false, 2>(a, grid, st);
+                if (v6_ok(a, false)) {
+                    if (a.lam > 0.0)  // sum(q) unused: the epilogue variant without it
+                        return varnu ? go6<P, true, 3>(a, grid, st) : go6<P, false, 3>(a, grid, st);
+                    return varnu ? go6<P, true, 2>(a, grid, st) : go6<P, false, 2>(a, grid, st);
+                }
                 if (v5_ok(a, false)) return varnu ? go5<P, true, 2>(a, grid, st) : go5<P, false, 2>(a, grid, st);
                 return cudaErrorNotSupported;
             } else {

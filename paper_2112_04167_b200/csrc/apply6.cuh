@@ -1,5 +1,6 @@
 // MODE: 0 plain apply; 1 fused PCG operand (prologue p = z + beta p_old, dot epilogue);
-// 2 apply with the dot epilogue only (the split PCG path: p formed by k_pcg_pupd).
+// 2 apply with the dot epilogue only (the split PCG path: p formed by k_pcg_pupd); 3 as 2
+// without sum(out) (lam > 0: the mean of q is not used; one accumulator fewer at 80 registers).
 //
 // apply6.cuh -- 3-D SIP-DG apply, v6: one persistent CTA per SM, 4x4x1-element bricks,
 // warp-specialised producer / consumers, one element line per consumer thread with warp
@@ -247,7 +248,7 @@ __device__ __forceinline__ void cpass_z(const ApplyParams &a, const DevTab &T, c
         }
         if (K::MODE >= 1) {
             epi0 = fma(W, fma(c, zc.gP, f0 * zc.u), epi0);
-            epi1 += s1;
+            if (K::MODE != 3) epi1 += s1;
         }
         zc.held = false;
     };
@@ -298,7 +299,7 @@ __device__ __forceinline__ void cpass_z(const ApplyParams &a, const DevTab &T, c
         else zo[i * NCL + t] = o;
         if (K::MODE >= 1) {
             epi0 = fma(v[i], o, epi0);
-            epi1 += o;
+            if (K::MODE != 3) epi1 += o;
         }
     }
     if (!zlast) {
@@ -576,7 +577,7 @@ __global__ void __launch_bounds__((KC6<P, VARNU, MODE>::NT)) __maxnreg__((KC6<P,
         double *red = sm + K::OFF_RED;
         const int lane = tid & 31, wid = tid >> 5;
         epi0 = warp_sum(epi0);
-        epi1 = warp_sum(epi1);
+        if (MODE != 3) epi1 = warp_sum(epi1);
         if (lane == 0) {
             red[wid] = epi0;
             red[32 + wid] = epi1;
