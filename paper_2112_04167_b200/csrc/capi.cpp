@@ -564,10 +564,9 @@ dg_status pcg_impl(dg_mesh *m, double lam, const double *nu, double nu_const, co
     CK(launch_abssum(g, u, m->partial, m->st));
     m->launches += 1;
     CKS(reduce_fin(m, VG, FIN_ABSSUM));
-    double usum = 1.0;
     CK(cudaMemcpyAsync(&m->hscal->rz, m->aux, sizeof(double), cudaMemcpyDeviceToHost, m->st));
     CK(cudaStreamSynchronize(m->st));
-    usum = m->hscal->rz;
+    const double usum = m->hscal->rz;
     if (usum == 0.0) CK(cudaMemsetAsync(m->q, 0, sizeof(double) * (size_t)m->ndof, m->st));
     else CKS(apply_impl(m, lam, nu, nu_const, u, m->q));
     CK(launch_pcg_init(g, f, m->q, m->r, m->mass_e, m->scal, m->partial, m->st));
@@ -702,7 +701,6 @@ dg_status pcg_impl(dg_mesh *m, double lam, const double *nu, double nu_const, co
                 CKS(reduce_fin(m, VG, FIN_BETA));
             }
         }
-        (void)0;  // the next chunk is sized at the top of the loop
     }
     if (split || sw) {  // the deferred x update of the last iteration
         CK(launch_pcg_xfinal(g, u, p_old, m->scal, m->st));
