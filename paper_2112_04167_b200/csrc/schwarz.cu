@@ -584,7 +584,7 @@ __global__ void k_sw_cgather_local(SwCoarseParams a, int S, int off, int nl)
 // streaming of x, z, p
 // ---------------------------------------------------------------------------
 template <int DIM, int n>
-__global__ void __launch_bounds__(256) k_sw_pupd(SwPupdParams a, const __grid_constant__ SwLine<n> L)
+__global__ void __launch_bounds__(256, 4) k_sw_pupd(SwPupdParams a, const __grid_constant__ SwLine<n> L)
 {
     using C = SwCfg<DIM, n>;
     constexpr int NPE = C::NPE, NT = C::NT, EPC = C::EPC, NC = C::NC;
@@ -625,36 +625,40 @@ __global__ void __launch_bounds__(256) k_sw_pupd(SwPupdParams a, const __grid_co
         const long long g0 = e0 * NPE;
         const int cnt = ne * NPE;
         constexpr int PER = (EPC * NPE + NT - 1) / NT;
-        double rz[PER], rp[PER], rx[PER];
+        constexpr int CH = PER < 4 ? PER : 4;  // loads in flight per chunk (register budget)
+#pragma unroll 1
+        for (int q0 = 0; q0 < PER; q0 += CH) {
+            double rz[CH], rp[CH], rx[CH];
 #pragma unroll
-        for (int q = 0; q < PER; ++q) {
-            const int t = threadIdx.x + q * NT;
-            if (t < cnt) {
-                rz[q] = zb[g0 + t];
-                rp[q] = upd ? p[g0 + t] : 0.0;
-                rx[q] = (upd && x) ? x[g0 + t] : 0.0;
-            }
-        }
-#pragma unroll
-        for (int q = 0; q < PER; ++q) {
-            const int t = threadIdx.x + q * NT;
-            if (t < cnt) {
-                const int el = t / NPE, tn = t - el * NPE;
-                // trilinear (bilinear) interpolation of the element's vertex values at node tn
-                const int i = tn % n, j = (tn / n) % n;
-                const double hx0 = sh[0][i], hx1 = sh[1][i], hy0 = sh[0][j], hy1 = sh[1][j];
-                const double *xv = sxv[el];
-                double zc = hy0 * fma(hx1, xv[1], hx0 * xv[0]) + hy1 * fma(hx1, xv[3], hx0 * xv[2]);
-                if (DIM == 3) {
-                    const int k = tn / (n * n);
-                    const double zc1 = hy0 * fma(hx1, xv[5], hx0 * xv[4]) + hy1 * fma(hx1, xv[7], hx0 * xv[6]);
-                    zc = fma(sh[1][k], zc1, sh[0][k] * zc);
+            for (int qq = 0; qq < CH; ++qq) {
+                const int t = threadIdx.x + (q0 + qq) * NT;
+                if (q0 + qq < PER && t < cnt) {
+                    rz[qq] = zb[g0 + t];
+                    rp[qq] = upd ? p[g0 + t] : 0.0;
+                    rx[qq] = (upd && x) ? x[g0 + t] : 0.0;
                 }
-                if (upd) {
-                    if (x) x[g0 + t] = fma(alpha, rp[q], rx[q]);
-                    p[g0 + t] = fma(beta, rp[q], rz[q] + zc);
-                } else {
-                    p[g0 + t] = rz[q] + zc;
+            }
+#pragma unroll
+            for (int qq = 0; qq < CH; ++qq) {
+                const int t = threadIdx.x + (q0 + qq) * NT;
+                if (q0 + qq < PER && t < cnt) {
+                    const int el = t / NPE, tn = t - el * NPE;
+                    // trilinear (bilinear) interpolation of the element's vertex values at node tn
+                    const int i = tn % n, j = (tn / n) % n;
+                    const double hx0 = sh[0][i], hx1 = sh[1][i], hy0 = sh[0][j], hy1 = sh[1][j];
+                    const double *xv = sxv[el];
+                    double zc = hy0 * fma(hx1, xv[1], hx0 * xv[0]) + hy1 * fma(hx1, xv[3], hx0 * xv[2]);
+                    if (DIM == 3) {
+                        const int k = tn / (n * n);
+                        const double zc1 = hy0 * fma(hx1, xv[5], hx0 * xv[4]) + hy1 * fma(hx1, xv[7], hx0 * xv[6]);
+                        zc = fma(sh[1][k], zc1, sh[0][k] * zc);
+                    }
+                    if (upd) {
+                        if (x) x[g0 + t] = fma(alpha, rp[qq], rx[qq]);
+                        p[g0 + t] = fma(beta, rp[qq], rz[qq] + zc);
+                    } else {
+                        p[g0 + t] = rz[qq] + zc;
+                    }
                 }
             }
         }
