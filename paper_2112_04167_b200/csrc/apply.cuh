@@ -611,9 +611,20 @@ struct ApplyDispatch {
         bool self = false;
         for (int dd = 0; dd < DIM; ++dd) self = self || g.N[dd] == 1;
         if (!self) {  // closed form, one CTA per element (grid-stride)
-            if (!getenv("DG_DIAG_V1")) {  // one thread per node (measured faster)
+            if (!getenv("DG_DIAG_V1")) {  // one thread per node (measured faster), one resident wave
+                static int resident[2] = {0, 0};
+                const int vi = nu ? 1 : 0;
+                if (!resident[vi]) {
+                    int dev = 0, nsm = 148, occ = 1;
+                    cudaGetDevice(&dev);
+                    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+                    cudaError_t e = nu ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_diag_cf2<DIM, P, true>, 256, 0)
+                                       : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_diag_cf2<DIM, P, false>, 256, 0);
+                    if (e != cudaSuccess || occ < 1) occ = 1;
+                    resident[vi] = nsm * occ;
+                }
                 long long blocks = (tot + 255) / 256;
-                if (blocks > 148LL * 8) blocks = 148LL * 8;
+                if (blocks > resident[vi]) blocks = resident[vi];
                 if (nu) k_diag_cf2<DIM, P, true><<<(int)blocks, 256, 0, st>>>(g, lam, nu, nuc, h, d, invert);
                 else k_diag_cf2<DIM, P, false><<<(int)blocks, 256, 0, st>>>(g, lam, nu, nuc, h, d, invert);
                 return cudaGetLastError();
