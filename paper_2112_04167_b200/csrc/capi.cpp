@@ -172,6 +172,7 @@ struct dg_mesh {
     double *d_swF = nullptr, *rc_el = nullptr, *chat = nullptr, *xc = nullptr, *rc = nullptr;
     double sw_nu = -1.0;
     bool sw_coarse_on = true;
+    double dinv_lam = -1.0, dinv_nu = -1.0;  // (lam, nu_const) the dinv workspace holds (constant nu)
 };
 
 #define CK(call)                                                                                         \
@@ -534,6 +535,9 @@ dg_status pcg_impl(dg_mesh *m, double lam, const double *nu, double nu_const, co
     bool self = false;
     for (int d = 0; d < g.dim; ++d) self = self || g.N[d] == 1;
     if (sw) {
+    } else if (!self && !nu && m->dinv_lam == lam && m->dinv_nu == nu_const) {
+        // constant nu: D^-1 depends on (lam, nu) and the geometry only -- kept from the last
+        // solve with the same pair (e.g. the three velocity components of a stage)
     } else if (!self) {
         Halo hd;
         if (multi && nu) {
@@ -545,10 +549,13 @@ dg_status pcg_impl(dg_mesh *m, double lam, const double *nu, double nu_const, co
         CK(g.dim == 3 ? launch_diag3(g, lam, nu, nu_const, hd, m->dinv, m->st, 1)
                       : launch_diag2(g, lam, nu, nu_const, hd, m->dinv, m->st, 1));
         m->launches += 1;
+        m->dinv_lam = nu ? -1.0 : lam;
+        m->dinv_nu = nu ? -1.0 : nu_const;
     } else {
         CKS(diag_impl(m, lam, nu, nu_const, m->q));
         CK(launch_recip(g, m->q, m->dinv, m->st));
         m->launches += 1;
+        m->dinv_lam = m->dinv_nu = -1.0;
     }
     Halo hnu;
     if (multi && nu) {  // diag_impl exchanged nu already
