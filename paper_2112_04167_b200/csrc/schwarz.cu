@@ -118,7 +118,41 @@ void build_sw_tab(const Geom &g, double nu, SwTab *t, std::vector<double> &F)
         for (int i = 0; i < n; ++i)
             for (int j = 0; j < n; ++j)
                 A[i][j] = (long double)nu * (2.0L / (long double)g.h[d]) * (long double)T.Kref[i][j] / (ms[i] * ms[j]);
-        jacobi_eig(n, A, V, ev);
+        // A is centro-symmetric (Kref and the GLL weights are): its eigenvectors are taken in the
+        // even / odd subspaces separately, so that S[P-i][k] = +S[i][k] for the even modes
+        // k < he and -S[i][k] for the odd modes k >= he (the block kernel's even-odd transforms)
+        const int he = (n + 1) / 2, ho = n / 2, P = n - 1;
+        long double Be[NMAX][NMAX] = {}, Bo[NMAX][NMAX] = {};  // basis columns (n x he, n x ho)
+        const long double r2 = 1.0L / sqrtl(2.0L);
+        for (int c = 0; c < he; ++c) {
+            if (c == P - c) Be[c][c] = 1.0L;
+            else Be[c][c] = Be[P - c][c] = r2;
+        }
+        for (int c = 0; c < ho; ++c) {
+            Bo[c][c] = r2;
+            Bo[P - c][c] = -r2;
+        }
+        auto sub = [&](long double (&Bm)[NMAX][NMAX], int m, int k0) {
+            long double As[NMAX][NMAX], Vs[NMAX][NMAX], es[NMAX];
+            for (int a = 0; a < m; ++a)
+                for (int b = 0; b < m; ++b) {
+                    long double acc = 0.0L;
+                    for (int i = 0; i < n; ++i)
+                        for (int j = 0; j < n; ++j) acc += Bm[i][a] * A[i][j] * Bm[j][b];
+                    As[a][b] = acc;
+                }
+            jacobi_eig(m, As, Vs, es);
+            for (int kk = 0; kk < m; ++kk) {
+                ev[k0 + kk] = es[kk];
+                for (int i = 0; i < n; ++i) {
+                    long double acc = 0.0L;
+                    for (int a = 0; a < m; ++a) acc += Bm[i][a] * Vs[a][kk];
+                    V[i][k0 + kk] = acc;
+                }
+            }
+        };
+        sub(Be, he, 0);
+        if (ho > 0) sub(Bo, ho, he);
         for (int i = 0; i < n; ++i) {
             t->Lam[d][i] = (double)ev[i];
             for (int k = 0; k < n; ++k) t->S[d][i * n + k] = (double)(V[i][k] / ms[i]);
@@ -207,6 +241,56 @@ __device__ __forceinline__ void line_xform(const double (&S)[n * n], const doubl
 #pragma unroll
         for (int m = 0; m < n; ++m) acc = fma(TR ? S[m * n + k] : S[k * n + m], v[m], acc);
         o[k] = acc;
+    }
+}
+
+// even-odd forms of the S transforms (S[P-i][k] = +-S[i][k] for the even / odd modes, see
+// build_sw_tab): half the FMAs of line_xform
+template <int n>
+__device__ __forceinline__ void eo_fwd(const double (&S)[n * n], const double (&v)[n], double (&o)[n])
+{
+    constexpr int h = n / 2, he = (n + 1) / 2, P = n - 1;
+    double sp[h > 0 ? h : 1], sm[h > 0 ? h : 1];
+#pragma unroll
+    for (int i = 0; i < h; ++i) {
+        sp[i] = v[i] + v[P - i];
+        sm[i] = v[i] - v[P - i];
+    }
+#pragma unroll
+    for (int k = 0; k < he; ++k) {
+        double acc = (n % 2) ? S[h * n + k] * v[h] : 0.0;
+#pragma unroll
+        for (int i = 0; i < h; ++i) acc = fma(S[i * n + k], sp[i], acc);
+        o[k] = acc;
+    }
+#pragma unroll
+    for (int k = he; k < n; ++k) {
+        double acc = 0.0;
+#pragma unroll
+        for (int i = 0; i < h; ++i) acc = fma(S[i * n + k], sm[i], acc);
+        o[k] = acc;
+    }
+}
+
+template <int n>
+__device__ __forceinline__ void eo_bwd(const double (&S)[n * n], const double (&t)[n], double (&o)[n])
+{
+    constexpr int h = n / 2, he = (n + 1) / 2, P = n - 1;
+#pragma unroll
+    for (int i = 0; i < h; ++i) {
+        double e = 0.0, q = 0.0;
+#pragma unroll
+        for (int k = 0; k < he; ++k) e = fma(S[i * n + k], t[k], e);
+#pragma unroll
+        for (int k = he; k < n; ++k) q = fma(S[i * n + k], t[k], q);
+        o[i] = e + q;
+        o[P - i] = e - q;
+    }
+    if (n % 2) {
+        double e = 0.0;
+#pragma unroll
+        for (int k = 0; k < he; ++k) e = fma(S[h * n + k], t[k], e);
+        o[h] = e;
     }
 }
 
@@ -330,7 +414,7 @@ __global__ void __launch_bounds__(256) k_sw_block(SwBlockParams a, const __grid_
             }
             sx[(le * NL + ln) * 2 + 0] = h0;
             sx[(le * NL + ln) * 2 + 1] = h1;
-            line_xform<n, true>(L.S[0], v, o);
+            eo_fwd<n>(L.S[0], v, o);
 #pragma unroll
             for (int m = 0; m < n; ++m) sA[b + m] = o[m];
         }
@@ -356,7 +440,7 @@ __global__ void __launch_bounds__(256) k_sw_block(SwBlockParams a, const __grid_
                 const int i = ln % n, k = ln / n, b = le * NPE + i + n * n * k;
 #pragma unroll
                 for (int m = 0; m < n; ++m) v[m] = sA[b + m * n];
-                line_xform<n, true>(L.S[1], v, o);
+                eo_fwd<n>(L.S[1], v, o);
 #pragma unroll
                 for (int m = 0; m < n; ++m) sA[b + m * n] = o[m];
             }
@@ -366,14 +450,14 @@ __global__ void __launch_bounds__(256) k_sw_block(SwBlockParams a, const __grid_
                 const int b = le * NPE + ln;
 #pragma unroll
                 for (int m = 0; m < n; ++m) v[m] = sA[b + m * n * n];
-                line_xform<n, true>(L.S[2], v, o);
+                eo_fwd<n>(L.S[2], v, o);
 #pragma unroll
                 for (int m = 0; m < n; ++m) {
                     const double oi = o[m] * sInv[ln + m * n * n];
                     acc_rz = fma(oi, o[m], acc_rz);
                     o[m] = oi;
                 }
-                line_xform<n, false>(L.S[2], o, v);
+                eo_bwd<n>(L.S[2], o, v);
 #pragma unroll
                 for (int m = 0; m < n; ++m) sA[b + m * n * n] = v[m];
             }
@@ -383,7 +467,7 @@ __global__ void __launch_bounds__(256) k_sw_block(SwBlockParams a, const __grid_
                 const int i = ln % n, k = ln / n, b = le * NPE + i + n * n * k;
 #pragma unroll
                 for (int m = 0; m < n; ++m) v[m] = sA[b + m * n];
-                line_xform<n, false>(L.S[1], v, o);
+                eo_bwd<n>(L.S[1], v, o);
 #pragma unroll
                 for (int m = 0; m < n; ++m) sA[b + m * n] = o[m];
             }
@@ -394,14 +478,14 @@ __global__ void __launch_bounds__(256) k_sw_block(SwBlockParams a, const __grid_
                 const int b = le * NPE + ln;
 #pragma unroll
                 for (int m = 0; m < n; ++m) v[m] = sA[b + m * n];
-                line_xform<n, true>(L.S[1], v, o);
+                eo_fwd<n>(L.S[1], v, o);
 #pragma unroll
                 for (int m = 0; m < n; ++m) {
                     const double oi = o[m] * sInv[ln + m * n];
                     acc_rz = fma(oi, o[m], acc_rz);
                     o[m] = oi;
                 }
-                line_xform<n, false>(L.S[1], o, v);
+                eo_bwd<n>(L.S[1], o, v);
 #pragma unroll
                 for (int m = 0; m < n; ++m) sA[b + m * n] = v[m];
             }
@@ -412,7 +496,7 @@ __global__ void __launch_bounds__(256) k_sw_block(SwBlockParams a, const __grid_
             const int b = le * NPE + ln * n;
 #pragma unroll
             for (int m = 0; m < n; ++m) v[m] = sA[b + m];
-            line_xform<n, false>(L.S[0], v, o);
+            eo_bwd<n>(L.S[0], v, o);
 #pragma unroll
             for (int m = 0; m < n; ++m) sA[b + m] = o[m];
         }
