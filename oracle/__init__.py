@@ -57,6 +57,7 @@ def lib():
                                        ctypes.c_int, ctypes.c_int, _dp, ctypes.POINTER(ctypes.c_int),
                                        ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)]
         L.oracle_convect.argtypes = [mp, ctypes.POINTER(_dp), ctypes.POINTER(_dp), _lp, ctypes.c_long]
+        L.oracle_convect_q.argtypes = [mp, ctypes.c_int, ctypes.POINTER(_dp), ctypes.POINTER(_dp), _lp, ctypes.c_long]
         _lib = L
     return _lib
 
@@ -180,15 +181,18 @@ def pcg_solve(mesh: Mesh, lam, f, nu=None, nu_const=1.0, tol=1e-14, maxit=100000
     return u.reshape(mesh.n_el, mesh.npe), it.value, rr.value, rm.value, st
 
 
-def convect(mesh: Mesh, v, elems=None):
-    """LLF DG convective tendency F_c (nodal), per component; rows of ``elems``."""
+def convect(mesh: Mesh, v, elems=None, Q=None):
+    """LLF DG convective tendency F_c (nodal), per component; rows of ``elems``.  Q: Gauss
+    points per direction (default: reading A13, floor(3P/2)+1)."""
     vs = [_f64(x).reshape(-1) for x in v[: mesh.dim]]
     e, k, ep = _elems(elems)
     cnt = mesh.n_el if e is None else k
     outs = [np.zeros((cnt, mesh.npe)) for _ in range(mesh.dim)]
     vin = (_dp * 3)(*[_ptr(x) for x in vs] + [None] * (3 - mesh.dim))
     vout = (_dp * 3)(*[_ptr(x) for x in outs] + [None] * (3 - mesh.dim))
-    if lib().oracle_convect(mesh.ref(), vin, vout, ep, k):
+    rc = (lib().oracle_convect(mesh.ref(), vin, vout, ep, k) if Q is None
+          else lib().oracle_convect_q(mesh.ref(), int(Q), vin, vout, ep, k))
+    if rc:
         raise ValueError("oracle_convect failed")
     return outs
 

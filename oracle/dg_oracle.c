@@ -702,12 +702,18 @@ static void convect_element(const ctx_t *c, int Q, const double *zeta, const dou
 int oracle_convect(const oracle_mesh *m, const double *const *v, double *const *out,
                    const long *elems, long nel)
 {
+    /* reading A13: Q = floor(3P/2) + 1 Gauss points per direction (2Q - 1 >= 3P) */
+    return oracle_convect_q(m, (3 * m->P) / 2 + 1, v, out, elems, nel);
+}
+
+int oracle_convect_q(const oracle_mesh *m, int Q, const double *const *v, double *const *out,
+                     const long *elems, long nel)
+{
     ctx_t c;
     if (ctx_init(m, &c) || !v || !out) return -1;
     for (int cc = 0; cc < c.dim; ++cc)
         if (!v[cc] || !out[cc]) return -1;
-    const int Q = (3 * c.P) / 2 + 1;
-    if (Q > MAXN) return -1;
+    if (Q < 1 || Q > MAXN) return -1;
     double zeta[MAXN], omega[MAXN];
     double Bq[MAXN][MAXN], Gq[MAXN][MAXN], Bend[2][MAXN], Gend[2][MAXN];
     if (oracle_gauss(Q, zeta, omega)) return -1;

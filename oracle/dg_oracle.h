@@ -88,6 +88,10 @@ int oracle_pcg_solve(const oracle_mesh *m, double lam, const double *nu, double 
  * Values at Gauss points by dense basis evaluation sum_J v_J phi_J(x_q). */
 int oracle_convect(const oracle_mesh *m, const double *const *v, double *const *out,
                    const long *elems, long nel);
+/* The same with an explicit Gauss point count Q per direction (1 <= Q <= 18): used by the
+ * pins that show Q = floor(3P/2)+1 is the smallest exact rule (tests/test_oracle_convect.py). */
+int oracle_convect_q(const oracle_mesh *m, int Q, const double *const *v, double *const *out,
+                     const long *elems, long nel);
 
 #ifdef __cplusplus
 }

@@ -394,7 +394,7 @@ struct ApplyDispatch {
                     }
                 }
             }
-            if (const char *ev = getenv("DG_V5_NSEG")) {  // development override
+            if (const char *ev = DG_DEV_ENV("DG_V5_NSEG")) {  // development override
                 const int want = atoi(ev);
                 if (want >= 1 && nbS % want == 0) nseg = want;
             }
@@ -417,6 +417,28 @@ struct ApplyDispatch {
             return cudaErrorNotSupported;
         } else {
             auto kern = v6::k_apply6<P, VARNU, MODE>;
+            if (VARNU) {  // weight-folded constants (V6Fold, dg_internal.h)
+                const Tab &t = host_tab(P);
+                const double w0 = t.w[0];
+                a.f6.kL = 0.5 / w0;
+                for (int d = 0; d < 3; ++d) {
+                    const double C = a.g.wfac[d] * a.g.sd[d];
+                    a.f6.kF[d] = a.g.tau[d] * a.g.wfac[d] / (2.0 * w0);
+                    a.f6.kS[d] = 0.5 * C / w0;
+                    a.f6.kCL[d] = C * a.f6.kL;
+                    EOTab e = t.eE;
+                    for (int i = 0; i < HMAX; ++i) {
+                        for (int j = 0; j < HMAX; ++j) {
+                            e.Te[i][j] *= C;
+                            e.To[i][j] *= C;
+                        }
+                        e.Tc[i] *= C;
+                        e.Mr[i] *= C;
+                    }
+                    e.Mmid *= C;
+                    a.f6.eE[d] = e;
+                }
+            }
             static int nsm = 0;
             cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, K::SMEM_BYTES);
             if (e != cudaSuccess) return e;
@@ -448,7 +470,7 @@ struct ApplyDispatch {
                 }
             }
             if (nbS < 2) nseg = 1;
-            if (const char *ev = getenv("DG_V6_NSEG")) {  // development override
+            if (const char *ev = DG_DEV_ENV("DG_V6_NSEG")) {  // development override
                 const int want = atoi(ev);
                 if (want >= 1 && nbS % want == 0 && nbS / want >= 2) nseg = want;
             }
@@ -465,7 +487,7 @@ struct ApplyDispatch {
     static bool v6_ok(const ApplyParams &a, bool pcg)
     {
         static const bool off = [] {
-            const char *e = getenv("DG_APPLY_IMPL");
+            const char *e = DG_DEV_ENV("DG_APPLY_IMPL");
             return e && e[0] == 'v' && (e[1] == '4' || e[1] == '5');
         }();
         // TMA copies single elements: n^3 doubles must be a multiple of 16 bytes (n even)
@@ -515,14 +537,14 @@ struct ApplyDispatch {
     }
     static bool ranges_ok(const Geom &g)
     {
-        const char *e = getenv("DG_APPLY_IMPL");
+        const char *e = DG_DEV_ENV("DG_APPLY_IMPL");
         if (e && e[0] == 'v' && e[1] == '4') return false;
         return DIM == 3 && g.Nl[0] % 2 == 0 && g.Nl[1] % 2 == 0 && g.Nl[2] % 2 == 0;
     }
     static bool v5_ok(const ApplyParams &a, bool pcg)
     {
         static const bool off = [] {
-            const char *e = getenv("DG_APPLY_IMPL");
+            const char *e = DG_DEV_ENV("DG_APPLY_IMPL");
             return e && e[0] == 'v' && e[1] == '4';
         }();
         if (off || DIM != 3) return false;
@@ -539,7 +561,7 @@ struct ApplyDispatch {
     static cudaError_t pick(const ApplyParams &a, int *grid, cudaStream_t st)
     {
         static const int budget = [] {
-            const char *e = getenv("DG_SMEM_BUDGET_KB");
+            const char *e = DG_DEV_ENV("DG_SMEM_BUDGET_KB");
             return (e ? atoi(e) : 110) * 1024;
         }();
         const int *N = a.g.Nl;
@@ -611,7 +633,15 @@ struct ApplyDispatch {
         bool self = false;
         for (int dd = 0; dd < DIM; ++dd) self = self || g.N[dd] == 1;
         if (!self) {  // closed form, one CTA per element (grid-stride)
-            if (!getenv("DG_DIAG_V1")) {  // one thread per node (measured faster), one resident wave
+#ifdef DG_DEVELOPMENT  // DG_DIAG_V1: the first one-CTA-per-element closed-form kernel (A/B only)
+            if (DG_DEV_ENV("DG_DIAG_V1")) {
+                const long long blocks = g.nel < 148LL * 16 ? g.nel : 148LL * 16;
+                if (nu) k_diag_cf<DIM, P, true><<<(int)blocks, 256, 0, st>>>(g, lam, nu, nuc, h, d, invert);
+                else k_diag_cf<DIM, P, false><<<(int)blocks, 256, 0, st>>>(g, lam, nu, nuc, h, d, invert);
+                return cudaGetLastError();
+            }
+#endif
+            {  // one thread per node (measured faster), one resident wave
                 static int resident[2] = {0, 0};
                 const int vi = nu ? 1 : 0;
                 if (!resident[vi]) {
@@ -629,10 +659,6 @@ struct ApplyDispatch {
                 else k_diag_cf2<DIM, P, false><<<(int)blocks, 256, 0, st>>>(g, lam, nu, nuc, h, d, invert);
                 return cudaGetLastError();
             }
-            const long long blocks = g.nel < 148LL * 16 ? g.nel : 148LL * 16;
-            if (nu) k_diag_cf<DIM, P, true><<<(int)blocks, 256, 0, st>>>(g, lam, nu, nuc, h, d, invert);
-            else k_diag_cf<DIM, P, false><<<(int)blocks, 256, 0, st>>>(g, lam, nu, nuc, h, d, invert);
-            return cudaGetLastError();
         }
         if (invert) return cudaErrorInvalidValue;  // N_d = 1 meshes: caller inverts separately
         long long blocks = (tot + 255) / 256;

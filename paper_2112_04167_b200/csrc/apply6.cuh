@@ -37,6 +37,7 @@ using v5::eo;
 using v5::fence_proxy_async;
 using v5::l2_prefetch;
 using v5::mbar_arrive;
+using v5::mbar_arrive_expect_tx;
 using v5::mbar_expect_tx;
 using v5::mbar_init;
 using v5::mbar_wait;
@@ -74,7 +75,8 @@ struct KC6 {
     static constexpr int OFF_ZO = OFF_TZ + 2 * NV * NCL;         // parked z-pass outputs [n][NCL]
     static constexpr int OFF_RED = OFF_ZO + n * NCL;
     static constexpr int OFF_BAR = OFF_RED + 64;
-    static constexpr int SMEM_DOUBLES = OFF_BAR + 4;
+    static constexpr int OFF_W = OFF_BAR + 4;          // full[2], empty[2]
+    static constexpr int SMEM_DOUBLES = OFF_W + n;     // GLL weights (per-lane indexed reads)
     static constexpr int SMEM_BYTES = SMEM_DOUBLES * 8;
     static constexpr int REG_C = 65536 / NT / 8 * 8 > 80 ? 80 : 65536 / NT / 8 * 8;  // launch registers
 };
@@ -90,8 +92,8 @@ struct ZC6 {
 // consumer x / y pass: one element line per thread, 4 lanes per brick row
 // ---------------------------------------------------------------------------
 template <class K, int D, bool FIRST>
-__device__ __forceinline__ void cpass_xy(const ApplyParams &a, const DevTab &T, const double *su, const double *snu,
-                                         double *sacc, const double *tr, int t)
+__device__ __forceinline__ void cpass_xy(const ApplyParams &a, const DevTab &T, const double *su, double *snu,
+                                         double *sacc, const double *tr, int t, const double *sw)
 {
     constexpr int P = K::P, n = K::n, NN = K::NN, LR = K::LR, NV = K::NV, SE = K::SE;
     constexpr int SSD = D == 0 ? 1 : n;
@@ -104,22 +106,29 @@ __device__ __forceinline__ void cpass_xy(const ApplyParams &a, const DevTab &T, 
     const int lx = D == 0 ? l : ce, ly = D == 0 ? ce : l;
     const int base = lx * SE + ly * K::SY + (D == 0 ? ta * n + tb * NN : ta + tb * NN);
     const Geom &g = a.g;
-    const double W = T.w[ta] * T.w[tb] * g.wfac[D];
-    const double sd = g.sd[D], htau = 0.5 * g.tau[D];
+    const double sd = g.sd[D];
 
     double v[n], nv[n];
     if (D == 0 && (n % 2) == 0) {
+        // VARNU: the x pass folds the GLL weights into the staged viscosity, nu~ = nu w_i w_j w_k
+        // (V6Fold), in registers and in place for the y and z passes (each x line has one owner)
+        const double wjk = K::VARNU ? sw[ta] * sw[tb] : 0.0;
 #pragma unroll
         for (int i = 0; i < n; i += 2) {
             const double2 x = *reinterpret_cast<const double2 *>(su + base + i);
             v[i] = x.x;
             v[i + 1] = x.y;
             if (K::VARNU) {
-                const double2 y = *reinterpret_cast<const double2 *>(snu + base + i);
+                double2 y = *reinterpret_cast<const double2 *>(snu + base + i);
+                y.x *= T.w[i] * wjk;
+                y.y *= T.w[i + 1] * wjk;
                 nv[i] = y.x;
                 nv[i + 1] = y.y;
+                if (act) *reinterpret_cast<double2 *>(snu + base + i) = y;
             }
         }
+        // generic-proxy writes into a TMA-refilled slot: order them before later async-proxy writes
+        if (K::VARNU) fence_proxy_async();
     } else {
 #pragma unroll
         for (int i = 0; i < n; ++i) {
@@ -142,9 +151,15 @@ __device__ __forceinline__ void cpass_xy(const ApplyParams &a, const DevTab &T, 
     }
     double r[n];
     if (K::VARNU) {
-        double gg[n];
+        // weight-folded form (V6Fold): nv = nu~ = nu w_i w_j w_k (staged by the producers), so
+        // W (w_k (2/h) nu_k g_k) = C nu~_k g_k with g = D v on the reference line, the own flux
+        // s~ = nu~ g at the line ends, and the whole line result is already W-weighted
+        const V6Fold &F = a.f6;
+        double gg[n], tv[n];
         eo<P, true>(T.eD, v, gg);
-        const double s0 = nv[0] * sd * gg[0], sP = nv[P] * sd * gg[P];
+#pragma unroll
+        for (int k = 0; k < n; ++k) tv[k] = nv[k] * gg[k];
+        const double s0 = tv[0], sP = tv[P];
         // in-brick faces: the left neighbour's right end arrives from lane - 1, the right
         // neighbour's left end from lane + 1
         const double xu = __shfl_up_sync(0xffffffffu, v[P], 1), xs = __shfl_up_sync(0xffffffffu, sP, 1),
@@ -162,16 +177,18 @@ __device__ __forceinline__ void cpass_xy(const ApplyParams &a, const DevTab &T, 
             nuR = yn;
         }
         const double JL = uL - v[0], JR = v[P] - uR;
-        const double FL = fma(htau * (nuL + nv[0]), JL, -0.5 * (sL + s0));
-        const double FR = fma(htau * (nv[P] + nuR), JR, -0.5 * (sP + sR));
-        double tv[n];
-#pragma unroll
-        for (int k = 0; k < n; ++k) tv[k] = g.wsd[D][k] * (nv[k] * gg[k]);
-        tv[P] = fma(-0.5 * sd * nv[P], JR, tv[P]);
-        tv[0] = fma(-0.5 * sd * nv[0], JL, tv[0]);
-        eo<P, true>(T.eE, tv, r);
+        const double FL = fma(F.kF[D] * (nuL + nv[0]), JL, -F.kS[D] * (sL + s0));
+        const double FR = fma(F.kF[D] * (nv[P] + nuR), JR, -F.kS[D] * (sP + sR));
+        tv[P] = fma(-F.kL * nv[P], JR, tv[P]);
+        tv[0] = fma(-F.kL * nv[0], JL, tv[0]);
+        eo<P, true>(F.eE[D], tv, r);
         r[P] += FR;
         r[0] -= FL;
+        if (!act) return;
+        double *pa = sacc + base;
+#pragma unroll
+        for (int i = 0; i < n; ++i) pa[i * SSD] = FIRST ? r[i] : pa[i * SSD] + r[i];
+        return;
     } else {
         const double c = a.nu_const * sd, ck = c * (0.5 * (P + 1) * (P + 1));
         const double d0 = rdot<P>(T, 0, v), dP = rdot<P>(T, P, v);
@@ -194,6 +211,7 @@ __device__ __forceinline__ void cpass_xy(const ApplyParams &a, const DevTab &T, 
         r[0] += fma(-ck, uL, 0.5 * sL);
     }
     if (!act) return;
+    const double W = sw[ta] * sw[tb] * g.wfac[D];
     double *pa = sacc + base;
 #pragma unroll
     for (int i = 0; i < n; ++i) pa[i * SSD] = FIRST ? W * r[i] : fma(W, r[i], pa[i * SSD]);
@@ -205,7 +223,7 @@ __device__ __forceinline__ void cpass_xy(const ApplyParams &a, const DevTab &T, 
 template <class K>
 __device__ __forceinline__ void cpass_z(const ApplyParams &a, const DevTab &T, const double *su, const double *snu,
                                         const double *sacc, const double *tz, double *zo, long long eb, int t,
-                                        bool zfirst, bool zlast, ZC6 &zc, double &epi0, double &epi1)
+                                        bool zfirst, bool zlast, ZC6 &zc, double &epi0, double &epi1, const double *sw)
 {
     constexpr int P = K::P, n = K::n, NN = K::NN, NPE = K::NPE, NCL = K::NCL, NV = K::NV, SE = K::SE;
     if (t >= NCL) return;
@@ -213,8 +231,8 @@ __device__ __forceinline__ void cpass_z(const ApplyParams &a, const DevTab &T, c
     const int slot = t / NN, tn = t - slot * NN;
     const int ta = tn % n, tb = tn / n;
     const int base = (slot & 3) * SE + (slot >> 2) * K::SY + ta + tb * n;
-    const double W = T.w[ta] * T.w[tb] * g.wfac[2];
-    const double sd = g.sd[2], htau = 0.5 * g.tau[2];
+    const double W = sw[ta] * sw[tb] * g.wfac[2];
+    const double sd = g.sd[2];
     double v[n], nv[n];
 #pragma unroll
     for (int i = 0; i < n; ++i) {
@@ -229,7 +247,7 @@ __device__ __forceinline__ void cpass_z(const ApplyParams &a, const DevTab &T, c
     } else {
         uL = zc.u;
         nuL = K::VARNU ? zc.nu : a.nu_const;
-        sL = nuL * sd * zc.gP;
+        sL = K::VARNU ? nuL * zc.gP : nuL * sd * zc.gP;  // VARNU: s~ = nu~ g (weight-folded)
     }
     if (zlast) {
         uR = tz[NV * NCL + t];
@@ -238,39 +256,42 @@ __device__ __forceinline__ void cpass_z(const ApplyParams &a, const DevTab &T, c
     }
     // release the previous brick's parked output: its top-face terms
     // dr_i = c D_{P,i} + [i == P] f0 with the face shared with our bottom
+    const double Wr = K::VARNU ? 1.0 : W;  // VARNU: c and f0 arrive W-weighted
     auto release = [&](double c, double f0) {
         double s1 = 0.0;
 #pragma unroll
         for (int i = 0; i < n; ++i) {
-            const double d = W * fma(c, T.D[P][i], i == P ? f0 : 0.0);
+            const double d = K::VARNU ? fma(c, T.D[P][i], i == P ? f0 : 0.0) : W * fma(c, T.D[P][i], i == P ? f0 : 0.0);
             zc.po[i * NN] = zo[i * NCL + t] + d;
             s1 += d;
         }
         if (K::MODE >= 1) {
-            epi0 = fma(W, fma(c, zc.gP, f0 * zc.u), epi0);
+            epi0 = fma(Wr, fma(c, zc.gP, f0 * zc.u), epi0);
             if (K::MODE != 3) epi1 += s1;
         }
         zc.held = false;
     };
     double r[n], gP;
     if (K::VARNU) {
-        double gg[n];
+        // weight-folded form (see cpass_xy): results are W-weighted, the parked output and
+        // its release too (release() takes W = 1)
+        const V6Fold &F = a.f6;
+        double gg[n], tv[n];
         eo<P, true>(T.eD, v, gg);
-        const double s0 = nv[0] * sd * gg[0], sP = nv[P] * sd * gg[P];
+#pragma unroll
+        for (int k = 0; k < n; ++k) tv[k] = nv[k] * gg[k];
+        const double s0 = tv[0], sP = tv[P];
         const double JL = uL - v[0];
-        const double FL = fma(htau * (nuL + nv[0]), JL, -0.5 * (sL + s0));
+        const double FL = fma(F.kF[2] * (nuL + nv[0]), JL, -F.kS[2] * (sL + s0));
         double JR = 0.0, FR = 0.0;
         if (zlast) {
             JR = v[P] - uR;
-            FR = fma(htau * (nv[P] + nuR), JR, -0.5 * (sP + sR));
+            FR = fma(F.kF[2] * (nv[P] + nuR), JR, -F.kS[2] * (sP + sR));
         }
-        if (!zfirst && zc.held) release(-0.5 * sd * zc.nu * JL, FL);
-        double tv[n];
-#pragma unroll
-        for (int k = 0; k < n; ++k) tv[k] = g.wsd[2][k] * (nv[k] * gg[k]);
-        tv[P] = fma(-0.5 * sd * nv[P], JR, tv[P]);
-        tv[0] = fma(-0.5 * sd * nv[0], JL, tv[0]);
-        eo<P, true>(T.eE, tv, r);
+        if (!zfirst && zc.held) release(-F.kCL[2] * zc.nu * JL, FL);
+        tv[P] = fma(-F.kL * nv[P], JR, tv[P]);
+        tv[0] = fma(-F.kL * nv[0], JL, tv[0]);
+        eo<P, true>(F.eE[2], tv, r);
         r[P] += FR;
         r[0] -= FL;
         gP = gg[P];
@@ -294,7 +315,7 @@ __device__ __forceinline__ void cpass_z(const ApplyParams &a, const DevTab &T, c
     const double *pa = sacc + base;
 #pragma unroll
     for (int i = 0; i < n; ++i) {
-        const double o = fma(lw * T.w[i], v[i], fma(W, r[i], pa[i * NN]));
+        const double o = fma(lw * T.w[i], v[i], K::VARNU ? r[i] + pa[i * NN] : fma(W, r[i], pa[i * NN]));
         if (zlast) po[i * NN] = o;
         else zo[i * NCL + t] = o;
         if (K::MODE >= 1) {
@@ -316,7 +337,7 @@ __device__ __forceinline__ void cpass_z(const ApplyParams &a, const DevTab &T, c
 // ---------------------------------------------------------------------------
 template <class K, int K0, int K1>
 __device__ __forceinline__ void ptraces_xy(const ApplyParams &a, const DevTab &T, double *tr, const int (&e0)[3],
-                                           long long eb, int ptid, double beta)
+                                           long long eb, int ptid, double beta, const double *sw)
 {
     constexpr int P = K::P, n = K::n, NN = K::NN, NPE = K::NPE, LR = K::LR, NV = K::NV, KT = K1 - K0;
     const Geom &g = a.g;
@@ -368,15 +389,21 @@ __device__ __forceinline__ void ptraces_xy(const ApplyParams &a, const DevTab &T
         const double dd = rdot<P>(T, 0, v[k]);  // v[0] is the face node (see v5::ptraces)
         double *trd = tr + D * 2 * NV * LR + side * NV * LR;
         trd[L] = v[k][0];
-        trd[LR + L] = nuf[k] * g.sd[D] * (side ? dd : -dd);
-        if (K::VARNU) trd[2 * LR + L] = nuf[k];
+        if (K::VARNU) {  // weight-folded: nu~ = nu w_a w_b w_0, s~ = nu~ (D v)_face (reference derivative)
+            const int tn = L % NN;
+            const double nw = nuf[k] * (sw[tn % n] * sw[tn / n] * sw[0]);
+            trd[LR + L] = nw * (side ? dd : -dd);
+            trd[2 * LR + L] = nw;
+        } else {
+            trd[LR + L] = nuf[k] * g.sd[D] * (side ? dd : -dd);
+        }
     }
 }
 
 // z traces at column-segment ends (global memory; halo layers for multi-rank slabs)
 template <class K>
 __device__ __noinline__ void ptraces_z(const ApplyParams &a, const DevTab &T, double *tz, const int (&e0)[3], int ptid,
-                                       double beta, int side)
+                                       double beta, int side, const double *sw)
 {
     constexpr int P = K::P, n = K::n, NN = K::NN, NPE = K::NPE, NCL = K::NCL, NV = K::NV;
     const Geom &g = a.g;
@@ -404,8 +431,13 @@ __device__ __noinline__ void ptraces_z(const ApplyParams &a, const DevTab &T, do
         const double dd = rdot<P>(T, 0, v);
         double *t0 = tz + side * NV * NCL;
         t0[t] = v[0];
-        t0[NCL + t] = nuf * g.sd[2] * (side ? dd : -dd);
-        if (K::VARNU) t0[2 * NCL + t] = nuf;
+        if (K::VARNU) {  // weight-folded (see ptraces_xy)
+            const double nw = nuf * (sw[ta] * sw[tb] * sw[0]);
+            t0[NCL + t] = nw * (side ? dd : -dd);
+            t0[2 * NCL + t] = nw;
+        } else {
+            t0[NCL + t] = nuf * g.sd[2] * (side ? dd : -dd);
+        }
     }
 }
 
@@ -419,7 +451,9 @@ __global__ void __launch_bounds__((KC6<P, VARNU, MODE>::NT)) __maxnreg__((KC6<P,
     const DevTab &T = c_tab[P];
     extern __shared__ __align__(16) double sm[];
     uint64_t *bar = reinterpret_cast<uint64_t *>(sm + K::OFF_BAR);  // full[0..1], empty[0..1]
+    double *sw = sm + K::OFF_W;
     const int tid = threadIdx.x;
+    if (tid < K::n) sw[tid] = T.w[tid];
     if (MODE >= 1 && *a.pro.done) return;  // PCG converged: nothing to do
     const double beta = MODE == 1 ? *a.pro.beta : 0.0;
     if (tid == 0) {
@@ -517,15 +551,15 @@ __global__ void __launch_bounds__((KC6<P, VARNU, MODE>::NT)) __maxnreg__((KC6<P,
                 // x/y traces (warps 1-3) in rounds of at most 3 lines per thread (register budget)
                 if (ptid >= 32) {
                     constexpr int R = MODE == 1 ? 2 : 3;  // lines in flight per thread (two loads each in MODE 1)
-                    ptraces_xy<K, 0, (K::KT < R ? K::KT : R)>(a, T, tr, e0, eb, ptid - 32, beta);
+                    ptraces_xy<K, 0, (K::KT < R ? K::KT : R)>(a, T, tr, e0, eb, ptid - 32, beta, sw);
                     if (ptid == 32) V5_ACC(9, tx);
                     V5_T0(ty);
-                    if constexpr (K::KT > R) ptraces_xy<K, R, (K::KT < 2 * R ? K::KT : 2 * R)>(a, T, tr, e0, eb, ptid - 32, beta);
-                    if constexpr (K::KT > 2 * R) ptraces_xy<K, 2 * R, K::KT>(a, T, tr, e0, eb, ptid - 32, beta);
+                    if constexpr (K::KT > R) ptraces_xy<K, R, (K::KT < 2 * R ? K::KT : 2 * R)>(a, T, tr, e0, eb, ptid - 32, beta, sw);
+                    if constexpr (K::KT > 2 * R) ptraces_xy<K, 2 * R, K::KT>(a, T, tr, e0, eb, ptid - 32, beta, sw);
                     if (ptid == 32) V5_ACC(10, ty);
                 }
-                if (j == 0) ptraces_z<K>(a, T, sm + K::OFF_TZ, e0, ptid, beta, 0);
-                if (j == seglen - 1) ptraces_z<K>(a, T, sm + K::OFF_TZ, e0, ptid, beta, 1);
+                if (j == 0) ptraces_z<K>(a, T, sm + K::OFF_TZ, e0, ptid, beta, 0, sw);
+                if (j == seglen - 1) ptraces_z<K>(a, T, sm + K::OFF_TZ, e0, ptid, beta, 1, sw);
                 if (ptid == 0) V5_ACC(3, tx);
                 mbar_arrive(&bar[buf]);
             }
@@ -546,22 +580,22 @@ __global__ void __launch_bounds__((KC6<P, VARNU, MODE>::NT)) __maxnreg__((KC6<P,
         for (int j = 0; j < seglen; ++j, ++it, ++e0[2]) {
             const int buf = it & 1;
             const double *su = sm + K::OFF_U + buf * BRK;
-            const double *snu = sm + K::OFF_NU + buf * BRK;
+            double *snu = sm + K::OFF_NU + buf * BRK;
             const double *tr = sm + K::OFF_TR + buf * K::TRXY;
             const long long eb = e0[0] + s1 * e0[1] + s2 * e0[2];
             V5_T0(tw);
             mbar_wait(&bar[buf], (it >> 1) & 1);
             if (tid == 0) V5_ACC(0, tw);
             V5_T0(tp);
-            cpass_xy<K, 0, true>(a, T, su, snu, sacc, tr, tid);
+            cpass_xy<K, 0, true>(a, T, su, snu, sacc, tr, tid, sw);
             if (tid == 0) V5_ACC(6, tp);
             named_sync(1, NC);
             V5_T0(t1);
-            cpass_xy<K, 1, false>(a, T, su, snu, sacc, tr, tid);
+            cpass_xy<K, 1, false>(a, T, su, snu, sacc, tr, tid, sw);
             if (tid == 0) V5_ACC(7, t1);
             named_sync(1, NC);
             V5_T0(t2);
-            cpass_z<K>(a, T, su, snu, sacc, tz, zo, eb, tid, j == 0, j == seglen - 1, zc, epi0, epi1);
+            cpass_z<K>(a, T, su, snu, sacc, tz, zo, eb, tid, j == 0, j == seglen - 1, zc, epi0, epi1, sw);
             if (tid == 0) V5_ACC(8, t2);
             mbar_arrive(&bar[2 + buf]);
             named_sync(1, NC);  // ACC and the parked outputs are rewritten by the next brick

@@ -172,7 +172,10 @@ struct dg_mesh {
     double *d_swF = nullptr, *rc_el = nullptr, *chat = nullptr, *xc = nullptr, *rc = nullptr;
     double sw_nu = -1.0;
     bool sw_coarse_on = true;
-    double dinv_lam = -1.0, dinv_nu = -1.0;  // (lam, nu_const) the dinv workspace holds (constant nu)
+    // D^-1 cache: `dinv` is reserved for the Jacobi preconditioner and written only by
+    // pcg_impl; (dinv_lam, dinv_nu) name the constant-nu operator it holds (-1: invalid).  Any
+    // other writer of `dinv` (or a stream change) must reset both to -1.
+    double dinv_lam = -1.0, dinv_nu = -1.0;
 };
 
 #define CK(call)                                                                                         \
@@ -193,8 +196,6 @@ namespace {
 
 long long nbricks(const Geom &g) { return (long long)g.nbk[0] * g.nbk[1] * g.nbk[2]; }
 
-constexpr int APPLY_GRID_MAX = 148 * 8;
-
 dg_status alloc(void **p, size_t bytes)
 {
     if (cudaMalloc(p, bytes) != cudaSuccess) {
@@ -210,26 +211,28 @@ dg_status alloc(void **p, size_t bytes)
         if (_s != DG_OK) return _s;   \
     } while (0)
 
-dg_status ensure_workspace(dg_mesh *m)
+// PCG workspace (x, r, p_a, p_b, q, z, D^-1 and the alpha/beta history): allocated once by
+// dg_mesh_create, so dg_pcg_solve never allocates.  All-or-nothing: on a partial failure
+// every buffer is released again and nulled (the mesh creation then fails).
+dg_status alloc_workspace(dg_mesh *m)
 {
-    if (m->r) return DG_OK;
     const size_t b = sizeof(double) * (size_t)m->ndof;
-    CKS(alloc((void **)&m->r, b));
-    CKS(alloc((void **)&m->q, b));
-    CKS(alloc((void **)&m->pa, b));
-    CKS(alloc((void **)&m->pb, b));
-    CKS(alloc((void **)&m->dinv, b));
-    CKS(alloc((void **)&m->z, b));
+    double **bufs[] = {&m->r, &m->q, &m->pa, &m->pb, &m->dinv, &m->z};
+    dg_status s = DG_OK;
+    for (double **p : bufs)
+        if ((s = alloc((void **)p, b)) != DG_OK) break;
+    if (s == DG_OK) s = alloc((void **)&m->hist, sizeof(double) * 2 * (size_t)PCG_HIST_CAP);
+    if (s != DG_OK) {
+        for (double **p : bufs) {
+            if (*p) cudaFree(*p);
+            *p = nullptr;
+        }
+        if (m->hist) cudaFree(m->hist);
+        m->hist = nullptr;
+        return s;
+    }
+    m->hist_cap = PCG_HIST_CAP;
     return DG_OK;
-}
-
-dg_status ensure_hist(dg_mesh *m, int maxit)
-{
-    if (m->hist_cap >= maxit + 2) return DG_OK;
-    if (m->hist) cudaFree(m->hist);
-    m->hist = nullptr;
-    m->hist_cap = maxit + 2;
-    return alloc((void **)&m->hist, sizeof(double) * 2 * (size_t)m->hist_cap);
 }
 
 dg_status ensure_halos(dg_mesh *m, bool vel)
@@ -494,8 +497,6 @@ dg_status sw_pcg_step(dg_mesh *m, double lam, int mode, int fin)
 dg_status pcg_impl(dg_mesh *m, double lam, const double *nu, double nu_const, const double *f, double tol,
                    int maxit, double *u, dg_solve_info *info)
 {
-    CKS(ensure_workspace(m));
-    CKS(ensure_hist(m, maxit));
     const Geom &g = m->g;
     const int VG = vec_grid();
     const bool multi = m->nranks > 1;
@@ -506,6 +507,7 @@ dg_status pcg_impl(dg_mesh *m, double lam, const double *nu, double nu_const, co
     s0.tol2 = tol * tol;
     s0.ndof_global = m->ndof_global;
     s0.maxit = maxit;
+    s0.hist_cap = m->hist_cap;
     s0.nu_eff = nu ? 1.0 : nu_const;
     CK(cudaMemcpyAsync(m->scal, &s0, sizeof(s0), cudaMemcpyHostToDevice, m->st));
 
@@ -592,10 +594,10 @@ dg_status pcg_impl(dg_mesh *m, double lam, const double *nu, double nu_const, co
     // split PCG step (pupd kernel + apply with the dot epilogue) where the v6 apply runs:
     // measured faster than the fused prologue of v5
     const bool split_ok = !multi && g.dim == 3 && apply3_split_pcg_ok(g, nu);
-    const bool split = !sw && split_ok && !getenv("DG_PCG_FUSED");
+    const bool split = !sw && split_ok && !DG_DEV_ENV("DG_PCG_FUSED");
     // constant nu on the uniform periodic mesh (N_d >= 2: the closed-form diagonal): the first
     // element's D^-1 serves every element
-    const bool table = split && !nu && !self && !getenv("DG_PCG_NOTABLE");
+    const bool table = split && !nu && !self && !DG_DEV_ENV("DG_PCG_NOTABLE");
     // iterations are enqueued in chunks between host convergence checks; after the first chunk
     // the next one is sized from the observed residual reduction per iteration (launches past
     // convergence exit at their first instruction but still cost a few microseconds each)
@@ -731,9 +733,10 @@ dg_status pcg_impl(dg_mesh *m, double lam, const double *nu, double nu_const, co
         info->f_norm = std::sqrt(hs.fnorm2);
         info->kappa_est = NAN;
         if (hs.iter >= 2) {
-            std::vector<double> hh(2 * (size_t)hs.iter);
+            const int k = std::min(hs.iter, m->hist_cap);
+            std::vector<double> hh(2 * (size_t)k);
             CK(cudaMemcpy(hh.data(), m->hist, sizeof(double) * hh.size(), cudaMemcpyDeviceToHost));
-            info->kappa_est = lanczos_kappa(hh.data(), hs.iter);
+            info->kappa_est = lanczos_kappa(hh.data(), k);
         }
     }
     if (hs.status == PCG_ST_BREAKDOWN) return set_error(DG_EBREAKDOWN, "PCG breakdown (p.Ap <= 0 or non-finite)");
@@ -890,8 +893,13 @@ dg_status dg_mesh_create(int dim, const int N[3], const double L[3], int P, int 
             done.push_back(m->device);
         }
     }
-    const int pcap = 2 * (std::max(APPLY_GRID_MAX, std::max(vec_grid(), 148 * 12)) + SW_NCMAX * SW_NCMAX / 32) + 64;
+    // block-partial capacity: every persistent / reduction grid is at most 16 resident CTAs per SM
+    // (the apply grids at most 8, the vector reductions 6-8), plus the coarse-solve slots
+    int nsm = 148;
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, m->device);
+    const int pcap = 2 * (std::max(nsm, 148) * 16 + SW_NCMAX * SW_NCMAX / 32) + 64;
     dg_status s;
+    if ((s = alloc_workspace(m)) != DG_OK) return fail(s);
     if ((s = alloc((void **)&m->partial, sizeof(double) * pcap)) != DG_OK) return fail(s);
     m->partial_cap = pcap;
     if ((s = alloc((void **)&m->sums, sizeof(double) * 8)) != DG_OK) return fail(s);
@@ -952,6 +960,11 @@ void dg_mesh_destroy(dg_mesh *m)
 dg_status dg_mesh_set_stream(dg_mesh *m, void *cuda_stream)
 {
     if (!m) return set_error(DG_EINVAL, "null mesh");
+    if (m->st != (cudaStream_t)cuda_stream) {
+        // work on the old stream must finish before the new one may overwrite the cached D^-1
+        if (m->st) cudaStreamSynchronize(m->st);
+        m->dinv_lam = m->dinv_nu = -1.0;
+    }
     m->st = (cudaStream_t)cuda_stream;
     return DG_OK;
 }

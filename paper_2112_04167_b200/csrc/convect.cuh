@@ -592,7 +592,7 @@ struct ConvDispatch {
     static cudaError_t go(const ConvParams &a, cudaStream_t st)
     {
         if constexpr (DIM == 3 && C3Cfg<P>::SMEM <= 227 * 1024) {
-            static const bool v1 = getenv("DG_CONVECT_V1") != nullptr;
+            static const bool v1 = DG_DEV_ENV("DG_CONVECT_V1") != nullptr;
             if (!v1) {
                 constexpr int smem3 = C3Cfg<P>::SMEM;
                 static int resident = 0;  // persistent: one full wave of CTAs

@@ -9,6 +9,15 @@
 
 #include "dg.h"
 
+// Development switches (A/B measurements quoted in DESIGN.md) exist only in builds with
+// -DDG_DEVELOPMENT (DG_EXTRA_DEFS=-DDG_DEVELOPMENT python paper_2112_04167_b200/build.py);
+// the default build reads no environment variable on the product path.
+#ifdef DG_DEVELOPMENT
+#define DG_DEV_ENV(name) getenv(name)
+#else
+#define DG_DEV_ENV(name) ((const char *)nullptr)
+#endif
+
 namespace dg {
 
 constexpr int PMAX = 10;         // highest compiled degree
@@ -94,6 +103,17 @@ struct PProl {
     const int *done = nullptr;     // device flag: skip all work when set
 };                                 // (single-rank only; multi-rank runs the unfused path)
 
+// Weight-folded constants of the v6 variable-nu apply (apply6.cuh): the staged
+// viscosity is nu~ = nu w_i w_j w_k, so every transverse weight W = w_a w_b wfac_d and the
+// derivative factor 2/h_d fold into per-direction constants and one scaled D^T table.
+struct V6Fold {
+    EOTab eE[3];      // C_d D^T (even-odd form), C_d = wfac_d (2/h_d)
+    double kF[3];     // tau_d wfac_d / (2 w_0):      W sigma (nu- + nu+)  = kF (nu~- + nu~+)
+    double kS[3];     // wfac_d (2/h_d) / (2 w_0):    W (s- + s+) / 2     = kS (s~- + s~+)
+    double kL;        // 1 / (2 w_0):                  lifting coefficient of nu~ (before C_d D^T)
+    double kCL[3];    // C_d kL
+};
+
 struct ApplyParams {
     Geom g;
     double lam, nu_const;
@@ -104,6 +124,7 @@ struct ApplyParams {
     PProl pro;
     long long b0, b1;   // brick range [b0, b1)
     int seglen = 1, nseg = 1;  // column segments along the slowest direction (apply kernel)
+    V6Fold f6;                 // filled by the v6 dispatch (variable nu)
     int zlo = 0, zhi = -1;     // element layers [zlo, zhi) of the slowest direction to apply
                                // (3-D v5 kernel only; -1 = all), for the pipelined host call
 };
@@ -174,7 +195,9 @@ struct PcgScal {                 // device-resident scalars of one solve
     double lam;
     long long ndof_global;
     int iter, done, status, maxit;
+    int hist_cap;                  // alpha/beta history capacity (iterations), fixed at mesh creation
 };
+constexpr int PCG_HIST_CAP = 8192;
 enum { PCG_ST_RUN = 0, PCG_ST_CONV = 1, PCG_ST_MAXIT = 2, PCG_ST_BREAKDOWN = 3 };
 
 cudaError_t launch_abssum(const Geom &g, const double *u, double *partial, cudaStream_t st);

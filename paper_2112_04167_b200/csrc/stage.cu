@@ -633,6 +633,17 @@ cudaError_t dg2_launch(const Geom &g, const DivGradParams &a, cudaStream_t st)
     return cudaGetLastError();
 }
 
+#ifdef DG_DEVELOPMENT  // first-generation one-CTA-per-element kernels (A/B measurements only)
+#define DG_DIVGRAD_V1_CASE(p)                                                                              \
+    if (DG_DEV_ENV("DG_DIVGRAD_V1")) {                                                                     \
+        if (DIV) k_dg_div<DIM, p><<<(int)blocks, 256, 0, st>>>(g, a);                                     \
+        else k_dg_grad<DIM, p><<<(int)blocks, 256, 0, st>>>(g, a);                                        \
+        return cudaGetLastError();                                                                         \
+    }
+#else
+#define DG_DIVGRAD_V1_CASE(p)
+#endif
+
 template <int DIM, bool DIV>
 cudaError_t dg_dispatch(const Geom &g, const DivGradParams &a, cudaStream_t st)
 {
@@ -641,10 +652,8 @@ cudaError_t dg_dispatch(const Geom &g, const DivGradParams &a, cudaStream_t st)
 #define DG_CASE(p)                                                                                         \
     case p:                                                                                                \
         if constexpr (DG_HAS_P(p) && (DIM == 2 || 3 * (p + 1) * (p + 1) * (p + 1) * 8 <= 40 * 1024)) {     \
-            if (!getenv("DG_DIVGRAD_V1")) return dg2_launch<DIM, DIV, p>(g, a, st);                        \
-            if (DIV) k_dg_div<DIM, p><<<(int)blocks, 256, 0, st>>>(g, a);                                 \
-            else k_dg_grad<DIM, p><<<(int)blocks, 256, 0, st>>>(g, a);                                    \
-            return cudaGetLastError();                                                                     \
+            DG_DIVGRAD_V1_CASE(p)                                                                          \
+            return dg2_launch<DIM, DIV, p>(g, a, st);                                                      \
         } else {                                                                                           \
             return cudaErrorNotSupported;                                                                  \
         }

@@ -302,8 +302,10 @@ __device__ void finalize(int mode, const double *sums, PcgScal *s, double *hist,
         if (s->done) return;
         const double rz_new = sums[0];
         s->beta = rz_new / s->rz;
-        hist[2 * s->iter + 0] = s->alpha;
-        hist[2 * s->iter + 1] = s->beta;
+        if (s->iter < s->hist_cap) {  // Lanczos history of the first hist_cap iterations
+            hist[2 * s->iter + 0] = s->alpha;
+            hist[2 * s->iter + 1] = s->beta;
+        }
         s->rz = rz_new;
         s->res2 = sums[1];
         s->iter += 1;

@@ -65,10 +65,9 @@ def lagrange_np(nodes, j):
     return p / p(nodes[j])
 
 
-@pytest.mark.parametrize("P", [2, 3])
-def test_polynomial_exactness_3d(P):
-    """Interior element, v in Q_P globally continuous: LLF dissipation vanishes ([v] = 0) and
-    Gauss Q = floor(3P/2)+1 integrates (v v) . grad phi exactly, so M F_c = int -div(v v_c) phi_I."""
+def _poly_exactness_err(P, Q=None):
+    """max_c |M F_c - int -div(v v_c) phi_I| / max |ref| on the interior element of a 3^3 mesh
+    for a globally continuous v in Q_P (oracle with Q Gauss points per direction)."""
     N = 3
     L = [1.0, 1.2, 0.9]
     m = oracle.Mesh(3, (N, N, N), L, P)
@@ -87,7 +86,7 @@ def test_polynomial_exactness_3d(P):
 
     v = [val(c, X[0], X[1], X[2]) for c in range(3)]
     e = 1 + N * (1 + N * 1)  # the interior element (1,1,1)
-    out = oracle.convect(m, v, elems=[e])
+    out = oracle.convect(m, v, elems=[e], Q=Q)
     mass = oracle.mass(m)[e]
     xi, _ = oracle.gll(P)
     basis = [lagrange_np(xi, j) for j in range(P + 1)]
@@ -105,6 +104,7 @@ def test_polynomial_exactness_3d(P):
         return fs[0](x - cen[0]) * fs[1](y - cen[1]) * fs[2](z - cen[2])
 
     V = [val(c, Xg, Yg, Zg) for c in range(3)]
+    worst = 0.0
     for c in range(3):
         g = np.zeros_like(Xg)
         for d in range(3):  # -d_d(v_d v_c)
@@ -116,7 +116,73 @@ def test_polynomial_exactness_3d(P):
                     phi = (basis[i](zg)[:, None, None] * basis[j](zg)[None, :, None] * basis[k](zg)[None, None, :])
                     ref[i + (P + 1) * (j + (P + 1) * k)] = np.sum(Wg * g * phi)
         got = mass * out[c][0]
-        assert np.abs(got - ref).max() < 1e-12 * np.abs(ref).max(), c
+        worst = max(worst, np.abs(got - ref).max() / np.abs(ref).max())
+    return worst
+
+
+@pytest.mark.parametrize("P", [2, 3])
+def test_polynomial_exactness_3d(P):
+    """Interior element, v in Q_P globally continuous: LLF dissipation vanishes ([v] = 0) and
+    Gauss Q = floor(3P/2)+1 integrates (v v) . grad phi exactly, so M F_c = int -div(v v_c) phi_I."""
+    assert _poly_exactness_err(P) < 1e-12
+
+
+@pytest.mark.parametrize("P", [2, 3, 4])
+def test_gauss_count_is_the_smallest_exact_rule(P):
+    """Reading A13 pinned as 'consistent integration' = the smallest exact Gauss rule: the
+    integrands (v v_c) d_e phi (degree 3P-1 along e, 3P across) and (v.n) v_c phi on faces
+    (degree 3P) need 2Q - 1 >= 3P.  The oracle's default Q = floor(3P/2)+1 is exact, one
+    point more changes nothing beyond rounding, one point fewer is not exact."""
+    Q = (3 * P) // 2 + 1
+    assert 2 * Q - 1 >= 3 * P > 2 * (Q - 1) - 1
+    assert _poly_exactness_err(P) < 1e-12
+    assert _poly_exactness_err(P, Q=Q) < 1e-12
+    assert _poly_exactness_err(P, Q=Q + 1) < 1e-12
+    assert _poly_exactness_err(P, Q=Q - 1) > 1e-8
+
+
+@pytest.mark.parametrize("P,seed", [(2, 1), (3, 2), (4, 3)])
+def test_llf_flux_constant_states(P, seed):
+    """Reading A12 pinned on a two-element mesh (N = (2,1,1)) with constant, different states
+    v^0, v^1: every face integrand is then constant, so the node at the middle of element 0's
+    +x face gives the numerical flux exactly, h_c = f_c(v^0) - F_c,I w_P h/2 (the volume term
+    integrates to f(v^0) times the face moment of phi_I and the face term subtracts h times the
+    same moment).  Compared with the local Lax-Friedrichs flux of f(v) = (v.n) v written from
+    its definition: 1/2 (f^- + f^+) + 1/2 Lambda (v^- - v^+), Lambda = the larger spectral
+    radius of the flux Jacobian J = (v.n) I + v n^T on the two sides (numpy.linalg.eigvals)."""
+    rng = np.random.default_rng(seed)
+    L = [1.3, 0.8, 1.1]
+    m = oracle.Mesh(3, (2, 1, 1), L, P)
+    v0, v1 = rng.uniform(-1, 1, 3), rng.uniform(-1, 1, 3)
+    v0[0], v1[0] = 0.35, -0.9   # |v.n| differs on the two sides (tests the max)
+    v = [np.concatenate([np.full(m.npe, v0[c]), np.full(m.npe, v1[c])]) for c in range(3)]
+    out = oracle.convect(m, v)
+    n_ = np.array([1.0, 0.0, 0.0])
+
+    def f(w):
+        return np.dot(w, n_) * w
+
+    def rho(w):
+        J = np.dot(w, n_) * np.eye(3) + np.outer(w, n_)
+        return np.abs(np.linalg.eigvals(J)).max()
+
+    lam = max(rho(v0), rho(v1))
+    h_ref = 0.5 * (f(v0) + f(v1)) + 0.5 * lam * (v0 - v1)     # face +x of element 0: '-' = v0
+    h_ref_w = 0.5 * (f(v1) + f(v0)) + 0.5 * lam * (v1 - v0)   # face -x of element 0: '-' = v1
+    _, w = oracle.gll(P)
+    hx = L[0] / 2
+    mid = P // 2
+    I_p = P + (P + 1) * (mid + (P + 1) * mid)   # node (P, mid, mid) of element 0
+    I_m = 0 + (P + 1) * (mid + (P + 1) * mid)   # node (0, mid, mid)
+    for c in range(3):
+        h_got = f(v0)[c] - out[c][0, I_p] * w[P] * hx / 2
+        assert abs(h_got - h_ref[c]) < 1e-13 * (1 + abs(h_ref[c])), (c, h_got, h_ref[c])
+        # -x face of element 0 (outward normal -x): M F = (h(v1, v0) - f(v0)) * moment
+        h_got_w = f(v0)[c] + out[c][0, I_m] * w[0] * hx / 2
+        assert abs(h_got_w - h_ref_w[c]) < 1e-13 * (1 + abs(h_ref_w[c])), (c, h_got_w, h_ref_w[c])
+    # a dissipation constant without the factor 2 (max |v.n|) would miss by
+    # 1/2 max|v.n| |v0 - v1| -- far outside the tolerance above
+    assert 0.5 * max(abs(v0[0]), abs(v1[0])) * np.abs(v0 - v1).max() > 1e-3
 
 
 def test_taylor_green_limit_2d():
