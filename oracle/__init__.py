@@ -380,6 +380,14 @@ def dg_gradient_weak(mp: Mesh, psi):
 # Tableaux typed from the paper's appendix, independently of the product's.
 # ---------------------------------------------------------------------------
 ORACLE_TABLEAUX = {
+    "RK-TR": dict(
+        a_im=[[0, 0, 0], [0, 1, 0], [1 / 2, 0, 1 / 2]],
+        a_ex=[[0, 0, 0], [1, 0, 0], [1 / 2, 1 / 2, 0]],
+        b_im=[1 / 2, 0, 1 / 2], b_ex=[1 / 2, 1 / 2, 0]),
+    "RK-CB2": dict(
+        a_im=[[0, 0, 0], [0, 2 / 5, 0], [0, 5 / 6, 1 / 6]],
+        a_ex=[[0, 0, 0], [2 / 5, 0, 0], [0, 1, 0]],
+        b_im=[0, 5 / 6, 1 / 6], b_ex=[0, 5 / 6, 1 / 6]),
     "RK-CB3e": dict(  # implicit (left), explicit (right)
         a_im=[[0, 0, 0, 0], [0, 1 / 3, 0, 0], [0, 1 / 2, 1 / 2, 0], [0, 3 / 4, -1 / 4, 1 / 2]],
         a_ex=[[0, 0, 0, 0], [1 / 3, 0, 0, 0], [0, 1, 0, 0], [0, 3 / 4, 1 / 4, 0]],

@@ -178,3 +178,38 @@ def test_rk_step_shear_mode_is_the_dirk_stability_function(name, z):
     # a wrong tableau entry or sign moves the result by O(|z| 1e-1)
     assert np.abs(out[0] - R * ev).max() <= 1e-7
     assert np.abs(out[1]).max() <= 1e-7
+
+
+ORDER = {"RK-TR": 2, "RK-CB2": 2, "RK-CB3e": 3, "RK-ARS3": 3}
+
+
+def imex_order_defects(t, order):
+    """Defects of the IMEX Runge-Kutta order conditions up to `order` (coupled conditions of
+    the additive/partitioned RK theory): sum b = 1; b.c = 1/2; b.c^2 = 1/3 and b.A.c = 1/6 for
+    every pairing of b in {b_im, b_ex} with A in {A_im, A_ex}; and the shared abscissae
+    A_im 1 = A_ex 1 = c."""
+    Ai, Ae = np.asarray(t["a_im"], float), np.asarray(t["a_ex"], float)
+    bi, be = np.asarray(t["b_im"], float), np.asarray(t["b_ex"], float)
+    c = Ae.sum(1)
+    d = [np.abs(Ai.sum(1) - c).max()]
+    for b in (bi, be):
+        d += [b.sum() - 1.0, b @ c - 0.5]
+        if order >= 3:
+            d += [b @ c ** 2 - 1.0 / 3.0] + [b @ A @ c - 1.0 / 6.0 for A in (Ai, Ae)]
+    return np.abs(np.array(d))
+
+
+@pytest.mark.parametrize("name", sorted(ORDER))
+def test_oracle_tableaux_order_conditions(name):
+    """Every tableau typed from the paper's appendix satisfies the IMEX order
+    conditions of its stated order, and every single non-zero explicit or implicit entry is
+    pinned: perturbing it by 1e-3 violates at least one condition."""
+    t = oracle.ORACLE_TABLEAUX[name]
+    k = ORDER[name]
+    assert imex_order_defects(t, k).max() < 1e-14
+    for key in ("a_ex", "a_im"):
+        A = np.asarray(t[key], float)
+        for i, j in zip(*np.nonzero(A)):
+            tp = {kk: np.array(v, float) for kk, v in t.items()}
+            tp[key][i, j] += 1e-3
+            assert imex_order_defects(tp, k).max() > 1e-4, (key, i, j)
