@@ -77,9 +77,20 @@ typedef struct {
 dg_status dg_nccl_unique_id(unsigned char out[128]);
 
 /* Create a mesh: GLL tables for degree P, periodic
- * structured connectivity, the slab of rank `rank` out of `nranks`, and all workspace.
+ * structured connectivity, the slab of rank `rank` out of `nranks`, and all workspace
+ * (PCG vectors, reduction scratch, halo buffers, NCCL communicator and exchange stream:
+ * the hot calls never allocate).
  * dim in {2,3}; N[d] >= 1; L[d] > 0; 1 <= P <= 10; N[dim-1] % nranks == 0.
- * nccl_uid: NULL when nranks == 1.  cuda_stream: a cudaStream_t (may be NULL).
+ * nccl_uid: required when nranks > 1.  With nranks == 1, NULL gives the plain single-GPU
+ * mesh (the slab wraps onto itself); a non-NULL id selects the HALO MODE: a 1-rank NCCL
+ * communicator, and every slab-boundary face of the slowest direction goes through the same
+ * face-trace exchange (self send/recv) and halo-consuming kernels as a multi-rank slab -- the
+ * multi-GPU data plane, testable on one GPU (SURVEY.md:311; results equal the plain mesh's).
+ * Face-trace halo (operator apply, diagonal, PCG): per face node of the neighbour's boundary
+ * layer, u, nu d_n u and nu (nu once per solve), exchanged on a separate stream while the
+ * interior element layers are applied; the once-per-stage kernels (convection,
+ * DG pair, DG derivative) exchange the boundary element layers.
+ * cuda_stream: a cudaStream_t (may be NULL).
  * The caller must have selected the device (cudaSetDevice) before the call.  */
 dg_status dg_mesh_create(int dim, const int N[3], const double L[3], int P, int rank, int nranks,
                          const unsigned char *nccl_uid, void *cuda_stream, dg_mesh **out);

@@ -231,10 +231,14 @@ def dg_nccl_unique_id() -> bytes:
     return buf.raw
 
 
-def dg_mesh_create(dim, N, L, P, rank=0, nranks=1, nccl_uid=None, stream=None) -> Mesh:
+def dg_mesh_create(dim, N, L, P, rank=0, nranks=1, nccl_uid=None, stream=None, halo_mode=False) -> Mesh:
+    """halo_mode (one rank): route the slab-boundary faces through the NCCL face-trace exchange
+    (a 1-rank communicator, self send/recv) instead of the local periodic wrap (dg.h)."""
     N3 = (list(N) + [1, 1, 1])[:3]
     L3 = (list(L) + [1.0, 1.0, 1.0])[:3]
     h = _vp()
+    if halo_mode and nccl_uid is None:
+        nccl_uid = dg_nccl_unique_id()
     uid = None if nccl_uid is None else bytes(nccl_uid)
     _check(_c["dg_mesh_create"](int(dim), (_i * 3)(*N3), (_d * 3)(*L3), int(P), int(rank), int(nranks), uid,
                                 _stream_ptr(stream), ctypes.byref(h)))

@@ -145,8 +145,7 @@ __global__ void __launch_bounds__(256) k_diag_cf(const Geom g, double lam, const
                     int cn[3] = {ec[0], ec[1], ec[2]};
                     cn[D] += (i == P) ? 1 : -1;
                     const double nown = VARNU ? snu[q] : nu_const;
-                    const double nnb = VARNU ? __ldg(elem_ptr(g, nu, halo.nu_lo, halo.nu_hi, cn[0], cn[1], cn[2]) + goff +
-                                                      (i == P ? 0 : P * GS))
+                    const double nnb = VARNU ? nbr_face_nu(g, nu, halo, n, cn, D, goff, i == P ? 0 : P * GS)
                                              : nu_const;
                     acc += (i == P ? -1.0 : 1.0) * nown * sd * sdd[i] + 0.5 * g.tau[D] * (nown + nnb);
                 }
@@ -207,8 +206,7 @@ __global__ void __launch_bounds__(256) k_diag_cf2(const Geom g, double lam, cons
                 int cn[3] = {ec[0], ec[1], ec[2]};
                 cn[D] += (i == P) ? 1 : -1;
                 const double nown = VARNU ? __ldg(ne + q) : nu_const;
-                const double nnb = VARNU ? __ldg(elem_ptr(g, nu, halo.nu_lo, halo.nu_hi, cn[0], cn[1], cn[2]) + goff +
-                                                  (i == P ? 0 : P * GS))
+                const double nnb = VARNU ? nbr_face_nu(g, nu, halo, n, cn, D, goff, i == P ? 0 : P * GS)
                                          : nu_const;
                 acc += (i == P ? -1.0 : 1.0) * nown * sd * sdd[i] + 0.5 * g.tau[D] * (nown + nnb);
             }
@@ -270,8 +268,7 @@ __global__ void __launch_bounds__(256) k_diag(const Geom g, double lam, const do
                     int cn[3] = {ec[0], ec[1], ec[2]};
                     cn[D] += (i == P) ? 1 : -1;
                     const double nown = VARNU ? __ldg(nu + e * C::NPE + goff + i * GS) : nu_const;
-                    const double nnb = VARNU ? __ldg(elem_ptr(g, nu, halo.nu_lo, halo.nu_hi, cn[0], cn[1], cn[2]) + goff +
-                                                      (i == P ? 0 : P * GS))
+                    const double nnb = VARNU ? nbr_face_nu(g, nu, halo, n, cn, D, goff, i == P ? 0 : P * GS)
                                              : nu_const;
                     acc += (i == P ? -1.0 : 1.0) * nown * sd * T.D[i][i] + 0.5 * g.tau[D] * (nown + nnb);
                 }
@@ -288,8 +285,8 @@ __global__ void __launch_bounds__(256) k_diag(const Geom g, double lam, const do
                 cr[D] += 1;
                 uL = sL = uR = sR = 0.0;
                 if (VARNU) {
-                    nuL = __ldg(elem_ptr(g, nu, halo.nu_lo, halo.nu_hi, cl[0], cl[1], cl[2]) + goff + P * GS);
-                    nuR = __ldg(elem_ptr(g, nu, halo.nu_lo, halo.nu_hi, cr[0], cr[1], cr[2]) + goff);
+                    nuL = nbr_face_nu(g, nu, halo, n, cl, D, goff, P * GS);
+                    nuR = nbr_face_nu(g, nu, halo, n, cr, D, goff, 0);
                 } else {
                     nuL = nuR = nu_const;
                 }

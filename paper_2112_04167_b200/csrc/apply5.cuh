@@ -435,8 +435,18 @@ __device__ __noinline__ void ptraces(const ApplyParams &a, const DevTab &T, doub
         c[D] = side ? e0[D] + B : e0[D] - 1;
         const int goff = ta * GS[O1] + tb * GS[O2] + (side ? 0 : P * GS[D]);  // face node of the line
         const int step = side ? GS[D] : -GS[D];  // walk away from the shared face
-        const double *pu = nbr<D>(g, fu, K::MODE == 1 ? nullptr : a.halo.u_lo, K::MODE == 1 ? nullptr : a.halo.u_hi,
-                                  c[0], c[1], c[2], NPE) + goff;
+        if (D == 2 && K::MODE != 1) {  // slab boundary of a multi-rank / halo-mode mesh: received trace
+            const double *trh = halo_trace(g, a.halo, c[2]);
+            if (trh) {  // (u, s = nu d_z u, nu): the table's canonical form, stored directly
+                const long long F = halo_F(g, n), f = halo_f(g, n, c[0], c[1], ta + n * tb);
+                double *o = tr + D * K::TRD + side * NV * LN + L;
+                o[0] = __ldg(trh + f);
+                o[LN] = __ldg(trh + F + f);
+                if (K::VARNU) o[2 * LN] = __ldg(trh + 2 * F + f);
+                continue;
+            }
+        }
+        const double *pu = nbr<D>(g, fu, nullptr, nullptr, c[0], c[1], c[2], NPE) + goff;
         if (K::MODE == 1) {
             const long long off = pu - fu;
             const double *pp = a.pro.p_old + off;
@@ -446,7 +456,7 @@ __device__ __noinline__ void ptraces(const ApplyParams &a, const DevTab &T, doub
 #pragma unroll
             for (int i = 0; i < n; ++i) v[k][i] = __ldg(pu + i * step);
         }
-        nuf[k] = K::VARNU ? __ldg(nbr<D>(g, a.nu, a.halo.nu_lo, a.halo.nu_hi, c[0], c[1], c[2], NPE) + goff) : a.nu_const;
+        nuf[k] = K::VARNU ? __ldg(nbr<D>(g, a.nu, nullptr, nullptr, c[0], c[1], c[2], NPE) + goff) : a.nu_const;
         slot[k] = side * NV * LN + L;
     }
     double *trd = tr + D * K::TRD;

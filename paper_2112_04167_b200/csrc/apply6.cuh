@@ -35,7 +35,6 @@ using v5::g_dbg;
 
 using v5::eo;
 using v5::fence_proxy_async;
-using v5::l2_prefetch;
 using v5::mbar_arrive;
 using v5::mbar_arrive_expect_tx;
 using v5::mbar_expect_tx;
@@ -414,8 +413,24 @@ __device__ __noinline__ void ptraces_z(const ApplyParams &a, const DevTab &T, do
         const int cz = side ? e0[2] + 1 : e0[2] - 1;
         const int goff = ta + tb * n + (side ? 0 : P * NN);
         const int step = side ? NN : -NN;
-        const double *pu = v5::nbr<2>(g, fu, K::MODE == 1 ? nullptr : a.halo.u_lo, K::MODE == 1 ? nullptr : a.halo.u_hi,
-                                      e0[0] + (slot & 3), e0[1] + (slot >> 2), cz, NPE) + goff;
+        double *t0 = tz + side * NV * NCL;
+        if (K::MODE != 1) {  // slab boundary of a multi-rank / halo-mode mesh: received face trace
+            const double *trh = halo_trace(g, a.halo, cz);
+            if (trh) {
+                const long long F = halo_F(g, n), f = halo_f(g, n, e0[0] + (slot & 3), e0[1] + (slot >> 2), ta + tb * n);
+                const double hu = __ldg(trh + f), hs = __ldg(trh + F + f);
+                t0[t] = hu;
+                if (K::VARNU) {  // weight-folded (see ptraces_xy): s~ = s w_a w_b w_0 h_z / 2, nu~ = nu w_a w_b w_0
+                    const double wab = sw[ta] * sw[tb] * sw[0];
+                    t0[NCL + t] = hs * wab * (0.5 * g.h[2]);
+                    t0[2 * NCL + t] = __ldg(trh + 2 * F + f) * wab;
+                } else {
+                    t0[NCL + t] = hs;
+                }
+                continue;
+            }
+        }
+        const double *pu = v5::nbr<2>(g, fu, nullptr, nullptr, e0[0] + (slot & 3), e0[1] + (slot >> 2), cz, NPE) + goff;
         double v[n];
         if (K::MODE == 1) {
             const double *pp = a.pro.p_old + (pu - fu);
@@ -425,11 +440,10 @@ __device__ __noinline__ void ptraces_z(const ApplyParams &a, const DevTab &T, do
 #pragma unroll
             for (int i = 0; i < n; ++i) v[i] = __ldg(pu + i * step);
         }
-        const double nuf = K::VARNU ? __ldg(v5::nbr<2>(g, a.nu, a.halo.nu_lo, a.halo.nu_hi, e0[0] + (slot & 3),
+        const double nuf = K::VARNU ? __ldg(v5::nbr<2>(g, a.nu, nullptr, nullptr, e0[0] + (slot & 3),
                                                        e0[1] + (slot >> 2), cz, NPE) + goff)
                                     : a.nu_const;
         const double dd = rdot<P>(T, 0, v);
-        double *t0 = tz + side * NV * NCL;
         t0[t] = v[0];
         if (K::VARNU) {  // weight-folded (see ptraces_xy)
             const double nw = nuf * (sw[ta] * sw[tb] * sw[0]);
@@ -500,36 +514,6 @@ __global__ void __launch_bounds__((KC6<P, VARNU, MODE>::NT)) __maxnreg__((KC6<P,
                     const int so = (el & 3) * SE + (el >> 2) * K::SY;
                     if (lane < 16 && MODE != 1) tma_load(su + so, a.u + ge * NPE, EB, &bar[buf]);
                     if (lane >= 16 && VARNU) tma_load(snu + so, a.nu + ge * NPE, EB, &bar[buf]);
-                    // warm L2 with the next brick's x / y neighbour elements (4 single elements
-                    // per x side, one contiguous x-row of 4 per y side)
-                    int n0[3] = {e0[0], e0[1], e0[2] + 1};
-                    bool ok = j + 1 < seglen;
-                    if (!ok && u + (int)gridDim.x < nunits) {
-                        const int u2 = u + gridDim.x, c2 = u2 % ncols, z2 = u2 / ncols;
-                        n0[0] = (c2 % nb0) * K::BX;
-                        n0[1] = (c2 / nb0) * K::BY;
-                        n0[2] = a.zlo + z2 * seglen;
-                        ok = true;
-                    }
-                    const int q = lane % 10, f = lane / 10;
-                    constexpr int NF = (MODE == 1 ? 2 : 1) + (VARNU ? 1 : 0);
-                    if (ok && f < NF) {
-                        const double *fb = MODE == 1 ? (f == 0 ? a.pro.z : (f == 1 ? a.pro.p_old : a.nu))
-                                                     : (f == 0 ? a.u : a.nu);
-                        int cx, cy, cnt;
-                        if (q < 8) {
-                            cx = (q >> 2) ? n0[0] + 4 : n0[0] - 1;
-                            cx = cx < 0 ? cx + g.Nl[0] : (cx >= g.Nl[0] ? cx - g.Nl[0] : cx);
-                            cy = n0[1] + (q & 3);
-                            cnt = 1;
-                        } else {
-                            cx = n0[0];
-                            cy = (q & 1) ? n0[1] + 4 : n0[1] - 1;
-                            cy = cy < 0 ? cy + g.Nl[1] : (cy >= g.Nl[1] ? cy - g.Nl[1] : cy);
-                            cnt = 4;
-                        }
-                        l2_prefetch(fb + (cx + s1 * cy + s2 * n0[2]) * NPE, (unsigned)(cnt * NPE * 8));
-                    }
                 }
                 if (MODE == 1) {  // p = z + beta p_old -> shared (operand) and p_out (fused CG prologue)
                     constexpr int H = NPE / 2;  // double2 per element (n even)

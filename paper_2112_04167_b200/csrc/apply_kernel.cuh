@@ -143,6 +143,17 @@ __device__ __forceinline__ void traces(const ApplyParams &a, const DevTab &T, do
         if (DIM == 3) c[O2] += ce / BO1;
         c[D] += side ? K::B[D] : -1;
         const int goff = ta * GS[O1] + (DIM == 3 ? tb * GS[O2] : 0);
+        if (D == DIM - 1) {  // slab boundary of a multi-rank / halo-mode mesh: received face trace
+            const double *tr = halo_trace(g, a.halo, c[D]);
+            if (tr) {
+                const long long F = halo_F(g, n), f = halo_f(g, n, c[0], c[1], goff);
+                double *o = str + K::TRO[D] + L * 3;
+                o[0] = __ldg(tr + f);
+                o[1] = __ldg(tr + F + f);
+                o[2] = VARNU ? __ldg(tr + 2 * F + f) : a.nu_const;
+                continue;
+            }
+        }
         double v[n];
         if (MODE == 1) {
             const double *pz = nb_elem<DIM, D>(g, a.pro.z, nullptr, nullptr, c[0], c[1], c[2]) + goff;
@@ -150,14 +161,14 @@ __device__ __forceinline__ void traces(const ApplyParams &a, const DevTab &T, do
 #pragma unroll
             for (int i = 0; i < n; ++i) v[i] = fma(beta, __ldg(pp + i * GS[D]), __ldg(pz + i * GS[D]));
         } else {
-            const double *pu = nb_elem<DIM, D>(g, a.u, a.halo.u_lo, a.halo.u_hi, c[0], c[1], c[2]) + goff;
+            const double *pu = nb_elem<DIM, D>(g, a.u, nullptr, nullptr, c[0], c[1], c[2]) + goff;
 #pragma unroll
             for (int i = 0; i < n; ++i) v[i] = __ldg(pu + i * GS[D]);
         }
         double nuf = a.nu_const;
         // side 1: right neighbour, its node 0 faces us; side 0: left neighbour, its node P
         if (VARNU)
-            nuf = __ldg(nb_elem<DIM, D>(g, a.nu, a.halo.nu_lo, a.halo.nu_hi, c[0], c[1], c[2]) + goff +
+            nuf = __ldg(nb_elem<DIM, D>(g, a.nu, nullptr, nullptr, c[0], c[1], c[2]) + goff +
                         (side ? 0 : P * GS[D]));
         const double s = nuf * sd * (side ? row_dot<P>(T, 0, v) : row_dot<P>(T, P, v));
         double *o = str + K::TRO[D] + L * 3;

@@ -33,6 +33,7 @@ cudaError_t upload_tables()
     if ((e = upload_tables_stage()) != cudaSuccess) return e;
     if ((e = upload_tables_stage_interp()) != cudaSuccess) return e;
     if ((e = upload_tables_visc()) != cudaSuccess) return e;
+    if ((e = upload_tables_halo()) != cudaSuccess) return e;
     return upload_tables_convect();
 }
 
@@ -151,8 +152,14 @@ struct dg_mesh {
     double *sums = nullptr, *aux = nullptr, *mass_e = nullptr, *hist = nullptr;
     int hist_cap = 0;
     PcgScal *scal = nullptr, *hscal = nullptr;
-    // halos (multi-rank)
-    double *h_lo = nullptr, *h_hi = nullptr, *hn_lo = nullptr, *hn_hi = nullptr;
+    // halos: multi-rank slabs, or the 1-rank halo mode (dg_mesh_create with nranks == 1 and an
+    // NCCL id: the slab-boundary faces go through a self send/recv instead of the local wrap)
+    bool halo = false;
+    long long F = 0;  // face nodes of one slab layer (trace arrays hold 3 F doubles)
+    double *ts_lo = nullptr, *ts_hi = nullptr, *tr_lo = nullptr, *tr_hi = nullptr;  // face traces
+    cudaStream_t cs_comm = nullptr;                                                   // exchange stream
+    cudaEvent_t ev_a = nullptr, ev_b = nullptr;
+    double *h_lo = nullptr, *h_hi = nullptr, *hn_lo = nullptr, *hn_hi = nullptr;       // element layers
     double *hv_lo[3] = {nullptr, nullptr, nullptr}, *hv_hi[3] = {nullptr, nullptr, nullptr};
     ncclComm_t comm = nullptr;
     // host-variant staging
@@ -237,7 +244,7 @@ dg_status alloc_workspace(dg_mesh *m)
 
 dg_status ensure_halos(dg_mesh *m, bool vel)
 {
-    if (m->nranks == 1) return DG_OK;
+    if (!m->halo) return DG_OK;
     const size_t b = sizeof(double) * (size_t)m->layer;
     if (!m->h_lo) {
         CKS(alloc((void **)&m->h_lo, b));
@@ -274,7 +281,7 @@ dg_status exchange(dg_mesh *m, const double *field, double *lo, double *hi)
 
 dg_status allreduce(dg_mesh *m, double *buf, int count)
 {
-    if (m->nranks == 1) return DG_OK;
+    if (!m->halo) return DG_OK;
     CKN(nccl()->AllReduce(buf, buf, (size_t)count, ncclDouble, ncclSum, m->comm, m->st));
     return DG_OK;
 }
@@ -300,6 +307,10 @@ dg_status run_apply(dg_mesh *m, double lam, const double *nu, double nu_const, c
     a.nu = nu;
     a.out = out;
     a.halo = halo;
+    if (m->halo) {
+        a.halo.tr_lo = m->tr_lo;
+        a.halo.tr_hi = m->tr_hi;
+    }
     a.epi = epi;
     a.pro = pro;
     a.b0 = 0;
@@ -317,31 +328,96 @@ dg_status run_apply(dg_mesh *m, double lam, const double *nu, double nu_const, c
     return DG_OK;
 }
 
-dg_status apply_impl(dg_mesh *m, double lam, const double *nu, double nu_const, const double *u, double *out)
+// Face-trace exchange: on the exchange stream, after the work already enqueued on
+// the mesh stream, compute the (u, s = nu d_S u[, nu]) traces of the slab's two boundary faces
+// and swap them with the neighbouring ranks (grouped NCCL send/recv; the ring order pairs the
+// two messages correctly also for two ranks, where prev == next, and for the 1-rank halo mode,
+// where both peers are this rank).  ev_b marks the received halo (tr_lo, tr_hi).  nu_too: also
+// the nu traces (once per solve / per standalone call); otherwise the nu part of the halo
+// buffers is kept from the last exchange.
+dg_status trace_exchange(dg_mesh *m, const double *u, const double *nu, double nu_const, bool nu_too)
 {
-    Halo h;
-    if (m->nranks > 1) {
-        CKS(ensure_halos(m, false));
-        CKS(exchange(m, u, m->h_lo, m->h_hi));
-        h.u_lo = m->h_lo;
-        h.u_hi = m->h_hi;
-        if (nu) {
-            CKS(exchange(m, nu, m->hn_lo, m->hn_hi));
-            h.nu_lo = m->hn_lo;
-            h.nu_hi = m->hn_hi;
-        }
-    }
-    return run_apply(m, lam, nu, nu_const, u, out, h, DotEpi{}, PProl{});
+    NcclApi *nc = nccl();
+    CK(cudaEventRecord(m->ev_a, m->st));
+    CK(cudaStreamWaitEvent(m->cs_comm, m->ev_a, 0));
+    CK(launch_slab_traces(m->g, u, nu, nu_const, m->ts_lo, m->ts_hi, nu_too ? 1 : 0, m->cs_comm));
+    m->launches += 1;
+    const int R = m->nranks, prev = (m->rank - 1 + R) % R, next = (m->rank + 1) % R;
+    const size_t cnt = (size_t)(nu_too ? 3 : 2) * (size_t)m->F;
+    CKN(nc->GroupStart());
+    CKN(nc->Send(m->ts_hi, cnt, ncclDouble, next, m->comm, m->cs_comm));
+    CKN(nc->Send(m->ts_lo, cnt, ncclDouble, prev, m->comm, m->cs_comm));
+    CKN(nc->Recv(m->tr_lo, cnt, ncclDouble, prev, m->comm, m->cs_comm));
+    CKN(nc->Recv(m->tr_hi, cnt, ncclDouble, next, m->comm, m->cs_comm));
+    CKN(nc->GroupEnd());
+    CK(cudaEventRecord(m->ev_b, m->cs_comm));
+    return DG_OK;
 }
 
-dg_status diag_impl(dg_mesh *m, double lam, const double *nu, double nu_const, double *diag)
+// q = A u over the slab with the face-trace halo.  Single rank: one launch.  Halo meshes: the
+// trace exchange runs on the exchange stream while the interior element layers [2, Nl - 2) are
+// applied; the two boundary layer pairs [0, 2) and [Nl - 2, Nl) follow once the halo has arrived
+// (3-D meshes the v5 / v6 layer-range kernels run; otherwise one launch after the exchange).
+// partial != null: dot epilogue (MODE 2/3), the launches' block partials back to back; *G =
+// their total count.  nu_traced: the nu halo of this nu is already in place (PCG iterations).
+dg_status halo_apply(dg_mesh *m, double lam, const double *nu, double nu_const, const double *u, double *out,
+                     double *partial, int *G, const int *done, bool nu_traced)
 {
+    DotEpi epi;
+    epi.partial = partial;
+    PProl pro;
+    pro.done = done;
+    int g1 = 0, g2 = 0, g3 = 0;
+    if (!m->halo) {
+        CKS(run_apply(m, lam, nu, nu_const, u, out, Halo{}, epi, pro, &g1));
+        if (G) *G = g1;
+        return DG_OK;
+    }
+    CKS(trace_exchange(m, u, nu, nu_const, !nu_traced));
+    const Geom &g = m->g;
+    const int Nl = g.Nl[g.dim - 1];
+    bool ranges = g.dim == 3 && apply3_ranges_ok(g) && Nl >= 6 && Nl % 2 == 0 &&
+                  (!partial || apply3_split_pcg_ok(g, nu));
+    if (ranges) {  // (the layer-range kernels exist for most (P, nu) pairs; otherwise one launch)
+        const dg_status st = run_apply(m, lam, nu, nu_const, u, out, Halo{}, epi, pro, &g1, 2, Nl - 2);
+        if (st == DG_EUNSUPPORTED) ranges = false;  // nothing was enqueued
+        else if (st != DG_OK) return st;
+    }
+    if (ranges) {
+        CK(cudaStreamWaitEvent(m->st, m->ev_b, 0));
+        if (partial) epi.partial = partial + 2 * g1;
+        CKS(run_apply(m, lam, nu, nu_const, u, out, Halo{}, epi, pro, &g2, 0, 2));
+        if (partial) epi.partial = partial + 2 * (g1 + g2);
+        CKS(run_apply(m, lam, nu, nu_const, u, out, Halo{}, epi, pro, &g3, Nl - 2, Nl));
+    } else {
+        CK(cudaStreamWaitEvent(m->st, m->ev_b, 0));
+        CKS(run_apply(m, lam, nu, nu_const, u, out, Halo{}, epi, pro, &g1));
+    }
+    if (G) *G = g1 + g2 + g3;
+    return DG_OK;
+}
+
+dg_status apply_impl(dg_mesh *m, double lam, const double *nu, double nu_const, const double *u, double *out)
+{
+    return halo_apply(m, lam, nu, nu_const, u, out, nullptr, nullptr, nullptr, false);
+}
+
+// the nu face traces for the diagonal and the PCG iterations of one solve
+dg_status nu_halo(dg_mesh *m, const double *nu, double nu_const)
+{
+    if (!m->halo || !nu) return DG_OK;  // constant nu: the kernels use nu_const
+    CKS(trace_exchange(m, nu, nu, nu_const, true));  // (the u part of this exchange is unused)
+    CK(cudaStreamWaitEvent(m->st, m->ev_b, 0));
+    return DG_OK;
+}
+
+dg_status diag_impl(dg_mesh *m, double lam, const double *nu, double nu_const, double *diag, bool nu_traced = false)
+{
+    if (!nu_traced) CKS(nu_halo(m, nu, nu_const));
     Halo h;
-    if (m->nranks > 1 && nu) {
-        CKS(ensure_halos(m, false));
-        CKS(exchange(m, nu, m->hn_lo, m->hn_hi));
-        h.nu_lo = m->hn_lo;
-        h.nu_hi = m->hn_hi;
+    if (m->halo) {
+        h.tr_lo = m->tr_lo;
+        h.tr_hi = m->tr_hi;
     }
     CK(m->g.dim == 3 ? launch_diag3(m->g, lam, nu, nu_const, h, diag, m->st)
                      : launch_diag2(m->g, lam, nu, nu_const, h, diag, m->st));
@@ -352,7 +428,7 @@ dg_status diag_impl(dg_mesh *m, double lam, const double *nu, double nu_const, d
 // reduce partial[G][2] -> sums[2] (+ allreduce) -> finalize(mode)
 dg_status reduce_fin(dg_mesh *m, int G, int mode)
 {
-    if (m->nranks == 1) {
+    if (!m->halo) {
         CK(launch_reduce_fin(m->partial, G, 2, m->sums, mode, m->scal, m->hist, m->aux, m->st));
         m->launches += 1;
     } else {
@@ -386,7 +462,7 @@ dg_status ensure_sw(dg_mesh *m, double nu_const)
         CKS(alloc((void **)&m->rc_el, sizeof(double) * (size_t)g.nel * (g.dim == 3 ? 8 : 4)));
         CKS(alloc((void **)&m->chat, sizeof(double) * (size_t)NV));
         CKS(alloc((void **)&m->xc, sizeof(double) * (size_t)NV));
-        if (m->nranks > 1) CKS(alloc((void **)&m->rc, sizeof(double) * (size_t)NV));
+        if (m->halo) CKS(alloc((void **)&m->rc, sizeof(double) * (size_t)NV));
     }
     (void)nu_const;  // the tables are built once for nu = 1 (nu scales eigenvalues / symbols only)
     if (m->sw_nu != 1.0) {
@@ -420,7 +496,7 @@ dg_status sw_coarse(dg_mesh *m, double lam, double nu, const double *nu_eff, dou
     c.pslot = pslot;
     c.count_dot = m->rank == 0;
     c.nel = g.nel;
-    if (m->nranks == 1) {
+    if (!m->halo) {
         c.rc_el = m->rc_el;
     } else {
         const long long NV = (long long)g.N[0] * g.N[1] * (g.dim == 3 ? g.N[2] : 1);
@@ -499,7 +575,6 @@ dg_status pcg_impl(dg_mesh *m, double lam, const double *nu, double nu_const, co
 {
     const Geom &g = m->g;
     const int VG = vec_grid();
-    const bool multi = m->nranks > 1;
 
     // scalars
     PcgScal s0{};
@@ -533,6 +608,9 @@ dg_status pcg_impl(dg_mesh *m, double lam, const double *nu, double nu_const, co
         if (!m->sw_coarse_on) CK(cudaMemsetAsync(m->xc, 0, sizeof(double) * (size_t)g.N[0] * g.N[1] *
                                                               (g.dim == 3 ? g.N[2] : 1), m->st));
     }
+    // halo meshes: the nu face traces once per solve (the diagonal and every apply of the
+    // iterations read them; the per-iteration exchanges carry only u and s)
+    CKS(nu_halo(m, nu, nu_const));
     // Jacobi preconditioner: D^-1 straight from the closed-form kernel where it applies
     bool self = false;
     for (int d = 0; d < g.dim; ++d) self = self || g.N[d] == 1;
@@ -542,11 +620,9 @@ dg_status pcg_impl(dg_mesh *m, double lam, const double *nu, double nu_const, co
         // solve with the same pair (e.g. the three velocity components of a stage)
     } else if (!self) {
         Halo hd;
-        if (multi && nu) {
-            CKS(ensure_halos(m, false));
-            CKS(exchange(m, nu, m->hn_lo, m->hn_hi));
-            hd.nu_lo = m->hn_lo;
-            hd.nu_hi = m->hn_hi;
+        if (m->halo) {
+            hd.tr_lo = m->tr_lo;
+            hd.tr_hi = m->tr_hi;
         }
         CK(g.dim == 3 ? launch_diag3(g, lam, nu, nu_const, hd, m->dinv, m->st, 1)
                       : launch_diag2(g, lam, nu, nu_const, hd, m->dinv, m->st, 1));
@@ -554,15 +630,10 @@ dg_status pcg_impl(dg_mesh *m, double lam, const double *nu, double nu_const, co
         m->dinv_lam = nu ? -1.0 : lam;
         m->dinv_nu = nu ? -1.0 : nu_const;
     } else {
-        CKS(diag_impl(m, lam, nu, nu_const, m->q));
+        CKS(diag_impl(m, lam, nu, nu_const, m->q, true));
         CK(launch_recip(g, m->q, m->dinv, m->st));
         m->launches += 1;
         m->dinv_lam = m->dinv_nu = -1.0;
-    }
-    Halo hnu;
-    if (multi && nu) {  // diag_impl exchanged nu already
-        hnu.nu_lo = m->hn_lo;
-        hnu.nu_hi = m->hn_hi;
     }
     // f mean (lam == 0) and total mass
     CK(launch_mass_moments(g, f, m->mass_e, m->partial, m->st));
@@ -577,7 +648,7 @@ dg_status pcg_impl(dg_mesh *m, double lam, const double *nu, double nu_const, co
     CK(cudaStreamSynchronize(m->st));
     const double usum = m->hscal->rz;
     if (usum == 0.0) CK(cudaMemsetAsync(m->q, 0, sizeof(double) * (size_t)m->ndof, m->st));
-    else CKS(apply_impl(m, lam, nu, nu_const, u, m->q));
+    else CKS(halo_apply(m, lam, nu, nu_const, u, m->q, nullptr, nullptr, nullptr, true));
     CK(launch_pcg_init(g, f, m->q, m->r, m->mass_e, m->scal, m->partial, m->st));
     m->launches += 1;
     CKS(reduce_fin(m, VG, FIN_INIT));
@@ -591,9 +662,10 @@ dg_status pcg_impl(dg_mesh *m, double lam, const double *nu, double nu_const, co
     CK(cudaMemsetAsync(m->pa, 0, sizeof(double) * (size_t)m->ndof, m->st));
 
     double *p_old = m->pa, *p_new = m->pb;
-    // split PCG step (pupd kernel + apply with the dot epilogue) where the v6 apply runs:
-    // measured faster than the fused prologue of v5
-    const bool split_ok = !multi && g.dim == 3 && apply3_split_pcg_ok(g, nu);
+    // split PCG step (pupd kernel + apply with the dot epilogue) where the v5 / v6 applies run:
+    // measured faster than the fused prologue of v5; halo meshes too (the apply
+    // overlaps the face-trace exchange with the interior layers)
+    const bool split_ok = g.dim == 3 && apply3_split_pcg_ok(g, nu);
     const bool split = !sw && split_ok && !DG_DEV_ENV("DG_PCG_FUSED");
     // constant nu on the uniform periodic mesh (N_d >= 2: the closed-form diagonal): the first
     // element's D^-1 serves every element
@@ -635,22 +707,11 @@ dg_status pcg_impl(dg_mesh *m, double lam, const double *nu, double nu_const, co
                 CK(launch_sw_pupd(g, m->h_sw, pp, m->st));
                 m->launches += 1;
                 if (split_ok) {
-                    PProl pro;
-                    pro.done = &m->scal->done;
-                    DotEpi epi;
-                    epi.partial = m->partial;
                     int grid = 0;
-                    CKS(run_apply(m, lam, nu, nu_const, p_old, m->q, Halo{}, epi, pro, &grid));
+                    CKS(halo_apply(m, lam, nu, nu_const, p_old, m->q, m->partial, &grid, &m->scal->done, true));
                     CKS(reduce_fin(m, grid, FIN_ALPHA));
                 } else {
-                    Halo h;
-                    if (multi) {
-                        CKS(ensure_halos(m, false));
-                        CKS(exchange(m, p_old, m->h_lo, m->h_hi));
-                        h.u_lo = m->h_lo;
-                        h.u_hi = m->h_hi;
-                    }
-                    CKS(run_apply(m, lam, nu, nu_const, p_old, m->q, h, DotEpi{}, PProl{}));
+                    CKS(halo_apply(m, lam, nu, nu_const, p_old, m->q, nullptr, nullptr, nullptr, true));
                     CK(launch_dot_pq(g, p_old, m->q, m->scal, m->partial, m->st));
                     m->launches += 1;
                     CKS(reduce_fin(m, VG, FIN_ALPHA));
@@ -663,18 +724,14 @@ dg_status pcg_impl(dg_mesh *m, double lam, const double *nu, double nu_const, co
                 if (table) CK(launch_pcg_pupd_xt(g, u, p_old, m->r, m->dinv, m->scal, m->st));
                 else CK(launch_pcg_pupd_x(g, u, p_old, m->z, m->scal, m->st));
                 m->launches += 1;
-                PProl pro;
-                pro.done = &m->scal->done;
-                DotEpi epi;
-                epi.partial = m->partial;
                 int grid = 0;
-                CKS(run_apply(m, lam, nu, nu_const, p_old, m->q, Halo{}, epi, pro, &grid));
+                CKS(halo_apply(m, lam, nu, nu_const, p_old, m->q, m->partial, &grid, &m->scal->done, true));
                 CKS(reduce_fin(m, grid, FIN_ALPHA));
                 if (table) CK(launch_pcg_update_t(g, m->r, m->q, m->dinv, m->mass_e, m->scal, m->partial, m->st));
                 else CK(launch_pcg_update_nox(g, m->r, m->q, m->dinv, m->z, m->mass_e, m->scal, m->partial, m->st));
                 m->launches += 1;
                 CKS(reduce_fin(m, table ? vec_grid_wide() : VG, FIN_BETA));
-            } else if (!multi) {
+            } else if (!m->halo) {
                 // q = A p with p = dinv r + beta p_old (prologue), partials p.q, sum q (epilogue)
                 PProl pro;
                 pro.on = true;
@@ -696,12 +753,7 @@ dg_status pcg_impl(dg_mesh *m, double lam, const double *nu, double nu_const, co
                 // unfused: p = dinv r + beta p ; halo(p) ; q = A p ; p.q
                 CK(launch_pcg_pupd(g, p_old, m->z, m->scal, m->st));
                 m->launches += 1;
-                CKS(ensure_halos(m, false));
-                CKS(exchange(m, p_old, m->h_lo, m->h_hi));
-                Halo h = hnu;
-                h.u_lo = m->h_lo;
-                h.u_hi = m->h_hi;
-                CKS(run_apply(m, lam, nu, nu_const, p_old, m->q, h, DotEpi{}, PProl{}));
+                CKS(halo_apply(m, lam, nu, nu_const, p_old, m->q, nullptr, nullptr, nullptr, true));
                 CK(launch_dot_pq(g, p_old, m->q, m->scal, m->partial, m->st));
                 m->launches += 1;
                 CKS(reduce_fin(m, VG, FIN_ALPHA));
@@ -768,7 +820,7 @@ dg_status div_impl(dg_mesh *mv, const double *const v[3], double *div)
 {
     DivGradParams a;
     for (int c = 0; c < mv->g.dim; ++c) a.v[c] = v[c];
-    if (mv->nranks > 1) {
+    if (mv->halo) {
         CKS(ensure_halos(mv, true));
         for (int c = 0; c < mv->g.dim; ++c) {
             CKS(exchange(mv, v[c], mv->hv_lo[c], mv->hv_hi[c]));
@@ -787,7 +839,7 @@ dg_status grad_impl(dg_mesh *mp, dg_mesh *mv, const double *psi, double *const g
 {
     DivGradParams a;
     a.psi = psi;
-    if (mp->nranks > 1) {
+    if (mp->halo) {
         cudaStream_t s0 = mp->st;
         mp->st = mv->st;
         dg_status s = ensure_halos(mp, false);
@@ -918,13 +970,27 @@ dg_status dg_mesh_create(int dim, const int N[3], const double L[3], int P, int 
         if (e != cudaSuccess) return fail(set_error(DG_ECUDA, cudaGetErrorString(e)));
         m->launches += 2;
     }
-    if (nranks > 1) {
+    // halo meshes (nranks > 1, or the 1-rank halo mode: an NCCL id with nranks == 1): the
+    // communicator, the exchange stream and events, the face-trace buffers and the element-layer
+    // buffers of the once-per-stage kernels -- all allocated here, none in the hot calls
+    m->halo = nranks > 1 || nccl_uid != nullptr;
+    if (m->halo) {
         NcclApi *nc = nccl();
         if (!nc->ok) return fail(set_error(DG_ENCCL, nc->why));
         ncclUniqueId id;
         std::memcpy(&id, nccl_uid, 128);
         ncclResult_t r = nc->CommInitRank(&m->comm, nranks, id, rank);
         if (r != ncclSuccess) return fail(set_error(DG_ENCCL, std::string("ncclCommInitRank: ") + nc->GetErrorString(r)));
+        m->F = (dim == 3 ? (long long)g.Nl[0] * g.Nl[1] * g.n * g.n : (long long)g.Nl[0] * g.n);
+        const size_t tb = sizeof(double) * 3 * (size_t)m->F;
+        double **tbufs[] = {&m->ts_lo, &m->ts_hi, &m->tr_lo, &m->tr_hi};
+        for (double **p : tbufs)
+            if ((s = alloc((void **)p, tb)) != DG_OK) return fail(s);
+        if ((s = ensure_halos(m, true)) != DG_OK) return fail(s);
+        if (cudaStreamCreateWithFlags(&m->cs_comm, cudaStreamNonBlocking) != cudaSuccess ||
+            cudaEventCreateWithFlags(&m->ev_a, cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&m->ev_b, cudaEventDisableTiming) != cudaSuccess)
+            return fail(set_error(DG_ECUDA, "exchange stream / event creation failed"));
     }
     *out = m;
     return DG_OK;
@@ -938,7 +1004,8 @@ void dg_mesh_destroy(dg_mesh *m)
     double *bufs[] = {m->r,    m->q,    m->pa,    m->pb,     m->dinv,   m->z,    m->partial,
                       m->sums, m->aux,  m->mass_e, m->hist,  m->h_lo,   m->h_hi, m->hn_lo,
                       m->hn_hi, m->st_a, m->st_b,  m->st_c,  m->sf[0], m->sf[1], m->sf[2], m->sf[3],
-                      m->sf[4], m->sf[5], m->d_swF, m->rc_el, m->chat, m->xc, m->rc};
+                      m->sf[4], m->sf[5], m->d_swF, m->rc_el, m->chat, m->xc, m->rc,
+                      m->ts_lo, m->ts_hi, m->tr_lo, m->tr_hi};
     for (double *b : bufs)
         if (b) cudaFree(b);
     for (int c = 0; c < 3; ++c) {
@@ -949,7 +1016,11 @@ void dg_mesh_destroy(dg_mesh *m)
     if (m->d_sw) cudaFree(m->d_sw);
     if (m->d_flag) cudaFree(m->d_flag);
     if (m->hscal) cudaFreeHost(m->hscal);
+    if (m->cs_comm) cudaStreamSynchronize(m->cs_comm);
     if (m->comm) nccl()->CommDestroy(m->comm);
+    if (m->ev_a) cudaEventDestroy(m->ev_a);
+    if (m->ev_b) cudaEventDestroy(m->ev_b);
+    if (m->cs_comm) cudaStreamDestroy(m->cs_comm);
     for (cudaEvent_t e : m->ev) cudaEventDestroy(e);
     for (double *b : m->rk) cudaFree(b);
     if (m->cs_in) cudaStreamDestroy(m->cs_in);
@@ -1054,7 +1125,7 @@ dg_status dg_convect_rhs(dg_mesh *m, const double *const v[3], double *const out
         a.v[c] = c < dim ? v[c] : nullptr;
         a.out[c] = c < dim ? out[c] : nullptr;
     }
-    if (m->nranks > 1) {
+    if (m->halo) {
         CKS(ensure_halos(m, true));
         for (int c = 0; c < dim; ++c) {
             CKS(exchange(m, v[c], m->hv_lo[c], m->hv_hi[c]));
@@ -1083,7 +1154,7 @@ dg_status dg_helmholtz_apply_host(dg_mesh *m, double lam, const double *nu_host,
     if (nu_host) CKS(stage(m, &m->st_c, b));
     const Geom &g = m->g;
     int C = 0;
-    if (m->nranks == 1 && g.dim == 3 && apply3_ranges_ok(g)) {
+    if (!m->halo && g.dim == 3 && apply3_ranges_ok(g)) {
         const int nbz = g.Nl[2] / 2;
         for (int c = 16; c >= 3; --c)
             if (nbz % c == 0) {
@@ -1430,7 +1501,7 @@ dg_status dg_derivative(dg_mesh *m, const double *u, double *const out[3])
             a.out[c] = out[c];
             a.dirs |= 1 << c;
         }
-    if (m->nranks > 1) {
+    if (m->halo) {
         CKS(ensure_halos(m, true));
         CKS(exchange(m, u, m->hv_lo[0], m->hv_hi[0]));
         a.lo = m->hv_lo[0];
@@ -1489,7 +1560,7 @@ dg_status dg_imex_rk_step_vv(dg_mesh *mv, dg_mesh *mp, const dg_tableau *tab, do
     auto TM = [&](int c) { return mv->rk[(4 * S + 1) * dim + c]; };
     double *NU = mv->rk[(4 * S + 2) * dim], *WK = mv->rk[(4 * S + 2) * dim + 1];
     auto DV = [&](int e, int c) { return mv->rk[(4 * S + 2) * dim + 2 + e * dim + c]; };  // D_c v_e
-    const bool multi = mv->nranks > 1;
+    const bool multi = mv->halo;
     if (multi) CKS(ensure_halos(mv, true));
     dg_step_info inf{};
     // D_c u for the selected directions (overwrite or accumulate scale * D_c u)

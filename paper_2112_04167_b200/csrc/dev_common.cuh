@@ -96,6 +96,25 @@ __device__ __forceinline__ long long elem_index(const Geom &g, int c0, int c1, i
     return (long long)c0 + (long long)g.Nl[0] * ((long long)c1 + (long long)g.Nl[1] * c2);
 }
 
+// Face-trace halo (dg_internal.h Halo) of the slowest direction: is the neighbour at local
+// slowest-direction coordinate cS outside the slab with a received trace, and where is it.
+// Returns the trace array of that side (or nullptr: wrap / local element), f = face node index.
+__device__ __forceinline__ const double *halo_trace(const Geom &g, const Halo &h, int cS)
+{
+    const int S = g.dim - 1;
+    if (cS < 0) return h.tr_lo;
+    if (cS >= g.Nl[S]) return h.tr_hi;
+    return nullptr;
+}
+__device__ __forceinline__ long long halo_F(const Geom &g, int n)
+{
+    return g.dim == 3 ? (long long)g.Nl[0] * g.Nl[1] * n * n : (long long)g.Nl[0] * n;
+}
+__device__ __forceinline__ long long halo_f(const Geom &g, int n, int c0, int c1, int inface)
+{
+    return g.dim == 3 ? ((long long)c0 + (long long)g.Nl[0] * c1) * (n * n) + inface : (long long)c0 * n + inface;
+}
+
 // Pointer to the nodal data of the element with local coordinates c (any direction may be
 // one step outside the slab).  Non-slowest directions wrap periodically (they are never
 // split).  The slowest direction wraps locally when the halo pointers are null (one rank),
@@ -123,6 +142,19 @@ __device__ __forceinline__ const double *elem_ptr(const Geom &g, const double *b
         c[S] -= g.Nl[S];
     }
     return base + elem_index(g, c[0], c[1], c[2]) * g.npe;
+}
+
+// viscosity at the neighbour element's face node across a face normal to D: the neighbour cn is
+// one step from the own element along D; goff = the node's offset with its D-coordinate removed
+// (= the in-face index for D = S), nboff = the neighbour face node's D-offset (0 or P * stride)
+__device__ __forceinline__ double nbr_face_nu(const Geom &g, const double *nu, const Halo &h, int n, const int (&cn)[3],
+                                              int D, int goff, int nboff)
+{
+    if (D == g.dim - 1) {
+        const double *tr = halo_trace(g, h, cn[D]);
+        if (tr) return __ldg(tr + 2 * halo_F(g, n) + halo_f(g, n, cn[0], cn[1], goff));
+    }
+    return __ldg(elem_ptr(g, nu, nullptr, nullptr, cn[0], cn[1], cn[2]) + goff + nboff);
 }
 
 __device__ __forceinline__ double warp_sum(double v)

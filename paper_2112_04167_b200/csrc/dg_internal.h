@@ -82,9 +82,15 @@ struct Geom {
     long long nel;   // local elements
 };
 
-struct Halo {        // neighbour element layers of the slowest direction (multi-rank)
-    const double *u_lo = nullptr, *u_hi = nullptr;
-    const double *nu_lo = nullptr, *nu_hi = nullptr;
+// Face-trace halos of the slab boundary faces of the slowest direction S (multi-rank slabs and
+// the 1-rank halo mode): per face node of the neighbouring rank's boundary layer,
+//   tr[0 F + f] = u,   tr[1 F + f] = s = nu d u / d x_S (physical, +S direction),   tr[2 F + f] = nu,
+// F = face nodes of one layer = Nl_0 (Nl_1) n^(dim-1); f = face element (c_0 + Nl_0 c_1) * n^(dim-1)
+// + the node's in-face index (a + n b).  tr_lo: the top face of the layer below the slab
+// (rank - 1), tr_hi: the bottom face of the layer above (rank + 1).  Null: the slab wraps
+// periodically onto itself (one rank, no halo mode).
+struct Halo {
+    const double *tr_lo = nullptr, *tr_hi = nullptr;
 };
 
 // Fused epilogue for the PCG apply: partial[blk*2 + 0] += dotv . out,  partial[blk*2+1] += sum(out)
@@ -150,12 +156,17 @@ cudaError_t launch_diag3(const Geom &g, double lam, const double *nu, double nuc
                          cudaStream_t st, int invert = 0);
 cudaError_t launch_convect_k(const ConvParams &a, cudaStream_t st);
 cudaError_t launch_coords(const Geom &g, long long el_offset, double *xyz, cudaStream_t st);
+// face traces (u, s, nu) of the slab's bottom face (layer 0, -> send_lo) and top face (layer
+// Nl_S - 1, -> send_hi) in the Halo layout; with_nu = 0 writes only u and s
+cudaError_t launch_slab_traces(const Geom &g, const double *u, const double *nu, double nu_const, double *send_lo,
+                               double *send_hi, int with_nu, cudaStream_t st);
 cudaError_t launch_mass(const Geom &g, double *mass, cudaStream_t st);
 cudaError_t upload_tables();   // all kernel TUs (capi.cpp)
 cudaError_t upload_tables_vec();
 cudaError_t upload_tables_apply2();
 cudaError_t upload_tables_apply3();
 cudaError_t upload_tables_convect();
+cudaError_t upload_tables_halo();
 cudaError_t upload_tables_stage();
 cudaError_t upload_tables_stage_interp();
 
