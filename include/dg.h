@@ -201,6 +201,7 @@ dg_status dg_gradient(dg_mesh *mp, dg_mesh *mv, const double *psi, double *const
 typedef struct {
     dg_solve_info pressure;
     dg_solve_info velocity[3];
+    dg_solve_info stab;  /* the divergence / mass-flux stabilisation solve (0 iterations when off) */
 } dg_stage_info;
 
 dg_status dg_imex_stage(dg_mesh *mv, dg_mesh *mp, double dt, double a_ex21, double a_im21, double a_im22,
@@ -239,6 +240,7 @@ typedef struct {
     int stages;          /* implicit stages performed (s - 1)                 */
     int pressure_iters;  /* CG iterations summed over the Poisson solves     */
     int velocity_iters;  /* CG iterations summed over the Helmholtz solves   */
+    int stab_iters;      /* CG iterations of the divergence stabilisation    */
 } dg_step_info;
 
 dg_status dg_imex_rk_step(dg_mesh *mv, dg_mesh *mp, const dg_tableau *tab, double dt, double nu,
@@ -277,6 +279,30 @@ dg_status dg_imex_rk_step_vv(dg_mesh *mv, dg_mesh *mp, const dg_tableau *tab, do
  * skip a direction), the operator of dg_imex_rk_step_vv's F_d2 / F_d3.  DEVICE arrays of m;
  * no aliasing of u with out.  Collective for multi-rank meshes. */
 dg_status dg_derivative(dg_mesh *m, const double *u, double *const out[3]);
+
+/* Divergence / mass-flux stabilisation of the projection step (§3.3: "For
+ * pressure robustness a divergence/mass-flux stabilization is added as proposed in [Joshi
+ * 2016, Akbas 2018]"; the formula is not in the paper -- reading A26; SURVEY
+ * NEXT-1).  After the projection v'' = v' - M^-1 G psi, solve for v^ in the velocity DG space
+ *   (M + a_D K_D + a_C K_C) v^ = M v'',
+ *   (K_D v)_{c,I} = sum_K sum_q W_q (div v)(x_q) d_c phi_I(x_q)       broken (element) divergence
+ *   (K_C v)_{c,I} = sum_{F normal to c} sum_q W^F_q [v_c] [phi_I]       normal-velocity jumps
+ * (GLL collocation quadrature, [g] = g^- - g^+), a_D = dt zeta_D U h / (P+1), a_C = dt zeta_C U,
+ * U = sqrt(sum m |v''|^2 / sum m) the RMS velocity, h = (prod_d h_d)^(1/dim).  SPD; Jacobi-
+ * preconditioned CG over the dim components, stopped at ||M^-1 r|| <= tol ||v''||, from v''.
+ *
+ * dg_mesh_set_div_stab(mv, zeta_D, zeta_C): zeta > 0 switches the step on for every projection
+ *   of dg_imex_stage, dg_imex_rk_step and dg_imex_rk_step_vv on this velocity mesh (after line 6
+ *   and after the final projection) and allocates its workspace (4 dim ndof doubles); 0, 0
+ *   switches it off.  Not a hot call.
+ * dg_div_stab_apply: out[c] = ((M + a_D K_D + a_C K_C) v)_c (weak), explicit coefficients.
+ * dg_div_stab_solve: v (in: v'', out: v^) for (dt, zeta_D, zeta_C); coef (may be NULL) returns
+ *   (a_D, a_C, U).  Needs the workspace of dg_mesh_set_div_stab (DG_EINVAL otherwise).
+ * DEVICE arrays [local_ndof]; collective for multi-rank meshes (element-layer halos). */
+dg_status dg_mesh_set_div_stab(dg_mesh *mv, double zeta_D, double zeta_C);
+dg_status dg_div_stab_apply(dg_mesh *m, double a_D, double a_C, const double *const v[3], double *const out[3]);
+dg_status dg_div_stab_solve(dg_mesh *m, double dt, double zeta_D, double zeta_C, double *const v[3], double tol,
+                            int maxit, double coef[3], dg_solve_info *info);
 
 /* Host-buffer variants: same operations on HOST arrays; H2D and D2H copies through
  * mesh-owned device staging buffers are part of the call (allocated on first use). */

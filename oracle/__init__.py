@@ -214,10 +214,11 @@ def mass(mesh: Mesh):
 # ---------------------------------------------------------------------------
 # IMEX-RK stage -- plain numpy composition of the functions above.
 # ---------------------------------------------------------------------------
-def imex_stage(mv: Mesh, mp: Mesh, dt, a_ex21, a_im21, a_im22, nu, v, tol=1e-14):
+def imex_stage(mv: Mesh, mp: Mesh, dt, a_ex21, a_im21, a_im22, nu, v, tol=1e-14, stab=None):
     """Alg. 3 stage i = 2, constant nu, F_s = 0, under the readings of
     include/dg.h dg_imex_stage: returns (vout[dim], psi, v'').  Exact discrete solves
-    (oracle PCG to tol)."""
+    (oracle PCG to tol).  stab = (zeta_D, zeta_C): the divergence / mass-flux stabilisation of
+    v'' after line 6 (reading A26; oracle.stab)."""
     dim = mv.dim
     m = mass(mv)
     Fc = convect(mv, v)                                                     # F_c(v)   (P:693)
@@ -229,6 +230,9 @@ def imex_stage(mv: Mesh, mp: Mesh, dt, a_ex21, a_im21, a_im22, nu, v, tol=1e-14)
     psi, *_ = pcg_solve(mp, 0.0, fp, nu_const=1.0, tol=tol)                 # line 5 (lam = 0)
     gw = dg_gradient_weak(mp, psi)
     vpp = [vp[c] - gw[c] / m for c in range(dim)]                           # line 6
+    if stab is not None:                                                    # P:1040 (reading A26)
+        from .stab import div_stab_solve
+        vpp, _, _ = div_stab_solve(mv, vpp, dt, stab[0], stab[1], tol=tol)
     lam = 1.0 / (dt * a_im22)
     out = []
     for c in range(dim):
@@ -401,7 +405,7 @@ ORACLE_TABLEAUX = {
 }
 
 
-def imex_rk_step(mv: Mesh, mp: Mesh, tab, dt, nu, v, tol=1e-14):
+def imex_rk_step(mv: Mesh, mp: Mesh, tab, dt, nu, v, tol=1e-14, stab=None):
     """One step of Alg. 3 under the readings of include/dg.h dg_imex_rk_step (constant nu,
     F_s = 0, F_d2 = -F_d3 = nu grad div u with the DG pair, final projection skipped):
     returns v^{n+1} (dim arrays)."""
@@ -425,6 +429,9 @@ def imex_rk_step(mv: Mesh, mp: Mesh, tab, dt, nu, v, tol=1e-14):
         psi, *_ = pcg_solve(mp, 0.0, -dg_divergence_weak(mv, vp) / mpm, nu_const=1.0, tol=tol)  # line 5
         gw = dg_gradient_weak(mp, psi)
         vpp = [vp[c] - gw[c] / m for c in range(dim)]                                   # line 6
+        if stab is not None:                                                            # P:1040, A26
+            from .stab import div_stab_solve
+            vpp, _, _ = div_stab_solve(mv, vpp, dt, stab[0], stab[1], tol=tol)
         u = []
         for c in range(dim):
             g = vpp[c] + dt * sum((A_im[i, j] - A_ex[i, j]) * Fd[j][c] + A_ex[i, j] * Fg[j][c]

@@ -28,6 +28,8 @@ from ._capi import (  # noqa: F401
     dg_convect_rhs,
     ViscModel,
     dg_derivative,
+    dg_div_stab_apply,
+    dg_div_stab_solve,
     dg_divergence,
     dg_gradient,
     dg_gll_tables,
@@ -40,6 +42,7 @@ from ._capi import (  # noqa: F401
     dg_last_error,
     dg_mesh_create,
     dg_mesh_destroy,
+    dg_mesh_set_div_stab,
     dg_mesh_element_offset,
     dg_mesh_launch_count,
     dg_mesh_local_elements,

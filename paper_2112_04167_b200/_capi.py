@@ -37,10 +37,11 @@ class SolveInfo(ctypes.Structure):
 
 
 class StageInfo(ctypes.Structure):
-    _fields_ = [("pressure", SolveInfo), ("velocity", SolveInfo * 3)]
+    _fields_ = [("pressure", SolveInfo), ("velocity", SolveInfo * 3), ("stab", SolveInfo)]
 
     def as_dict(self):
-        return {"pressure": self.pressure.as_dict(), "velocity": [x.as_dict() for x in self.velocity]}
+        return {"pressure": self.pressure.as_dict(), "velocity": [x.as_dict() for x in self.velocity],
+                "stab": self.stab.as_dict()}
 
 
 RK_MAX = 8
@@ -66,7 +67,7 @@ class Tableau(ctypes.Structure):
 
 
 class StepInfo(ctypes.Structure):
-    _fields_ = [("stages", _i), ("pressure_iters", _i), ("velocity_iters", _i)]
+    _fields_ = [("stages", _i), ("pressure_iters", _i), ("velocity_iters", _i), ("stab_iters", _i)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -101,6 +102,10 @@ _c = {
     "dg_pcg_solve": _sig("dg_pcg_solve", _i, [_vp, _d, _vp, _d, _vp, _d, _i, _vp, ctypes.POINTER(SolveInfo)]),
     "dg_convect_rhs": _sig("dg_convect_rhs", _i, [_vp, ctypes.POINTER(_vp), ctypes.POINTER(_vp)]),
     "dg_derivative": _sig("dg_derivative", _i, [_vp, _vp, ctypes.POINTER(_vp)]),
+    "dg_mesh_set_div_stab": _sig("dg_mesh_set_div_stab", _i, [_vp, _d, _d]),
+    "dg_div_stab_apply": _sig("dg_div_stab_apply", _i, [_vp, _d, _d, ctypes.POINTER(_vp), ctypes.POINTER(_vp)]),
+    "dg_div_stab_solve": _sig("dg_div_stab_solve", _i, [_vp, _d, _d, _d, ctypes.POINTER(_vp), _d, _i,
+                                                        ctypes.POINTER(_d), ctypes.POINTER(SolveInfo)]),
     "dg_imex_rk_step_vv": _sig("dg_imex_rk_step_vv", _i, [_vp, _vp, ctypes.POINTER(Tableau), _d,
                                                           ctypes.POINTER(ViscModel), ctypes.POINTER(_vp), _i,
                                                           ctypes.POINTER(_vp), _vp, _d, _i, ctypes.POINTER(StepInfo)]),
@@ -333,6 +338,27 @@ def dg_derivative(m: Mesh, u, out):
     """Velocity-level central-flux DG derivatives out[c] = D_c u (None skips c) -- include/dg.h."""
     o = (_vp * 3)(*([_ptr(x) for x in out] + [None] * (3 - len(out))))
     _check(_c["dg_derivative"](m.handle, _ptr(u), o))
+
+
+def dg_mesh_set_div_stab(mv: Mesh, zeta_D=1.0, zeta_C=1.0):
+    """Divergence / mass-flux stabilisation of every projection on this velocity mesh -- dg.h."""
+    _check(_c["dg_mesh_set_div_stab"](mv.handle, float(zeta_D), float(zeta_C)))
+
+
+def dg_div_stab_apply(m: Mesh, a_D, a_C, v, out):
+    vi = (_vp * 3)(*([_ptr(x) for x in v] + [None] * (3 - len(v))))
+    vo = (_vp * 3)(*([_ptr(x) for x in out] + [None] * (3 - len(out))))
+    _check(_c["dg_div_stab_apply"](m.handle, float(a_D), float(a_C), vi, vo))
+
+
+def dg_div_stab_solve(m: Mesh, dt, zeta_D, zeta_C, v, tol=1e-12, maxit=2000):
+    """v (in: v'', out: v^) in place; returns (SolveInfo, (a_D, a_C, U)) -- dg.h."""
+    vi = (_vp * 3)(*([_ptr(x) for x in v] + [None] * (3 - len(v))))
+    coef = (_d * 3)()
+    info = SolveInfo()
+    _check(_c["dg_div_stab_solve"](m.handle, float(dt), float(zeta_D), float(zeta_C), vi, float(tol), int(maxit),
+                                   coef, ctypes.byref(info)), info)
+    return info, (coef[0], coef[1], coef[2])
 
 
 def dg_imex_rk_step_vv(mv: Mesh, mp: Mesh, tableau, dt, visc, v, psi, tol, maxit, fs=None, final_projection=True):

@@ -34,6 +34,7 @@ cudaError_t upload_tables()
     if ((e = upload_tables_stage_interp()) != cudaSuccess) return e;
     if ((e = upload_tables_visc()) != cudaSuccess) return e;
     if ((e = upload_tables_halo()) != cudaSuccess) return e;
+    if ((e = upload_tables_stab()) != cudaSuccess) return e;
     return upload_tables_convect();
 }
 
@@ -183,6 +184,11 @@ struct dg_mesh {
     // pcg_impl; (dinv_lam, dinv_nu) name the constant-nu operator it holds (-1: invalid).  Any
     // other writer of `dinv` (or a stream change) must reset both to -1.
     double dinv_lam = -1.0, dinv_nu = -1.0;
+    // divergence / mass-flux stabilisation (stab.cu; dg_mesh_set_div_stab): zeta_D, zeta_C, the
+    // CG workspace [r | p | q | v''] of dim * ndof doubles each and the Jacobi table [dim][npe]
+    double stab_zD = 0.0, stab_zC = 0.0;
+    double *stab_ws = nullptr, *stab_dinv = nullptr;
+    double stab_dinv_aD = -1.0, stab_dinv_aC = -1.0;
 };
 
 #define CK(call)                                                                                         \
@@ -426,13 +432,14 @@ dg_status diag_impl(dg_mesh *m, double lam, const double *nu, double nu_const, d
 }
 
 // reduce partial[G][2] -> sums[2] (+ allreduce) -> finalize(mode)
-dg_status reduce_fin(dg_mesh *m, int G, int mode)
+dg_status reduce_fin(dg_mesh *m, int G, int mode, const double *partial = nullptr)
 {
+    if (!partial) partial = m->partial;
     if (!m->halo) {
-        CK(launch_reduce_fin(m->partial, G, 2, m->sums, mode, m->scal, m->hist, m->aux, m->st));
+        CK(launch_reduce_fin(partial, G, 2, m->sums, mode, m->scal, m->hist, m->aux, m->st));
         m->launches += 1;
     } else {
-        CK(launch_reduce_s(m->partial, G, 2, m->sums,
+        CK(launch_reduce_s(partial, G, 2, m->sums,
                            (mode == FIN_ALPHA || mode == FIN_BETA) ? m->scal : nullptr, m->st));
         CKS(allreduce(m, m->sums, 2));
         CK(launch_finalize(mode, m->sums, m->scal, m->hist, m->aux, m->st));
@@ -855,6 +862,143 @@ dg_status grad_impl(dg_mesh *mp, dg_mesh *mv, const double *psi, double *const g
     return DG_OK;
 }
 
+// ---------------------------------------------------------------------------
+// divergence / mass-flux stabilisation (stab.cu, reading A26)
+// ---------------------------------------------------------------------------
+dg_status stab_apply_impl(dg_mesh *m, const double *const in[3], double *const out[3], double aD, double aC,
+                          double *partial, const PcgScal *s)
+{
+    StabParams a;
+    const int dim = m->g.dim;
+    for (int c = 0; c < dim; ++c) {
+        a.in[c] = in[c];
+        a.out[c] = out[c];
+        if (m->halo) {
+            CKS(exchange(m, in[c], m->hv_lo[c], m->hv_hi[c]));
+            a.lo[c] = m->hv_lo[c];
+            a.hi[c] = m->hv_hi[c];
+        }
+    }
+    a.aD = aD;
+    a.aC = aC;
+    a.partial = partial;
+    a.s = s;
+    CK(launch_stab_apply(m->g, a, m->st));
+    m->launches += 1;
+    return DG_OK;
+}
+
+// v^ = (M + a_D K_D + a_C K_C)^-1 M v'' in place (v), a_D = dt zeta_D U h / (P+1),
+// a_C = dt zeta_C U with U the RMS of v''; v'' is kept in the workspace's last block
+dg_status stab_solve_impl(dg_mesh *m, double dt, double zD, double zC, double *const v[3], double tol, int maxit,
+                          dg_solve_info *info, double *coef)
+{
+    if (!m->stab_ws) return set_error(DG_EINVAL, "divergence stabilisation workspace missing: call dg_mesh_set_div_stab first");
+    const Geom &g = m->g;
+    const int dim = g.dim, npe = g.npe;
+    const long long nd = m->ndof;
+    StabVec sv;
+    sv.dim = dim;
+    sv.npe = npe;
+    sv.ndof = nd;
+    for (int c = 0; c < dim; ++c) sv.x[c] = v[c];
+    sv.r = m->stab_ws;
+    sv.p = m->stab_ws + dim * nd;
+    sv.q = m->stab_ws + 2 * dim * nd;
+    double *vkeep = m->stab_ws + 3 * dim * nd;
+    sv.dinv = m->stab_dinv;
+    sv.mass_e = m->mass_e;
+    sv.s = m->scal;
+    sv.partial = m->partial;
+    const int G = stab_grid();
+    sv.partial2 = m->partial + 2 * G;
+    for (int c = 0; c < dim; ++c)
+        CK(cudaMemcpyAsync(vkeep + c * nd, v[c], sizeof(double) * (size_t)nd, cudaMemcpyDeviceToDevice, m->st));
+    // U^2 = sum m |v''|^2 / sum m (one device reduction, read by the host for the coefficients)
+    PcgScal s0{};
+    s0.lam = 1.0;  // no null space
+    s0.tol2 = tol * tol;
+    s0.ndof_global = m->ndof_global * dim;
+    s0.maxit = maxit;
+    s0.hist_cap = m->hist_cap;
+    CK(cudaMemcpyAsync(m->scal, &s0, sizeof(s0), cudaMemcpyHostToDevice, m->st));
+    CK(launch_stab_vec(STAB_U2, sv, m->st));
+    m->launches += 1;
+    CKS(reduce_fin(m, G, FIN_NUMEAN));
+    CK(cudaMemcpyAsync(m->hscal, m->scal, sizeof(PcgScal), cudaMemcpyDeviceToHost, m->st));
+    CK(cudaStreamSynchronize(m->st));
+    const double U = std::sqrt(std::max(m->hscal->nu_eff, 0.0));
+    double hh = 1.0;
+    for (int d = 0; d < dim; ++d) hh *= g.h[d];
+    hh = std::pow(hh, 1.0 / dim);
+    const double aD = dt * zD * U * hh / (g.P + 1), aC = dt * zC * U;
+    if (coef) {
+        coef[0] = aD;
+        coef[1] = aC;
+        coef[2] = U;
+    }
+    // Jacobi table 1/diag, diag_{c,I} = m_I + W_perp [a_D (2/h_c) sum_k w_k D_ki^2 + a_C (i in {0, P})]
+    if (aD != m->stab_dinv_aD || aC != m->stab_dinv_aC) {
+        const Tab &t = host_tab(g.P);
+        const int n = g.n;
+        std::vector<double> tab((size_t)dim * npe);
+        for (int c = 0; c < dim; ++c)
+            for (int I = 0; I < npe; ++I) {
+                const int qc[3] = {I % n, (I / n) % n, dim == 3 ? I / (n * n) : 0};
+                double mI = g.mfac;
+                for (int d = 0; d < dim; ++d) mI *= t.w[qc[d]];
+                const int i = qc[c];
+                const double Wp = mI / (t.w[i] * 0.5 * g.h[c]);
+                double kd = 0.0;
+                for (int k = 0; k < n; ++k) kd += t.w[k] * t.D[k][i] * t.D[k][i];
+                const double dg = mI + Wp * (aD * g.sd[c] * kd + ((i == 0 || i == g.P) ? aC : 0.0));
+                tab[(size_t)c * npe + I] = 1.0 / dg;
+            }
+        CK(cudaMemcpyAsync(m->stab_dinv, tab.data(), sizeof(double) * tab.size(), cudaMemcpyHostToDevice, m->st));
+        CK(cudaStreamSynchronize(m->st));  // tab is a host temporary
+        m->stab_dinv_aD = aD;
+        m->stab_dinv_aC = aC;
+    }
+    // r = M v'' - A v'' ; z = D^-1 r (never stored)
+    {
+        double *qq[3] = {sv.q, sv.q + nd, sv.q + 2 * nd};
+        const double *xx[3] = {v[0], v[1], dim == 3 ? v[2] : nullptr};
+        CKS(stab_apply_impl(m, xx, qq, aD, aC, nullptr, nullptr));
+    }
+    CK(launch_stab_vec(STAB_INIT, sv, m->st));
+    m->launches += 1;
+    CKS(reduce_fin(m, G, FIN_INIT, sv.partial2));   // fnorm2 = ||v''||^2
+    CKS(reduce_fin(m, G, FIN_INIT2));                // r.z, ||M^-1 r||^2, convergence test
+    CK(cudaMemsetAsync(sv.p, 0, sizeof(double) * (size_t)dim * nd, m->st));
+    const int GA = (int)std::min<long long>(g.nel, G);
+    for (;;) {
+        CK(cudaMemcpyAsync(m->hscal, m->scal, sizeof(PcgScal), cudaMemcpyDeviceToHost, m->st));
+        CK(cudaStreamSynchronize(m->st));
+        if (m->hscal->done) break;
+        for (int it = 0; it < 8; ++it) {
+            CK(launch_stab_vec(STAB_PUPD, sv, m->st));
+            const double *pp[3] = {sv.p, sv.p + nd, dim == 3 ? sv.p + 2 * nd : nullptr};
+            double *qq[3] = {sv.q, sv.q + nd, dim == 3 ? sv.q + 2 * nd : nullptr};
+            CKS(stab_apply_impl(m, pp, qq, aD, aC, m->partial, m->scal));
+            CKS(reduce_fin(m, GA, FIN_ALPHA));
+            CK(launch_stab_vec(STAB_UPDATE, sv, m->st));
+            CKS(reduce_fin(m, G, FIN_BETA));
+            m->launches += 2;
+        }
+    }
+    const PcgScal hs = *m->hscal;
+    if (info) {
+        info->iters = hs.iter;
+        info->rel_res = hs.fnorm2 > 0 ? std::sqrt(hs.res2 / hs.fnorm2) : std::sqrt(hs.res2);
+        info->removed_mean = 0.0;
+        info->f_norm = std::sqrt(hs.fnorm2);
+        info->kappa_est = NAN;
+    }
+    if (hs.status == PCG_ST_BREAKDOWN) return set_error(DG_EBREAKDOWN, "stabilisation CG breakdown");
+    if (hs.status == PCG_ST_MAXIT) return set_error(DG_ENOTCONV, "stabilisation CG reached maxit");
+    return DG_OK;
+}
+
 }  // namespace
 
 // ---------------------------------------------------------------------------
@@ -1005,7 +1149,7 @@ void dg_mesh_destroy(dg_mesh *m)
                       m->sums, m->aux,  m->mass_e, m->hist,  m->h_lo,   m->h_hi, m->hn_lo,
                       m->hn_hi, m->st_a, m->st_b,  m->st_c,  m->sf[0], m->sf[1], m->sf[2], m->sf[3],
                       m->sf[4], m->sf[5], m->d_swF, m->rc_el, m->chat, m->xc, m->rc,
-                      m->ts_lo, m->ts_hi, m->tr_lo, m->tr_hi};
+                      m->ts_lo, m->ts_hi, m->tr_lo, m->tr_hi, m->stab_ws, m->stab_dinv};
     for (double *b : bufs)
         if (b) cudaFree(b);
     for (int c = 0; c < 3; ++c) {
@@ -1304,6 +1448,26 @@ dg_status dg_imex_stage(dg_mesh *mv, dg_mesh *mp, double dt, double a_ex21, doub
         CK(launch_stage_project(g, mv->mass_e, lamH, gw[c], vout[c], Fc[c], mv->st));
         mv->launches += 1;
     }
+    // divergence / mass-flux stabilisation of v'' (reading A26; dg_mesh_set_div_stab),
+    // and line 8's rhs follows: f_H += lam (v^ - v'')
+    if (mv->stab_zD > 0.0 || mv->stab_zC > 0.0) {
+        dg_solve_info is{};
+        s = stab_solve_impl(mv, dt, mv->stab_zD, mv->stab_zC, vout, tol, maxit, &is, nullptr);
+        if (info) info->stab = is;
+        if (s != DG_OK) return s;
+        const double *vkeep = mv->stab_ws + 3 * (long long)dim * mv->ndof;
+        for (int c = 0; c < dim; ++c) {
+            LinComb lc;
+            lc.x0 = Fc[c];
+            lc.c0 = 1.0;
+            lc.c[lc.n] = lamH;
+            lc.y[lc.n++] = vout[c];
+            lc.c[lc.n] = -lamH;
+            lc.y[lc.n++] = vkeep + c * mv->ndof;
+            CK(launch_lincomb(g, lc, mv->mass_e, Fc[c], mv->st));
+            mv->launches += 1;
+        }
+    }
     // line 9: v_i - dt a_ii div(nu grad v_i) = g_i per component, from the guess v''
     for (int c = 0; c < dim; ++c) {
         dg_solve_info iv{};
@@ -1429,6 +1593,15 @@ dg_status dg_imex_rk_step(dg_mesh *mv, dg_mesh *mp, const dg_tableau *tab, doubl
             CK(launch_lincomb(g, lc, mv->mass_e, vp[c], mv->st));
             mv->launches += 1;
         }
+        if (mv->stab_zD > 0.0 || mv->stab_zC > 0.0) {  // P:1040, reading A26
+            dg_solve_info is{};
+            st = stab_solve_impl(mv, dt, mv->stab_zD, mv->stab_zC, vp, tol, maxit, &is, nullptr);
+            inf.stab_iters += is.iters;
+            if (st != DG_OK) {
+                if (info) *info = inf;
+                return st;
+            }
+        }
         // lines 8-9: g_i = v'' + dt sum_j [(a_im - a_ex)[i][j] F_d1,j - a_ex[i][j] F_d3,j],
         // F_d3,j = -nu grad div u_j ;  v_i - dt a_ii nu lap v_i = g_i
         const double aii = tab->a_im[i][i];
@@ -1487,6 +1660,43 @@ dg_status dg_imex_rk_step(dg_mesh *mv, dg_mesh *mp, const dg_tableau *tab, doubl
     CK(cudaStreamSynchronize(mv->st));
     if (info) *info = inf;
     return DG_OK;
+}
+
+dg_status dg_mesh_set_div_stab(dg_mesh *mv, double zeta_D, double zeta_C)
+{
+    if (!mv) return set_error(DG_EINVAL, "null mesh");
+    if (!(zeta_D >= 0.0) || !(zeta_C >= 0.0) || !std::isfinite(zeta_D) || !std::isfinite(zeta_C))
+        return set_error(DG_EINVAL, "zeta_D, zeta_C must be finite and >= 0");
+    if ((zeta_D > 0.0 || zeta_C > 0.0) && !mv->stab_ws) {
+        CKS(alloc((void **)&mv->stab_ws, sizeof(double) * 4 * (size_t)mv->g.dim * (size_t)mv->ndof));
+        CKS(alloc((void **)&mv->stab_dinv, sizeof(double) * (size_t)mv->g.dim * (size_t)mv->g.npe));
+    }
+    mv->stab_zD = zeta_D;
+    mv->stab_zC = zeta_C;
+    return DG_OK;
+}
+
+dg_status dg_div_stab_apply(dg_mesh *m, double a_D, double a_C, const double *const v[3], double *const out[3])
+{
+    if (!m || !v || !out) return set_error(DG_EINVAL, "null argument");
+    for (int c = 0; c < m->g.dim; ++c) {
+        if (!v[c] || !out[c]) return set_error(DG_EINVAL, "null component pointer");
+        for (int c2 = 0; c2 < m->g.dim; ++c2)
+            if (out[c] == v[c2]) return set_error(DG_EINVAL, "out must not alias v");
+    }
+    if (!(a_D >= 0.0) || !(a_C >= 0.0)) return set_error(DG_EINVAL, "a_D, a_C must be >= 0");
+    return stab_apply_impl(m, v, out, a_D, a_C, nullptr, nullptr);
+}
+
+dg_status dg_div_stab_solve(dg_mesh *m, double dt, double zeta_D, double zeta_C, double *const v[3], double tol,
+                            int maxit, double coef[3], dg_solve_info *info)
+{
+    if (!m || !v) return set_error(DG_EINVAL, "null argument");
+    for (int c = 0; c < m->g.dim; ++c)
+        if (!v[c]) return set_error(DG_EINVAL, "null component pointer");
+    if (!(dt > 0.0) || !(zeta_D >= 0.0) || !(zeta_C >= 0.0) || !(tol > 0.0) || maxit < 1)
+        return set_error(DG_EINVAL, "dt > 0, zeta >= 0, tol > 0, maxit >= 1 required");
+    return stab_solve_impl(m, dt, zeta_D, zeta_C, v, tol, maxit, info, coef);
 }
 
 dg_status dg_derivative(dg_mesh *m, const double *u, double *const out[3])
@@ -1647,6 +1857,12 @@ dg_status dg_imex_rk_step_vv(dg_mesh *mv, dg_mesh *mp, const dg_tableau *tab, do
             lc.cm = -1.0;
             CK(launch_lincomb(g, lc, mv->mass_e, w[c], mv->st));
             mv->launches += 1;
+        }
+        if (mv->stab_zD > 0.0 || mv->stab_zC > 0.0) {  // P:1040, reading A26
+            dg_solve_info is{};
+            const dg_status ss = stab_solve_impl(mv, dt, mv->stab_zD, mv->stab_zC, w, tol, maxit, &is, nullptr);
+            inf.stab_iters += is.iters;
+            if (ss != DG_OK) return ss;
         }
         return DG_OK;
     };

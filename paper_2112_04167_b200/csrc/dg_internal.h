@@ -313,6 +313,31 @@ cudaError_t launch_sw_coarse(const SwCoarseParams &a, const SwTab &h, int stage,
 cudaError_t launch_sw_gather_local(const SwCoarseParams &a, int S, int off, int nl, cudaStream_t st);
 int sw_cz_grid(const SwTab &h);
 
+// stab.cu -- divergence / mass-flux stabilisation of the projection (reading A26)
+struct StabParams {
+    const double *in[3] = {nullptr, nullptr, nullptr};   // velocity components (apply operand)
+    const double *lo[3] = {nullptr, nullptr, nullptr}, *hi[3] = {nullptr, nullptr, nullptr};  // rank halo layers
+    double *out[3] = {nullptr, nullptr, nullptr};        // (M + a_D K_D + a_C K_C) in (weak)
+    double aD = 0.0, aC = 0.0;
+    double *partial = nullptr;                           // [grid][2]: in . out, 0
+    const PcgScal *s = nullptr;                          // done flag (CG) or null
+};
+struct StabVec {                                          // CG vectors: r, p, q are [dim][ndof] blocks
+    int dim = 3, npe = 0;
+    long long ndof = 0;
+    double *x[3] = {nullptr, nullptr, nullptr};           // the solution (in place: v'' on entry)
+    double *r = nullptr, *p = nullptr, *q = nullptr;
+    const double *dinv = nullptr;                         // [dim][npe] Jacobi table
+    const double *mass_e = nullptr;                       // [npe] m, [npe] 1/m
+    const PcgScal *s = nullptr;
+    double *partial = nullptr, *partial2 = nullptr;
+};
+enum { STAB_INIT = 0, STAB_PUPD = 1, STAB_UPDATE = 2, STAB_U2 = 3 };
+int stab_grid();
+cudaError_t launch_stab_apply(const Geom &g, const StabParams &a, cudaStream_t st);
+cudaError_t launch_stab_vec(int op, const StabVec &a, cudaStream_t st);
+cudaError_t upload_tables_stab();
+
 // visc.cu -- variable-viscosity step pieces
 struct DerivParams {
     const double *u = nullptr;

@@ -19,11 +19,15 @@ def tg(X, t, nu):
     return vx, vy
 
 
-def run(name, N=8, P=8, ks=(5, 6, 7, 8), nu=0.02, T=0.25):
+def run(name, N=8, P=8, ks=(5, 6, 7, 8), nu=0.02, T=0.25, stab=None):
+    """stab = (zeta_D, zeta_C): divergence / mass-flux stabilisation after every projection
+    (reading A26); None: off."""
     dev = torch.device("cuda")
     st = torch.cuda.current_stream()
     mv = dg.dg_mesh_create(2, (N, N), (1.0, 1.0), P, stream=st)
     mp = dg.dg_mesh_create(2, (N, N), (1.0, 1.0), P - 1, stream=st)
+    if stab is not None:
+        dg.dg_mesh_set_div_stab(mv, *stab)
     X = node_coords(2, (N, N), (1.0, 1.0), P)
     errs = []
     for k in ks:
@@ -35,12 +39,18 @@ def run(name, N=8, P=8, ks=(5, 6, 7, 8), nu=0.02, T=0.25):
             dg.dg_imex_rk_step(mv, mp, dg.TABLEAUX[name], dt, nu, v, psi, 1e-13, 20000)
         ve = tg(X, T, nu)
         err = math.sqrt(sum(float(((v[c].cpu().numpy() - ve[c]) ** 2).mean()) for c in range(2)) / 2)
-        errs.append(err)
-    eoc = [math.log2(errs[i] / errs[i + 1]) for i in range(len(errs) - 1)]
+        errs.append(err if math.isfinite(err) else float("inf"))
+    eoc = [math.log2(errs[i] / errs[i + 1]) if math.isfinite(errs[i]) and errs[i + 1] > 0 else float("nan")
+           for i in range(len(errs) - 1)]
     return errs, eoc
 
 
 if __name__ == "__main__":
-    for name in ("RK-ARS3", "RK-CB3e", "RK-CB2"):
-        errs, eoc = run(name)
-        print(name, ["%.3e" % e for e in errs], ["%.2f" % x for x in eoc], flush=True)
+    for stab in (None, (1.0, 1.0)):
+        for name in ("RK-ARS3", "RK-CB3e", "RK-CB2", "RK-TR"):
+            try:
+                errs, eoc = run(name, stab=stab)
+            except Exception as e:  # a diverging run may fail inside a solve
+                print(name, "stab" if stab else "nostab", "failed:", str(e)[:100], flush=True)
+                continue
+            print(name, "stab" if stab else "nostab", ["%.3e" % e for e in errs], ["%.2f" % x for x in eoc], flush=True)
