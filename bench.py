@@ -43,6 +43,15 @@ BYTES_PER_DOF = {True: 24.0, False: 16.0}  # algorithmic bytes per DOF per apply
 PCG_BYTES_PER_DOF = {True: 104.0, False: 96.0}
 
 
+_JSON_FD = None
+
+
+def emit(line):
+    """The one JSON line on the ORIGINAL stdout (everything else -- NCCL's banner, library
+    prints -- goes to stderr, see main)."""
+    os.write(_JSON_FD if _JSON_FD is not None else 1, (json.dumps(line) + "\n").encode())
+
+
 def measured_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -112,6 +121,47 @@ class Clocks:
 # seeded inputs for one rank's slab (identical values to the global canonical arrays;
 # tests/test_multirank_gloo.py checks that)
 # ---------------------------------------------------------------------------
+def measure_traffic(workload_id, kernel_regex="k_apply", timeout_s=240):
+    """DRAM bytes (read + write) of one launch of the dispatched apply kernel, measured by ncu
+    on tools/one_apply.py for THIS build (a byte count, not a timing).  None + reason if ncu is
+    unavailable or fails."""
+    ncu = None
+    for cand in ("/usr/local/cuda/bin/ncu", "ncu"):
+        try:
+            subprocess.run([cand, "--version"], capture_output=True, timeout=30, check=True)
+            ncu = cand
+            break
+        except Exception:
+            continue
+    if ncu is None:
+        return None, "ncu not available"
+    cmd = [ncu, "--metrics", "dram__bytes_read.sum,dram__bytes_write.sum", "-k", "regex:" + kernel_regex, "-s", "1",
+           "-c", "1", "--csv", sys.executable, os.path.join(ROOT, "tools", "one_apply.py"), str(workload_id)]
+    try:
+        r = subprocess.run(cmd, capture_output=True, text=True, timeout=timeout_s)
+    except Exception as e:
+        return None, "ncu run failed: %s" % str(e)[:80]
+    tot, seen = 0.0, 0
+    for ln in r.stdout.splitlines():
+        f = [x.strip().strip('"') for x in ln.split('","')]
+        if len(f) > 3 and f[-3].startswith("dram__bytes_"):
+            unit, val = f[-2], float(f[-1].replace(",", ""))
+            scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "KB": 1e3, "MB": 1e6, "GB": 1e9}.get(unit, 1)
+            tot += val * scale
+            seen += 1
+    if seen < 2:
+        return None, "ncu output not parsed (rc %d): %s" % (r.returncode, (r.stderr or r.stdout)[-120:])
+    return tot, "ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum, one launch of the dispatched kernel"
+
+
+def config_dict(c, world):
+    """The workload description both arms report (identical keys and values)."""
+    nu = {5: "1e-3(1+0.5tanh(4 sin x sin y sin z)) at GLL nodes", 2: "0.01(1+0.5 sin x cos y) at GLL nodes"}
+    return {"workload": c.name, "N": list(c.N[: c.dim]), "P": c.P, "ndof": c.ndof, "lam": c.lam,
+            "nu": nu.get(c.cid, c.nu0), "parallelism": "z-slabs x%d" % world,
+            "l2": "inputs larger than L2 (%.0f MB per field)" % (c.ndof * 8 / 1e6)}
+
+
 def slab_inputs(c, el_off, nel):
     return c.apply_input_slab(el_off, nel), c.rhs_slab(0, el_off, nel), c.nu_slab(el_off, nel)
 
@@ -151,7 +201,6 @@ def run_reference(args, rank, world):
     if rank != 0:
         return
     c = get_config(WORKLOADS[args.workload])
-    cb = time_oracle(c)
     steps_t = []
     import oracle
 
@@ -166,14 +215,18 @@ def run_reference(args, rank, world):
             steps_t.append(dt)
     t = statistics.mean(steps_t)
     val = len(elems) * c.n ** c.dim / t / 1e9
+    cb = {"value": val, "unit": "GDOF/s", "cores": int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1)),
+          "kind": "oracle",
+          "sample": "each step: oracle_sip_apply (explicit GLL quadrature, C/OpenMP, as it stands) on the same %d "
+                    "seeded random elements of %s (%d DOF); value = sampled DOF / mean step time"
+                    % (len(elems), c.name, len(elems) * c.n ** c.dim)}
     line = {"metric": "GDOF/s SIP-DG Helmholtz apply", "value": val, "unit": "GDOF/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
-            "config": {"workload": c.name, "N": list(c.N), "P": c.P, "ndof": c.ndof,
-                       "sample_elements": int(len(elems))},
+            "config": config_dict(c, world),
             "cpu_baseline": cb, "e2e": {"value": val, "unit": "GDOF/s", "h2d_bytes_per_step": 0,
                                         "d2h_bytes_per_step": 0}}
-    print(json.dumps(line), flush=True)
+    emit(line)
 
 
 # ---------------------------------------------------------------------------
@@ -236,6 +289,7 @@ def run_product(args, rank, world, local_rank):
     t_end.record(stream)
     barrier()
     launches = dg.dg_mesh_launch_count(m) - l0
+    kernel_name = dg.dg_last_apply_kernel()
     total_ms = max_over_ranks(t_start.elapsed_time(t_end))
     per_launch_ms = statistics.mean(ev[2 * k].elapsed_time(ev[2 * k + 1]) for k in range(args.steps))
     per_launch_ms = max_over_ranks(per_launch_ms)
@@ -269,6 +323,13 @@ def run_product(args, rank, world, local_rank):
         stage = run_stage(dg, torch, stream, barrier)
         stage["vv_step"] = run_vv_step(dg, torch, stream, barrier)
 
+    # ---- per-config legs (c1..c4) and the halo-mode data plane (1 GPU)
+    configs = halo = None
+    peak0, _ = measured_peaks()
+    if world == 1 and not args.no_configs:
+        configs = run_configs(dg, torch, stream, peak0)
+        halo = run_halo(dg, torch, stream, c, u, nu, f, peak0)
+
     # ---- e2e through the host-buffer C-ABI call (rank-local slab)
     u_np = np.ascontiguousarray(u_h)
     nu_np = None if nu_h is None else np.ascontiguousarray(nu_h)
@@ -295,14 +356,9 @@ def run_product(args, rank, world, local_rank):
     bpd = BYTES_PER_DOF[varnu]
     nd_local = m.ndof
     achieved = nd_local * bpd / (per_launch_ms * 1e-3) / 1e9
-    traffic = None
-    prof = os.path.join(ROOT, "profiles", "ncu_summary.json")
-    if os.path.exists(prof):
-        try:
-            with open(prof) as fh:
-                traffic = json.load(fh).get(args.workload, {}).get("apply_dram_bytes_per_launch")
-        except Exception:
-            traffic = None
+    traffic, traffic_how = (None, "skipped (--no-traffic)")
+    if world == 1 and not args.no_traffic:
+        traffic, traffic_how = measure_traffic(WORKLOADS[args.workload])
     cb = None
     if world == 1 and not args.no_cpu_baseline:
         cb = time_oracle(c)
@@ -320,9 +376,7 @@ def run_product(args, rank, world, local_rank):
         "dtype": "f64",
         "data": "synthetic",
         "impl": "product",
-        "config": {"workload": c.name, "N": list(c.N), "P": c.P, "ndof": ndof_global, "lam": c.lam,
-                   "nu": "1e-3(1+0.5tanh(4 sin x sin y sin z)) at GLL nodes", "parallelism": "z-slabs x%d" % world,
-                   "bricks": None, "l2": "inputs larger than L2 (%.0f MB per field)" % (ndof_global * 8 / 1e6)},
+        "config": config_dict(c, world),
         "pcg": {"iters_per_s": it / (t_solve * 1e-3), "iters": it, "ms_per_solve": t_solve, "tol": c.tol,
                 "solves": args.solves, "rel_res": infos[-1]["rel_res"], "kappa_est": infos[-1]["kappa_est"],
                 "gdof_iter_per_s": ndof_global * it / (t_solve * 1e-3) / 1e9,
@@ -330,15 +384,112 @@ def run_product(args, rank, world, local_rank):
                 "achieved_gbs_incl_setup": ndof_global * it * PCG_BYTES_PER_DOF[varnu] / (t_solve * 1e-3) / 1e9},
         "stage": stage,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": traffic, "kernel": ("v6::k_apply6<%d,%s,0>" if c.P <= 5 and c.P % 2 else "v5::k_apply5<%d,%s,0>") % (c.P, "1" if varnu else "0"),
-                     "bytes_per_dof": bpd, "peak_kind": peak_kind, "launch_ms": per_launch_ms},
+                     "traffic": traffic, "traffic_how": traffic_how,
+                     "traffic_over_algorithmic": (traffic / (nd_local * bpd)) if traffic else None,
+                     "kernel": kernel_name, "bytes_per_dof": bpd, "peak_kind": peak_kind, "launch_ms": per_launch_ms},
+        "configs": configs,
+        "halo": halo,
+        "paper_context": PAPER_CONTEXT,
         "e2e": {"value": ndof_global / e2e_s / 1e9, "unit": "GDOF/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "ms_per_step": e2e_s * 1e3},
         "gpu_launches": launches,
         "clocks": clk.summary(),
         "cpu_baseline": cb,
     }
-    print(json.dumps(line), flush=True)
+    emit(line)
+
+
+def time_apply(dg, torch, stream, m, lam, nu, nu0, u, out, reps=20, warm=3):
+    """Mean CUDA-event time (ms) of one apply launch on the mesh stream, and the kernel name."""
+    for _ in range(warm):
+        dg.dg_helmholtz_apply(m, lam, nu, nu0, u, out)
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    for _ in range(reps):
+        dg.dg_helmholtz_apply(m, lam, nu, nu0, u, out)
+    b.record(stream)
+    torch.cuda.synchronize()
+    return a.elapsed_time(b) / reps, dg.dg_last_apply_kernel()
+
+
+def time_solves(dg, torch, stream, m, lam, nu, nu0, f, tol, maxit, reps=2):
+    """(ms per solve, iterations) of Jacobi-PCG (or the mesh's preconditioner) from u0 = 0."""
+    times, info = [], None
+    for k in range(reps + 1):
+        x = torch.zeros_like(f)
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        info = dg.dg_pcg_solve(m, lam, nu, nu0, f, tol, maxit, x)
+        b.record(stream)
+        torch.cuda.synchronize()
+        if k > 0:
+            times.append(a.elapsed_time(b))
+    return statistics.mean(times), info.iters
+
+
+def run_configs(dg, torch, stream, peak):
+    """Per-config measurements (SURVEY §8(d) roofline table) for BASELINE configs[0..3]: apply
+    time (c1 in us per call: launch-bound), GDOF/s and fraction of the measured HBM bandwidth at
+    the algorithmic 16 (constant nu) / 24 (variable nu) B per DOF, and PCG iterations/s of the
+    config's solves (c3: the three-component velocity Helmholtz and the P-1 pressure Poisson with
+    Jacobi and with the two-level Schwarz preconditioner)."""
+    from workloads import config
+
+    dev = torch.device("cuda", torch.cuda.current_device())
+    out = {}
+    for cid in (1, 2, 3, 4):
+        c = config(cid)
+        m = dg.dg_mesh_create(c.dim, c.N[: c.dim], c.L[: c.dim], c.P, stream=stream)
+        u = torch.from_numpy(c.apply_input()).to(dev)
+        nuh = c.nu()
+        nu = None if nuh is None else torch.from_numpy(nuh).to(dev)
+        o = torch.empty_like(u)
+        ms, kern = time_apply(dg, torch, stream, m, c.lam, nu, c.nu0, u, o, reps=200 if cid == 1 else 20)
+        bpd = BYTES_PER_DOF[nu is not None]
+        d = {"workload": c.name, "ndof": c.ndof, "apply_us": ms * 1e3, "apply_gdofs": c.ndof / (ms * 1e-3) / 1e9,
+             "apply_frac_hbm": c.ndof * bpd / (ms * 1e-3) / 1e9 / peak, "bytes_per_dof": bpd, "kernel": kern}
+        f = torch.from_numpy(c.rhs(0)).to(dev)
+        tol = 1e-11 if cid in (1, 2) else c.tol
+        t, it = time_solves(dg, torch, stream, m, c.lam, nu, c.nu0, f, tol, 5000)
+        d["helmholtz"] = {"ms_per_solve": t, "iters": it, "iters_per_s": it / (t * 1e-3), "tol": tol}
+        if cid == 3:
+            mp = dg.dg_mesh_create(3, c.N, c.L, c.P_p, stream=stream)
+            fp = torch.from_numpy(c.poisson_rhs_raw()).to(dev)
+            tj, ij = time_solves(dg, torch, stream, mp, 0.0, None, 1.0, fp, c.tol, 20000, reps=1)
+            dg.dg_mesh_set_precond(mp, dg.DG_PC_SCHWARZ2)
+            ts, isw = time_solves(dg, torch, stream, mp, 0.0, None, 1.0, fp, c.tol, 20000, reps=1)
+            d["poisson_P%d" % c.P_p] = {"jacobi": {"ms_per_solve": tj, "iters": ij, "iters_per_s": ij / (tj * 1e-3)},
+                                        "schwarz2": {"ms_per_solve": ts, "iters": isw, "iters_per_s": isw / (ts * 1e-3)},
+                                        "ndof": mp.ndof}
+            dg.dg_mesh_destroy(mp)
+        dg.dg_mesh_destroy(m)
+        out["c%d" % cid] = d
+    return out
+
+
+def run_halo(dg, torch, stream, c, u, nu, f, peak, reps=20):
+    """The multi-GPU data plane on one GPU (1-rank halo mode: face traces through NCCL self
+    send/recv on the exchange stream, interior / boundary layer split): c5 apply and PCG."""
+    m = dg.dg_mesh_create(c.dim, c.N[: c.dim], c.L[: c.dim], c.P, stream=stream, halo_mode=True)
+    o = torch.empty_like(u)
+    ms, _ = time_apply(dg, torch, stream, m, c.lam, nu, c.nu0, u, o, reps=reps)
+    t, it = time_solves(dg, torch, stream, m, c.lam, nu, c.nu0, f, c.tol, 5000)
+    dg.dg_mesh_destroy(m)
+    bpd = BYTES_PER_DOF[nu is not None]
+    return {"mode": "1-rank halo mode (NCCL self send/recv of the slab face traces)", "apply_ms": ms,
+            "apply_gdofs": c.ndof / (ms * 1e-3) / 1e9, "apply_frac_hbm": c.ndof * bpd / (ms * 1e-3) / 1e9 / peak,
+            "pcg_iters": it, "pcg_ms_per_solve": t, "pcg_iters_per_s": it / (t * 1e-3)}
+
+
+PAPER_CONTEXT = {
+    "source": "PAPER.md Table 3 (P:1499-1505), Taylor-Green DNS, 32^3 elements, P = 15 velocity / 14 pressure, "
+              "512 cores Intel Xeon E5-2680 v3, precision not stated; context only (no throughput of this path "
+              "is reported in the paper)",
+    "avg_runtime_per_step_s": {"BDF2 dt=2e-4": 4.26, "BDF2 dt=1.2e-3": 3.61, "RK-CB3e dt=2.4e-3": 14.77,
+                               "RK-ARS3 dt=8e-4": 18.19, "RK-ARS3 dt=1.6e-3": 14.71},
+}
 
 
 def run_vv_step(dg, torch, stream, barrier, N=16, P=7, reps=2):
@@ -420,6 +571,11 @@ def run_stage(dg, torch, stream, barrier, reps=2):
     ms_j, dj = timed(0, 1)
     dg.dg_mesh_set_precond(mp, dg.DG_PC_SCHWARZ2)
     times = [ms_sw]
+    # the same stage with the divergence / mass-flux stabilisation after the projection
+    # (reading A26, zeta_D = zeta_C = 1)
+    dg.dg_mesh_set_div_stab(mv, 1.0, 1.0)
+    ms_st, dst = timed(0, 1)
+    dg.dg_mesh_set_div_stab(mv, 0.0, 0.0)
     # one whole constant-nu IMEX-RK step (NEXT-2, Alg. 3 with RK-ARS3: 4 implicit stages) on the
     # same mesh pair and velocity, Schwarz Poisson
     vs = [x.clone() for x in v]
@@ -458,12 +614,17 @@ def run_stage(dg, torch, stream, barrier, reps=2):
     return {"workload": c4.name, "ms_per_stage": statistics.mean(times), "stages": reps, "convect": conv,
             "pressure_precond": "schwarz2 (element FDM blocks + Q1 coarse)", "rk_step": rk,
             "jacobi": {"ms_per_stage": ms_j, "pressure_iters": dj["pressure"]["iters"]},
+            "div_stab": {"ms_per_stage": ms_st, "stab_iters": dst["stab"]["iters"], "zeta": [1.0, 1.0]},
             "pressure_P": c4.P_p, "pressure_iters": d["pressure"]["iters"],
             "velocity_iters": [x["iters"] for x in d["velocity"]], "tol": c4.tol,
             "dofs": {"velocity_per_component": mv.ndof, "pressure": mp.ndof}}
 
 
 def main():
+    global _JSON_FD
+    sys.stdout.flush()
+    _JSON_FD = os.dup(1)   # keep the real stdout for the JSON line ...
+    os.dup2(2, 1)          # ... and route every other write to fd 1 (native libraries too) to stderr
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=100)
@@ -474,6 +635,8 @@ def main():
     ap.add_argument("--workload", default="c5", choices=sorted(WORKLOADS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-stage", action="store_true", help="skip the config-4 IMEX stage leg")
+    ap.add_argument("--no-configs", action="store_true", help="skip the per-config (c1..c4) and halo-mode legs")
+    ap.add_argument("--no-traffic", action="store_true", help="skip the ncu DRAM-traffic measurement")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -488,6 +651,7 @@ def main():
         import torch
         import torch.distributed as dist
 
+        os.environ.setdefault("NCCL_DEBUG", "INFO")  # the NCCL transport (NVLink / NVLS) in the log
         torch.cuda.set_device(local_rank)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     try:

@@ -323,6 +323,11 @@ dg_status dg_gll_tables(int P, double *xi, double *w, double *D);
 /* Number of kernel launches this mesh enqueued since creation (evidence for bench.py). */
 long long dg_mesh_launch_count(const dg_mesh *m);
 
+/* The last operator-apply kernel this thread dispatched (generation, template parameters, grid,
+ * brick shape), e.g. "v6::k_apply6<dim=3,P=5,varnu=1,mode=0> grid=148 brick=4x4x1" (evidence for
+ * bench.py's roofline line). */
+const char *dg_last_apply_kernel(void);
+
 /* Message for the last failing call on this thread ("" if none). */
 const char *dg_last_error(void);
 

@@ -39,6 +39,7 @@ from ._capi import (  # noqa: F401
     dg_imex_rk_step,
     dg_imex_rk_step_vv,
     dg_imex_stage,
+    dg_last_apply_kernel,
     dg_last_error,
     dg_mesh_create,
     dg_mesh_destroy,

@@ -101,6 +101,7 @@ _c = {
     "dg_helmholtz_diag": _sig("dg_helmholtz_diag", _i, [_vp, _d, _vp, _d, _vp]),
     "dg_pcg_solve": _sig("dg_pcg_solve", _i, [_vp, _d, _vp, _d, _vp, _d, _i, _vp, ctypes.POINTER(SolveInfo)]),
     "dg_convect_rhs": _sig("dg_convect_rhs", _i, [_vp, ctypes.POINTER(_vp), ctypes.POINTER(_vp)]),
+    "dg_last_apply_kernel": _sig("dg_last_apply_kernel", ctypes.c_char_p, []),
     "dg_derivative": _sig("dg_derivative", _i, [_vp, _vp, ctypes.POINTER(_vp)]),
     "dg_mesh_set_div_stab": _sig("dg_mesh_set_div_stab", _i, [_vp, _d, _d]),
     "dg_div_stab_apply": _sig("dg_div_stab_apply", _i, [_vp, _d, _d, ctypes.POINTER(_vp), ctypes.POINTER(_vp)]),
@@ -338,6 +339,10 @@ def dg_derivative(m: Mesh, u, out):
     """Velocity-level central-flux DG derivatives out[c] = D_c u (None skips c) -- include/dg.h."""
     o = (_vp * 3)(*([_ptr(x) for x in out] + [None] * (3 - len(out))))
     _check(_c["dg_derivative"](m.handle, _ptr(u), o))
+
+
+def dg_last_apply_kernel() -> str:
+    return _c["dg_last_apply_kernel"]().decode()
 
 
 def dg_mesh_set_div_stab(mv: Mesh, zeta_D=1.0, zeta_C=1.0):

@@ -29,6 +29,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdio>
 #include <cstdlib>
 
 #include "dev_common.cuh"
@@ -302,6 +303,13 @@ __global__ void __launch_bounds__(256) k_diag(const Geom g, double lam, const do
 // ---------------------------------------------------------------------------
 // host-side dispatch for one dimension
 // ---------------------------------------------------------------------------
+// name of the last dispatched apply kernel of this thread (bench / profiling evidence)
+inline void note_kernel(const char *gen, int dim, int P, bool varnu, int mode, int grid, int bx, int by, int bz)
+{
+    snprintf(last_apply_kernel(), 160, "%s<dim=%d,P=%d,varnu=%d,mode=%d> grid=%d brick=%dx%dx%d", gen, dim, P, varnu ? 1 : 0,
+             mode, grid, bx, by, bz);
+}
+
 template <int DIM>
 struct ApplyDispatch {
     // launch one compile-time brick shape (persistent grid: #SM x occupancy, <= 148 x 8)
@@ -344,6 +352,7 @@ struct ApplyDispatch {
             if (gsz > nunits) gsz = nunits;
             if (gsz < 1) gsz = 1;
             *grid = (int)gsz;
+            note_kernel("k_apply(v4)", DIM, P, VARNU, MODE, (int)gsz, BX, BY, BZ);
             kern<<<(int)gsz, K::NT, K::SMEM_BYTES, st>>>(a);
             return cudaGetLastError();
         }
@@ -401,6 +410,7 @@ struct ApplyDispatch {
             if (gsz > nunits) gsz = nunits;
             if (gsz < 1) gsz = 1;
             *grid = (int)gsz;
+            note_kernel("v5::k_apply5", 3, P, VARNU, MODE, (int)gsz, 2, 2, 2);
             kern<<<(int)gsz, K::NT, K::SMEM_BYTES, st>>>(a);
             return cudaGetLastError();
         }
@@ -477,6 +487,7 @@ struct ApplyDispatch {
             if (gsz > nunits) gsz = nunits;
             if (gsz < 1) gsz = 1;
             *grid = (int)gsz;
+            note_kernel("v6::k_apply6", 3, P, VARNU, MODE, (int)gsz, 4, 4, 1);
             kern<<<(int)gsz, K::NT, K::SMEM_BYTES, st>>>(a);
             return cudaGetLastError();
         }

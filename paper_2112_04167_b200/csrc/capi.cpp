@@ -17,6 +17,9 @@
 namespace dg {
 
 thread_local std::string g_err;
+thread_local char g_last_kernel[160] = "";
+
+char *last_apply_kernel() { return g_last_kernel; }
 
 dg_status set_error(dg_status s, const std::string &msg)
 {
@@ -1007,6 +1010,8 @@ dg_status stab_solve_impl(dg_mesh *m, double dt, double zD, double zC, double *c
 extern "C" {
 
 const char *dg_last_error(void) { return g_err.c_str(); }
+
+const char *dg_last_apply_kernel(void) { return g_last_kernel; }
 
 const char *dg_version(void) { return "dgsip 0.1 (sm_100a, fp64)"; }
 

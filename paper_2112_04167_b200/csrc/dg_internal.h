@@ -63,6 +63,7 @@ const Tab &host_tab(int P);
 
 // error plumbing (capi.cpp)
 dg_status set_error(dg_status s, const std::string &msg);
+char *last_apply_kernel();  // thread-local buffer (160 bytes): the last dispatched apply kernel
 
 // ---------------------------------------------------------------------------
 // kernel launch interface (kernels.cu)
