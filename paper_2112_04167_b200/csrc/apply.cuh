@@ -649,7 +649,7 @@ struct ApplyDispatch {
                 return cudaGetLastError();
             }
 #endif
-            {  // one thread per node (measured faster), one resident wave
+            {  // one thread per node (measured faster than one CTA per element: 1.39 vs 1.73 ms on c5), one resident wave
                 static int resident[2] = {0, 0};
                 const int vi = nu ? 1 : 0;
                 if (!resident[vi]) {

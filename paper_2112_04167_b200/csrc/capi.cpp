@@ -645,33 +645,6 @@ dg_status pcg_impl(dg_mesh *m, double lam, const double *nu, double nu_const, co
         m->launches += 1;
         m->dinv_lam = m->dinv_nu = -1.0;
     }
-    // f mean (lam == 0) and total mass
-    CK(launch_mass_moments(g, f, m->mass_e, m->partial, m->st));
-    m->launches += 1;
-    CKS(reduce_fin(m, VG, FIN_FMEAN));
-    // r = M (f - fmean) - A u; an all-zero guess (one reduction and a host read instead of an
-    // operator application) takes A u = 0
-    CK(launch_abssum(g, u, m->partial, m->st));
-    m->launches += 1;
-    CKS(reduce_fin(m, VG, FIN_ABSSUM));
-    CK(cudaMemcpyAsync(&m->hscal->rz, m->aux, sizeof(double), cudaMemcpyDeviceToHost, m->st));
-    CK(cudaStreamSynchronize(m->st));
-    const double usum = m->hscal->rz;
-    if (usum == 0.0) CK(cudaMemsetAsync(m->q, 0, sizeof(double) * (size_t)m->ndof, m->st));
-    else CKS(halo_apply(m, lam, nu, nu_const, u, m->q, nullptr, nullptr, nullptr, true));
-    CK(launch_pcg_init(g, f, m->q, m->r, m->mass_e, m->scal, m->partial, m->st));
-    m->launches += 1;
-    CKS(reduce_fin(m, VG, FIN_INIT));
-    if (sw) {
-        CKS(sw_pcg_step(m, lam, SW_INIT, FIN_INIT2));
-    } else {
-        CK(launch_pcg_init2(g, m->r, m->dinv, m->z, m->mass_e, m->scal, m->partial, m->st));
-        m->launches += 1;
-        CKS(reduce_fin(m, VG, FIN_INIT2));
-    }
-    CK(cudaMemsetAsync(m->pa, 0, sizeof(double) * (size_t)m->ndof, m->st));
-
-    double *p_old = m->pa, *p_new = m->pb;
     // split PCG step (pupd kernel + apply with the dot epilogue) where the v5 / v6 applies run:
     // measured faster than the fused prologue of v5; halo meshes too (the apply
     // overlaps the face-trace exchange with the interior layers)
@@ -680,6 +653,44 @@ dg_status pcg_impl(dg_mesh *m, double lam, const double *nu, double nu_const, co
     // constant nu on the uniform periodic mesh (N_d >= 2: the closed-form diagonal): the first
     // element's D^-1 serves every element
     const bool table = split && !nu && !self && !DG_DEV_ENV("DG_PCG_NOTABLE");
+    // r = M (f - fmean) - A u; an all-zero guess (one reduction and a host read instead of an
+    // operator application) takes A u = 0
+    CK(launch_abssum(g, u, m->partial, m->st));
+    m->launches += 1;
+    CKS(reduce_fin(m, VG, FIN_ABSSUM));
+    CK(cudaMemcpyAsync(&m->hscal->rz, m->aux, sizeof(double), cudaMemcpyDeviceToHost, m->st));
+    CK(cudaStreamSynchronize(m->st));
+    const double usum = m->hscal->rz;
+    if (usum != 0.0) CKS(halo_apply(m, lam, nu, nu_const, u, m->q, nullptr, nullptr, nullptr, true));
+    if (lam > 0.0 && !sw) {
+        // no mean projection: r, z (or nothing with the D^-1 table) and both partial sets in one pass
+        CK(launch_pcg_init_fused(g, f, usum != 0.0 ? m->q : nullptr, m->r, m->dinv, table ? 1 : 0,
+                                 table ? nullptr : m->z, m->mass_e, m->partial, m->partial + 2 * VG, m->st));
+        m->launches += 1;
+        CKS(reduce_fin(m, VG, FIN_INIT, m->partial + 2 * VG));
+        CKS(reduce_fin(m, VG, FIN_INIT2));
+    } else {
+        // f mean (lam == 0) and total mass
+        CK(launch_mass_moments(g, f, m->mass_e, m->partial, m->st));
+        m->launches += 1;
+        CKS(reduce_fin(m, VG, FIN_FMEAN));
+        if (usum == 0.0) CK(cudaMemsetAsync(m->q, 0, sizeof(double) * (size_t)m->ndof, m->st));
+        CK(launch_pcg_init(g, f, m->q, m->r, m->mass_e, m->scal, m->partial, m->st));
+        m->launches += 1;
+        CKS(reduce_fin(m, VG, FIN_INIT));
+        if (sw) {
+            CKS(sw_pcg_step(m, lam, SW_INIT, FIN_INIT2));
+        } else {
+            CK(launch_pcg_init2(g, m->r, m->dinv, m->z, m->mass_e, m->scal, m->partial, m->st));
+            m->launches += 1;
+            CKS(reduce_fin(m, VG, FIN_INIT2));
+        }
+    }
+    // the split p updates treat alpha = beta = 0 (before the first iteration) as p = z without
+    // reading p; the other variants read p_old from the start
+    if (!split) CK(cudaMemsetAsync(m->pa, 0, sizeof(double) * (size_t)m->ndof, m->st));
+
+    double *p_old = m->pa, *p_new = m->pb;
     // iterations are enqueued in chunks between host convergence checks; after the first chunk
     // the next one is sized from the observed residual reduction per iteration (launches past
     // convergence exit at their first instruction but still cost a few microseconds each)

@@ -221,6 +221,11 @@ cudaError_t launch_mass_moments(const Geom &g, const double *f, const double *ma
 // r = m (f - fmean) - Ar ; partial: sum r, sum (f-fmean)^2
 cudaError_t launch_pcg_init(const Geom &g, const double *f, const double *Ar, double *r, const double *mass_e,
                             const PcgScal *s, double *partial, cudaStream_t st);
+// lam > 0: r = M f - Ar (Ar may be null), z = D^-1 r (dinv_table: dinv is the [npe] table, z may be
+// null), partials [r.z, sum (r/m)^2] -> partial, [0, sum f^2] -> partial2
+cudaError_t launch_pcg_init_fused(const Geom &g, const double *f, const double *Ar, double *r, const double *dinv,
+                                  int dinv_table, double *z, const double *mass_e, double *partial, double *partial2,
+                                  cudaStream_t st);
 // r -= rmean (lam==0) ; z = dinv r ; partial: r.z, sum (r/m)^2
 cudaError_t launch_pcg_init2(const Geom &g, double *r, const double *dinv, double *z, const double *mass_e,
                              const PcgScal *s, double *partial, cudaStream_t st);

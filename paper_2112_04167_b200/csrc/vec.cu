@@ -85,6 +85,33 @@ __global__ void __launch_bounds__(256, 8) k_pcg_init(long long ndof, int npe, co
     write_partials<2>(v, partial);
 }
 
+// lam > 0 (no mean projection) in one pass: r = M f - A u (Ar null: zero guess), z = D^-1 r
+// (z null with a dinv table: z is applied on the fly later), partials [r.z, sum (r/m)^2] and
+// [0, sum f^2] (the latter -> FIN_INIT, the former -> FIN_INIT2)
+__global__ void __launch_bounds__(256) k_pcg_init_fused(long long ndof, int npe, const double *__restrict__ f,
+                                                        const double *__restrict__ Ar, double *__restrict__ r,
+                                                        const double *__restrict__ dinv, int dinv_table,
+                                                        double *__restrict__ z, const double *__restrict__ me,
+                                                        double *partial, double *partial2)
+{
+    double v[2] = {0.0, 0.0}, w[2] = {0.0, 0.0};
+    const long long i0 = blockIdx.x * (long long)blockDim.x + threadIdx.x, st = (long long)gridDim.x * blockDim.x;
+    NodeIdx nq(i0, st, npe);
+    for (long long i = i0; i < ndof; i += st, nq.next()) {
+        const double fi = f[i];
+        const double ri = Ar ? fma(__ldg(me + nq.q), fi, -Ar[i]) : __ldg(me + nq.q) * fi;
+        r[i] = ri;
+        const double zi = (dinv_table ? __ldg(dinv + nq.q) : dinv[i]) * ri;
+        if (z) z[i] = zi;
+        v[0] = fma(ri, zi, v[0]);
+        const double rm = ri * __ldg(me + npe + nq.q);
+        v[1] = fma(rm, rm, v[1]);
+        w[1] = fma(fi, fi, w[1]);
+    }
+    write_partials<2>(v, partial);
+    write_partials<2>(w, partial2);
+}
+
 __global__ void k_pcg_init2(long long ndof, int npe, double *__restrict__ r, const double *__restrict__ dinv,
                             double *__restrict__ z, const double *__restrict__ me, const PcgScal *s, double *partial)
 {
@@ -133,7 +160,12 @@ __global__ void k_pcg_pupd_x(long long ndof, double *__restrict__ x, double *__r
                              const double *__restrict__ z, const PcgScal *s)
 {
     if (s->done) return;
-    const double alpha = s->alpha, beta = s->beta;  // alpha = 0 before the first iteration
+    const double alpha = s->alpha, beta = s->beta;  // alpha = beta = 0 before the first iteration
+    if (alpha == 0.0 && beta == 0.0) {               // p = z; p_old is not read (not initialised)
+        for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < ndof; i += (long long)gridDim.x * blockDim.x)
+            p[i] = z[i];
+        return;
+    }
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < ndof; i += (long long)gridDim.x * blockDim.x) {
         const double pi = p[i];
         x[i] = fma(alpha, pi, x[i]);
@@ -192,6 +224,10 @@ __global__ void k_pcg_pupd_xt(long long ndof, int npe, double *__restrict__ x, d
     const double alpha = s->alpha, beta = s->beta;
     const long long i0 = blockIdx.x * (long long)blockDim.x + threadIdx.x, st = (long long)gridDim.x * blockDim.x;
     NodeIdx nq(i0, st, npe);
+    if (alpha == 0.0 && beta == 0.0) {  // before the first iteration: p = D^-1 r, p_old not read
+        for (long long i = i0; i < ndof; i += st, nq.next()) p[i] = r[i] * __ldg(dinv_t + nq.q);
+        return;
+    }
     for (long long i = i0; i < ndof; i += st, nq.next()) {
         const double pi = p[i];
         x[i] = fma(alpha, pi, x[i]);
@@ -409,6 +445,14 @@ cudaError_t launch_pcg_init(const Geom &g, const double *f, const double *Ar, do
                             const PcgScal *s, double *partial, cudaStream_t st)
 {
     k_pcg_init<<<vec_grid(), 256, 0, st>>>(nd(g), g.npe, f, Ar, r, mass_e, s, partial);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_pcg_init_fused(const Geom &g, const double *f, const double *Ar, double *r, const double *dinv,
+                                  int dinv_table, double *z, const double *mass_e, double *partial, double *partial2,
+                                  cudaStream_t st)
+{
+    k_pcg_init_fused<<<vec_grid(), 256, 0, st>>>(nd(g), g.npe, f, Ar, r, dinv, dinv_table, z, mass_e, partial, partial2);
     return cudaGetLastError();
 }
 
