@@ -39,6 +39,8 @@ def _worker(rank, world, port, case):
     try:
         if case == "apply":
             _check_apply(rank, world)
+        elif case == "traces":
+            _check_traces(rank, world)
         else:
             _check_inputs(rank, world)
     finally:
@@ -74,6 +76,56 @@ def _check_apply(rank, world):
     assert np.allclose(loc.numpy(), glob, rtol=1e-13, atol=1e-13 * np.abs(ref).sum())
 
 
+def _face_traces(u, nu, dim, Nl, n, D0, sd, layer_idx, node):
+    """(u, nu (2/h) (D u)_node, nu) at the S-face node ``node`` (0 or P) of one element layer,
+    written with the oracle's differentiation matrix (test-side arithmetic, not product code)."""
+    npe = n ** dim
+    lay = int(np.prod(Nl[: dim - 1]))
+    NF = n ** (dim - 1)
+    F = lay * NF
+    out = np.zeros(3 * F)
+    for fe in range(lay):
+        e = layer_idx * lay + fe
+        for inface in range(NF):
+            line = u[e, inface + NF * np.arange(n)]
+            f = fe * NF + inface
+            out[f] = line[node]
+            nv = nu[e, inface + NF * node]
+            out[F + f] = nv * sd * float(D0[node] @ line)
+            out[2 * F + f] = nv
+    return out
+
+
+def _check_traces(rank, world):
+    """The face-trace pairing of capi.cpp trace_exchange: every rank receives the top-face
+    traces of the layer below its slab (tr_lo) and the bottom-face traces of the layer above
+    (tr_hi), periodic; R = 1 (halo mode) receives its own faces (the local wrap)."""
+    dim, N, L, P = 3, (3, 2, 8), (1.0, 1.3, 0.9), 3
+    n = P + 1
+    om = oracle.Mesh(dim, N, L, P)
+    g = np.random.default_rng(8)
+    u = g.uniform(-1, 1, (om.n_el, om.npe))
+    nu = 0.5 + g.uniform(0, 1, (om.n_el, om.npe))
+    xi, _ = oracle.gll(P)
+    D0 = np.array([oracle.lagrange(P, xi, x)[1] for x in xi])  # D[i][j] = l_j'(xi_i)
+    sd = 2.0 / (L[2] / N[2])
+    off, nel, layer = slabs.slab(dim, N, rank, world)
+    Nl = (N[0], N[1], N[2] // world)
+    us, nus = u[off:off + nel], nu[off:off + nel]
+    send_lo = torch.from_numpy(_face_traces(us, nus, dim, Nl, n, D0, sd, 0, 0))
+    send_hi = torch.from_numpy(_face_traces(us, nus, dim, Nl, n, D0, sd, Nl[2] - 1, P))
+    assert send_lo.numel() == 3 * slabs.face_count(dim, Nl, n)
+    tr_lo, tr_hi = slabs.exchange_traces(send_lo, send_hi, rank, world, dist)
+    # the neighbours' faces from the global arrays
+    zl = (rank * Nl[2] - 1) % N[2]
+    zh = ((rank + 1) * Nl[2]) % N[2]
+    want_lo = _face_traces(u, nu, dim, N, n, D0, sd, zl, P)
+    want_hi = _face_traces(u, nu, dim, N, n, D0, sd, zh, 0)
+    assert np.array_equal(tr_lo.numpy(), want_lo)
+    assert np.array_equal(tr_hi.numpy(), want_hi)
+    assert slabs.face_index(dim, Nl, n, 2, 1, 5) == (2 + 3 * 1) * 16 + 5
+
+
 def _check_inputs(rank, world):
     for cid in (2, 3):
         c = config(cid)
@@ -95,6 +147,11 @@ def _check_inputs(rank, world):
 @pytest.mark.parametrize("world", [2, 4])
 def test_halo_exchange_reproduces_global_apply(world):
     mp.spawn(_worker, args=(world, _free_port(), "apply"), nprocs=world, join=True)
+
+
+@pytest.mark.parametrize("world", [1, 2, 4])
+def test_face_trace_exchange_pairing(world):
+    mp.spawn(_worker, args=(world, _free_port(), "traces"), nprocs=world, join=True)
 
 
 @pytest.mark.parametrize("world", [2, 4])
