@@ -65,7 +65,12 @@ struct KC6 {
     static constexpr int NV = VARNU ? 3 : 2;                     // trace values: u, s (, nu)
     static constexpr int LR = 4 * NN;                            // x / y brick-face lines per side
     static constexpr int TRXY = 2 * 2 * NV * LR;                 // x/y trace table per buffer
-    static constexpr int NPT = NP - 32;                          // producer trace threads (warp 0: TMA)
+#ifndef DG_V6_TMATRACE
+#define DG_V6_TMATRACE 0
+#endif
+    // producer trace threads: warps 1-3 (the TMA warp joining them delays its next copies:
+    // measured 0.677 vs 0.516 ms with DG_V6_TMATRACE 1)
+    static constexpr int NPT = DG_V6_TMATRACE ? NP : NP - 32;
     static constexpr int KT = (4 * LR + NPT - 1) / NPT;          // producer x/y tasks per thread
     static constexpr int BRK = 4 * SY;
     static constexpr int OFF_U = 0;
@@ -344,6 +349,8 @@ __device__ __forceinline__ void ptraces_xy(const ApplyParams &a, const DevTab &T
     const Geom &g = a.g;
     const long long lay = (long long)g.Nl[0] * g.Nl[1];
     const double *fu = K::MODE == 1 ? a.pro.z : a.u;
+    // every neighbour line is read forward from its node 0 (x lines: contiguous, n even ->
+    // 16-byte vector loads); the face node is node P of the left / node 0 of the right neighbour
     double v[KT][n], nuf[KT];
     int meta[KT];
 #pragma unroll
@@ -354,31 +361,36 @@ __device__ __forceinline__ void ptraces_xy(const ApplyParams &a, const DevTab &T
         const int D = tk / (2 * LR), side = (tk / LR) & 1, L = tk % LR;
         const int ce = L / NN, tn = L - ce * NN;
         const int ta = tn % n, tb = tn / n;
-        // neighbour element (local coordinates) and the face node of its line
-        int cx, cy;
-        int off, step;
+        int cx, cy, off, step;
         if (D == 0) {
             cx = side ? e0[0] + 4 : e0[0] - 1;
             cx = cx < 0 ? cx + g.Nl[0] : (cx >= g.Nl[0] ? cx - g.Nl[0] : cx);
             cy = e0[1] + ce;
-            off = ta * n + tb * NN + (side ? 0 : P);
-            step = side ? 1 : -1;
+            off = ta * n + tb * NN;
+            step = 1;
         } else {
             cy = side ? e0[1] + 4 : e0[1] - 1;
             cy = cy < 0 ? cy + g.Nl[1] : (cy >= g.Nl[1] ? cy - g.Nl[1] : cy);
             cx = e0[0] + ce;
-            off = ta + tb * NN + (side ? 0 : P * n);
-            step = side ? n : -n;
+            off = ta + tb * NN;
+            step = n;
         }
         const long long o = (cx + (long long)g.Nl[0] * cy + lay * e0[2]) * NPE + off;
         if (K::MODE == 1) {
 #pragma unroll
             for (int i = 0; i < n; ++i) v[k][i] = fma(beta, __ldg(a.pro.p_old + o + i * step), __ldg(fu + o + i * step));
+        } else if ((n % 2) == 0 && D == 0) {
+#pragma unroll
+            for (int i = 0; i < n; i += 2) {
+                const double2 x = __ldg(reinterpret_cast<const double2 *>(fu + o + i));
+                v[k][i] = x.x;
+                v[k][i + 1] = x.y;
+            }
         } else {
 #pragma unroll
             for (int i = 0; i < n; ++i) v[k][i] = __ldg(fu + o + i * step);
         }
-        nuf[k] = K::VARNU ? __ldg(a.nu + o) : a.nu_const;
+        nuf[k] = K::VARNU ? __ldg(a.nu + o + (side ? 0 : P * step)) : a.nu_const;
         meta[k] = tk;
     }
     (void)eb;
@@ -387,16 +399,18 @@ __device__ __forceinline__ void ptraces_xy(const ApplyParams &a, const DevTab &T
         const int tk = meta[k];
         if (tk < 0) continue;
         const int D = tk / (2 * LR), side = (tk / LR) & 1, L = tk % LR;
-        const double dd = rdot<P>(T, 0, v[k]);  // v[0] is the face node (see v5::ptraces)
+        // the neighbour's face node and its derivative along +d there (reference coordinates)
+        const double uf = side ? v[k][0] : v[k][P];
+        const double dd = side ? rdot<P>(T, 0, v[k]) : rdot<P>(T, P, v[k]);
         double *trd = tr + D * 2 * NV * LR + side * NV * LR;
-        trd[L] = v[k][0];
+        trd[L] = uf;
         if (K::VARNU) {  // weight-folded: nu~ = nu w_a w_b w_0, s~ = nu~ (D v)_face (reference derivative)
             const int tn = L % NN;
             const double nw = nuf[k] * (sw[tn % n] * sw[tn / n] * sw[0]);
-            trd[LR + L] = nw * (side ? dd : -dd);
+            trd[LR + L] = nw * dd;
             trd[2 * LR + L] = nw;
         } else {
-            trd[LR + L] = nuf[k] * g.sd[D] * (side ? dd : -dd);
+            trd[LR + L] = nuf[k] * g.sd[D] * dd;
         }
     }
 }
@@ -535,13 +549,14 @@ __global__ void __launch_bounds__((KC6<P, VARNU, MODE>::NT)) __maxnreg__((KC6<P,
                 if (ptid == 0) V5_ACC(4, tt);
                 V5_T0(tx);
                 // x/y traces (warps 1-3) in rounds of at most 3 lines per thread (register budget)
-                if (ptid >= 32) {
+                if (DG_V6_TMATRACE || ptid >= 32) {
+                    const int pt = DG_V6_TMATRACE ? ptid : ptid - 32;
                     constexpr int R = MODE == 1 ? 2 : 3;  // lines in flight per thread (two loads each in MODE 1)
-                    ptraces_xy<K, 0, (K::KT < R ? K::KT : R)>(a, T, tr, e0, eb, ptid - 32, beta, sw);
+                    ptraces_xy<K, 0, (K::KT < R ? K::KT : R)>(a, T, tr, e0, eb, pt, beta, sw);
                     if (ptid == 32) V5_ACC(9, tx);
                     V5_T0(ty);
-                    if constexpr (K::KT > R) ptraces_xy<K, R, (K::KT < 2 * R ? K::KT : 2 * R)>(a, T, tr, e0, eb, ptid - 32, beta, sw);
-                    if constexpr (K::KT > 2 * R) ptraces_xy<K, 2 * R, K::KT>(a, T, tr, e0, eb, ptid - 32, beta, sw);
+                    if constexpr (K::KT > R) ptraces_xy<K, R, (K::KT < 2 * R ? K::KT : 2 * R)>(a, T, tr, e0, eb, pt, beta, sw);
+                    if constexpr (K::KT > 2 * R) ptraces_xy<K, 2 * R, K::KT>(a, T, tr, e0, eb, pt, beta, sw);
                     if (ptid == 32) V5_ACC(10, ty);
                 }
                 if (j == 0) ptraces_z<K>(a, T, sm + K::OFF_TZ, e0, ptid, beta, 0, sw);
