@@ -880,7 +880,7 @@ dg_status grad_impl(dg_mesh *mp, dg_mesh *mv, const double *psi, double *const g
 // divergence / mass-flux stabilisation (stab.cu, reading A26)
 // ---------------------------------------------------------------------------
 dg_status stab_apply_impl(dg_mesh *m, const double *const in[3], double *const out[3], double aD, double aC,
-                          double *partial, const PcgScal *s)
+                          double *partial, const PcgScal *s, int *grid = nullptr)
 {
     StabParams a;
     const int dim = m->g.dim;
@@ -897,7 +897,7 @@ dg_status stab_apply_impl(dg_mesh *m, const double *const in[3], double *const o
     a.aC = aC;
     a.partial = partial;
     a.s = s;
-    CK(launch_stab_apply(m->g, a, m->st));
+    CK(launch_stab_apply(m->g, a, m->st, grid));
     m->launches += 1;
     return DG_OK;
 }
@@ -984,7 +984,6 @@ dg_status stab_solve_impl(dg_mesh *m, double dt, double zD, double zC, double *c
     CKS(reduce_fin(m, G, FIN_INIT, sv.partial2));   // fnorm2 = ||v''||^2
     CKS(reduce_fin(m, G, FIN_INIT2));                // r.z, ||M^-1 r||^2, convergence test
     CK(cudaMemsetAsync(sv.p, 0, sizeof(double) * (size_t)dim * nd, m->st));
-    const int GA = (int)std::min<long long>(g.nel, G);
     for (;;) {
         CK(cudaMemcpyAsync(m->hscal, m->scal, sizeof(PcgScal), cudaMemcpyDeviceToHost, m->st));
         CK(cudaStreamSynchronize(m->st));
@@ -993,7 +992,8 @@ dg_status stab_solve_impl(dg_mesh *m, double dt, double zD, double zC, double *c
             CK(launch_stab_vec(STAB_PUPD, sv, m->st));
             const double *pp[3] = {sv.p, sv.p + nd, dim == 3 ? sv.p + 2 * nd : nullptr};
             double *qq[3] = {sv.q, sv.q + nd, dim == 3 ? sv.q + 2 * nd : nullptr};
-            CKS(stab_apply_impl(m, pp, qq, aD, aC, m->partial, m->scal));
+            int GA = 0;
+            CKS(stab_apply_impl(m, pp, qq, aD, aC, m->partial, m->scal, &GA));
             CKS(reduce_fin(m, GA, FIN_ALPHA));
             CK(launch_stab_vec(STAB_UPDATE, sv, m->st));
             CKS(reduce_fin(m, G, FIN_BETA));

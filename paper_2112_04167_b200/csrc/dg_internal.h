@@ -340,7 +340,7 @@ struct StabVec {                                          // CG vectors: r, p, q
 };
 enum { STAB_INIT = 0, STAB_PUPD = 1, STAB_UPDATE = 2, STAB_U2 = 3 };
 int stab_grid();
-cudaError_t launch_stab_apply(const Geom &g, const StabParams &a, cudaStream_t st);
+cudaError_t launch_stab_apply(const Geom &g, const StabParams &a, cudaStream_t st, int *grid = nullptr);
 cudaError_t launch_stab_vec(int op, const StabVec &a, cudaStream_t st);
 cudaError_t upload_tables_stab();
 

@@ -24,6 +24,18 @@ DG_DEFINE_CONST_TABLES(upload_tables_stab)
 
 namespace {
 
+// grid-stride DOF loops track the node index q = i mod npe incrementally (no 64-bit division)
+struct NodeQ {
+    int q, step, npe;
+    __device__ __forceinline__ NodeQ(long long i0, long long stride, int npe_)
+        : q((int)(i0 % npe_)), step((int)(stride % npe_)), npe(npe_) {}
+    __device__ __forceinline__ void next()
+    {
+        q += step;
+        if (q >= npe) q -= npe;
+    }
+};
+
 template <int K>
 __device__ __forceinline__ void write_partials_s(double (&v)[K], double *partial)
 {
@@ -35,14 +47,19 @@ __device__ __forceinline__ void write_partials_s(double (&v)[K], double *partial
 }
 
 template <int DIM, int P>
-__global__ void __launch_bounds__(256) k_stab_apply(const Geom g, StabParams a)
+__global__ void __launch_bounds__(256, 6) k_stab_apply(const Geom g, StabParams a)
 {
     constexpr int n = P + 1, NPE = DIM == 3 ? n * n * n : n * n;
     const DevTab &T = c_tab[P];
     __shared__ double sv[DIM][NPE];
     __shared__ double swd[NPE];
+    __shared__ double sD[n][n], sw[n];  // per-thread row indices: shared, not the constant bank
     double dot = 0.0;
     if (a.s && a.s->done) return;
+    for (int q = threadIdx.x; q < n * n; q += blockDim.x) {
+        sD[q / n][q % n] = T.D[q / n][q % n];
+        if (q < n) sw[q] = T.w[q];
+    }
     for (long long e = blockIdx.x; e < g.nel; e += gridDim.x) {
         for (int q = threadIdx.x; q < DIM * NPE; q += blockDim.x) {
             const int c = q / NPE, I = q - c * NPE;
@@ -58,9 +75,9 @@ __global__ void __launch_bounds__(256) k_stab_apply(const Geom g, StabParams a)
                 const int base = q - qc[d] * GS;
                 double t = 0.0;
 #pragma unroll
-                for (int j = 0; j < n; ++j) t = fma(T.D[qc[d]][j], sv[d][base + j * GS], t);
+                for (int j = 0; j < n; ++j) t = fma(sD[qc[d]][j], sv[d][base + j * GS], t);
                 div = fma(g.sd[d], t, div);
-                W *= T.w[qc[d]];
+                W *= sw[qc[d]];
             }
             swd[q] = a.aD * W * div;
         }
@@ -74,18 +91,18 @@ __global__ void __launch_bounds__(256) k_stab_apply(const Geom g, StabParams a)
             const int i = qc[c], base = I - i * GS;
             double m = g.mfac;
 #pragma unroll
-            for (int d = 0; d < DIM; ++d) m *= T.w[qc[d]];
+            for (int d = 0; d < DIM; ++d) m *= sw[qc[d]];
             const double vi = sv[c][I];
             double t = 0.0;  // sum_k (2/h_c) D[k][i] (a_D W div)(k along c)
 #pragma unroll
-            for (int k = 0; k < n; ++k) t = fma(T.D[k][i], swd[base + k * GS], t);
+            for (int k = 0; k < n; ++k) t = fma(sD[k][i], swd[base + k * GS], t);
             double acc = fma(g.sd[c], t, m * vi);
             if (i == P || i == 0) {  // [v_c][phi_I] on the face normal to c through I
                 int cn[3] = {ec[0], ec[1], ec[2]};
                 cn[c] += i == P ? 1 : -1;
                 const double *nb = elem_ptr(g, a.in[c], a.lo[c], a.hi[c], cn[0], cn[1], cn[2]);
                 const double vn = __ldg(nb + base + (i == P ? 0 : P * GS));
-                const double Wp = m / (T.w[i] * 0.5 * g.h[c]);
+                const double Wp = m / (sw[i] * 0.5 * g.h[c]);
                 acc = fma(a.aC * Wp, vi - vn, acc);
             }
             a.out[c][e * NPE + I] = acc;
@@ -105,8 +122,9 @@ __global__ void __launch_bounds__(256) k_stab_init(StabVec a)
     double v[2] = {0.0, 0.0}, f[2] = {0.0, 0.0};
     for (int c = 0; c < a.dim; ++c) {
         const long long i0 = blockIdx.x * (long long)blockDim.x + threadIdx.x, st = (long long)gridDim.x * blockDim.x;
-        for (long long i = i0; i < a.ndof; i += st) {
-            const int q = (int)(i % a.npe);
+        NodeQ nq(i0, st, a.npe);
+        for (long long i = i0; i < a.ndof; i += st, nq.next()) {
+            const int q = nq.q;
             const double x = a.x[c][i];
             const double r = fma(__ldg(a.mass_e + q), x, -a.q[c * a.ndof + i]);
             a.r[c * a.ndof + i] = r;
@@ -125,11 +143,13 @@ __global__ void __launch_bounds__(256) k_stab_pupd(StabVec a)
 {
     if (a.s->done) return;
     const double beta = a.s->beta;
-    const long long tot = (long long)a.dim * a.ndof;
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < tot; i += (long long)gridDim.x * blockDim.x) {
-        const long long c = i / a.ndof;
-        const int q = (int)((i - c * a.ndof) % a.npe);
-        a.p[i] = fma(beta, a.p[i], __ldg(a.dinv + c * a.npe + q) * a.r[i]);
+    for (int c = 0; c < a.dim; ++c) {
+        const long long i0 = blockIdx.x * (long long)blockDim.x + threadIdx.x, st = (long long)gridDim.x * blockDim.x;
+        NodeQ nq(i0, st, a.npe);
+        const double *dv = a.dinv + c * a.npe;
+        double *p = a.p + c * a.ndof;
+        const double *r = a.r + c * a.ndof;
+        for (long long i = i0; i < a.ndof; i += st, nq.next()) p[i] = fma(beta, p[i], __ldg(dv + nq.q) * r[i]);
     }
 }
 
@@ -141,8 +161,9 @@ __global__ void __launch_bounds__(256) k_stab_update(StabVec a)
     double v[2] = {0.0, 0.0};
     for (int c = 0; c < a.dim; ++c) {
         const long long i0 = blockIdx.x * (long long)blockDim.x + threadIdx.x, st = (long long)gridDim.x * blockDim.x;
-        for (long long i = i0; i < a.ndof; i += st) {
-            const int q = (int)(i % a.npe);
+        NodeQ nq(i0, st, a.npe);
+        for (long long i = i0; i < a.ndof; i += st, nq.next()) {
+            const int q = nq.q;
             const long long k = c * a.ndof + i;
             a.x[c][i] = fma(alpha, a.p[k], a.x[c][i]);
             const double r = fma(-alpha, a.q[k], a.r[k]);
@@ -160,8 +181,9 @@ __global__ void __launch_bounds__(256) k_stab_u2(StabVec a)
 {
     double v[2] = {0.0, 0.0};
     const long long i0 = blockIdx.x * (long long)blockDim.x + threadIdx.x, st = (long long)gridDim.x * blockDim.x;
-    for (long long i = i0; i < a.ndof; i += st) {
-        const double m = __ldg(a.mass_e + (int)(i % a.npe));
+    NodeQ nq(i0, st, a.npe);
+    for (long long i = i0; i < a.ndof; i += st, nq.next()) {
+        const double m = __ldg(a.mass_e + nq.q);
         double s2 = 0.0;
         for (int c = 0; c < a.dim; ++c) s2 = fma(a.x[c][i], a.x[c][i], s2);
         v[0] = fma(m, s2, v[0]);
@@ -174,9 +196,19 @@ __global__ void __launch_bounds__(256) k_stab_u2(StabVec a)
 
 int stab_grid() { return 148 * 4; }
 
-cudaError_t launch_stab_apply(const Geom &g, const StabParams &a, cudaStream_t st)
+cudaError_t launch_stab_apply(const Geom &g, const StabParams &a, cudaStream_t st, int *grid)
 {
-    const long long blocks = g.nel < stab_grid() ? g.nel : stab_grid();
+    // one resident wave of CTAs (one element per CTA in flight: more CTAs per SM hide the load
+    // latency of the next element); the partial-sum count stays <= 148 * 6
+    int nsm = 148;
+    {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    }
+    const long long cap = (long long)nsm * 6;
+    const long long blocks = g.nel < cap ? g.nel : cap;
+    if (grid) *grid = (int)blocks;
     switch (g.P) {
 #define DG_SA(p)                                                                                       \
     case p:                                                                                            \
