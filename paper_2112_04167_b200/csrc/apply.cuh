@@ -182,11 +182,13 @@ __global__ void __launch_bounds__(256) k_diag_cf2(const Geom g, double lam, cons
     }
     __syncthreads();
     const long long tot = g.nel * NPE;
+    // element coordinates in 32-bit arithmetic (local meshes below 2^31 elements: every config)
+    const unsigned nx = (unsigned)g.Nl[0], ny = (unsigned)g.Nl[1];
     for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < tot; t += (long long)gridDim.x * blockDim.x) {
-        const long long e = t / NPE;
+        const long long e = t / NPE;  // constant divisor: a multiply-shift
         const int q = (int)(t - e * NPE);
-        const int ec[3] = {(int)(e % g.Nl[0]), (int)((e / g.Nl[0]) % g.Nl[1]),
-                           DIM == 3 ? (int)(e / ((long long)g.Nl[0] * g.Nl[1])) : 0};
+        const unsigned e32 = (unsigned)e, exy = e32 / nx;
+        const int ec[3] = {(int)(e32 - exy * nx), (int)(DIM == 3 ? exy % ny : exy), DIM == 3 ? (int)(exy / ny) : 0};
         const int qc[3] = {q % n, (q / n) % n, DIM == 3 ? q / (n * n) : 0};
         const double *ne = VARNU ? nu + e * NPE : nullptr;
         double m = g.mfac;
