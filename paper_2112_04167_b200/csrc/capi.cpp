@@ -162,6 +162,20 @@ struct dg_mesh {
     long long F = 0;  // face nodes of one slab layer (trace arrays hold 3 F doubles)
     double *ts_lo = nullptr, *ts_hi = nullptr, *tr_lo = nullptr, *tr_hi = nullptr;  // face traces
     cudaStream_t cs_comm = nullptr;                                                   // exchange stream
+    cudaStream_t cs_cap = nullptr;  // non-blocking stream the PCG iteration graphs are captured on
+    // the last PCG iteration graph and what it was captured for (reused by the next solve with the
+    // same key: the stage's repeated solves skip the instantiation)
+    struct GraphKey {
+        int flags = -1;
+        const double *u = nullptr, *nu = nullptr;
+        double lam = 0.0, nu_const = 0.0;
+        bool operator==(const GraphKey &o) const
+        {
+            return flags == o.flags && u == o.u && nu == o.nu && lam == o.lam && nu_const == o.nu_const;
+        }
+    } gkey;
+    cudaGraphExec_t gexec = nullptr;
+    long long gexec_launches = 0;
     cudaEvent_t ev_a = nullptr, ev_b = nullptr;
     double *h_lo = nullptr, *h_hi = nullptr, *hn_lo = nullptr, *hn_hi = nullptr;       // element layers
     double *hv_lo[3] = {nullptr, nullptr, nullptr}, *hv_hi[3] = {nullptr, nullptr, nullptr};
@@ -691,6 +705,119 @@ dg_status pcg_impl(dg_mesh *m, double lam, const double *nu, double nu_const, co
     if (!split) CK(cudaMemsetAsync(m->pa, 0, sizeof(double) * (size_t)m->ndof, m->st));
 
     double *p_old = m->pa, *p_new = m->pb;
+    // one CG iteration, enqueued on the mesh stream (the fused variant swaps p_old / p_new)
+    auto iteration = [&]() -> dg_status {
+        if (sw) {
+            // x += alpha p, p = z_b + P_1 x_c + beta p (in place) ; q = A p ; Schwarz step
+            SwPupdParams pp;
+            pp.T = m->d_sw;
+            pp.nel = g.nel;
+            pp.el_off = m->el_off;
+            pp.zb = m->z;
+            pp.xc = m->xc;
+            pp.p_old = p_old;
+            pp.p = p_old;
+            pp.x = u;
+            pp.s = m->scal;
+            CK(launch_sw_pupd(g, m->h_sw, pp, m->st));
+            m->launches += 1;
+            if (split_ok) {
+                int grid = 0;
+                CKS(halo_apply(m, lam, nu, nu_const, p_old, m->q, m->partial, &grid, &m->scal->done, true));
+                CKS(reduce_fin(m, grid, FIN_ALPHA));
+            } else {
+                CKS(halo_apply(m, lam, nu, nu_const, p_old, m->q, nullptr, nullptr, nullptr, true));
+                CK(launch_dot_pq(g, p_old, m->q, m->scal, m->partial, m->st));
+                m->launches += 1;
+                CKS(reduce_fin(m, VG, FIN_ALPHA));
+            }
+            CKS(sw_pcg_step(m, lam, SW_UPDATE, FIN_BETA));
+        } else if (split) {
+            // x += alpha p, p = z + beta p (in place; x deferred by one iteration) ;
+            // q = A p with the dot epilogue (apply MODE 2) ; r, z update.  Constant nu: z is
+            // never stored (the diagonal is one [npe] table, applied on the fly)
+            if (table) CK(launch_pcg_pupd_xt(g, u, p_old, m->r, m->dinv, m->scal, m->st));
+            else CK(launch_pcg_pupd_x(g, u, p_old, m->z, m->scal, m->st));
+            m->launches += 1;
+            int grid = 0;
+            CKS(halo_apply(m, lam, nu, nu_const, p_old, m->q, m->partial, &grid, &m->scal->done, true));
+            CKS(reduce_fin(m, grid, FIN_ALPHA));
+            if (table) CK(launch_pcg_update_t(g, m->r, m->q, m->dinv, m->mass_e, m->scal, m->partial, m->st));
+            else CK(launch_pcg_update_nox(g, m->r, m->q, m->dinv, m->z, m->mass_e, m->scal, m->partial, m->st));
+            m->launches += 1;
+            CKS(reduce_fin(m, table ? vec_grid_wide() : VG, FIN_BETA));
+        } else if (!m->halo) {
+            // q = A p with p = dinv r + beta p_old (prologue), partials p.q, sum q (epilogue)
+            PProl pro;
+            pro.on = true;
+            pro.z = m->z;
+            pro.p_old = p_old;
+            pro.p_out = p_new;
+            pro.beta = &m->scal->beta;
+            pro.done = &m->scal->done;
+            DotEpi epi;
+            epi.partial = m->partial;
+            int grid = 0;
+            CKS(run_apply(m, lam, nu, nu_const, nullptr, m->q, Halo{}, epi, pro, &grid));
+            CKS(reduce_fin(m, grid, FIN_ALPHA));
+            CK(launch_pcg_update(g, u, m->r, p_new, m->q, m->dinv, m->z, m->mass_e, m->scal, m->partial, m->st));
+            m->launches += 1;
+            CKS(reduce_fin(m, VG, FIN_BETA));
+            std::swap(p_old, p_new);
+        } else {
+            // unfused: p = dinv r + beta p ; halo(p) ; q = A p ; p.q
+            CK(launch_pcg_pupd(g, p_old, m->z, m->scal, m->st));
+            m->launches += 1;
+            CKS(halo_apply(m, lam, nu, nu_const, p_old, m->q, nullptr, nullptr, nullptr, true));
+            CK(launch_dot_pq(g, p_old, m->q, m->scal, m->partial, m->st));
+            m->launches += 1;
+            CKS(reduce_fin(m, VG, FIN_ALPHA));
+            CK(launch_pcg_update(g, u, m->r, p_old, m->q, m->dinv, m->z, m->mass_e, m->scal, m->partial, m->st));
+            m->launches += 1;
+            CKS(reduce_fin(m, VG, FIN_BETA));
+        }
+        return DG_OK;
+    };
+    // Single-rank meshes replay the iterations as a CUDA graph (captured once per solve: two
+    // iterations for the fused variant, whose p buffers alternate): the launch-bound small
+    // configurations lose most of their per-kernel launch overhead.  Halo meshes enqueue the
+    // iterations directly (their exchange runs on a second stream).
+    const bool use_graph = !m->halo;
+    const int gper = (!sw && !split && !m->halo) ? 2 : 1;
+    dg_mesh::GraphKey key;
+    key.flags = (sw ? 1 : 0) | (split ? 2 : 0) | (table ? 4 : 0) | (split_ok ? 8 : 0) | (m->sw_coarse_on ? 16 : 0);
+    key.u = u;
+    key.nu = nu;
+    key.lam = lam;
+    key.nu_const = nu_const;
+    auto capture = [&]() -> dg_status {
+        if (m->gexec) cudaGraphExecDestroy(m->gexec);
+        m->gexec = nullptr;
+        m->gkey = dg_mesh::GraphKey{};
+        // captured on the mesh's private non-blocking stream (the caller's stream may be the
+        // legacy default stream, which cannot be captured); replayed on the caller's stream
+        cudaGraph_t gr = nullptr;
+        const long long l0 = m->launches;
+        cudaStream_t user = m->st;
+        CK(cudaStreamBeginCapture(m->cs_cap, cudaStreamCaptureModeRelaxed));
+        m->st = m->cs_cap;
+        dg_status cs = DG_OK;
+        for (int k = 0; k < gper && cs == DG_OK; ++k) cs = iteration();
+        m->st = user;
+        const cudaError_t ce = cudaStreamEndCapture(m->cs_cap, &gr);
+        if (cs != DG_OK) {
+            if (gr) cudaGraphDestroy(gr);
+            return cs;
+        }
+        CK(ce);
+        const cudaError_t ie = cudaGraphInstantiate(&m->gexec, gr, 0);
+        cudaGraphDestroy(gr);
+        CK(ie);
+        m->gexec_launches = m->launches - l0;  // kernels per graph replay (none ran during capture)
+        m->launches = l0;
+        m->gkey = key;
+        return DG_OK;
+    };
     // iterations are enqueued in chunks between host convergence checks; after the first chunk
     // the next one is sized from the observed residual reduction per iteration (launches past
     // convergence exit at their first instruction but still cost a few microseconds each)
@@ -712,76 +839,19 @@ dg_status pcg_impl(dg_mesh *m, double lam, const double *nu, double nu_const, co
             prev_iter = hs.iter;
             prev_res2 = hs.res2;
         }
-        for (int it = 0; it < chunk; ++it) {
-            if (sw) {
-                // x += alpha p, p = z_b + P_1 x_c + beta p (in place) ; q = A p ; Schwarz step
-                SwPupdParams pp;
-                pp.T = m->d_sw;
-                pp.nel = g.nel;
-                pp.el_off = m->el_off;
-                pp.zb = m->z;
-                pp.xc = m->xc;
-                pp.p_old = p_old;
-                pp.p = p_old;
-                pp.x = u;
-                pp.s = m->scal;
-                CK(launch_sw_pupd(g, m->h_sw, pp, m->st));
-                m->launches += 1;
-                if (split_ok) {
-                    int grid = 0;
-                    CKS(halo_apply(m, lam, nu, nu_const, p_old, m->q, m->partial, &grid, &m->scal->done, true));
-                    CKS(reduce_fin(m, grid, FIN_ALPHA));
-                } else {
-                    CKS(halo_apply(m, lam, nu, nu_const, p_old, m->q, nullptr, nullptr, nullptr, true));
-                    CK(launch_dot_pq(g, p_old, m->q, m->scal, m->partial, m->st));
-                    m->launches += 1;
-                    CKS(reduce_fin(m, VG, FIN_ALPHA));
-                }
-                CKS(sw_pcg_step(m, lam, SW_UPDATE, FIN_BETA));
-            } else if (split) {
-                // x += alpha p, p = z + beta p (in place; x deferred by one iteration) ;
-                // q = A p with the dot epilogue (apply MODE 2) ; r, z update.  Constant nu: z is
-                // never stored (the diagonal is one [npe] table, applied on the fly)
-                if (table) CK(launch_pcg_pupd_xt(g, u, p_old, m->r, m->dinv, m->scal, m->st));
-                else CK(launch_pcg_pupd_x(g, u, p_old, m->z, m->scal, m->st));
-                m->launches += 1;
-                int grid = 0;
-                CKS(halo_apply(m, lam, nu, nu_const, p_old, m->q, m->partial, &grid, &m->scal->done, true));
-                CKS(reduce_fin(m, grid, FIN_ALPHA));
-                if (table) CK(launch_pcg_update_t(g, m->r, m->q, m->dinv, m->mass_e, m->scal, m->partial, m->st));
-                else CK(launch_pcg_update_nox(g, m->r, m->q, m->dinv, m->z, m->mass_e, m->scal, m->partial, m->st));
-                m->launches += 1;
-                CKS(reduce_fin(m, table ? vec_grid_wide() : VG, FIN_BETA));
-            } else if (!m->halo) {
-                // q = A p with p = dinv r + beta p_old (prologue), partials p.q, sum q (epilogue)
-                PProl pro;
-                pro.on = true;
-                pro.z = m->z;
-                pro.p_old = p_old;
-                pro.p_out = p_new;
-                pro.beta = &m->scal->beta;
-                pro.done = &m->scal->done;
-                DotEpi epi;
-                epi.partial = m->partial;
-                int grid = 0;
-                CKS(run_apply(m, lam, nu, nu_const, nullptr, m->q, Halo{}, epi, pro, &grid));
-                CKS(reduce_fin(m, grid, FIN_ALPHA));
-                CK(launch_pcg_update(g, u, m->r, p_new, m->q, m->dinv, m->z, m->mass_e, m->scal, m->partial, m->st));
-                m->launches += 1;
-                CKS(reduce_fin(m, VG, FIN_BETA));
-                std::swap(p_old, p_new);
-            } else {
-                // unfused: p = dinv r + beta p ; halo(p) ; q = A p ; p.q
-                CK(launch_pcg_pupd(g, p_old, m->z, m->scal, m->st));
-                m->launches += 1;
-                CKS(halo_apply(m, lam, nu, nu_const, p_old, m->q, nullptr, nullptr, nullptr, true));
-                CK(launch_dot_pq(g, p_old, m->q, m->scal, m->partial, m->st));
-                m->launches += 1;
-                CKS(reduce_fin(m, VG, FIN_ALPHA));
-                CK(launch_pcg_update(g, u, m->r, p_old, m->q, m->dinv, m->z, m->mass_e, m->scal, m->partial, m->st));
-                m->launches += 1;
-                CKS(reduce_fin(m, VG, FIN_BETA));
+        // long runs replay the captured iteration graph (captured when a chunk of >= 8
+        // iterations is due, or reused from an earlier solve with the same key); short solves
+        // do not pay for the instantiation
+        key.flags = (key.flags & 31) | (p_old == m->pa ? 32 : 0);  // the fused variant's p parity
+        const bool have = use_graph && m->gexec && m->gkey == key;
+        if (use_graph && !have && chunk >= 8) CKS(capture());
+        if (use_graph && m->gexec && m->gkey == key) {
+            for (int it = 0; it < chunk; it += gper) {
+                CK(cudaGraphLaunch(m->gexec, m->st));
+                m->launches += m->gexec_launches;
             }
+        } else {
+            for (int it = 0; it < chunk; ++it) CKS(iteration());
         }
     }
     if (split || sw) {  // the deferred x update of the last iteration
@@ -1130,6 +1200,8 @@ dg_status dg_mesh_create(int dim, const int N[3], const double L[3], int P, int 
         if (e != cudaSuccess) return fail(set_error(DG_ECUDA, cudaGetErrorString(e)));
         m->launches += 2;
     }
+    if (cudaStreamCreateWithFlags(&m->cs_cap, cudaStreamNonBlocking) != cudaSuccess)
+        return fail(set_error(DG_ECUDA, "capture stream creation failed"));
     // halo meshes (nranks > 1, or the 1-rank halo mode: an NCCL id with nranks == 1): the
     // communicator, the exchange stream and events, the face-trace buffers and the element-layer
     // buffers of the once-per-stage kernels -- all allocated here, none in the hot calls
@@ -1181,6 +1253,8 @@ void dg_mesh_destroy(dg_mesh *m)
     if (m->ev_a) cudaEventDestroy(m->ev_a);
     if (m->ev_b) cudaEventDestroy(m->ev_b);
     if (m->cs_comm) cudaStreamDestroy(m->cs_comm);
+    if (m->gexec) cudaGraphExecDestroy(m->gexec);
+    if (m->cs_cap) cudaStreamDestroy(m->cs_cap);
     for (cudaEvent_t e : m->ev) cudaEventDestroy(e);
     for (double *b : m->rk) cudaFree(b);
     if (m->cs_in) cudaStreamDestroy(m->cs_in);
