@@ -1,1 +1,1 @@
-for v in V18 V20 V18 V20; do DG_LIBRARY=$PWD/build_ab/lib$v.so timeout 300 python tools/ab_c4.py; done
+for v in V22 V24 V22 V24; do DG_LIBRARY=$PWD/build_ab/lib$v.so timeout 300 python tools/ab_apply.py; done
