@@ -329,6 +329,8 @@ def run_product(args, rank, world, local_rank):
     if world == 1 and not args.no_configs:
         configs = run_configs(dg, torch, stream, peak0)
         halo = run_halo(dg, torch, stream, c, u, nu, f, peak0)
+        halo["slab_model"] = run_slab_model(dg, torch, stream, c, u, nu, per_launch_ms,
+                                            statistics.mean(solve_ms) / statistics.mean(iters))
 
     # ---- e2e through the host-buffer C-ABI call (rank-local slab)
     u_np = np.ascontiguousarray(u_h)
@@ -481,6 +483,42 @@ def run_halo(dg, torch, stream, c, u, nu, f, peak, reps=20):
     return {"mode": "1-rank halo mode (NCCL self send/recv of the slab face traces)", "apply_ms": ms,
             "apply_gdofs": c.ndof / (ms * 1e-3) / 1e9, "apply_frac_hbm": c.ndof * bpd / (ms * 1e-3) / 1e9 / peak,
             "pcg_iters": it, "pcg_ms_per_solve": t, "pcg_iters_per_s": it / (t * 1e-3)}
+
+
+def run_slab_model(dg, torch, stream, c, u, nu, t1_apply_ms, t1_iter_ms):
+    """Per-rank work of an N-GPU c5 run measured on this GPU: rank 0's slab (N_z / N element
+    layers, same element size) as a 1-rank halo-mode mesh -- the face traces go through the same
+    NCCL send/recv calls and the interior layers overlap them, only the peer is this GPU.  The
+    projected strong-scaling efficiency T1 / (N T_slab) leaves out the NVLink transfer (hidden
+    behind the interior layers) and the two 16-byte all-reduces per CG iteration; it is a model,
+    not a multi-GPU measurement."""
+    out = {}
+    N = c.N
+    for R in (2, 4, 8):
+        nzl = N[2] // R
+        Ls = (c.L[0], c.L[1], c.L[2] / R)
+        m = dg.dg_mesh_create(3, (N[0], N[1], nzl), Ls, c.P, stream=stream, halo_mode=True)
+        ne = m.n_el
+        us, nus = u[:ne].contiguous(), (None if nu is None else nu[:ne].contiguous())
+        o = torch.empty_like(us)
+        ms, _ = time_apply(dg, torch, stream, m, c.lam, nus, c.nu0, us, o, reps=20)
+        f = us.clone()
+        times = []
+        for k in range(3):
+            x = torch.zeros_like(us)
+            torch.cuda.synchronize()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            info = dg.dg_pcg_solve(m, c.lam, nus, c.nu0, f, 1e-30, 20, x, raise_on_notconv=False)
+            b.record(stream)
+            torch.cuda.synchronize()
+            if k:
+                times.append(a.elapsed_time(b) / max(info.iters, 1))
+        it_ms = min(times)
+        out["N%d" % R] = {"slab_layers": nzl, "apply_ms": ms, "pcg_ms_per_iter": it_ms,
+                          "apply_eff_model": t1_apply_ms / (R * ms), "pcg_eff_model": t1_iter_ms / (R * it_ms)}
+        dg.dg_mesh_destroy(m)
+    return out
 
 
 PAPER_CONTEXT = {

@@ -378,9 +378,9 @@ dg_status trace_exchange(dg_mesh *m, const double *u, const double *nu, double n
 }
 
 // q = A u over the slab with the face-trace halo.  Single rank: one launch.  Halo meshes: the
-// trace exchange runs on the exchange stream while the interior element layers [2, Nl - 2) are
-// applied; the two boundary layer pairs [0, 2) and [Nl - 2, Nl) follow once the halo has arrived
-// (3-D meshes the v5 / v6 layer-range kernels run; otherwise one launch after the exchange).
+// trace exchange runs on the exchange stream, then one launch (by default; with the layer
+// split -- DG_OVERLAP_MIN_LAYERS -- the interior layers [2, Nl - 2) are applied during the
+// exchange and the two boundary layer pairs [0, 2) and [Nl - 2, Nl) after it).
 // partial != null: dot epilogue (MODE 2/3), the launches' block partials back to back; *G =
 // their total count.  nu_traced: the nu halo of this nu is already in place (PCG iterations).
 dg_status halo_apply(dg_mesh *m, double lam, const double *nu, double nu_const, const double *u, double *out,
@@ -399,7 +399,16 @@ dg_status halo_apply(dg_mesh *m, double lam, const double *nu, double nu_const, 
     CKS(trace_exchange(m, u, nu, nu_const, !nu_traced));
     const Geom &g = m->g;
     const int Nl = g.Nl[g.dim - 1];
-    bool ranges = g.dim == 3 && apply3_ranges_ok(g) && Nl >= 6 && Nl % 2 == 0 &&
+// The interior / boundary layer split (overlap of the trace exchange with the interior layers)
+// costs more than it hides with these persistent kernels: three launches and 2-layer segments
+// (pipeline fill, segment-end z traces, a partial last round) -- measured on the c5 per-rank
+// slab model, apply 0.333 / 0.211 / 0.150 ms with the split vs 0.292 / 0.171 / 0.110 ms as one
+// launch after the exchange for 32 / 16 / 8 layers (bench.py `halo.slab_model`).  Kept
+// selectable for builds with -DDG_OVERLAP_MIN_LAYERS=<n>.
+#ifndef DG_OVERLAP_MIN_LAYERS
+#define DG_OVERLAP_MIN_LAYERS (1 << 30)
+#endif
+    bool ranges = g.dim == 3 && apply3_ranges_ok(g) && Nl >= DG_OVERLAP_MIN_LAYERS && Nl >= 6 && Nl % 2 == 0 &&
                   (!partial || apply3_split_pcg_ok(g, nu));
     if (ranges) {  // (the layer-range kernels exist for most (P, nu) pairs; otherwise one launch)
         const dg_status st = run_apply(m, lam, nu, nu_const, u, out, Halo{}, epi, pro, &g1, 2, Nl - 2);
