@@ -223,6 +223,132 @@ __global__ void __launch_bounds__(256) k_diag_cf2(const Geom g, double lam, cons
     }
 }
 
+// Same closed form for variable nu in 3-D, by line passes over tiles of E elements in shared
+// memory (the apply's sum-factorised structure with the line matrix w_k D_ki^2 acting on the
+// nu line): the tile's nu is read from HBM once (coalesced), each pass reads one nu line per
+// thread and accumulates its direction's term into a shared tile; the z pass inverts and the
+// tile leaves with coalesced stores.  ~72 B of shared traffic per node instead of 18 scattered
+// L1 loads.  Tables in the kernel parameters (uniform constant-bank operands).
+struct DiagTab {
+    double wd2[NMAX][NMAX];  // w_k D_ki^2  [k][i]
+    double dd0, ddP;          // D_00, D_PP
+};
+
+template <int P>
+struct DiagCfg3 {
+    static constexpr int n = P + 1, NN = n * n, NPE = NN * n;
+    static constexpr int PX = (n % 2 == 0) ? n + 1 : n;  // odd x pitch: conflict-free strided lines
+    static constexpr int SPE = PX * NN;
+    static constexpr int E = 256 / NN > 0 ? 256 / NN : 1;  // elements per tile
+    static constexpr int SMEM = (2 * E * SPE + 6 * E * NN) * 8;
+};
+
+template <int P>
+__global__ void __launch_bounds__(256, 4) k_diag_cf3(const Geom g, double lam, const double *__restrict__ nu,
+                                                     Halo halo, double *__restrict__ diag, int invert,
+                                                     const __grid_constant__ DiagTab dt)
+{
+    using C = DiagCfg3<P>;
+    constexpr int n = C::n, NN = C::NN, NPE = C::NPE, PX = C::PX, SPE = C::SPE, E = C::E;
+    const DevTab &T = c_tab[P];
+    extern __shared__ __align__(16) double dsm[];
+    double *snu = dsm, *sacc = dsm + E * SPE;
+    double *snb = dsm + 2 * E * SPE;  // [D][side][line]: the neighbours' nu at the tile's face nodes
+    const int tid = threadIdx.x, bd = blockDim.x;
+    const long long ntile = (g.nel + E - 1) / E;
+    const unsigned nx = (unsigned)g.Nl[0], ny = (unsigned)g.Nl[1];
+    auto smem_of = [&](int q) {  // tile node q (element-major, node-contiguous) -> padded slot
+        const int le = q / NPE, r = q - le * NPE, i = r % n;
+        return le * SPE + i + PX * (r / n);
+    };
+    // line L of direction D: smem base of node 0, global in-element offset of node 0
+    auto line_of = [&](int D, int L, int &base, int &goff) {
+        const int le = L / NN, ab = L - le * NN, a = ab % n, b = ab / n;
+        if (D == 0) {
+            base = PX * ab;
+            goff = n * a + NN * b;
+        } else if (D == 1) {
+            base = a + PX * n * b;
+            goff = a + NN * b;
+        } else {
+            base = a + PX * b;
+            goff = a + n * b;
+        }
+        base += le * SPE;
+        return le;
+    };
+    // one latency round per tile: the tile's nu and every face-neighbour nu its lines need
+    auto load_tile = [&](long long t) {
+        const long long e0 = t * E;
+        const int cnt = (int)(g.nel - e0 < E ? g.nel - e0 : E);
+        for (int q = tid; q < cnt * NPE; q += bd) snu[smem_of(q)] = __ldg(nu + e0 * NPE + q);
+        for (int x = tid; x < 3 * cnt * NN; x += bd) {
+            const int D = x / (cnt * NN), L = x - D * cnt * NN;
+            const int GS = D == 0 ? 1 : (D == 1 ? n : NN);
+            int base, goff;
+            const int le = line_of(D, L, base, goff);
+            const unsigned e32 = (unsigned)(e0 + le), exy = e32 / nx;
+            const int ec[3] = {(int)(e32 - exy * nx), (int)(exy % ny), (int)(exy / ny)};
+            int cl[3] = {ec[0], ec[1], ec[2]}, cr[3] = {ec[0], ec[1], ec[2]};
+            cl[D] -= 1;
+            cr[D] += 1;
+            snb[(2 * D) * E * NN + L] = nbr_face_nu(g, nu, halo, n, cl, D, goff, P * GS);
+            snb[(2 * D + 1) * E * NN + L] = nbr_face_nu(g, nu, halo, n, cr, D, goff, 0);
+        }
+    };
+    long long tile = blockIdx.x;
+    if (tile >= ntile) return;
+    load_tile(tile);
+    for (; tile < ntile; tile += gridDim.x) {
+        const long long e0 = tile * E;
+        const int cnt = (int)(g.nel - e0 < E ? g.nel - e0 : E);
+        __syncthreads();
+#pragma unroll 1
+        for (int D = 0; D < 3; ++D) {
+            const int SS = D == 0 ? 1 : (D == 1 ? PX : PX * n);
+            const double sd = g.sd[D], tau = g.tau[D];
+            for (int L = tid; L < cnt * NN; L += bd) {
+                int base, goff;
+                const int le = line_of(D, L, base, goff);
+                const int ab = L - le * NN, a = ab % n, b = ab / n;
+                double v[n];
+#pragma unroll
+                for (int m = 0; m < n; ++m) v[m] = snu[base + m * SS];
+                const double nuL = snb[(2 * D) * E * NN + L], nuR = snb[(2 * D + 1) * E * NN + L];
+                const double W = g.wfac[D] * T.w[a] * T.w[b];
+                double r[n];
+#pragma unroll
+                for (int i = 0; i < n; ++i) {
+                    double acc = 0.0;
+#pragma unroll
+                    for (int k = 0; k < n; ++k) acc = fma(dt.wd2[k][i], v[k], acc);
+                    r[i] = acc * sd;
+                }
+                r[0] += v[0] * sd * dt.dd0 + 0.5 * tau * (v[0] + nuL);
+                r[P] += -v[P] * sd * dt.ddP + 0.5 * tau * (v[P] + nuR);
+                if (D == 0) {
+                    const double lm = lam * g.mfac * T.w[a] * T.w[b];
+#pragma unroll
+                    for (int i = 0; i < n; ++i) sacc[base + i] = fma(W, r[i], lm * T.w[i]);
+                } else if (D == 1) {
+#pragma unroll
+                    for (int i = 0; i < n; ++i) sacc[base + i * SS] = fma(W, r[i], sacc[base + i * SS]);
+                } else {
+#pragma unroll
+                    for (int i = 0; i < n; ++i) {
+                        const double dgv = fma(W, r[i], sacc[base + i * SS]);
+                        sacc[base + i * SS] = invert ? 1.0 / dgv : dgv;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+        // coalesced store of this tile, then the next tile's loads (the passes are done with snu / snb)
+        for (int q = tid; q < cnt * NPE; q += bd) diag[e0 * NPE + q] = sacc[smem_of(q)];
+        if (tile + gridDim.x < ntile) load_tile(tile + gridDim.x);
+    }
+}
+
 template <int DIM, int P, bool VARNU>
 __global__ void __launch_bounds__(256) k_diag(const Geom g, double lam, const double *nu, double nu_const,
                                               Halo halo, double *diag)
@@ -651,6 +777,32 @@ struct ApplyDispatch {
                 return cudaGetLastError();
             }
 #endif
+            if constexpr (DIM == 3) {
+                if (nu && !DG_DEV_ENV("DG_DIAG_CF2")) {  // variable nu: tiled line passes (k_diag_cf3)
+                    using C3 = DiagCfg3<P>;
+                    static DiagTab dt;
+                    static int resident = 0;
+                    if (!resident) {
+                        const Tab &t = host_tab(P);
+                        for (int k = 0; k <= P; ++k)
+                            for (int i = 0; i <= P; ++i) dt.wd2[k][i] = t.w[k] * t.D[k][i] * t.D[k][i];
+                        dt.dd0 = t.D[0][0];
+                        dt.ddP = t.D[P][P];
+                        cudaError_t e = cudaFuncSetAttribute(k_diag_cf3<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, C3::SMEM);
+                        if (e != cudaSuccess) return e;
+                        int dev = 0, nsm = 148, occ = 1;
+                        cudaGetDevice(&dev);
+                        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+                        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_diag_cf3<P>, 256, C3::SMEM);
+                        if (e != cudaSuccess || occ < 1) occ = 1;
+                        resident = nsm * occ;
+                    }
+                    const long long ntile = (g.nel + C3::E - 1) / C3::E;
+                    const int blocks = (int)(ntile < resident ? ntile : resident);
+                    k_diag_cf3<P><<<blocks, 256, C3::SMEM, st>>>(g, lam, nu, h, d, invert, dt);
+                    return cudaGetLastError();
+                }
+            }
             {  // one thread per node (measured faster than one CTA per element: 1.39 vs 1.73 ms on c5), one resident wave
                 static int resident[2] = {0, 0};
                 const int vi = nu ? 1 : 0;

@@ -530,6 +530,25 @@ __global__ void __launch_bounds__((KC6<P, VARNU, MODE>::NT)) __maxnreg__((KC6<P,
                     const int so = (el & 3) * SE + (el >> 2) * K::SY;
                     if (lane < 16 && MODE != 1) tma_load(su + so, a.u + ge * NPE, EB, &bar[buf]);
                     if (lane >= 16 && VARNU) tma_load(snu + so, a.nu + ge * NPE, EB, &bar[buf]);
+                    if (j + 1 < seglen && MODE != 1) {
+                        // L2 prefetch of the x/y brick-face neighbour elements of the next brick
+                        // (their trace loads then hit L2; measured on c5: 0.517 vs 0.525 ms;
+                        // two layers ahead 0.519, four 0.54, eight 0.60)
+                        const int nb = lane & 15, side = (nb >> 2) & 1, r = nb & 3;
+                        int cx, cy;
+                        if (nb < 8) {
+                            cx = side ? e0[0] + 4 : e0[0] - 1;
+                            cx = cx < 0 ? cx + g.Nl[0] : (cx >= g.Nl[0] ? cx - g.Nl[0] : cx);
+                            cy = e0[1] + r;
+                        } else {
+                            cy = side ? e0[1] + 4 : e0[1] - 1;
+                            cy = cy < 0 ? cy + g.Nl[1] : (cy >= g.Nl[1] ? cy - g.Nl[1] : cy);
+                            cx = e0[0] + r;
+                        }
+                        const long long pe = cx + s1 * cy + s2 * (e0[2] + 1);
+                        if (lane < 16) v5::l2_prefetch(a.u + pe * NPE, EB);
+                        else if (VARNU) v5::l2_prefetch(a.nu + pe * NPE, EB);
+                    }
                 }
                 if (MODE == 1) {  // p = z + beta p_old -> shared (operand) and p_out (fused CG prologue)
                     constexpr int H = NPE / 2;  // double2 per element (n even)
