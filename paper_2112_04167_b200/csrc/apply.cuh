@@ -240,112 +240,164 @@ struct DiagCfg3 {
     static constexpr int PX = (n % 2 == 0) ? n + 1 : n;  // odd x pitch: conflict-free strided lines
     static constexpr int SPE = PX * NN;
     static constexpr int E = 256 / NN > 0 ? 256 / NN : 1;  // elements per tile
-    static constexpr int SMEM = (2 * E * SPE + 6 * E * NN) * 8;
+    static constexpr int SMEM = (2 * E * SPE + 6 * E * NN + 6 * E) * 8;
 };
 
+// line L of direction D in a tile: element le, shared base of node 0, global in-element offset of node 0
+template <int P, int D>
+__device__ __forceinline__ int diag3_line(int L, int &base, int &goff, int &a, int &b)
+{
+    using C = DiagCfg3<P>;
+    constexpr int n = C::n, NN = C::NN, PX = C::PX;
+    const int le = L / NN, ab = L - le * NN;
+    a = ab % n;
+    b = ab / n;
+    if (D == 0) {
+        base = PX * ab;
+        goff = n * a + NN * b;
+    } else if (D == 1) {
+        base = a + PX * n * b;
+        goff = a + NN * b;
+    } else {
+        base = a + PX * b;
+        goff = a + n * b;
+    }
+    base += le * C::SPE;
+    return le;
+}
+
+// the face-neighbour nu of every line of direction D in the tile -> snb[2D + side][L]
+template <int P, int D>
+__device__ __forceinline__ void diag3_nbr(const Geom &g, const double *__restrict__ nu, const Halo &halo, bool hmesh,
+                                          long long e0, int cnt, const long long *sne, double *snb)
+{
+    using C = DiagCfg3<P>;
+    constexpr int n = C::n, NN = C::NN, NPE = C::NPE, E = C::E;
+    constexpr int GS = D == 0 ? 1 : (D == 1 ? n : NN);
+    for (int L = threadIdx.x; L < cnt * NN; L += blockDim.x) {
+        int base, goff, a, b;
+        const int le = diag3_line<P, D>(L, base, goff, a, b);
+        double vl, vr;
+        if (!hmesh) {
+            vl = __ldg(nu + sne[le * 6 + 2 * D] * NPE + goff + P * GS);
+            vr = __ldg(nu + sne[le * 6 + 2 * D + 1] * NPE + goff);
+        } else {
+            const unsigned e32 = (unsigned)(e0 + le), exy = e32 / (unsigned)g.Nl[0];
+            const int c0 = (int)(e32 - exy * (unsigned)g.Nl[0]), c1 = (int)(exy % (unsigned)g.Nl[1]),
+                      c2 = (int)(exy / (unsigned)g.Nl[1]);
+            const int cl[3] = {c0 - (D == 0), c1 - (D == 1), c2 - (D == 2)};
+            const int cr[3] = {c0 + (D == 0), c1 + (D == 1), c2 + (D == 2)};
+            vl = nbr_face_nu(g, nu, halo, n, cl, D, goff, P * GS);
+            vr = nbr_face_nu(g, nu, halo, n, cr, D, goff, 0);
+        }
+        snb[(2 * D) * E * NN + L] = vl;
+        snb[(2 * D + 1) * E * NN + L] = vr;
+    }
+}
+
+// one pass: every line of direction D accumulates its term into sacc (D = 2 also inverts)
+template <int P, int D>
+__device__ __forceinline__ void diag3_pass(const Geom &g, double lam, int invert, const DiagTab &dt, int cnt,
+                                           const double *snu, const double *snb, double *sacc)
+{
+    using C = DiagCfg3<P>;
+    constexpr int n = C::n, NN = C::NN, PX = C::PX, E = C::E;
+    constexpr int SS = D == 0 ? 1 : (D == 1 ? PX : PX * n);
+    const DevTab &T = c_tab[P];
+    const double sd = g.sd[D], tau = g.tau[D];
+    for (int L = threadIdx.x; L < cnt * NN; L += blockDim.x) {
+        int base, goff, a, b;
+        diag3_line<P, D>(L, base, goff, a, b);
+        double v[n];
+#pragma unroll
+        for (int m = 0; m < n; ++m) v[m] = snu[base + m * SS];
+        const double nuL = snb[(2 * D) * E * NN + L], nuR = snb[(2 * D + 1) * E * NN + L];
+        const double W = g.wfac[D] * T.w[a] * T.w[b];
+        double r[n];
+#pragma unroll
+        for (int i = 0; i < n; ++i) {
+            double acc = 0.0;
+#pragma unroll
+            for (int k = 0; k < n; ++k) acc = fma(dt.wd2[k][i], v[k], acc);
+            r[i] = acc * sd;
+        }
+        r[0] += v[0] * sd * dt.dd0 + 0.5 * tau * (v[0] + nuL);
+        r[P] += -v[P] * sd * dt.ddP + 0.5 * tau * (v[P] + nuR);
+        if (D == 0) {
+            const double lm = lam * g.mfac * T.w[a] * T.w[b];
+#pragma unroll
+            for (int i = 0; i < n; ++i) sacc[base + i] = fma(W, r[i], lm * T.w[i]);
+        } else if (D == 1) {
+#pragma unroll
+            for (int i = 0; i < n; ++i) sacc[base + i * SS] = fma(W, r[i], sacc[base + i * SS]);
+        } else {
+#pragma unroll
+            for (int i = 0; i < n; ++i) {
+                const double dgv = fma(W, r[i], sacc[base + i * SS]);
+                double rv = dgv;
+                if (invert) {  // reciprocal: approximate + two Newton steps (no DDIV slow path)
+                    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(rv) : "d"(dgv));
+                    rv = fma(rv, fma(-dgv, rv, 1.0), rv);
+                    rv = fma(rv, fma(-dgv, rv, 1.0), rv);
+                }
+                sacc[base + i * SS] = rv;
+            }
+        }
+    }
+}
+
 template <int P>
-__global__ void __launch_bounds__(256, 4) k_diag_cf3(const Geom g, double lam, const double *__restrict__ nu,
+__global__ void __launch_bounds__(256, 3) k_diag_cf3(const Geom g, double lam, const double *__restrict__ nu,
                                                      Halo halo, double *__restrict__ diag, int invert,
                                                      const __grid_constant__ DiagTab dt)
 {
     using C = DiagCfg3<P>;
     constexpr int n = C::n, NN = C::NN, NPE = C::NPE, PX = C::PX, SPE = C::SPE, E = C::E;
-    const DevTab &T = c_tab[P];
     extern __shared__ __align__(16) double dsm[];
     double *snu = dsm, *sacc = dsm + E * SPE;
     double *snb = dsm + 2 * E * SPE;  // [D][side][line]: the neighbours' nu at the tile's face nodes
+    long long *sne = reinterpret_cast<long long *>(snb + 6 * E * NN);  // [le][D][side] neighbour elements
     const int tid = threadIdx.x, bd = blockDim.x;
     const long long ntile = (g.nel + E - 1) / E;
     const unsigned nx = (unsigned)g.Nl[0], ny = (unsigned)g.Nl[1];
-    auto smem_of = [&](int q) {  // tile node q (element-major, node-contiguous) -> padded slot
-        const int le = q / NPE, r = q - le * NPE, i = r % n;
-        return le * SPE + i + PX * (r / n);
-    };
-    // line L of direction D: smem base of node 0, global in-element offset of node 0
-    auto line_of = [&](int D, int L, int &base, int &goff) {
-        const int le = L / NN, ab = L - le * NN, a = ab % n, b = ab / n;
-        if (D == 0) {
-            base = PX * ab;
-            goff = n * a + NN * b;
-        } else if (D == 1) {
-            base = a + PX * n * b;
-            goff = a + NN * b;
-        } else {
-            base = a + PX * b;
-            goff = a + n * b;
-        }
-        base += le * SPE;
-        return le;
-    };
-    // one latency round per tile: the tile's nu and every face-neighbour nu its lines need
-    auto load_tile = [&](long long t) {
-        const long long e0 = t * E;
-        const int cnt = (int)(g.nel - e0 < E ? g.nel - e0 : E);
-        for (int q = tid; q < cnt * NPE; q += bd) snu[smem_of(q)] = __ldg(nu + e0 * NPE + q);
-        for (int x = tid; x < 3 * cnt * NN; x += bd) {
-            const int D = x / (cnt * NN), L = x - D * cnt * NN;
-            const int GS = D == 0 ? 1 : (D == 1 ? n : NN);
-            int base, goff;
-            const int le = line_of(D, L, base, goff);
-            const unsigned e32 = (unsigned)(e0 + le), exy = e32 / nx;
-            const int ec[3] = {(int)(e32 - exy * nx), (int)(exy % ny), (int)(exy / ny)};
-            int cl[3] = {ec[0], ec[1], ec[2]}, cr[3] = {ec[0], ec[1], ec[2]};
-            cl[D] -= 1;
-            cr[D] += 1;
-            snb[(2 * D) * E * NN + L] = nbr_face_nu(g, nu, halo, n, cl, D, goff, P * GS);
-            snb[(2 * D + 1) * E * NN + L] = nbr_face_nu(g, nu, halo, n, cr, D, goff, 0);
-        }
-    };
-    long long tile = blockIdx.x;
-    if (tile >= ntile) return;
-    load_tile(tile);
-    for (; tile < ntile; tile += gridDim.x) {
+    // slab meshes without halos: neighbour element indices once per (element, direction, side);
+    // halo meshes take the generic per-line lookup
+    const bool hmesh = halo.tr_lo != nullptr || halo.tr_hi != nullptr;
+    for (long long tile = blockIdx.x; tile < ntile; tile += gridDim.x) {
         const long long e0 = tile * E;
         const int cnt = (int)(g.nel - e0 < E ? g.nel - e0 : E);
-        __syncthreads();
-#pragma unroll 1
-        for (int D = 0; D < 3; ++D) {
-            const int SS = D == 0 ? 1 : (D == 1 ? PX : PX * n);
-            const double sd = g.sd[D], tau = g.tau[D];
-            for (int L = tid; L < cnt * NN; L += bd) {
-                int base, goff;
-                const int le = line_of(D, L, base, goff);
-                const int ab = L - le * NN, a = ab % n, b = ab / n;
-                double v[n];
-#pragma unroll
-                for (int m = 0; m < n; ++m) v[m] = snu[base + m * SS];
-                const double nuL = snb[(2 * D) * E * NN + L], nuR = snb[(2 * D + 1) * E * NN + L];
-                const double W = g.wfac[D] * T.w[a] * T.w[b];
-                double r[n];
-#pragma unroll
-                for (int i = 0; i < n; ++i) {
-                    double acc = 0.0;
-#pragma unroll
-                    for (int k = 0; k < n; ++k) acc = fma(dt.wd2[k][i], v[k], acc);
-                    r[i] = acc * sd;
-                }
-                r[0] += v[0] * sd * dt.dd0 + 0.5 * tau * (v[0] + nuL);
-                r[P] += -v[P] * sd * dt.ddP + 0.5 * tau * (v[P] + nuR);
-                if (D == 0) {
-                    const double lm = lam * g.mfac * T.w[a] * T.w[b];
-#pragma unroll
-                    for (int i = 0; i < n; ++i) sacc[base + i] = fma(W, r[i], lm * T.w[i]);
-                } else if (D == 1) {
-#pragma unroll
-                    for (int i = 0; i < n; ++i) sacc[base + i * SS] = fma(W, r[i], sacc[base + i * SS]);
-                } else {
-#pragma unroll
-                    for (int i = 0; i < n; ++i) {
-                        const double dgv = fma(W, r[i], sacc[base + i * SS]);
-                        sacc[base + i * SS] = invert ? 1.0 / dgv : dgv;
-                    }
-                }
+        __syncthreads();  // the previous tile's store has read sacc
+        for (int q = tid; q < cnt * NPE; q += bd) {
+            const int le = q / NPE, r = q - le * NPE;
+            snu[le * SPE + r % n + PX * (r / n)] = __ldg(nu + e0 * NPE + q);
+        }
+        if (!hmesh) {
+            for (int x = tid; x < cnt * 6; x += bd) {
+                const int le = x / 6, D = (x >> 1) % 3, side = x & 1;
+                const unsigned e32 = (unsigned)(e0 + le), exy = e32 / nx;
+                int c0 = (int)(e32 - exy * nx), c1 = (int)(exy % ny), c2 = (int)(exy / ny);
+                const int dd = side ? 1 : -1;
+                if (D == 0) c0 = (c0 + dd + g.Nl[0]) % g.Nl[0];
+                else if (D == 1) c1 = (c1 + dd + g.Nl[1]) % g.Nl[1];
+                else c2 = (c2 + dd + g.Nl[2]) % g.Nl[2];
+                sne[x] = (long long)c0 + (long long)g.Nl[0] * (c1 + (long long)g.Nl[1] * c2);
             }
             __syncthreads();
         }
-        // coalesced store of this tile, then the next tile's loads (the passes are done with snu / snb)
-        for (int q = tid; q < cnt * NPE; q += bd) diag[e0 * NPE + q] = sacc[smem_of(q)];
-        if (tile + gridDim.x < ntile) load_tile(tile + gridDim.x);
+        diag3_nbr<P, 0>(g, nu, halo, hmesh, e0, cnt, sne, snb);
+        diag3_nbr<P, 1>(g, nu, halo, hmesh, e0, cnt, sne, snb);
+        diag3_nbr<P, 2>(g, nu, halo, hmesh, e0, cnt, sne, snb);
+        __syncthreads();
+        diag3_pass<P, 0>(g, lam, invert, dt, cnt, snu, snb, sacc);
+        __syncthreads();
+        diag3_pass<P, 1>(g, lam, invert, dt, cnt, snu, snb, sacc);
+        __syncthreads();
+        diag3_pass<P, 2>(g, lam, invert, dt, cnt, snu, snb, sacc);
+        __syncthreads();
+        for (int q = tid; q < cnt * NPE; q += bd) {  // coalesced store
+            const int le = q / NPE, r = q - le * NPE;
+            diag[e0 * NPE + q] = sacc[le * SPE + r % n + PX * (r / n)];
+        }
     }
 }
 
