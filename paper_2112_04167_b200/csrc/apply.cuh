@@ -595,14 +595,19 @@ struct ApplyDispatch {
             return cudaGetLastError();
         }
     }
+    // degrees / viscosity kinds the v6 kernel has: P odd <= 5, and P = 6 with constant nu
+    template <int P, bool VARNU>
+    static constexpr bool v6_shape() { return (P <= 5 && P % 2 == 1) || (P == 6 && !VARNU); }
     // v6 (3-D, n <= 6): one CTA per SM, 4x4x1 bricks, warpgroup-specialised (apply6.cuh)
     template <int P, bool VARNU, int MODE>
     static cudaError_t go6(ApplyParams a, int *grid, cudaStream_t st)
     {
-        using K = v6::KC6<P, VARNU, MODE>;
-        if constexpr (K::n > 6 || K::SMEM_BYTES > 227 * 1024) {
+        if constexpr (!v6_shape<P, VARNU>() || MODE == 1) {
+            return cudaErrorNotSupported;
+        } else if constexpr (v6::KC6<P, VARNU, MODE>::SMEM_BYTES > 227 * 1024) {
             return cudaErrorNotSupported;
         } else {
+            using K = v6::KC6<P, VARNU, MODE>;
             auto kern = v6::k_apply6<P, VARNU, MODE>;
             if (VARNU) {  // weight-folded constants (V6Fold, dg_internal.h)
                 const Tab &t = host_tab(P);
@@ -642,15 +647,16 @@ struct ApplyDispatch {
             }
             const int nbS = a.zhi - a.zlo;  // one element layer per brick
             // column segments per column: the persistent CTAs take ceil(units / grid) units of
-            // seglen bricks each plus a per-segment cost (segment-end z traces, pipeline fill)
-            // of ~3.3 bricks (fitted on c5: nseg = 2, 4, 8, 16 -> 0.576, 0.551, 0.633, 0.761 ms);
-            // pick the divisor of nbS (seglen >= 2) with the least modelled time
+            // seglen bricks each plus a per-segment cost (the two halo bricks of the segment's z
+            // ends) of ~1.1 bricks (fitted on c5: nseg = 2, 4, 8, 16 -> 0.544, 0.494, 0.526,
+            // 0.579 ms; 3.3 bricks with the earlier segment-end trace loads); pick the divisor of
+            // nbS (seglen >= 2) with the least modelled time
             int nseg = 1;
             double best = 1e300;
             for (int ns = 1; ns <= nbS / 2; ++ns) {
                 if (nbS % ns) continue;
                 const long long units = ncols * ns;
-                const double cost = (double)((units + gsz - 1) / gsz) * (nbS / ns + 3.3);
+                const double cost = (double)((units + gsz - 1) / gsz) * (nbS / ns + 1.1);
                 if (cost <= best * 1.01) {  // near-ties: more units (finer balance; measured)
                     best = cost < best ? cost : best;
                     nseg = ns;
@@ -678,8 +684,9 @@ struct ApplyDispatch {
             const char *e = DG_DEV_ENV("DG_APPLY_IMPL");
             return e && e[0] == 'v' && (e[1] == '4' || e[1] == '5');
         }();
-        // TMA copies single elements: n^3 doubles must be a multiple of 16 bytes (n even)
-        if (off || DIM != 3 || a.g.P > 5 || (a.g.P % 2) == 0) return false;
+        // TMA copies single elements (n even) or brick rows (P = 6, constant nu)
+        if (off || DIM != 3) return false;
+        if (!((a.g.P <= 5 && a.g.P % 2 == 1) || (a.g.P == 6 && !a.nu))) return false;
         if (a.g.Nl[0] % 4 || a.g.Nl[1] % 4 || a.g.Nl[2] < 2) return false;
         const int nz = a.zhi >= 0 ? a.zhi - a.zlo : a.g.Nl[2];
         if (nz < 2) return false;
@@ -691,7 +698,7 @@ struct ApplyDispatch {
     template <int P, bool VARNU>
     static constexpr bool mode2_fits6()
     {
-        if constexpr (P <= 5 && P % 2 == 1) return v6::KC6<P, VARNU, 2>::SMEM_BYTES <= 227 * 1024;
+        if constexpr (v6_shape<P, VARNU>()) return v6::KC6<P, VARNU, 2>::SMEM_BYTES <= 227 * 1024;
         else return false;
     }
     template <int P, bool VARNU>

@@ -21,8 +21,14 @@
 //   * z pass: the bottom face comes from the thread's own carry (the previous brick's top
 //     line), the top face is deferred -- the element output is parked in shared memory and
 //     completed by the next brick (the v5 ZCarry, per element line);
+//   * segment ends: each column segment is walked with one halo brick below and above it,
+//     staged by TMA like the others (periodic layers; received face traces at the slab ends of
+//     a halo mesh): the bottom halo seeds the z carry, the top halo releases the last parked
+//     outputs -- no per-line global loads for the segment-end z traces (round 3: c5
+//     0.517 -> 0.493 ms, per-segment cost 3.3 -> 1.1 bricks);
 //   * staging: TMA bulk copies, one element per lane, into odd-chunk padded slots
-//     (conflict-free 16-byte x-line loads).
+//     (conflict-free 16-byte x-line loads); odd n (P = 6, constant nu only): one copy per
+//     brick row of 4 x-consecutive elements (an element is not a multiple of 16 bytes).
 #pragma once
 
 #include "apply5.cuh"
@@ -53,14 +59,21 @@ struct KC6 {
     static constexpr int NN = n * n;
     static constexpr int NPE = n * n * n;
     static constexpr int BX = 4, BY = 4, BE = 16;               // brick: 4 x 4 x 1 elements
-    static constexpr int SE = ((NPE + 1) / 2) * 2 + 4;          // padded element slot (doubles)
-    static constexpr int SY = 4 * SE + 4;                        // slot stride along y (bank spread)
+    // odd n (P = 6, constant nu): an element is not a multiple of 16 bytes, so the TMA copies
+    // whole brick rows (4 x-consecutive elements, contiguous in HBM and in shared memory)
+    static constexpr bool ROWTMA = (NPE % 2) != 0;
+    static_assert(!(ROWTMA && VARNU_), "odd n: constant nu only");
+    static constexpr int SE = ROWTMA ? NPE : ((NPE + 1) / 2) * 2 + 4;  // element slot (doubles)
+    static constexpr int SY0 = ROWTMA ? 4 * SE : 4 * SE + 4;
+    static constexpr int SY = ROWTMA ? SY0 + ((4 - SY0 % 16) + 16) % 16 : SY0;  // row stride (== 4 mod 16)
     static constexpr int NCL = BE * NN;                          // consumer lines per pass
     // consumer warps, warpgroup-aligned (18 of 20 busy at P = 5; measured: 18 consumer + 6 producer
     // warps 0.573 ms, 18 + 5 0.605 ms, 20 + 4 0.520 ms on c5)
-    static constexpr int NCW = ((NCL + 31) / 32 + 3) / 4 * 4;
+    static constexpr int NCW = ROWTMA ? (NCL + 31) / 32 : ((NCL + 31) / 32 + 3) / 4 * 4;
     static constexpr int NC = NCW * 32;
-    static constexpr int NP = 128;                               // producer warpgroup
+    // producer: one TMA warp and NTW trace warps (n = 7: 25 consumer + 1 + 6 = 32 warps at 64 registers)
+    static constexpr int NTW = ROWTMA ? 6 : 3;
+    static constexpr int NP = 32 * (1 + NTW);
     static constexpr int NT = NC + NP;
     static constexpr int NV = VARNU ? 3 : 2;                     // trace values: u, s (, nu)
     static constexpr int LR = 4 * NN;                            // x / y brick-face lines per side
@@ -77,8 +90,7 @@ struct KC6 {
     static constexpr int OFF_NU = OFF_U + 2 * BRK;
     static constexpr int OFF_ACC = OFF_NU + (VARNU ? 2 * BRK : 0);
     static constexpr int OFF_TR = OFF_ACC + BRK;                 // [2][d][side][c][LR]
-    static constexpr int OFF_TZ = OFF_TR + 2 * TRXY;             // [side][c][NCL] (segment ends)
-    static constexpr int OFF_ZO = OFF_TZ + 2 * NV * NCL;         // parked z-pass outputs [n][NCL]
+    static constexpr int OFF_ZO = OFF_TR + 2 * TRXY;             // parked z-pass outputs [n][NCL]
     static constexpr int OFF_RED = OFF_ZO + n * NCL;
     static constexpr int OFF_BAR = OFF_RED + 64;
     static constexpr int OFF_W = OFF_BAR + 4;          // full[2], empty[2]
@@ -91,7 +103,7 @@ struct KC6 {
 struct ZC6 {
     bool held = false;
     double *po = nullptr;
-    double u, gP, nu;
+    double u, gP, nu, s;  // top node: u, reference derivative, nu (VARNU: nu~), flux s (VARNU: s~)
 };
 
 // ---------------------------------------------------------------------------
@@ -226,12 +238,34 @@ __device__ __forceinline__ void cpass_xy(const ApplyParams &a, const DevTab &T, 
 // ---------------------------------------------------------------------------
 // consumer z pass (last): carry, deferred top face, output
 // ---------------------------------------------------------------------------
+// release the previous brick's parked output: its top-face terms dr_i = c D_{P,i} + [i == P] f0
+// with the face shared with the current bottom (VARNU: c and f0 arrive W-weighted)
+template <class K>
+__device__ __forceinline__ void zrelease(const DevTab &T, double c, double f0, double W, const double *zo, int t,
+                                         ZC6 &zc, double &epi0, double &epi1)
+{
+    constexpr int P = K::P, n = K::n, NN = K::NN, NCL = K::NCL;
+    const double Wr = K::VARNU ? 1.0 : W;
+    double s1 = 0.0;
+#pragma unroll
+    for (int i = 0; i < n; ++i) {
+        const double d = K::VARNU ? fma(c, T.D[P][i], i == P ? f0 : 0.0) : W * fma(c, T.D[P][i], i == P ? f0 : 0.0);
+        zc.po[i * NN] = zo[i * NCL + t] + d;
+        s1 += d;
+    }
+    if (K::MODE >= 1) {
+        epi0 = fma(Wr, fma(c, zc.gP, f0 * zc.u), epi0);
+        if (K::MODE != 3) epi1 += s1;
+    }
+    zc.held = false;
+}
+
 template <class K>
 __device__ __forceinline__ void cpass_z(const ApplyParams &a, const DevTab &T, const double *su, const double *snu,
-                                        const double *sacc, const double *tz, double *zo, long long eb, int t,
-                                        bool zfirst, bool zlast, ZC6 &zc, double &epi0, double &epi1, const double *sw)
+                                        const double *sacc, double *zo, long long eb, int t, ZC6 &zc, double &epi0,
+                                        double &epi1, const double *sw)
 {
-    constexpr int P = K::P, n = K::n, NN = K::NN, NPE = K::NPE, NCL = K::NCL, NV = K::NV, SE = K::SE;
+    constexpr int P = K::P, n = K::n, NN = K::NN, NPE = K::NPE, NCL = K::NCL, SE = K::SE;
     if (t >= NCL) return;
     const Geom &g = a.g;
     const int slot = t / NN, tn = t - slot * NN;
@@ -245,96 +279,120 @@ __device__ __forceinline__ void cpass_z(const ApplyParams &a, const DevTab &T, c
         v[i] = su[base + i * NN];
         nv[i] = K::VARNU ? snu[base + i * NN] : a.nu_const;
     }
-    double uL, sL, nuL, uR = 0.0, sR = 0.0, nuR = a.nu_const;
-    if (zfirst) {
-        uL = tz[t];
-        sL = tz[NCL + t];
-        nuL = K::VARNU ? tz[2 * NCL + t] : a.nu_const;
-    } else {
-        uL = zc.u;
-        nuL = K::VARNU ? zc.nu : a.nu_const;
-        sL = K::VARNU ? nuL * zc.gP : nuL * sd * zc.gP;  // VARNU: s~ = nu~ g (weight-folded)
-    }
-    if (zlast) {
-        uR = tz[NV * NCL + t];
-        sR = tz[(NV + 1) * NCL + t];
-        nuR = K::VARNU ? tz[(NV + 2) * NCL + t] : a.nu_const;
-    }
-    // release the previous brick's parked output: its top-face terms
-    // dr_i = c D_{P,i} + [i == P] f0 with the face shared with our bottom
-    const double Wr = K::VARNU ? 1.0 : W;  // VARNU: c and f0 arrive W-weighted
-    auto release = [&](double c, double f0) {
-        double s1 = 0.0;
-#pragma unroll
-        for (int i = 0; i < n; ++i) {
-            const double d = K::VARNU ? fma(c, T.D[P][i], i == P ? f0 : 0.0) : W * fma(c, T.D[P][i], i == P ? f0 : 0.0);
-            zc.po[i * NN] = zo[i * NCL + t] + d;
-            s1 += d;
-        }
-        if (K::MODE >= 1) {
-            epi0 = fma(Wr, fma(c, zc.gP, f0 * zc.u), epi0);
-            if (K::MODE != 3) epi1 += s1;
-        }
-        zc.held = false;
-    };
-    double r[n], gP;
+    // bottom face: the carry of the brick below (or of the segment's bottom halo brick)
+    const double uL = zc.u, nuL = K::VARNU ? zc.nu : a.nu_const, sL = zc.s;
+    double r[n], gP, sP;
     if (K::VARNU) {
         // weight-folded form (see cpass_xy): results are W-weighted, the parked output and
-        // its release too (release() takes W = 1)
+        // its release too
         const V6Fold &F = a.f6;
         double gg[n], tv[n];
         eo<P, true>(T.eD, v, gg);
 #pragma unroll
         for (int k = 0; k < n; ++k) tv[k] = nv[k] * gg[k];
-        const double s0 = tv[0], sP = tv[P];
+        const double s0 = tv[0];
+        sP = tv[P];
         const double JL = uL - v[0];
         const double FL = fma(F.kF[2] * (nuL + nv[0]), JL, -F.kS[2] * (sL + s0));
-        double JR = 0.0, FR = 0.0;
-        if (zlast) {
-            JR = v[P] - uR;
-            FR = fma(F.kF[2] * (nv[P] + nuR), JR, -F.kS[2] * (sP + sR));
-        }
-        if (!zfirst && zc.held) release(-F.kCL[2] * zc.nu * JL, FL);
-        tv[P] = fma(-F.kL * nv[P], JR, tv[P]);
+        if (zc.held) zrelease<K>(T, -F.kCL[2] * zc.nu * JL, FL, W, zo, t, zc, epi0, epi1);
         tv[0] = fma(-F.kL * nv[0], JL, tv[0]);
         eo<P, true>(F.eE[2], tv, r);
-        r[P] += FR;
         r[0] -= FL;
         gP = gg[P];
     } else {
         const double c = a.nu_const * sd, ck = c * (0.5 * (P + 1) * (P + 1));
         const double d0 = rdot<P>(T, 0, v), dP = rdot<P>(T, P, v);
-        if (!zfirst && zc.held) release(0.5 * c * v[0], fma(-ck, v[0], -0.5 * c * d0));
+        if (zc.held) zrelease<K>(T, 0.5 * c * v[0], fma(-ck, v[0], -0.5 * c * d0), W, zo, t, zc, epi0, epi1);
         double kv[n];
         eo<P, false>(T.eK, v, kv);
-        const double aR = 0.5 * c * uR, aL = -0.5 * c * uL;
+        const double aL = -0.5 * c * uL;
 #pragma unroll
-        for (int i = 0; i < n; ++i) r[i] = fma(c, kv[i], fma(aR, T.D[P][i], aL * T.D[0][i]));
-        r[P] += fma(-ck, uR, -0.5 * sR);
+        for (int i = 0; i < n; ++i) r[i] = fma(c, kv[i], aL * T.D[0][i]);
         r[0] += fma(-ck, uL, 0.5 * sL);
         gP = dP;
+        sP = c * dP;
     }
-    // output: element (slot % 4, slot / 4) of the brick layer
+    // output of element (slot % 4, slot / 4) of the brick layer: parked without its top-face
+    // terms until the brick above (or the top halo brick) supplies the other side
     const long long ge = eb + (slot & 3) + (long long)g.Nl[0] * (slot >> 2);
-    double *po = a.out + ge * NPE + ta + tb * n;
     const double lw = a.lam * W * (0.5 * g.h[2]);
     const double *pa = sacc + base;
 #pragma unroll
     for (int i = 0; i < n; ++i) {
         const double o = fma(lw * T.w[i], v[i], K::VARNU ? r[i] + pa[i * NN] : fma(W, r[i], pa[i * NN]));
-        if (zlast) po[i * NN] = o;
-        else zo[i * NCL + t] = o;
+        zo[i * NCL + t] = o;
         if (K::MODE >= 1) {
             epi0 = fma(v[i], o, epi0);
             if (K::MODE != 3) epi1 += o;
         }
     }
-    if (!zlast) {
-        zc.held = true;
-        zc.po = po;
-        zc.u = v[P];
-        zc.gP = gP;
-        zc.nu = nv[P];
+    zc.held = true;
+    zc.po = a.out + ge * NPE + ta + tb * n;
+    zc.u = v[P];
+    zc.gP = gP;
+    zc.nu = nv[P];
+    zc.s = sP;
+}
+
+// the halo bricks of a column segment (the layer below its first brick, TOP: above its last):
+// only their face lines adjacent to the segment are used -- the bottom halo sets the z carry,
+// the top halo releases the parked outputs of the last brick.  The brick was staged like any
+// other (TMA, local or periodic layer); at a slab boundary of a halo mesh the face traces
+// received from the neighbouring rank are read instead (su == nullptr).
+template <class K, bool TOP>
+__device__ __forceinline__ void czhalo(const ApplyParams &a, const DevTab &T, const double *su, const double *snu,
+                                       const double *zo, const int (&e0)[3], int cz, int t, ZC6 &zc, double &epi0,
+                                       double &epi1, const double *sw)
+{
+    constexpr int P = K::P, n = K::n, NN = K::NN, NCL = K::NCL, SE = K::SE;
+    if (t >= NCL) return;
+    const Geom &g = a.g;
+    const int slot = t / NN, tn = t - slot * NN;
+    const int ta = tn % n, tb = tn / n;
+    const double W = sw[ta] * sw[tb] * g.wfac[2];
+    const double sd = g.sd[2];
+    constexpr int fi = TOP ? 0 : P;  // the face node of the halo element
+    double uf, nuf, sf, gf = 0.0;    // face u, nu (VARNU: nu~), flux (VARNU: s~), reference derivative
+    if (su) {
+        const int base = (slot & 3) * SE + (slot >> 2) * K::SY + ta + tb * n;
+        double v[n];
+#pragma unroll
+        for (int i = 0; i < n; ++i) v[i] = su[base + i * NN];
+        gf = rdot<P>(T, fi, v);
+        uf = v[fi];
+        nuf = K::VARNU ? snu[base + fi * NN] * (sw[ta] * sw[tb] * T.w[fi]) : a.nu_const;
+        sf = K::VARNU ? nuf * gf : a.nu_const * sd * gf;
+    } else {
+        const double *trh = halo_trace(g, a.halo, cz);
+        const long long F = halo_F(g, n), f = halo_f(g, n, e0[0] + (slot & 3), e0[1] + (slot >> 2), ta + tb * n);
+        uf = __ldg(trh + f);
+        const double hs = __ldg(trh + F + f);  // physical s = nu d u / d x_S
+        if (K::VARNU) {  // weight-folded: nu~ = nu w_a w_b w_0, s~ = s w_a w_b w_0 h_z / 2
+            const double wab = sw[ta] * sw[tb] * sw[0];
+            nuf = __ldg(trh + 2 * F + f) * wab;
+            sf = hs * wab * (0.5 * g.h[2]);
+        } else {
+            nuf = a.nu_const;
+            sf = hs;
+        }
+    }
+    if (!TOP) {
+        zc.held = false;
+        zc.u = uf;
+        zc.gP = gf;
+        zc.nu = nuf;
+        zc.s = sf;
+        return;
+    }
+    if (!zc.held) return;
+    if (K::VARNU) {
+        const V6Fold &F = a.f6;
+        const double JL = zc.u - uf;
+        const double FL = fma(F.kF[2] * (zc.nu + nuf), JL, -F.kS[2] * (zc.s + sf));
+        zrelease<K>(T, -F.kCL[2] * zc.nu * JL, FL, W, zo, t, zc, epi0, epi1);
+    } else {
+        const double c = a.nu_const * sd, ck = c * (0.5 * (P + 1) * (P + 1));
+        zrelease<K>(T, 0.5 * c * uf, fma(-ck, uf, -0.5 * sf), W, zo, t, zc, epi0, epi1);
     }
 }
 
@@ -415,62 +473,6 @@ __device__ __forceinline__ void ptraces_xy(const ApplyParams &a, const DevTab &T
     }
 }
 
-// z traces at column-segment ends (global memory; halo layers for multi-rank slabs)
-template <class K>
-__device__ __noinline__ void ptraces_z(const ApplyParams &a, const DevTab &T, double *tz, const int (&e0)[3], int ptid,
-                                       double beta, int side, const double *sw)
-{
-    constexpr int P = K::P, n = K::n, NN = K::NN, NPE = K::NPE, NCL = K::NCL, NV = K::NV;
-    const Geom &g = a.g;
-    const double *fu = K::MODE == 1 ? a.pro.z : a.u;
-    for (int t = ptid; t < NCL; t += K::NP) {
-        const int slot = t / NN, tn = t - slot * NN;
-        const int ta = tn % n, tb = tn / n;
-        const int cz = side ? e0[2] + 1 : e0[2] - 1;
-        const int goff = ta + tb * n + (side ? 0 : P * NN);
-        const int step = side ? NN : -NN;
-        double *t0 = tz + side * NV * NCL;
-        if (K::MODE != 1) {  // slab boundary of a multi-rank / halo-mode mesh: received face trace
-            const double *trh = halo_trace(g, a.halo, cz);
-            if (trh) {
-                const long long F = halo_F(g, n), f = halo_f(g, n, e0[0] + (slot & 3), e0[1] + (slot >> 2), ta + tb * n);
-                const double hu = __ldg(trh + f), hs = __ldg(trh + F + f);
-                t0[t] = hu;
-                if (K::VARNU) {  // weight-folded (see ptraces_xy): s~ = s w_a w_b w_0 h_z / 2, nu~ = nu w_a w_b w_0
-                    const double wab = sw[ta] * sw[tb] * sw[0];
-                    t0[NCL + t] = hs * wab * (0.5 * g.h[2]);
-                    t0[2 * NCL + t] = __ldg(trh + 2 * F + f) * wab;
-                } else {
-                    t0[NCL + t] = hs;
-                }
-                continue;
-            }
-        }
-        const double *pu = v5::nbr<2>(g, fu, nullptr, nullptr, e0[0] + (slot & 3), e0[1] + (slot >> 2), cz, NPE) + goff;
-        double v[n];
-        if (K::MODE == 1) {
-            const double *pp = a.pro.p_old + (pu - fu);
-#pragma unroll
-            for (int i = 0; i < n; ++i) v[i] = fma(beta, __ldg(pp + i * step), __ldg(pu + i * step));
-        } else {
-#pragma unroll
-            for (int i = 0; i < n; ++i) v[i] = __ldg(pu + i * step);
-        }
-        const double nuf = K::VARNU ? __ldg(v5::nbr<2>(g, a.nu, nullptr, nullptr, e0[0] + (slot & 3),
-                                                       e0[1] + (slot >> 2), cz, NPE) + goff)
-                                    : a.nu_const;
-        const double dd = rdot<P>(T, 0, v);
-        t0[t] = v[0];
-        if (K::VARNU) {  // weight-folded (see ptraces_xy)
-            const double nw = nuf * (sw[ta] * sw[tb] * sw[0]);
-            t0[NCL + t] = nw * (side ? dd : -dd);
-            t0[2 * NCL + t] = nw;
-        } else {
-            t0[NCL + t] = nuf * g.sd[2] * (side ? dd : -dd);
-        }
-    }
-}
-
 template <int P, bool VARNU, int MODE>
 __global__ void __launch_bounds__((KC6<P, VARNU, MODE>::NT)) __maxnreg__((KC6<P, VARNU, MODE>::REG_C))
     k_apply6(const __grid_constant__ ApplyParams a)
@@ -507,17 +509,27 @@ __global__ void __launch_bounds__((KC6<P, VARNU, MODE>::NT)) __maxnreg__((KC6<P,
         int it = 0;
         for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
             const int col = u % ncols, zs = u / ncols;
-            int e0[3] = {(col % nb0) * K::BX, (col / nb0) * K::BY, a.zlo + zs * seglen};
-            for (int j = 0; j < seglen; ++j, ++it, ++e0[2]) {
+            // bricks j = -1 and j = seglen are the segment's halo bricks (z faces of its ends)
+            int e0[3] = {(col % nb0) * K::BX, (col / nb0) * K::BY, a.zlo + zs * seglen - 1};
+            for (int j = -1; j <= seglen; ++j, ++it, ++e0[2]) {
                 const int buf = it & 1;
+                const bool hb = j < 0 || j == seglen;
                 V5_T0(tw);
                 if (it >= 2) mbar_wait(&bar[2 + buf], ((it >> 1) - 1) & 1);
                 if (ptid == 0) V5_ACC(2, tw);
                 V5_T0(tt);
                 double *su = sm + K::OFF_U + buf * BRK;
                 double *snu = sm + K::OFF_NU + buf * BRK;
-                const long long eb = e0[0] + s1 * e0[1] + s2 * e0[2];
-                if (ptid < 32) {
+                // halo layer outside the slab: periodic wrap on a plain mesh; on a halo mesh the
+                // consumers read the received face traces instead (nothing staged)
+                int zl = e0[2];
+                bool staged = true;
+                if (zl < 0 || zl >= g.Nl[2]) {
+                    if (a.halo.tr_lo || a.halo.tr_hi) staged = false;
+                    else zl = zl < 0 ? zl + g.Nl[2] : zl - g.Nl[2];
+                }
+                const long long eb = e0[0] + s1 * e0[1] + s2 * zl;
+                if (ptid < 32 && staged) {
                     // TMA: one element per lane into its padded slot (u lanes 0-15, nu 16-31)
                     constexpr unsigned EB = NPE * 8u;
                     if (lane == 0) {
@@ -528,9 +540,13 @@ __global__ void __launch_bounds__((KC6<P, VARNU, MODE>::NT)) __maxnreg__((KC6<P,
                     const int el = lane & 15;
                     const long long ge = eb + (el & 3) + s1 * (el >> 2);
                     const int so = (el & 3) * SE + (el >> 2) * K::SY;
-                    if (lane < 16 && MODE != 1) tma_load(su + so, a.u + ge * NPE, EB, &bar[buf]);
-                    if (lane >= 16 && VARNU) tma_load(snu + so, a.nu + ge * NPE, EB, &bar[buf]);
-                    if (j + 1 < seglen && MODE != 1) {
+                    if (K::ROWTMA) {  // brick row r = lane: elements (e0x .. e0x + 3, e0y + r)
+                        if (lane < 4 && MODE != 1) tma_load(su + lane * K::SY, a.u + (eb + s1 * lane) * NPE, 4 * EB, &bar[buf]);
+                    } else {
+                        if (lane < 16 && MODE != 1) tma_load(su + so, a.u + ge * NPE, EB, &bar[buf]);
+                        if (lane >= 16 && VARNU) tma_load(snu + so, a.nu + ge * NPE, EB, &bar[buf]);
+                    }
+                    if (j >= 0 && j + 1 < seglen && MODE != 1) {
                         // L2 prefetch of the x/y brick-face neighbour elements of the next brick
                         // (their trace loads then hit L2; measured on c5: 0.517 vs 0.525 ms;
                         // two layers ahead 0.519, four 0.54, eight 0.60)
@@ -550,7 +566,7 @@ __global__ void __launch_bounds__((KC6<P, VARNU, MODE>::NT)) __maxnreg__((KC6<P,
                         else if (VARNU) v5::l2_prefetch(a.nu + pe * NPE, EB);
                     }
                 }
-                if (MODE == 1) {  // p = z + beta p_old -> shared (operand) and p_out (fused CG prologue)
+                if (MODE == 1 && !hb) {  // p = z + beta p_old -> shared (operand) and p_out (fused CG prologue)
                     constexpr int H = NPE / 2;  // double2 per element (n even)
                     for (int q = ptid; q < 16 * H; q += NP) {
                         const int el = q / H, w = q - el * H;
@@ -568,7 +584,7 @@ __global__ void __launch_bounds__((KC6<P, VARNU, MODE>::NT)) __maxnreg__((KC6<P,
                 if (ptid == 0) V5_ACC(4, tt);
                 V5_T0(tx);
                 // x/y traces (warps 1-3) in rounds of at most 3 lines per thread (register budget)
-                if (DG_V6_TMATRACE || ptid >= 32) {
+                if (!hb && (DG_V6_TMATRACE || ptid >= 32)) {
                     const int pt = DG_V6_TMATRACE ? ptid : ptid - 32;
                     constexpr int R = MODE == 1 ? 2 : 3;  // lines in flight per thread (two loads each in MODE 1)
                     ptraces_xy<K, 0, (K::KT < R ? K::KT : R)>(a, T, tr, e0, eb, pt, beta, sw);
@@ -578,8 +594,6 @@ __global__ void __launch_bounds__((KC6<P, VARNU, MODE>::NT)) __maxnreg__((KC6<P,
                     if constexpr (K::KT > 2 * R) ptraces_xy<K, 2 * R, K::KT>(a, T, tr, e0, eb, pt, beta, sw);
                     if (ptid == 32) V5_ACC(10, ty);
                 }
-                if (j == 0) ptraces_z<K>(a, T, sm + K::OFF_TZ, e0, ptid, beta, 0, sw);
-                if (j == seglen - 1) ptraces_z<K>(a, T, sm + K::OFF_TZ, e0, ptid, beta, 1, sw);
                 if (ptid == 0) V5_ACC(3, tx);
                 mbar_arrive(&bar[buf]);
             }
@@ -593,11 +607,10 @@ __global__ void __launch_bounds__((KC6<P, VARNU, MODE>::NT)) __maxnreg__((KC6<P,
     ZC6 zc;
     double *sacc = sm + K::OFF_ACC;
     double *zo = sm + K::OFF_ZO;
-    const double *tz = sm + K::OFF_TZ;
     for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
         const int col = u % ncols, zs = u / ncols;
-        int e0[3] = {(col % nb0) * K::BX, (col / nb0) * K::BY, a.zlo + zs * seglen};
-        for (int j = 0; j < seglen; ++j, ++it, ++e0[2]) {
+        int e0[3] = {(col % nb0) * K::BX, (col / nb0) * K::BY, a.zlo + zs * seglen - 1};
+        for (int j = -1; j <= seglen; ++j, ++it, ++e0[2]) {
             const int buf = it & 1;
             const double *su = sm + K::OFF_U + buf * BRK;
             double *snu = sm + K::OFF_NU + buf * BRK;
@@ -606,6 +619,14 @@ __global__ void __launch_bounds__((KC6<P, VARNU, MODE>::NT)) __maxnreg__((KC6<P,
             V5_T0(tw);
             mbar_wait(&bar[buf], (it >> 1) & 1);
             if (tid == 0) V5_ACC(0, tw);
+            if (j < 0 || j == seglen) {  // halo brick: the segment's bottom carry / top release
+                const bool staged = !((e0[2] < 0 || e0[2] >= g.Nl[2]) && (a.halo.tr_lo || a.halo.tr_hi));
+                if (j < 0) czhalo<K, false>(a, T, staged ? su : nullptr, snu, zo, e0, e0[2], tid, zc, epi0, epi1, sw);
+                else czhalo<K, true>(a, T, staged ? su : nullptr, snu, zo, e0, e0[2], tid, zc, epi0, epi1, sw);
+                mbar_arrive(&bar[2 + buf]);
+                named_sync(1, NC);  // the parked outputs are rewritten by the next brick
+                continue;
+            }
             V5_T0(tp);
             cpass_xy<K, 0, true>(a, T, su, snu, sacc, tr, tid, sw);
             if (tid == 0) V5_ACC(6, tp);
@@ -615,7 +636,7 @@ __global__ void __launch_bounds__((KC6<P, VARNU, MODE>::NT)) __maxnreg__((KC6<P,
             if (tid == 0) V5_ACC(7, t1);
             named_sync(1, NC);
             V5_T0(t2);
-            cpass_z<K>(a, T, su, snu, sacc, tz, zo, eb, tid, j == 0, j == seglen - 1, zc, epi0, epi1, sw);
+            cpass_z<K>(a, T, su, snu, sacc, zo, eb, tid, zc, epi0, epi1, sw);
             if (tid == 0) V5_ACC(8, t2);
             mbar_arrive(&bar[2 + buf]);
             named_sync(1, NC);  // ACC and the parked outputs are rewritten by the next brick
