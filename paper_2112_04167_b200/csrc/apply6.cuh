@@ -31,6 +31,10 @@
 //     brick row of 4 x-consecutive elements (an element is not a multiple of 16 bytes).
 #pragma once
 
+#ifndef DG_V6_EXP
+#define DG_V6_EXP 0  // development bound experiments: 1 = no x/y traces, 2 = consumers skip the passes
+#endif
+
 #include "apply5.cuh"
 
 namespace dg {
@@ -78,22 +82,20 @@ struct KC6 {
     static constexpr int NV = VARNU ? 3 : 2;                     // trace values: u, s (, nu)
     static constexpr int LR = 4 * NN;                            // x / y brick-face lines per side
     static constexpr int TRXY = 2 * 2 * NV * LR;                 // x/y trace table per buffer
-#ifndef DG_V6_TMATRACE
-#define DG_V6_TMATRACE 0
-#endif
-    // producer trace threads: warps 1-3 (the TMA warp joining them delays its next copies:
-    // measured 0.677 vs 0.516 ms with DG_V6_TMATRACE 1)
-    static constexpr int NPT = DG_V6_TMATRACE ? NP : NP - 32;
+    // trace threads: producer warps 1..NTW (the TMA warp joining them delayed its next copies:
+    // measured 0.677 vs 0.516 ms in round 2)
+    static constexpr int NPT = NP - 32;
     static constexpr int KT = (4 * LR + NPT - 1) / NPT;          // producer x/y tasks per thread
     static constexpr int BRK = 4 * SY;
     static constexpr int OFF_U = 0;
     static constexpr int OFF_NU = OFF_U + 2 * BRK;
     static constexpr int OFF_ACC = OFF_NU + (VARNU ? 2 * BRK : 0);
     static constexpr int OFF_TR = OFF_ACC + BRK;                 // [2][d][side][c][LR]
-    static constexpr int OFF_ZO = OFF_TR + 2 * TRXY;             // parked z-pass outputs [n][NCL]
+    static constexpr int NTR = 3;                                // trace-table slots (traces run ahead)
+    static constexpr int OFF_ZO = OFF_TR + NTR * TRXY;           // parked z-pass outputs [n][NCL]
     static constexpr int OFF_RED = OFF_ZO + n * NCL;
     static constexpr int OFF_BAR = OFF_RED + 64;
-    static constexpr int OFF_W = OFF_BAR + 4;          // full[2], empty[2]
+    static constexpr int OFF_W = OFF_BAR + 10;         // full_uv[2] empty_uv[2] full_tr[3] empty_tr[3]
     static constexpr int SMEM_DOUBLES = OFF_W + n;     // GLL weights (per-lane indexed reads)
     static constexpr int SMEM_BYTES = SMEM_DOUBLES * 8;
     static constexpr int REG_C = 65536 / NT / 8 * 8 > 80 ? 80 : 65536 / NT / 8 * 8;  // launch registers
@@ -478,21 +480,28 @@ __global__ void __launch_bounds__((KC6<P, VARNU, MODE>::NT)) __maxnreg__((KC6<P,
     k_apply6(const __grid_constant__ ApplyParams a)
 {
     using K = KC6<P, VARNU, MODE>;
-    constexpr int NPE = K::NPE, SE = K::SE, BRK = K::BRK, NC = K::NC, NP = K::NP, NCL = K::NCL;
+    static_assert(MODE != 1, "v6 has no fused-PCG (MODE 1) variant");
+    constexpr int NPE = K::NPE, SE = K::SE, BRK = K::BRK, NC = K::NC, NCL = K::NCL, NTR = K::NTR;
     const Geom &g = a.g;
     const DevTab &T = c_tab[P];
     extern __shared__ __align__(16) double sm[];
-    uint64_t *bar = reinterpret_cast<uint64_t *>(sm + K::OFF_BAR);  // full[0..1], empty[0..1]
+    // the TMA warp runs on two u / nu slots, the trace warps on NTR trace-table slots: the
+    // brick-face traces are formed up to NTR - 1 bricks ahead of the consumers
+    uint64_t *bar = reinterpret_cast<uint64_t *>(sm + K::OFF_BAR);
+    uint64_t *full_uv = bar, *empty_uv = bar + 2, *full_tr = bar + 4, *empty_tr = bar + 4 + NTR;
     double *sw = sm + K::OFF_W;
     const int tid = threadIdx.x;
     if (tid < K::n) sw[tid] = T.w[tid];
     if (MODE >= 1 && *a.pro.done) return;  // PCG converged: nothing to do
-    const double beta = MODE == 1 ? *a.pro.beta : 0.0;
     if (tid == 0) {
-        mbar_init(&bar[0], NP);
-        mbar_init(&bar[1], NP);
-        mbar_init(&bar[2], NC);
-        mbar_init(&bar[3], NC);
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&full_uv[b], 1);
+            mbar_init(&empty_uv[b], NC);
+        }
+        for (int b = 0; b < NTR; ++b) {
+            mbar_init(&full_tr[b], K::NPT);
+            mbar_init(&empty_tr[b], NC);
+        }
         fence_proxy_async();
     }
     __syncthreads();
@@ -502,22 +511,47 @@ __global__ void __launch_bounds__((KC6<P, VARNU, MODE>::NT)) __maxnreg__((KC6<P,
     const int nunits = ncols * a.nseg;
     const int seglen = a.seglen;
     const long long s1 = g.Nl[0], s2 = (long long)g.Nl[0] * g.Nl[1];
+    const bool hmesh = a.halo.tr_lo != nullptr || a.halo.tr_hi != nullptr;
 
-    if (tid >= NC) {
-        // ------------------------------- producer -------------------------------
-        const int ptid = tid - NC, lane = ptid & 31;
+    if (tid >= NC + 32) {
+        // ------------------------------ trace warps ------------------------------
+        const int pt = tid - NC - 32;
         int it = 0;
         for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
             const int col = u % ncols, zs = u / ncols;
             // bricks j = -1 and j = seglen are the segment's halo bricks (z faces of its ends)
             int e0[3] = {(col % nb0) * K::BX, (col / nb0) * K::BY, a.zlo + zs * seglen - 1};
             for (int j = -1; j <= seglen; ++j, ++it, ++e0[2]) {
-                const int buf = it & 1;
-                const bool hb = j < 0 || j == seglen;
+                const int slot = it % NTR;
                 V5_T0(tw);
-                if (it >= 2) mbar_wait(&bar[2 + buf], ((it >> 1) - 1) & 1);
-                if (ptid == 0) V5_ACC(2, tw);
-                V5_T0(tt);
+                if (it >= NTR) mbar_wait(&empty_tr[slot], ((it / NTR) - 1) & 1);
+                if (pt == 0) V5_ACC(2, tw);
+                V5_T0(tx);
+                if (j >= 0 && j < seglen && (DG_V6_EXP & 1) == 0) {
+                    double *tr = sm + K::OFF_TR + slot * K::TRXY;
+                    constexpr int R = 3;  // lines in flight per thread (register budget)
+                    ptraces_xy<K, 0, (K::KT < R ? K::KT : R)>(a, T, tr, e0, 0, pt, 0.0, sw);
+                    if constexpr (K::KT > R) ptraces_xy<K, R, (K::KT < 2 * R ? K::KT : 2 * R)>(a, T, tr, e0, 0, pt, 0.0, sw);
+                    if constexpr (K::KT > 2 * R) ptraces_xy<K, 2 * R, K::KT>(a, T, tr, e0, 0, pt, 0.0, sw);
+                }
+                if (pt == 0) V5_ACC(3, tx);
+                mbar_arrive(&full_tr[slot]);
+            }
+        }
+        return;
+    }
+    if (tid >= NC) {
+        // ------------------------------- TMA warp -------------------------------
+        const int lane = tid - NC;
+        int it = 0;
+        for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
+            const int col = u % ncols, zs = u / ncols;
+            int e0[3] = {(col % nb0) * K::BX, (col / nb0) * K::BY, a.zlo + zs * seglen - 1};
+            for (int j = -1; j <= seglen; ++j, ++it, ++e0[2]) {
+                const int buf = it & 1;
+                V5_T0(tw);
+                if (it >= 2) mbar_wait(&empty_uv[buf], ((it >> 1) - 1) & 1);
+                if (lane == 0) V5_ACC(4, tw);
                 double *su = sm + K::OFF_U + buf * BRK;
                 double *snu = sm + K::OFF_NU + buf * BRK;
                 // halo layer outside the slab: periodic wrap on a plain mesh; on a halo mesh the
@@ -525,77 +559,46 @@ __global__ void __launch_bounds__((KC6<P, VARNU, MODE>::NT)) __maxnreg__((KC6<P,
                 int zl = e0[2];
                 bool staged = true;
                 if (zl < 0 || zl >= g.Nl[2]) {
-                    if (a.halo.tr_lo || a.halo.tr_hi) staged = false;
+                    if (hmesh) staged = false;
                     else zl = zl < 0 ? zl + g.Nl[2] : zl - g.Nl[2];
                 }
                 const long long eb = e0[0] + s1 * e0[1] + s2 * zl;
-                if (ptid < 32 && staged) {
-                    // TMA: one element per lane into its padded slot (u lanes 0-15, nu 16-31)
-                    constexpr unsigned EB = NPE * 8u;
-                    if (lane == 0) {
-                        const unsigned bytes = (MODE != 1 ? 16u * EB : 0u) + (VARNU ? 16u * EB : 0u);
-                        if (bytes) mbar_expect_tx(&bar[buf], bytes);
-                    }
-                    __syncwarp();
-                    const int el = lane & 15;
-                    const long long ge = eb + (el & 3) + s1 * (el >> 2);
-                    const int so = (el & 3) * SE + (el >> 2) * K::SY;
+                constexpr unsigned EB = NPE * 8u;
+                if (lane == 0) {
+                    if (staged) mbar_arrive_expect_tx(&full_uv[buf], 16u * EB + (VARNU ? 16u * EB : 0u));
+                    else mbar_arrive(&full_uv[buf]);
+                }
+                __syncwarp();
+                if (staged) {
                     if (K::ROWTMA) {  // brick row r = lane: elements (e0x .. e0x + 3, e0y + r)
-                        if (lane < 4 && MODE != 1) tma_load(su + lane * K::SY, a.u + (eb + s1 * lane) * NPE, 4 * EB, &bar[buf]);
+                        if (lane < 4) tma_load(su + lane * K::SY, a.u + (eb + s1 * lane) * NPE, 4 * EB, &full_uv[buf]);
+                    } else {  // one element per lane into its padded slot (u lanes 0-15, nu 16-31)
+                        const int el = lane & 15;
+                        const long long ge = eb + (el & 3) + s1 * (el >> 2);
+                        const int so = (el & 3) * SE + (el >> 2) * K::SY;
+                        if (lane < 16) tma_load(su + so, a.u + ge * NPE, EB, &full_uv[buf]);
+                        if (lane >= 16 && VARNU) tma_load(snu + so, a.nu + ge * NPE, EB, &full_uv[buf]);
+                    }
+                }
+                if (j >= 0 && j + 1 < seglen) {
+                    // L2 prefetch of the x/y brick-face neighbour elements of the next brick
+                    // (their trace loads then hit L2; measured on c5: 0.517 vs 0.525 ms;
+                    // two layers ahead 0.519, four 0.54, eight 0.60)
+                    const int nb = lane & 15, side = (nb >> 2) & 1, r = nb & 3;
+                    int cx, cy;
+                    if (nb < 8) {
+                        cx = side ? e0[0] + 4 : e0[0] - 1;
+                        cx = cx < 0 ? cx + g.Nl[0] : (cx >= g.Nl[0] ? cx - g.Nl[0] : cx);
+                        cy = e0[1] + r;
                     } else {
-                        if (lane < 16 && MODE != 1) tma_load(su + so, a.u + ge * NPE, EB, &bar[buf]);
-                        if (lane >= 16 && VARNU) tma_load(snu + so, a.nu + ge * NPE, EB, &bar[buf]);
+                        cy = side ? e0[1] + 4 : e0[1] - 1;
+                        cy = cy < 0 ? cy + g.Nl[1] : (cy >= g.Nl[1] ? cy - g.Nl[1] : cy);
+                        cx = e0[0] + r;
                     }
-                    if (j >= 0 && j + 1 < seglen && MODE != 1) {
-                        // L2 prefetch of the x/y brick-face neighbour elements of the next brick
-                        // (their trace loads then hit L2; measured on c5: 0.517 vs 0.525 ms;
-                        // two layers ahead 0.519, four 0.54, eight 0.60)
-                        const int nb = lane & 15, side = (nb >> 2) & 1, r = nb & 3;
-                        int cx, cy;
-                        if (nb < 8) {
-                            cx = side ? e0[0] + 4 : e0[0] - 1;
-                            cx = cx < 0 ? cx + g.Nl[0] : (cx >= g.Nl[0] ? cx - g.Nl[0] : cx);
-                            cy = e0[1] + r;
-                        } else {
-                            cy = side ? e0[1] + 4 : e0[1] - 1;
-                            cy = cy < 0 ? cy + g.Nl[1] : (cy >= g.Nl[1] ? cy - g.Nl[1] : cy);
-                            cx = e0[0] + r;
-                        }
-                        const long long pe = cx + s1 * cy + s2 * (e0[2] + 1);
-                        if (lane < 16) v5::l2_prefetch(a.u + pe * NPE, EB);
-                        else if (VARNU) v5::l2_prefetch(a.nu + pe * NPE, EB);
-                    }
+                    const long long pe = cx + s1 * cy + s2 * (e0[2] + 1);
+                    if (lane < 16) v5::l2_prefetch(a.u + pe * NPE, EB);
+                    else if (VARNU) v5::l2_prefetch(a.nu + pe * NPE, EB);
                 }
-                if (MODE == 1 && !hb) {  // p = z + beta p_old -> shared (operand) and p_out (fused CG prologue)
-                    constexpr int H = NPE / 2;  // double2 per element (n even)
-                    for (int q = ptid; q < 16 * H; q += NP) {
-                        const int el = q / H, w = q - el * H;
-                        const long long go = (eb + (el & 3) + s1 * (el >> 2)) * NPE + 2 * w;
-                        const double2 z = __ldg(reinterpret_cast<const double2 *>(a.pro.z + go));
-                        const double2 po = __ldg(reinterpret_cast<const double2 *>(a.pro.p_old + go));
-                        double2 p;
-                        p.x = fma(beta, po.x, z.x);
-                        p.y = fma(beta, po.y, z.y);
-                        *reinterpret_cast<double2 *>(su + (el & 3) * SE + (el >> 2) * K::SY + 2 * w) = p;
-                        *reinterpret_cast<double2 *>(a.pro.p_out + go) = p;
-                    }
-                }
-                double *tr = sm + K::OFF_TR + buf * K::TRXY;
-                if (ptid == 0) V5_ACC(4, tt);
-                V5_T0(tx);
-                // x/y traces (warps 1-3) in rounds of at most 3 lines per thread (register budget)
-                if (!hb && (DG_V6_TMATRACE || ptid >= 32)) {
-                    const int pt = DG_V6_TMATRACE ? ptid : ptid - 32;
-                    constexpr int R = MODE == 1 ? 2 : 3;  // lines in flight per thread (two loads each in MODE 1)
-                    ptraces_xy<K, 0, (K::KT < R ? K::KT : R)>(a, T, tr, e0, eb, pt, beta, sw);
-                    if (ptid == 32) V5_ACC(9, tx);
-                    V5_T0(ty);
-                    if constexpr (K::KT > R) ptraces_xy<K, R, (K::KT < 2 * R ? K::KT : 2 * R)>(a, T, tr, e0, eb, pt, beta, sw);
-                    if constexpr (K::KT > 2 * R) ptraces_xy<K, 2 * R, K::KT>(a, T, tr, e0, eb, pt, beta, sw);
-                    if (ptid == 32) V5_ACC(10, ty);
-                }
-                if (ptid == 0) V5_ACC(3, tx);
-                mbar_arrive(&bar[buf]);
             }
         }
         return;
@@ -611,34 +614,42 @@ __global__ void __launch_bounds__((KC6<P, VARNU, MODE>::NT)) __maxnreg__((KC6<P,
         const int col = u % ncols, zs = u / ncols;
         int e0[3] = {(col % nb0) * K::BX, (col / nb0) * K::BY, a.zlo + zs * seglen - 1};
         for (int j = -1; j <= seglen; ++j, ++it, ++e0[2]) {
-            const int buf = it & 1;
+            const int buf = it & 1, slot = it % NTR;
             const double *su = sm + K::OFF_U + buf * BRK;
             double *snu = sm + K::OFF_NU + buf * BRK;
-            const double *tr = sm + K::OFF_TR + buf * K::TRXY;
+            const double *tr = sm + K::OFF_TR + slot * K::TRXY;
             const long long eb = e0[0] + s1 * e0[1] + s2 * e0[2];
             V5_T0(tw);
-            mbar_wait(&bar[buf], (it >> 1) & 1);
+            mbar_wait(&full_uv[buf], (it >> 1) & 1);
+            mbar_wait(&full_tr[slot], (it / NTR) & 1);
             if (tid == 0) V5_ACC(0, tw);
             if (j < 0 || j == seglen) {  // halo brick: the segment's bottom carry / top release
-                const bool staged = !((e0[2] < 0 || e0[2] >= g.Nl[2]) && (a.halo.tr_lo || a.halo.tr_hi));
+                const bool staged = !((e0[2] < 0 || e0[2] >= g.Nl[2]) && hmesh);
                 if (j < 0) czhalo<K, false>(a, T, staged ? su : nullptr, snu, zo, e0, e0[2], tid, zc, epi0, epi1, sw);
                 else czhalo<K, true>(a, T, staged ? su : nullptr, snu, zo, e0, e0[2], tid, zc, epi0, epi1, sw);
-                mbar_arrive(&bar[2 + buf]);
+                mbar_arrive(&empty_tr[slot]);
+                mbar_arrive(&empty_uv[buf]);
                 named_sync(1, NC);  // the parked outputs are rewritten by the next brick
                 continue;
             }
             V5_T0(tp);
+            if (DG_V6_EXP & 2) {
+                mbar_arrive(&empty_tr[slot]);
+                mbar_arrive(&empty_uv[buf]);
+                continue;
+            }
             cpass_xy<K, 0, true>(a, T, su, snu, sacc, tr, tid, sw);
             if (tid == 0) V5_ACC(6, tp);
             named_sync(1, NC);
             V5_T0(t1);
             cpass_xy<K, 1, false>(a, T, su, snu, sacc, tr, tid, sw);
             if (tid == 0) V5_ACC(7, t1);
+            mbar_arrive(&empty_tr[slot]);  // the trace table is read by the x and y passes only
             named_sync(1, NC);
             V5_T0(t2);
             cpass_z<K>(a, T, su, snu, sacc, zo, eb, tid, zc, epi0, epi1, sw);
             if (tid == 0) V5_ACC(8, t2);
-            mbar_arrive(&bar[2 + buf]);
+            mbar_arrive(&empty_uv[buf]);
             named_sync(1, NC);  // ACC and the parked outputs are rewritten by the next brick
             if (tid == 0) {
                 V5_ACC(1, tp);

@@ -24,6 +24,7 @@ for P in (6, 7):
     b.record(st)
     torch.cuda.synchronize()
     res.append("P%d apply %.1f us (%s)" % (P, a.elapsed_time(b) / 20 * 1e3, dg.dg_last_apply_kernel().split(' ')[0]))
+    print(res[-1], flush=True)
     if P == 6:
         dg.dg_mesh_set_precond(m, dg.DG_PC_SCHWARZ2)
         f = u - u.mean()
