@@ -90,8 +90,15 @@ struct KC6 {
     static constexpr int OFF_U = 0;
     static constexpr int OFF_NU = OFF_U + 2 * BRK;
     static constexpr int OFF_ACC = OFF_NU + (VARNU ? 2 * BRK : 0);
-    static constexpr int OFF_TR = OFF_ACC + BRK;                 // [2][d][side][c][LR]
-    static constexpr int NTR = 3;                                // trace-table slots (traces run ahead)
+#ifndef DG_V6_ACC2
+#define DG_V6_ACC2 0
+#endif
+    // development: two accumulator tiles (even n) let brick k+1's x pass start while brick k's
+    // z pass finishes (one named barrier less per brick; then only two trace-table slots fit):
+    // measured unchanged on c5 (0.449 ms), so one tile and three trace slots
+    static constexpr int NACC = (DG_V6_ACC2 && !ROWTMA) ? 2 : 1;
+    static constexpr int OFF_TR = OFF_ACC + NACC * BRK;          // [NTR][d][side][c][LR]
+    static constexpr int NTR = NACC == 2 ? 2 : 3;                // trace-table slots (traces run ahead)
     static constexpr int OFF_ZO = OFF_TR + NTR * TRXY;           // parked z-pass outputs [n][NCL]
     static constexpr int OFF_RED = OFF_ZO + n * NCL;
     static constexpr int OFF_BAR = OFF_RED + 64;
@@ -608,7 +615,6 @@ __global__ void __launch_bounds__((KC6<P, VARNU, MODE>::NT)) __maxnreg__((KC6<P,
     double epi0 = 0.0, epi1 = 0.0;
     int it = 0;
     ZC6 zc;
-    double *sacc = sm + K::OFF_ACC;
     double *zo = sm + K::OFF_ZO;
     for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
         const int col = u % ncols, zs = u / ncols;
@@ -618,6 +624,7 @@ __global__ void __launch_bounds__((KC6<P, VARNU, MODE>::NT)) __maxnreg__((KC6<P,
             const double *su = sm + K::OFF_U + buf * BRK;
             double *snu = sm + K::OFF_NU + buf * BRK;
             const double *tr = sm + K::OFF_TR + slot * K::TRXY;
+            double *sacc = sm + K::OFF_ACC + (K::NACC == 2 ? buf * BRK : 0);
             const long long eb = e0[0] + s1 * e0[1] + s2 * e0[2];
             V5_T0(tw);
             mbar_wait(&full_uv[buf], (it >> 1) & 1);
@@ -629,7 +636,7 @@ __global__ void __launch_bounds__((KC6<P, VARNU, MODE>::NT)) __maxnreg__((KC6<P,
                 else czhalo<K, true>(a, T, staged ? su : nullptr, snu, zo, e0, e0[2], tid, zc, epi0, epi1, sw);
                 mbar_arrive(&empty_tr[slot]);
                 mbar_arrive(&empty_uv[buf]);
-                named_sync(1, NC);  // the parked outputs are rewritten by the next brick
+                if (K::NACC == 1) named_sync(1, NC);  // ACC is rewritten by the next brick
                 continue;
             }
             V5_T0(tp);
@@ -650,7 +657,9 @@ __global__ void __launch_bounds__((KC6<P, VARNU, MODE>::NT)) __maxnreg__((KC6<P,
             cpass_z<K>(a, T, su, snu, sacc, zo, eb, tid, zc, epi0, epi1, sw);
             if (tid == 0) V5_ACC(8, t2);
             mbar_arrive(&empty_uv[buf]);
-            named_sync(1, NC);  // ACC and the parked outputs are rewritten by the next brick
+            // single ACC: rewritten by the next brick's x pass (the parked outputs are
+            // thread-private); two ACC tiles: the next x pass writes the other one
+            if (K::NACC == 1) named_sync(1, NC);
             if (tid == 0) {
                 V5_ACC(1, tp);
 #ifdef DG_V5_DEBUG
