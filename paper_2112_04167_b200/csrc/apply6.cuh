@@ -67,7 +67,12 @@ struct KC6 {
     // whole brick rows (4 x-consecutive elements, contiguous in HBM and in shared memory)
     static constexpr bool ROWTMA = (NPE % 2) != 0;
     static_assert(!(ROWTMA && VARNU_), "odd n: constant nu only");
-    static constexpr int SE = ROWTMA ? NPE : ((NPE + 1) / 2) * 2 + 4;  // element slot (doubles)
+#ifndef DG_V6_SE228
+#define DG_V6_SE228 1
+#endif
+    // element slot (doubles); n = 6: SE = 228 == NN (mod 16) keeps the z-pass lines (stride NN,
+    // consecutive lanes crossing slot boundaries) and the x-line LDS.128 loads conflict-free
+    static constexpr int SE = ROWTMA ? NPE : (n == 6 && DG_V6_SE228) ? 228 : ((NPE + 1) / 2) * 2 + 4;
     static constexpr int SY0 = ROWTMA ? 4 * SE : 4 * SE + 4;
     static constexpr int SY = ROWTMA ? SY0 + ((4 - SY0 % 16) + 16) % 16 : SY0;  // row stride (== 4 mod 16)
     static constexpr int NCL = BE * NN;                          // consumer lines per pass
@@ -213,6 +218,11 @@ __device__ __forceinline__ void cpass_xy(const ApplyParams &a, const DevTab &T, 
         r[0] -= FL;
         if (!act) return;
         double *pa = sacc + base;
+        if (D == 0 && FIRST && (n % 2) == 0 && DG_V6_SE228) {  // contiguous x line: 16-byte stores
+#pragma unroll
+            for (int i = 0; i < n; i += 2) *reinterpret_cast<double2 *>(pa + i) = make_double2(r[i], r[i + 1]);
+            return;
+        }
 #pragma unroll
         for (int i = 0; i < n; ++i) pa[i * SSD] = FIRST ? r[i] : pa[i * SSD] + r[i];
         return;
