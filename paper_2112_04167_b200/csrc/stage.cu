@@ -359,6 +359,7 @@ __global__ void __launch_bounds__(256, 2) k_dg_grad2(const Geom g, DivGradParams
     double *sX = sPs + EPC * NPp;            // [EPC][NV] (interpolation stages, output staging)
     double *sH = sX + EPC * NV;              // [EPC][NV] psi_h
     double *sF = sH + EPC * NV;              // [EPC][DIM][2][FP] neighbour pressure face layers
+    __shared__ const double *sNb[EPC * DIM * 2];  // face-neighbour element pointers of the tile
     const int le = threadIdx.x / NL, ln = threadIdx.x % NL;
     Geom gp = g;
     gp.npe = NPp;
@@ -367,14 +368,20 @@ __global__ void __launch_bounds__(256, 2) k_dg_grad2(const Geom g, DivGradParams
         const bool act = le < ne;
         __syncthreads();
         for (int t = threadIdx.x; t < ne * NPp; t += NT) sPs[t] = a.psi[e0 * NPp + t];
-        // neighbour face layers: element el, direction d, side s (s = 1: the +d neighbour's layer 0)
-        for (int t = threadIdx.x; t < ne * DIM * 2 * FP; t += NT) {
-            const int f = t % FP, r = t / FP, s = r % 2, d = (r / 2) % DIM, el = r / (2 * DIM);
+        // the tile's face-neighbour element pointers, once per (element, direction, side)
+        for (int t = threadIdx.x; t < ne * DIM * 2; t += NT) {
+            const int s = t % 2, d = (t / 2) % DIM, el = t / (2 * DIM);
             const long long e = e0 + el;
             int cn[3] = {(int)(e % g.Nl[0]), (int)((e / g.Nl[0]) % g.Nl[1]),
                          DIM == 3 ? (int)(e / ((long long)g.Nl[0] * g.Nl[1])) : 0};
             cn[d] += s ? 1 : -1;
-            const double *nb = elem_ptr(gp, a.psi, a.plo, a.phi, cn[0], cn[1], cn[2]);
+            sNb[t] = elem_ptr(gp, a.psi, a.plo, a.phi, cn[0], cn[1], cn[2]);
+        }
+        __syncthreads();
+        // neighbour face layers: element el, direction d, side s (s = 1: the +d neighbour's layer 0)
+        for (int t = threadIdx.x; t < ne * DIM * 2 * FP; t += NT) {
+            const int f = t % FP, r = t / FP, s = r % 2, d = (r / 2) % DIM;
+            const double *nb = sNb[r];
             const int o1 = d == 0 ? 1 : 0, o2 = d == 2 ? 1 : 2;
             const int fa = f % m, fb = DIM == 3 ? f / m : 0;
             sF[t] = nb[fa * gstride(o1, m, m) + (DIM == 3 ? fb * gstride(o2, m, m) : 0) + (s ? 0 : m - 1) * gstride(d, m, m)];
@@ -504,23 +511,39 @@ __global__ void __launch_bounds__(256, 2) k_dg_div2(const Geom g, DivGradParams 
     double *sY = sX + EPC * NV;              // [EPC][NV] work
     double *sO = sY + EPC * NV;              // [EPC][NPp] accumulated divergence
     double *sF = sO + EPC * NPp;             // [EPC][2][FV] neighbour velocity face layers
+    __shared__ long long sNe[EPC * DIM * 2];  // face-neighbour element indices of the tile (-1 - i: halo layer i)
     const int le = threadIdx.x / NL, ln = threadIdx.x % NL;
     for (long long e0 = (long long)blockIdx.x * EPC; e0 < g.nel; e0 += (long long)gridDim.x * EPC) {
         const int ne = g.nel - e0 < EPC ? (int)(g.nel - e0) : EPC;
         const bool act = le < ne;
         __syncthreads();
         for (int t = threadIdx.x; t < ne * NPp; t += NT) sO[t] = 0.0;
+        // the tile's face-neighbour elements, once per (element, direction, side): the local
+        // element index, or for a slab-boundary layer of a halo mesh the halo's in-layer index
+        // encoded as -1 - li (elem_ptr's convention, resolved per component below)
+        for (int t = threadIdx.x; t < ne * DIM * 2; t += NT) {
+            const int s = t % 2, d = (t / 2) % DIM, el = t / (2 * DIM);
+            const long long e = e0 + el;
+            int cn[3] = {(int)(e % g.Nl[0]), (int)((e / g.Nl[0]) % g.Nl[1]),
+                         DIM == 3 ? (int)(e / ((long long)g.Nl[0] * g.Nl[1])) : 0};
+            cn[d] += s ? 1 : -1;
+            // pointer offset from component 0's base; elem_ptr resolves wraps and halo layers
+            const double *p0 = elem_ptr(g, a.v[0], a.vlo[0], a.vhi[0], cn[0], cn[1], cn[2]);
+            const bool lo = a.vlo[0] && p0 >= a.vlo[0] && p0 < a.vlo[0] + (long long)g.Nl[0] * (DIM == 3 ? g.Nl[1] : 1) * NV;
+            const bool hi = a.vhi[0] && p0 >= a.vhi[0] && p0 < a.vhi[0] + (long long)g.Nl[0] * (DIM == 3 ? g.Nl[1] : 1) * NV;
+            const long long off = lo ? p0 - a.vlo[0] : (hi ? p0 - a.vhi[0] : p0 - a.v[0]);
+            sNe[t] = 2 * off + (lo || hi ? 1 : 0) + (hi ? 0x4000000000000000LL : 0);
+        }
         for (int c = 0; c < DIM; ++c) {
             const int o1 = c == 0 ? 1 : 0, o2 = c == 2 ? 1 : 2;
             __syncthreads();
             for (int t = threadIdx.x; t < ne * NV; t += NT) sV[t] = a.v[c][e0 * NV + t];
             for (int t = threadIdx.x; t < ne * 2 * FV; t += NT) {
                 const int f = t % FV, s = (t / FV) % 2, el = t / (2 * FV);
-                const long long e = e0 + el;
-                int cn[3] = {(int)(e % g.Nl[0]), (int)((e / g.Nl[0]) % g.Nl[1]),
-                             DIM == 3 ? (int)(e / ((long long)g.Nl[0] * g.Nl[1])) : 0};
-                cn[c] += s ? 1 : -1;
-                const double *nb = elem_ptr(g, a.v[c], a.vlo[c], a.vhi[c], cn[0], cn[1], cn[2]);
+                const long long code = sNe[(el * DIM + c) * 2 + s];
+                const long long off = (code & 0x3FFFFFFFFFFFFFFFLL) >> 1;
+                const double *base = (code & 1) ? ((code & 0x4000000000000000LL) ? a.vhi[c] : a.vlo[c]) : a.v[c];
+                const double *nb = base + off;
                 const int fa = f % n, fb = DIM == 3 ? f / n : 0;
                 sF[t] = nb[fa * gstride(o1, n, n) + (DIM == 3 ? fb * gstride(o2, n, n) : 0) + (s ? 0 : P) * gstride(c, n, n)];
             }
