@@ -597,7 +597,7 @@ struct ApplyDispatch {
     }
     // degrees / viscosity kinds the v6 kernel has: P odd <= 5, and P = 6 with constant nu
     template <int P, bool VARNU>
-    static constexpr bool v6_shape() { return (P <= 5 && P % 2 == 1) || (P == 6 && !VARNU); }
+    static constexpr bool v6_shape() { return (P <= 5 && P % 2 == 1) || ((P == 6 || P == 7) && !VARNU); }
     // v6 (3-D, n <= 6): one CTA per SM, 4x4x1 bricks, warpgroup-specialised (apply6.cuh)
     template <int P, bool VARNU, int MODE>
     static cudaError_t go6(ApplyParams a, int *grid, cudaStream_t st)
@@ -640,7 +640,7 @@ struct ApplyDispatch {
                 cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
             }
             long long gsz = nsm;
-            const long long ncols = (long long)(a.g.Nl[0] / 4) * (a.g.Nl[1] / 4);
+            const long long ncols = (long long)(a.g.Nl[0] / K::BX) * (a.g.Nl[1] / K::BY);
             if (a.zhi < 0) {
                 a.zlo = 0;
                 a.zhi = a.g.Nl[2];
@@ -673,7 +673,7 @@ struct ApplyDispatch {
             if (gsz > nunits) gsz = nunits;
             if (gsz < 1) gsz = 1;
             *grid = (int)gsz;
-            note_kernel("v6::k_apply6", 3, P, VARNU, MODE, (int)gsz, 4, 4, 1);
+            note_kernel("v6::k_apply6", 3, P, VARNU, MODE, (int)gsz, K::BX, K::BY, 1);
             kern<<<(int)gsz, K::NT, K::SMEM_BYTES, st>>>(a);
             return cudaGetLastError();
         }
@@ -684,10 +684,12 @@ struct ApplyDispatch {
             const char *e = DG_DEV_ENV("DG_APPLY_IMPL");
             return e && e[0] == 'v' && (e[1] == '4' || e[1] == '5');
         }();
-        // TMA copies single elements (n even) or brick rows (P = 6, constant nu)
+        // TMA copies single elements (n even) or brick rows (P = 6, constant nu); P = 7 (constant
+        // nu) takes 4 x 2 x 1 bricks
         if (off || DIM != 3) return false;
-        if (!((a.g.P <= 5 && a.g.P % 2 == 1) || (a.g.P == 6 && !a.nu))) return false;
-        if (a.g.Nl[0] % 4 || a.g.Nl[1] % 4 || a.g.Nl[2] < 2) return false;
+        if (!((a.g.P <= 5 && a.g.P % 2 == 1) || ((a.g.P == 6 || a.g.P == 7) && !a.nu))) return false;
+        const int by = a.g.P == 7 ? 2 : 4;
+        if (a.g.Nl[0] % 4 || a.g.Nl[1] % by || a.g.Nl[2] < 2) return false;
         const int nz = a.zhi >= 0 ? a.zhi - a.zlo : a.g.Nl[2];
         if (nz < 2) return false;
         auto al = [](const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };

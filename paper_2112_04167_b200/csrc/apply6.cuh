@@ -62,7 +62,8 @@ struct KC6 {
     static constexpr int n = P + 1;
     static constexpr int NN = n * n;
     static constexpr int NPE = n * n * n;
-    static constexpr int BX = 4, BY = 4, BE = 16;               // brick: 4 x 4 x 1 elements
+    // brick: 4 x 4 x 1 elements (n = 8: 4 x 2 x 1, the shared-memory budget)
+    static constexpr int BX = 4, BY = (n == 8) ? 2 : 4, BE = BX * BY;
     // odd n (P = 6, constant nu): an element is not a multiple of 16 bytes, so the TMA copies
     // whole brick rows (4 x-consecutive elements, contiguous in HBM and in shared memory)
     static constexpr bool ROWTMA = (NPE % 2) != 0;
@@ -81,17 +82,23 @@ struct KC6 {
     static constexpr int NCW = ROWTMA ? (NCL + 31) / 32 : ((NCL + 31) / 32 + 3) / 4 * 4;
     static constexpr int NC = NCW * 32;
     // producer: one TMA warp and NTW trace warps (n = 7: 25 consumer + 1 + 6 = 32 warps at 64 registers)
-    static constexpr int NTW = ROWTMA ? 6 : 3;
+    static constexpr int NTW = (ROWTMA || n == 8) ? 6 : 3;
     static constexpr int NP = 32 * (1 + NTW);
     static constexpr int NT = NC + NP;
     static constexpr int NV = VARNU ? 3 : 2;                     // trace values: u, s (, nu)
-    static constexpr int LR = 4 * NN;                            // x / y brick-face lines per side
-    static constexpr int TRXY = 2 * 2 * NV * LR;                 // x/y trace table per buffer
+    // brick-face lines per side: x faces BY rows of n^2 lines, y faces BX columns
+    static constexpr int LRX = BY * NN, LRY = BX * NN;
+    static constexpr int NTASK = 2 * (LRX + LRY);                 // x/y trace lines per brick
+    static constexpr int TRXY = NV * NTASK;                      // x/y trace table per slot: [d][side][c][LR_d]
+    template <int D>
+    __host__ __device__ static constexpr int lr() { return D == 0 ? LRX : LRY; }
+    template <int D>
+    __host__ __device__ static constexpr int troff() { return D == 0 ? 0 : 2 * NV * LRX; }
     // trace threads: producer warps 1..NTW (the TMA warp joining them delayed its next copies:
     // measured 0.677 vs 0.516 ms in round 2)
     static constexpr int NPT = NP - 32;
-    static constexpr int KT = (4 * LR + NPT - 1) / NPT;          // producer x/y tasks per thread
-    static constexpr int BRK = 4 * SY;
+    static constexpr int KT = (NTASK + NPT - 1) / NPT;          // producer x/y tasks per thread
+    static constexpr int BRK = BY * SY;
     static constexpr int OFF_U = 0;
     static constexpr int OFF_NU = OFF_U + 2 * BRK;
     static constexpr int OFF_ACC = OFF_NU + (VARNU ? 2 * BRK : 0);
@@ -127,12 +134,13 @@ template <class K, int D, bool FIRST>
 __device__ __forceinline__ void cpass_xy(const ApplyParams &a, const DevTab &T, const double *su, double *snu,
                                          double *sacc, const double *tr, int t, const double *sw)
 {
-    constexpr int P = K::P, n = K::n, NN = K::NN, LR = K::LR, NV = K::NV, SE = K::SE;
+    constexpr int P = K::P, n = K::n, NN = K::NN, LR = K::template lr<D>(), NV = K::NV, SE = K::SE;
     constexpr int SSD = D == 0 ? 1 : n;
+    constexpr int BD = D == 0 ? K::BX : K::BY;  // elements along D in a brick row (adjacent lanes)
     if ((t & ~31) >= K::NCL) return;  // fully idle warp (warp-uniform: no shuffle partners lost)
     const bool act = t < K::NCL;
     const int tt = act ? t : 0;
-    const int l = tt & 3, L = tt >> 2;  // position along D in the brick row, row index
+    const int l = tt % BD, L = tt / BD;  // position along D in the brick row, row index
     const int ce = L / NN, tn = L - ce * NN;
     const int ta = tn % n, tb = tn / n;
     const int lx = D == 0 ? l : ce, ly = D == 0 ? ce : l;
@@ -169,14 +177,14 @@ __device__ __forceinline__ void cpass_xy(const ApplyParams &a, const DevTab &T, 
         }
     }
     // brick-face traces (only the end lanes use them)
-    const double *trd = tr + D * 2 * NV * LR;
+    const double *trd = tr + K::template troff<D>();
     double uL = 0.0, sL = 0.0, nuL = a.nu_const, uR = 0.0, sR = 0.0, nuR = a.nu_const;
     if (act && l == 0) {
         uL = trd[L];
         sL = trd[LR + L];
         if (K::VARNU) nuL = trd[2 * LR + L];
     }
-    if (act && l == 3) {
+    if (act && l == BD - 1) {
         uR = trd[NV * LR + L];
         sR = trd[(NV + 1) * LR + L];
         if (K::VARNU) nuR = trd[(NV + 2) * LR + L];
@@ -203,7 +211,7 @@ __device__ __forceinline__ void cpass_xy(const ApplyParams &a, const DevTab &T, 
             sL = xs;
             nuL = xn;
         }
-        if (l != 3) {
+        if (l != BD - 1) {
             uR = yu;
             sR = ys;
             nuR = yn;
@@ -235,7 +243,7 @@ __device__ __forceinline__ void cpass_xy(const ApplyParams &a, const DevTab &T, 
             uL = xu;
             sL = xs;
         }
-        if (l != 3) {
+        if (l != BD - 1) {
             uR = yu;
             sR = ys;
         }
@@ -422,9 +430,16 @@ template <class K, int K0, int K1>
 __device__ __forceinline__ void ptraces_xy(const ApplyParams &a, const DevTab &T, double *tr, const int (&e0)[3],
                                            long long eb, int ptid, double beta, const double *sw)
 {
-    constexpr int P = K::P, n = K::n, NN = K::NN, NPE = K::NPE, LR = K::LR, NV = K::NV, KT = K1 - K0;
+    constexpr int P = K::P, n = K::n, NN = K::NN, NPE = K::NPE, LRX = K::LRX, LRY = K::LRY, NV = K::NV, KT = K1 - K0;
     const Geom &g = a.g;
     const long long lay = (long long)g.Nl[0] * g.Nl[1];
+    // task tk: x faces [0, 2 LRX) (side-major), then y faces [2 LRX, 2 LRX + 2 LRY)
+    auto decode = [&](int tk, int &D, int &side, int &L) {
+        D = tk >= 2 * LRX;
+        const int r = D ? tk - 2 * LRX : tk, lr = D ? LRY : LRX;
+        side = r / lr;
+        L = r - side * lr;
+    };
     const double *fu = K::MODE == 1 ? a.pro.z : a.u;
     // every neighbour line is read forward from its node 0 (x lines: contiguous, n even ->
     // 16-byte vector loads); the face node is node P of the left / node 0 of the right neighbour
@@ -434,19 +449,20 @@ __device__ __forceinline__ void ptraces_xy(const ApplyParams &a, const DevTab &T
     for (int k = 0; k < KT; ++k) {
         const int tk = ptid + (K0 + k) * K::NPT;
         meta[k] = -1;
-        if (tk >= 4 * LR) continue;
-        const int D = tk / (2 * LR), side = (tk / LR) & 1, L = tk % LR;
+        if (tk >= K::NTASK) continue;
+        int D, side, L;
+        decode(tk, D, side, L);
         const int ce = L / NN, tn = L - ce * NN;
         const int ta = tn % n, tb = tn / n;
         int cx, cy, off, step;
         if (D == 0) {
-            cx = side ? e0[0] + 4 : e0[0] - 1;
+            cx = side ? e0[0] + K::BX : e0[0] - 1;
             cx = cx < 0 ? cx + g.Nl[0] : (cx >= g.Nl[0] ? cx - g.Nl[0] : cx);
             cy = e0[1] + ce;
             off = ta * n + tb * NN;
             step = 1;
         } else {
-            cy = side ? e0[1] + 4 : e0[1] - 1;
+            cy = side ? e0[1] + K::BY : e0[1] - 1;
             cy = cy < 0 ? cy + g.Nl[1] : (cy >= g.Nl[1] ? cy - g.Nl[1] : cy);
             cx = e0[0] + ce;
             off = ta + tb * NN;
@@ -475,11 +491,13 @@ __device__ __forceinline__ void ptraces_xy(const ApplyParams &a, const DevTab &T
     for (int k = 0; k < KT; ++k) {
         const int tk = meta[k];
         if (tk < 0) continue;
-        const int D = tk / (2 * LR), side = (tk / LR) & 1, L = tk % LR;
+        int D, side, L;
+        decode(tk, D, side, L);
+        const int LR = D ? LRY : LRX;
         // the neighbour's face node and its derivative along +d there (reference coordinates)
         const double uf = side ? v[k][0] : v[k][P];
         const double dd = side ? rdot<P>(T, 0, v[k]) : rdot<P>(T, P, v[k]);
-        double *trd = tr + D * 2 * NV * LR + side * NV * LR;
+        double *trd = tr + (D ? 2 * NV * LRX : 0) + side * NV * LR;
         trd[L] = uf;
         if (K::VARNU) {  // weight-folded: nu~ = nu w_a w_b w_0, s~ = nu~ (D v)_face (reference derivative)
             const int tn = L % NN;
@@ -581,8 +599,9 @@ __global__ void __launch_bounds__((KC6<P, VARNU, MODE>::NT)) __maxnreg__((KC6<P,
                 }
                 const long long eb = e0[0] + s1 * e0[1] + s2 * zl;
                 constexpr unsigned EB = NPE * 8u;
+                constexpr unsigned BE = K::BE;
                 if (lane == 0) {
-                    if (staged) mbar_arrive_expect_tx(&full_uv[buf], 16u * EB + (VARNU ? 16u * EB : 0u));
+                    if (staged) mbar_arrive_expect_tx(&full_uv[buf], BE * EB + (VARNU ? BE * EB : 0u));
                     else mbar_arrive(&full_uv[buf]);
                 }
                 __syncwarp();
@@ -593,28 +612,33 @@ __global__ void __launch_bounds__((KC6<P, VARNU, MODE>::NT)) __maxnreg__((KC6<P,
                         const int el = lane & 15;
                         const long long ge = eb + (el & 3) + s1 * (el >> 2);
                         const int so = (el & 3) * SE + (el >> 2) * K::SY;
-                        if (lane < 16) tma_load(su + so, a.u + ge * NPE, EB, &full_uv[buf]);
-                        if (lane >= 16 && VARNU) tma_load(snu + so, a.nu + ge * NPE, EB, &full_uv[buf]);
+                        if (lane < (int)BE) tma_load(su + so, a.u + ge * NPE, EB, &full_uv[buf]);
+                        if (lane >= 16 && el < (int)BE && VARNU) tma_load(snu + so, a.nu + ge * NPE, EB, &full_uv[buf]);
                     }
                 }
                 if (j >= 0 && j + 1 < seglen) {
                     // L2 prefetch of the x/y brick-face neighbour elements of the next brick
                     // (their trace loads then hit L2; measured on c5: 0.517 vs 0.525 ms;
                     // two layers ahead 0.519, four 0.54, eight 0.60)
-                    const int nb = lane & 15, side = (nb >> 2) & 1, r = nb & 3;
+                    // lanes 0-15 u, 16-31 nu: neighbour nb < 2 BY on the x sides, then 2 BX on the y sides
+                    const int nb = lane & 15;
                     int cx, cy;
-                    if (nb < 8) {
-                        cx = side ? e0[0] + 4 : e0[0] - 1;
+                    if (nb < 2 * K::BY) {
+                        const int side = nb / K::BY, r = nb % K::BY;
+                        cx = side ? e0[0] + K::BX : e0[0] - 1;
                         cx = cx < 0 ? cx + g.Nl[0] : (cx >= g.Nl[0] ? cx - g.Nl[0] : cx);
                         cy = e0[1] + r;
                     } else {
-                        cy = side ? e0[1] + 4 : e0[1] - 1;
+                        const int q = nb - 2 * K::BY, side = q / K::BX, r = q % K::BX;
+                        cy = side ? e0[1] + K::BY : e0[1] - 1;
                         cy = cy < 0 ? cy + g.Nl[1] : (cy >= g.Nl[1] ? cy - g.Nl[1] : cy);
                         cx = e0[0] + r;
                     }
                     const long long pe = cx + s1 * cy + s2 * (e0[2] + 1);
-                    if (lane < 16) v5::l2_prefetch(a.u + pe * NPE, EB);
-                    else if (VARNU) v5::l2_prefetch(a.nu + pe * NPE, EB);
+                    if (nb < 2 * (K::BX + K::BY)) {
+                        if (lane < 16) v5::l2_prefetch(a.u + pe * NPE, EB);
+                        else if (VARNU) v5::l2_prefetch(a.nu + pe * NPE, EB);
+                    }
                 }
             }
         }

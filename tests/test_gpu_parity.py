@@ -68,6 +68,8 @@ SMALL = [
     # v6 kernel shapes (N_x, N_y multiples of 4, P <= 5): segments of 2..5 layers, 1..4 columns
     (3, (4, 4, 2), 3), (3, (4, 8, 3), 5), (3, (8, 4, 4), 2), (3, (4, 4, 5), 4), (3, (8, 8, 6), 5),
     (3, (4, 4, 7), 1),
+    # v6 constant-nu shapes: P = 6 (brick-row TMA copies), P = 7 (4 x 2 x 1 bricks)
+    (3, (4, 4, 3), 6), (3, (4, 2, 3), 7), (3, (8, 4, 2), 7),
 ]
 
 
