@@ -405,7 +405,11 @@ __global__ void __launch_bounds__(C3Cfg<P>::NT, P >= 7 ? 3 : 1) k_convect3(const
         }
         // ---- volume, per component
         for (int c = 0; c < 3; ++c) {
-            __syncthreads();  // R2 (T2 / previous A) and R1 (previous D) are free
+            // c = 0: T2 (R2) has been read by the z interpolation.  c > 0: no barrier -- the z
+            // test writes R2 (read by the previous y test, behind its barrier) while slower
+            // threads finish the previous x test (R1 -> sy); the barrier after the z test orders
+            // that x test before the next y test rewrites R1
+            if (c == 0) __syncthreads();
             if (col) {
                 const double wxy = T.wq[qx] * T.wq[qy] * Wc;
                 double ax[n], ay[n], az[n];
@@ -481,7 +485,10 @@ __global__ void __launch_bounds__(C3Cfg<P>::NT, P >= 7 ? 3 : 1) k_convect3(const
             const int o1 = d == 0 ? 1 : 0, o2 = d == 2 ? 1 : 2;
             const int S[3] = {1, NX, NX * n};
             const double ho1 = 0.5 * g.h[o1], ho2 = 0.5 * g.h[o2];
-            __syncthreads();  // R1 / R2 free
+            // d = 0: the volume's x test has read R1.  d > 0: no barrier -- F1 (R1) was last read
+            // by the previous direction's P1 phase (behind its barrier); the previous back phase
+            // (reads R2, updates sy) is ordered before G2 rewrites R2 by the barrier after F1
+            if (d == 0) __syncthreads();
             // F1[s][side2][c][fb][qa]: along o1, n -> Q; s = 0: face at node 0 (side -1), s = 1: node P
             // side2 = 0: own trace, 1: neighbour trace
             double *F1 = R1, *G2 = R2;
