@@ -319,7 +319,12 @@ struct C3Cfg {
     static constexpr int NPE = n * n * n;
     static constexpr int NX = n % 2 == 0 ? n + 1 : n;   // padded x-line pitch of sv / sy (odd:
     static constexpr int NPEP = NX * n * n;             //  conflict-free strided line access)
-    static constexpr int NT = ((Q * Q + 31) / 32) * 32 < 128 ? 128 : ((Q * Q + 31) / 32) * 32;
+#ifndef DG_CONV_NT
+#define DG_CONV_NT 0  // development: threads per CTA (0: the Gauss column count rounded to warps, >= 128)
+#endif
+    static constexpr int NT0 = ((Q * Q + 31) / 32) * 32 < 128 ? 128 : ((Q * Q + 31) / 32) * 32;
+    static constexpr int NT = DG_CONV_NT > NT0 ? DG_CONV_NT : NT0;
+    static constexpr int MINB = NT > 128 ? 2 : (P >= 7 ? 3 : 1);
     static constexpr int W1 = 3 * n * n * Q;            // T1 / D region
     static constexpr int W2a = 3 * n * Q * Q, W2b = 2 * 3 * Q * (n + 1);
     static constexpr int W2 = W2a > W2b ? W2a : W2b;    // T2 / A / face G2, P1 region
@@ -330,7 +335,7 @@ struct C3Cfg {
 };
 
 template <int P>
-__global__ void __launch_bounds__(C3Cfg<P>::NT, P >= 7 ? 3 : 1) k_convect3(const ConvParams a)
+__global__ void __launch_bounds__(C3Cfg<P>::NT, C3Cfg<P>::MINB) k_convect3(const ConvParams a)
 {
     using C = C3Cfg<P>;
     constexpr int n = C::n, Q = C::Q, NPE = C::NPE, NT = C::NT, NX = C::NX, NPEP = C::NPEP;
