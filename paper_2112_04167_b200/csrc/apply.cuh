@@ -688,7 +688,7 @@ struct ApplyDispatch {
         // nu) takes 4 x 2 x 1 bricks
         if (off || DIM != 3) return false;
         if (!((a.g.P <= 5 && a.g.P % 2 == 1) || ((a.g.P == 6 || a.g.P == 7) && !a.nu))) return false;
-        const int by = a.g.P == 7 ? 2 : 4;
+        const int by = v6::v6_by(a.g.P);
         if (a.g.Nl[0] % 4 || a.g.Nl[1] % by || a.g.Nl[2] < 2) return false;
         const int nz = a.zhi >= 0 ? a.zhi - a.zlo : a.g.Nl[2];
         if (nz < 2) return false;

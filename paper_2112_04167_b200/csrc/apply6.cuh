@@ -54,6 +54,15 @@ using v5::named_sync;
 using v5::rdot;
 using v5::tma_load;
 
+#ifndef DG_V6_BY6
+#define DG_V6_BY6 4  // brick rows along y at P = 6
+#endif
+#ifndef DG_V6_REGCAP
+#define DG_V6_REGCAP 80  // register cap per thread
+#endif
+// brick rows along y (the host's divisibility check uses the same function)
+__host__ __device__ constexpr int v6_by(int P) { return P == 7 ? 2 : (P == 6 ? DG_V6_BY6 : 4); }
+
 template <int P_, bool VARNU_, int MODE_>
 struct KC6 {
     static constexpr int P = P_;
@@ -62,8 +71,8 @@ struct KC6 {
     static constexpr int n = P + 1;
     static constexpr int NN = n * n;
     static constexpr int NPE = n * n * n;
-    // brick: 4 x 4 x 1 elements (n = 8: 4 x 2 x 1, the shared-memory budget)
-    static constexpr int BX = 4, BY = (n == 8) ? 2 : 4, BE = BX * BY;
+    // brick: 4 x 4 x 1 elements (n = 8: 4 x 2 x 1, the shared-memory budget; n = 7: DG_V6_BY6)
+    static constexpr int BX = 4, BY = v6_by(P), BE = BX * BY;
     // odd n (P = 6, constant nu): an element is not a multiple of 16 bytes, so the TMA copies
     // whole brick rows (4 x-consecutive elements, contiguous in HBM and in shared memory)
     static constexpr bool ROWTMA = (NPE % 2) != 0;
@@ -117,7 +126,7 @@ struct KC6 {
     static constexpr int OFF_W = OFF_BAR + 10;         // full_uv[2] empty_uv[2] full_tr[3] empty_tr[3]
     static constexpr int SMEM_DOUBLES = OFF_W + n;     // GLL weights (per-lane indexed reads)
     static constexpr int SMEM_BYTES = SMEM_DOUBLES * 8;
-    static constexpr int REG_C = 65536 / NT / 8 * 8 > 80 ? 80 : 65536 / NT / 8 * 8;  // launch registers
+    static constexpr int REG_C = 65536 / NT / 8 * 8 > DG_V6_REGCAP ? DG_V6_REGCAP : 65536 / NT / 8 * 8;  // launch registers
 };
 
 // consumer z-line carry (the same thread owns the same z line in every brick of a column)
@@ -607,7 +616,7 @@ __global__ void __launch_bounds__((KC6<P, VARNU, MODE>::NT)) __maxnreg__((KC6<P,
                 __syncwarp();
                 if (staged) {
                     if (K::ROWTMA) {  // brick row r = lane: elements (e0x .. e0x + 3, e0y + r)
-                        if (lane < 4) tma_load(su + lane * K::SY, a.u + (eb + s1 * lane) * NPE, 4 * EB, &full_uv[buf]);
+                        if (lane < K::BY) tma_load(su + lane * K::SY, a.u + (eb + s1 * lane) * NPE, 4 * EB, &full_uv[buf]);
                     } else {  // one element per lane into its padded slot (u lanes 0-15, nu 16-31)
                         const int el = lane & 15;
                         const long long ge = eb + (el & 3) + s1 * (el >> 2);

@@ -302,6 +302,109 @@ __global__ void __launch_bounds__(256) k_convect(const ConvParams a)
 }
 
 // ---------------------------------------------------------------------------
+// even-odd products with the rectangular Gauss tables (CvTab Xe / Xo / Xc): X is B
+// (centro-symmetric, ANTI = false) or G (centro-antisymmetric, ANTI = true)
+// ---------------------------------------------------------------------------
+// out[q] = sum_j X[q][j] v[j], q < Q
+template <int n, int Q, bool ANTI>
+__device__ __forceinline__ void eo_fwd(const double (&Xe)[HQMAX][HMAX], const double (&Xo)[HQMAX][HMAX],
+                                       const double (&Xc)[HQMAX], const double (&v)[n], double (&out)[Q])
+{
+    constexpr int hn = n / 2, hq = Q / 2;
+    constexpr bool nodd = (n % 2) == 1, qodd = (Q % 2) == 1;
+    double ve[hn], vo[hn];
+#pragma unroll
+    for (int j = 0; j < hn; ++j) {
+        ve[j] = v[j] + v[n - 1 - j];
+        vo[j] = v[j] - v[n - 1 - j];
+    }
+    const double vm = nodd ? v[n / 2] : 0.0;
+#pragma unroll
+    for (int q = 0; q < hq; ++q) {
+        double e = nodd ? Xc[q] * vm : Xe[q][0] * ve[0];
+        double o = Xo[q][0] * vo[0];
+#pragma unroll
+        for (int j = nodd ? 0 : 1; j < hn; ++j) e = fma(Xe[q][j], ve[j], e);
+#pragma unroll
+        for (int j = 1; j < hn; ++j) o = fma(Xo[q][j], vo[j], o);
+        out[q] = e + o;
+        out[Q - 1 - q] = ANTI ? o - e : e - o;
+    }
+    if (qodd) {
+        double m;
+        if (!ANTI) {
+            m = nodd ? Xc[hq] * vm : 0.0;
+#pragma unroll
+            for (int j = 0; j < hn; ++j) m = fma(Xe[hq][j], ve[j], m);
+        } else {
+            m = 0.0;
+#pragma unroll
+            for (int j = 0; j < hn; ++j) m = fma(Xo[hq][j], vo[j], m);
+        }
+        out[hq] = m;
+    }
+}
+
+// transposed products out[j] = sum_q X[q][j] f[q], accumulated one Gauss pair (q, Q-1-q) at a
+// time into the even / odd halves E[j] = (out[j] + out[P-j]) / 2, O[j] = (out[j] - out[P-j]) / 2
+// and the middle output (odd n); eo_fin forms out
+template <int n, bool ANTI>
+__device__ __forceinline__ void eo_acc(const double (&Xe)[HQMAX][HMAX], const double (&Xo)[HQMAX][HMAX],
+                                       const double (&Xc)[HQMAX], int q, double f1, double f2, double (&E)[n / 2],
+                                       double (&O)[n / 2], double &M)
+{
+    const double fe = f1 + f2, fo = f1 - f2;
+#pragma unroll
+    for (int j = 0; j < n / 2; ++j) {
+        E[j] = fma(Xe[q][j], ANTI ? fo : fe, E[j]);
+        O[j] = fma(Xo[q][j], ANTI ? fe : fo, O[j]);
+    }
+    if (n % 2) M = fma(Xc[q], ANTI ? fo : fe, M);
+}
+// the middle Gauss point (odd Q)
+template <int n, bool ANTI>
+__device__ __forceinline__ void eo_acc_mid(const double (&Xe)[HQMAX][HMAX], const double (&Xo)[HQMAX][HMAX],
+                                           const double (&Xc)[HQMAX], int q, double f, double (&E)[n / 2],
+                                           double (&O)[n / 2], double &M)
+{
+#pragma unroll
+    for (int j = 0; j < n / 2; ++j) {
+        if (ANTI) O[j] = fma(Xo[q][j], f, O[j]);
+        else E[j] = fma(Xe[q][j], f, E[j]);
+    }
+    if ((n % 2) && !ANTI) M = fma(Xc[q], f, M);
+}
+template <int n>
+__device__ __forceinline__ void eo_zero(double (&E)[n / 2], double (&O)[n / 2], double &M)
+{
+#pragma unroll
+    for (int j = 0; j < n / 2; ++j) E[j] = O[j] = 0.0;
+    M = 0.0;
+}
+template <int n>
+__device__ __forceinline__ void eo_fin(const double (&E)[n / 2], const double (&O)[n / 2], double M, double (&out)[n])
+{
+#pragma unroll
+    for (int j = 0; j < n / 2; ++j) {
+        out[j] = E[j] + O[j];
+        out[n - 1 - j] = E[j] - O[j];
+    }
+    if (n % 2) out[n / 2] = M;
+}
+// out[j] = sum_q X[q][j] f[q] with f in registers
+template <int n, int Q, bool ANTI>
+__device__ __forceinline__ void eo_bwd(const double (&Xe)[HQMAX][HMAX], const double (&Xo)[HQMAX][HMAX],
+                                       const double (&Xc)[HQMAX], const double (&f)[Q], double (&out)[n])
+{
+    double E[n / 2], O[n / 2], M;
+    eo_zero<n>(E, O, M);
+#pragma unroll
+    for (int q = 0; q < Q / 2; ++q) eo_acc<n, ANTI>(Xe, Xo, Xc, q, f[q], f[Q - 1 - q], E, O, M);
+    if (Q % 2) eo_acc_mid<n, ANTI>(Xe, Xo, Xc, Q / 2, f[Q / 2], E, O, M);
+    eo_fin<n>(E, O, M, out);
+}
+
+// ---------------------------------------------------------------------------
 // k_convect3 (3-D, the dispatched kernel): one thread per element line, the 1-D tables of
 // __constant__ c_ctab as uniform operands of fully unrolled contractions.
 //   interpolation GLL -> Gauss: x lines (n^2), y lines (Q n), z lines (Q^2; the Gauss column
@@ -362,31 +465,23 @@ __global__ void __launch_bounds__(C3Cfg<P>::NT, C3Cfg<P>::MINB) k_convect3(const
         // ---- interpolation x: lines (c, j, k) -> T1[c][(k n + j) Q + qx]
         for (int l = tid; l < 3 * n * n; l += NT) {
             const double *src = sv + (l / (n * n)) * NPEP + (l % (n * n)) * NX;
-            double v[n];
+            double v[n], o[Q];
 #pragma unroll
             for (int i = 0; i < n; ++i) v[i] = src[i];
+            eo_fwd<n, Q, false>(T.Be, T.Bo, T.Bc, v, o);
 #pragma unroll
-            for (int q = 0; q < Q; ++q) {
-                double s = 0.0;
-#pragma unroll
-                for (int i = 0; i < n; ++i) s = fma(T.Bq[q][i], v[i], s);
-                R1[l * Q + q] = s;
-            }
+            for (int q = 0; q < Q; ++q) R1[l * Q + q] = o[q];
         }
         __syncthreads();
         // ---- y: lines (c, k, qx) over j -> T2[c][(k Q + qy) Q + qx]
         for (int l = tid; l < 3 * n * Q; l += NT) {
             const int qx = l % Q, ck = l / Q;  // ck = c n + k
-            double v[n];
+            double v[n], o[Q];
 #pragma unroll
             for (int j = 0; j < n; ++j) v[j] = R1[(ck * n + j) * Q + qx];
+            eo_fwd<n, Q, false>(T.Be, T.Bo, T.Bc, v, o);
 #pragma unroll
-            for (int q = 0; q < Q; ++q) {
-                double s = 0.0;
-#pragma unroll
-                for (int j = 0; j < n; ++j) s = fma(T.Bq[q][j], v[j], s);
-                R2[(ck * Q + q) * Q + qx] = s;
-            }
+            for (int q = 0; q < Q; ++q) R2[(ck * Q + q) * Q + qx] = o[q];
         }
         __syncthreads();
         // ---- z: column (qx, qy) of all three components, kept in registers
@@ -399,13 +494,7 @@ __global__ void __launch_bounds__(C3Cfg<P>::NT, C3Cfg<P>::MINB) k_convect3(const
                 double v[n];
 #pragma unroll
                 for (int k = 0; k < n; ++k) v[k] = R2[((c * n + k) * Q + qy) * Q + qx];
-#pragma unroll
-                for (int q = 0; q < Q; ++q) {
-                    double s = 0.0;
-#pragma unroll
-                    for (int k = 0; k < n; ++k) s = fma(T.Bq[q][k], v[k], s);
-                    vz[c][q] = s;
-                }
+                eo_fwd<n, Q, false>(T.Be, T.Bo, T.Bc, v, vz[c]);
             }
         }
         // ---- volume, per component
@@ -418,18 +507,30 @@ __global__ void __launch_bounds__(C3Cfg<P>::NT, C3Cfg<P>::MINB) k_convect3(const
             if (col) {
                 const double wxy = T.wq[qx] * T.wq[qy] * Wc;
                 double ax[n], ay[n], az[n];
+                {
+                    constexpr int hn = n / 2;
+                    double Ex[hn], Ox[hn], Mx, Ey[hn], Oy[hn], My, Ez[hn], Oz[hn], Mz;
+                    eo_zero<n>(Ex, Ox, Mx);
+                    eo_zero<n>(Ey, Oy, My);
+                    eo_zero<n>(Ez, Oz, Mz);
 #pragma unroll
-                for (int k = 0; k < n; ++k) ax[k] = ay[k] = az[k] = 0.0;
-#pragma unroll
-                for (int q = 0; q < Q; ++q) {
-                    const double w = wxy * T.wq[q] * vz[c][q];
-                    const double fx = w * vz[0][q], fy = w * vz[1][q], fz = w * vz[2][q];
-#pragma unroll
-                    for (int k = 0; k < n; ++k) {
-                        ax[k] = fma(T.Bq[q][k], fx, ax[k]);
-                        ay[k] = fma(T.Bq[q][k], fy, ay[k]);
-                        az[k] = fma(T.Gq[q][k], fz, az[k]);
+                    for (int q = 0; q < Q / 2; ++q) {
+                        const int q2 = Q - 1 - q;
+                        const double w1 = wxy * T.wq[q] * vz[c][q], w2 = wxy * T.wq[q2] * vz[c][q2];
+                        eo_acc<n, false>(T.Be, T.Bo, T.Bc, q, w1 * vz[0][q], w2 * vz[0][q2], Ex, Ox, Mx);
+                        eo_acc<n, false>(T.Be, T.Bo, T.Bc, q, w1 * vz[1][q], w2 * vz[1][q2], Ey, Oy, My);
+                        eo_acc<n, true>(T.Ge, T.Go, T.Gc, q, w1 * vz[2][q], w2 * vz[2][q2], Ez, Oz, Mz);
                     }
+                    if (Q % 2) {
+                        constexpr int qm = Q / 2;
+                        const double w = wxy * T.wq[qm] * vz[c][qm];
+                        eo_acc_mid<n, false>(T.Be, T.Bo, T.Bc, qm, w * vz[0][qm], Ex, Ox, Mx);
+                        eo_acc_mid<n, false>(T.Be, T.Bo, T.Bc, qm, w * vz[1][qm], Ey, Oy, My);
+                        eo_acc_mid<n, true>(T.Ge, T.Go, T.Gc, qm, w * vz[2][qm], Ez, Oz, Mz);
+                    }
+                    eo_fin<n>(Ex, Ox, Mx, ax);
+                    eo_fin<n>(Ey, Oy, My, ay);
+                    eo_fin<n>(Ez, Oz, Mz, az);
                 }
                 // A[t][(k Q + qy) Q + qx], t = x, y, z term
 #pragma unroll
@@ -447,18 +548,29 @@ __global__ void __launch_bounds__(C3Cfg<P>::NT, C3Cfg<P>::MINB) k_convect3(const
             for (int l = tid; l < n * Q; l += NT) {
                 const int lqx = l % Q, k = l / Q;
                 double d1[n], d2[n], d3[n];
+                {
+                    constexpr int hn = n / 2;
+                    double E1[hn], O1[hn], M1, E2[hn], O2[hn], M2, E3[hn], O3[hn], M3;
+                    eo_zero<n>(E1, O1, M1);
+                    eo_zero<n>(E2, O2, M2);
+                    eo_zero<n>(E3, O3, M3);
 #pragma unroll
-                for (int j = 0; j < n; ++j) d1[j] = d2[j] = d3[j] = 0.0;
-#pragma unroll
-                for (int q = 0; q < Q; ++q) {
-                    const int o = (k * Q + q) * Q + lqx;
-                    const double x1 = R2[o], x2 = R2[n * Q * Q + o], x3 = R2[2 * n * Q * Q + o];
-#pragma unroll
-                    for (int j = 0; j < n; ++j) {
-                        d1[j] = fma(T.Bq[q][j], x1, d1[j]);
-                        d2[j] = fma(T.Gq[q][j], x2, d2[j]);
-                        d3[j] = fma(T.Bq[q][j], x3, d3[j]);
+                    for (int q = 0; q < Q / 2; ++q) {
+                        const int o = (k * Q + q) * Q + lqx, o2 = (k * Q + (Q - 1 - q)) * Q + lqx;
+                        eo_acc<n, false>(T.Be, T.Bo, T.Bc, q, R2[o], R2[o2], E1, O1, M1);
+                        eo_acc<n, true>(T.Ge, T.Go, T.Gc, q, R2[n * Q * Q + o], R2[n * Q * Q + o2], E2, O2, M2);
+                        eo_acc<n, false>(T.Be, T.Bo, T.Bc, q, R2[2 * n * Q * Q + o], R2[2 * n * Q * Q + o2], E3, O3, M3);
                     }
+                    if (Q % 2) {
+                        constexpr int qm = Q / 2;
+                        const int o = (k * Q + qm) * Q + lqx;
+                        eo_acc_mid<n, false>(T.Be, T.Bo, T.Bc, qm, R2[o], E1, O1, M1);
+                        eo_acc_mid<n, true>(T.Ge, T.Go, T.Gc, qm, R2[n * Q * Q + o], E2, O2, M2);
+                        eo_acc_mid<n, false>(T.Be, T.Bo, T.Bc, qm, R2[2 * n * Q * Q + o], E3, O3, M3);
+                    }
+                    eo_fin<n>(E1, O1, M1, d1);
+                    eo_fin<n>(E2, O2, M2, d2);
+                    eo_fin<n>(E3, O3, M3, d3);
                 }
 #pragma unroll
                 for (int j = 0; j < n; ++j) {
@@ -470,16 +582,23 @@ __global__ void __launch_bounds__(C3Cfg<P>::NT, C3Cfg<P>::MINB) k_convect3(const
             // x: lines (j, k): out_i = (2/hx) sum G D1 + sum B D2 (q-outer)
             for (int l = tid; l < n * n; l += NT) {
                 double s1[n], s2[n];
+                {
+                    constexpr int hn = n / 2;
+                    double E1[hn], O1[hn], M1, E2[hn], O2[hn], M2;
+                    eo_zero<n>(E1, O1, M1);
+                    eo_zero<n>(E2, O2, M2);
+                    const double *r1 = R1 + l * Q, *r2 = R1 + n * n * Q + l * Q;
 #pragma unroll
-                for (int i = 0; i < n; ++i) s1[i] = s2[i] = 0.0;
-#pragma unroll
-                for (int q = 0; q < Q; ++q) {
-                    const double x1 = R1[l * Q + q], x2 = R1[n * n * Q + l * Q + q];
-#pragma unroll
-                    for (int i = 0; i < n; ++i) {
-                        s1[i] = fma(T.Gq[q][i], x1, s1[i]);
-                        s2[i] = fma(T.Bq[q][i], x2, s2[i]);
+                    for (int q = 0; q < Q / 2; ++q) {
+                        eo_acc<n, true>(T.Ge, T.Go, T.Gc, q, r1[q], r1[Q - 1 - q], E1, O1, M1);
+                        eo_acc<n, false>(T.Be, T.Bo, T.Bc, q, r2[q], r2[Q - 1 - q], E2, O2, M2);
                     }
+                    if (Q % 2) {
+                        eo_acc_mid<n, true>(T.Ge, T.Go, T.Gc, Q / 2, r1[Q / 2], E1, O1, M1);
+                        eo_acc_mid<n, false>(T.Be, T.Bo, T.Bc, Q / 2, r2[Q / 2], E2, O2, M2);
+                    }
+                    eo_fin<n>(E1, O1, M1, s1);
+                    eo_fin<n>(E2, O2, M2, s2);
                 }
 #pragma unroll
                 for (int i = 0; i < n; ++i) sy[c * NPEP + l * NX + i] = fma(s1[i], sdx, s2[i]);
@@ -513,13 +632,10 @@ __global__ void __launch_bounds__(C3Cfg<P>::NT, C3Cfg<P>::MINB) k_convect3(const
 #pragma unroll
                     for (int fa = 0; fa < n; ++fa) v[fa] = __ldg(nb + fa * G[o1]);
                 }
+                double o[Q];
+                eo_fwd<n, Q, false>(T.Be, T.Bo, T.Bc, v, o);
 #pragma unroll
-                for (int q = 0; q < Q; ++q) {
-                    double acc = 0.0;
-#pragma unroll
-                    for (int fa = 0; fa < n; ++fa) acc = fma(T.Bq[q][fa], v[fa], acc);
-                    F1[l * Q + q] = acc;
-                }
+                for (int q = 0; q < Q; ++q) F1[l * Q + q] = o[q];
             }
             __syncthreads();
             // G2[s][side2][c][qb][qa]: along o2, n -> Q
@@ -528,13 +644,10 @@ __global__ void __launch_bounds__(C3Cfg<P>::NT, C3Cfg<P>::MINB) k_convect3(const
                 double v[n];
 #pragma unroll
                 for (int fb = 0; fb < n; ++fb) v[fb] = F1[(r * n + fb) * Q + qa];
+                double o[Q];
+                eo_fwd<n, Q, false>(T.Be, T.Bo, T.Bc, v, o);
 #pragma unroll
-                for (int q = 0; q < Q; ++q) {
-                    double acc = 0.0;
-#pragma unroll
-                    for (int fb = 0; fb < n; ++fb) acc = fma(T.Bq[q][fb], v[fb], acc);
-                    G2[(r * Q + q) * Q + qa] = acc;
-                }
+                for (int q = 0; q < Q; ++q) G2[(r * Q + q) * Q + qa] = o[q];
             }
             __syncthreads();
             // LLF flux at the face Gauss points -> H[s][c][qb][qa] (in F1's region)
@@ -563,13 +676,10 @@ __global__ void __launch_bounds__(C3Cfg<P>::NT, C3Cfg<P>::MINB) k_convect3(const
                 double v[Q];
 #pragma unroll
                 for (int q = 0; q < Q; ++q) v[q] = H[l * Q + q];
+                double o[n];
+                eo_bwd<n, Q, false>(T.Be, T.Bo, T.Bc, v, o);
 #pragma unroll
-                for (int fa = 0; fa < n; ++fa) {
-                    double acc = 0.0;
-#pragma unroll
-                    for (int q = 0; q < Q; ++q) acc = fma(T.Bq[q][fa], v[q], acc);
-                    P1[l * NX + fa] = acc;
-                }
+                for (int fa = 0; fa < n; ++fa) P1[l * NX + fa] = o[fa];
             }
             __syncthreads();
             // back along o2: lines (s, c, fa): Q -> n, subtract at the face nodes
@@ -578,13 +688,10 @@ __global__ void __launch_bounds__(C3Cfg<P>::NT, C3Cfg<P>::MINB) k_convect3(const
                 double v[Q];
 #pragma unroll
                 for (int q = 0; q < Q; ++q) v[q] = P1[((s * 3 + c) * Q + q) * NX + fa];
+                double o[n];
+                eo_bwd<n, Q, false>(T.Be, T.Bo, T.Bc, v, o);
 #pragma unroll
-                for (int fb = 0; fb < n; ++fb) {
-                    double acc = 0.0;
-#pragma unroll
-                    for (int q = 0; q < Q; ++q) acc = fma(T.Bq[q][fb], v[q], acc);
-                    sy[c * NPEP + fa * S[o1] + fb * S[o2] + (s ? P : 0) * S[d]] -= acc;
-                }
+                for (int fb = 0; fb < n; ++fb) sy[c * NPEP + fa * S[o1] + fb * S[o2] + (s ? P : 0) * S[d]] -= o[fb];
             }
         }
         __syncthreads();

@@ -27,12 +27,19 @@ struct DevTab {
 };
 
 // convection tables (convect TU)
+constexpr int HQMAX = QMAX / 2 + 1;  // even-odd half size of the Gauss rows
 struct CvTab {
     double w[NMAX];
     double zq[QMAX];
     double wq[QMAX];
     double Bq[QMAX][NMAX];
     double Gq[QMAX][NMAX];
+    // even-odd forms of the rectangular Gauss tables: Gauss points and GLL nodes are both
+    // symmetric about 0, so B[Q-1-q][P-j] = B[q][j] and G[Q-1-q][P-j] = -G[q][j]; for q < Q/2 + 1,
+    // j < n/2:  Xe[q][j] = (X[q][j] + X[q][P-j]) / 2,  Xo[q][j] = (X[q][j] - X[q][P-j]) / 2,
+    // Xc[q] = X[q][P/2] (odd n).  Half the multiply-adds of X v and X^T f (convect.cuh eo_fwd / eo_acc).
+    double Be[HQMAX][HMAX], Bo[HQMAX][HMAX], Bc[HQMAX];
+    double Ge[HQMAX][HMAX], Go[HQMAX][HMAX], Gc[HQMAX];
 };
 
 inline void to_devtab(const Tab &t, DevTab *d)
@@ -50,8 +57,9 @@ inline void to_devtab(const Tab &t, DevTab *d)
     d->eK = t.eK;
 }
 
-inline void to_cvtab(const Tab &t, CvTab *d)
+inline void to_cvtab(const Tab &t, int P, CvTab *d)
 {
+    *d = CvTab{};
     for (int i = 0; i < NMAX; ++i) d->w[i] = t.w[i];
     for (int q = 0; q < QMAX; ++q) {
         d->zq[q] = t.zq[q];
@@ -60,6 +68,17 @@ inline void to_cvtab(const Tab &t, CvTab *d)
             d->Bq[q][j] = t.Bq[q][j];
             d->Gq[q][j] = t.Gq[q][j];
         }
+    }
+    const int n = P + 1, Q = t.Q;
+    for (int q = 0; q <= Q / 2; ++q) {
+        for (int j = 0; j < n / 2; ++j) {
+            d->Be[q][j] = 0.5 * (t.Bq[q][j] + t.Bq[q][P - j]);
+            d->Bo[q][j] = 0.5 * (t.Bq[q][j] - t.Bq[q][P - j]);
+            d->Ge[q][j] = 0.5 * (t.Gq[q][j] + t.Gq[q][P - j]);
+            d->Go[q][j] = 0.5 * (t.Gq[q][j] - t.Gq[q][P - j]);
+        }
+        d->Bc[q] = (n % 2) ? t.Bq[q][P / 2] : 0.0;
+        d->Gc[q] = (n % 2) ? t.Gq[q][P / 2] : 0.0;
     }
 }
 
@@ -77,7 +96,7 @@ inline void to_cvtab(const Tab &t, CvTab *d)
     cudaError_t fn_name()                                                                   \
     {                                                                                       \
         static CvTab h[PMAX + 1];                                                           \
-        for (int p = 1; p <= PMAX; ++p) to_cvtab(host_tab(p), &h[p]);                       \
+        for (int p = 1; p <= PMAX; ++p) to_cvtab(host_tab(p), p, &h[p]);                       \
         return cudaMemcpyToSymbol(c_ctab, h, sizeof(h));                                    \
     }
 

@@ -69,7 +69,7 @@ SMALL = [
     (3, (4, 4, 2), 3), (3, (4, 8, 3), 5), (3, (8, 4, 4), 2), (3, (4, 4, 5), 4), (3, (8, 8, 6), 5),
     (3, (4, 4, 7), 1),
     # v6 constant-nu shapes: P = 6 (brick-row TMA copies), P = 7 (4 x 2 x 1 bricks)
-    (3, (4, 4, 3), 6), (3, (4, 2, 3), 7), (3, (8, 4, 2), 7),
+    (3, (4, 4, 3), 6), (3, (4, 2, 3), 7), (3, (8, 4, 2), 7), (3, (4, 6, 2), 6), (3, (8, 2, 3), 6),
 ]
 
 
