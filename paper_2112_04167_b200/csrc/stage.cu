@@ -342,10 +342,24 @@ struct DG2 {
     static constexpr int FP = DIM == 3 ? m * m : m;       // pressure face nodes
     static constexpr int NT = 256;
     static constexpr int EPC = NT / NL > 16 ? 16 : (NT / NL < 1 ? 1 : NT / NL);
+    // shared-memory element slots with an odd x pitch (pit): lines along x, y and z hit distinct
+    // banks (an even pitch of 8 doubles put 16 lanes of an x-line pass on one bank pair)
+    __host__ __device__ static constexpr int pit(int e) { return e % 2 ? e : e + 1; }
+    static constexpr int NVS = DIM == 3 ? pit(n) * n * n : pit(n) * n;  // any array with extents <= n
+    static constexpr int NPS = DIM == 3 ? pit(m) * m * m : pit(m) * m;
 };
 
 // strides of direction d in an element array with extents (e0, e1, e2), x fastest
 __device__ __forceinline__ int gstride(int d, int e0, int e1) { return d == 0 ? 1 : (d == 1 ? e0 : e0 * e1); }
+// the same in a shared-memory slot with the odd x pitch
+__device__ __forceinline__ int pstride(int d, int e0, int e1)
+{
+    const int p0 = e0 % 2 ? e0 : e0 + 1;
+    return d == 0 ? 1 : (d == 1 ? p0 : p0 * e1);
+}
+// element-local linear index (x fastest, x extent E0) -> padded slot index
+template <int E0>
+__device__ __forceinline__ int pidx(int t) { return t % E0 + (E0 % 2 ? E0 : E0 + 1) * (t / E0); }
 
 // weak gradient (velocity layout) of the pressure psi, see k_dg_grad
 template <int DIM, int P>
@@ -353,12 +367,13 @@ __global__ void __launch_bounds__(256, 2) k_dg_grad2(const Geom g, DivGradParams
 {
     using C = DG2<DIM, P>;
     constexpr int n = C::n, m = C::m, NV = C::NV, NPp = C::NPp, NL = C::NL, FP = C::FP, NT = C::NT, EPC = C::EPC;
+    constexpr int NVS = C::NVS, NPS = C::NPS, PN = C::pit(n), PM = C::pit(m);
     const StTab &S = c_stab[P];
     extern __shared__ double dsm[];
-    double *sPs = dsm;                       // [EPC][NPp]
-    double *sX = sPs + EPC * NPp;            // [EPC][NV] (interpolation stages, output staging)
-    double *sH = sX + EPC * NV;              // [EPC][NV] psi_h
-    double *sF = sH + EPC * NV;              // [EPC][DIM][2][FP] neighbour pressure face layers
+    double *sPs = dsm;                       // [EPC][NPS]
+    double *sX = sPs + EPC * NPS;            // [EPC][NVS] (interpolation stages, output staging)
+    double *sH = sX + EPC * NVS;             // [EPC][NVS] psi_h
+    double *sF = sH + EPC * NVS;             // [EPC][DIM][2][FP] neighbour pressure face layers
     __shared__ const double *sNb[EPC * DIM * 2];  // face-neighbour element pointers of the tile
     const int le = threadIdx.x / NL, ln = threadIdx.x % NL;
     Geom gp = g;
@@ -367,7 +382,7 @@ __global__ void __launch_bounds__(256, 2) k_dg_grad2(const Geom g, DivGradParams
         const int ne = g.nel - e0 < EPC ? (int)(g.nel - e0) : EPC;
         const bool act = le < ne;
         __syncthreads();
-        for (int t = threadIdx.x; t < ne * NPp; t += NT) sPs[t] = a.psi[e0 * NPp + t];
+        for (int t = threadIdx.x; t < ne * NPp; t += NT) sPs[(t / NPp) * NPS + pidx<m>(t % NPp)] = a.psi[e0 * NPp + t];
         // the tile's face-neighbour element pointers, once per (element, direction, side)
         for (int t = threadIdx.x; t < ne * DIM * 2; t += NT) {
             const int s = t % 2, d = (t / 2) % DIM, el = t / (2 * DIM);
@@ -390,7 +405,7 @@ __global__ void __launch_bounds__(256, 2) k_dg_grad2(const Geom g, DivGradParams
         double v[n], o[n];
         // psi_h = (E (x) E (x) E) psi: x (m^(d-1) lines), y, z
         if (act && ln < (DIM == 3 ? m * m : m)) {
-            const int b = le * NPp + ln * m;
+            const int b = le * NPS + ln * PM;
 #pragma unroll
             for (int r = 0; r < m; ++r) v[r] = sPs[b + r];
 #pragma unroll
@@ -398,7 +413,7 @@ __global__ void __launch_bounds__(256, 2) k_dg_grad2(const Geom g, DivGradParams
                 double s = 0.0;
 #pragma unroll
                 for (int r = 0; r < m; ++r) s = fma(S.E[i][r], v[r], s);
-                sX[le * NV + ln * n + i] = s;  // layout (i, b, c): extents (n, m, m)
+                sX[le * NVS + ln * PN + i] = s;  // layout (i, b, c): extents (n, m, m)
             }
         }
         __syncthreads();
@@ -406,7 +421,7 @@ __global__ void __launch_bounds__(256, 2) k_dg_grad2(const Geom g, DivGradParams
             if (act && ln < n * m) {  // y lines (i, c) of the (n, m, m) array -> (n, n, m)
                 const int i = ln % n, c = ln / n;
 #pragma unroll
-                for (int r = 0; r < m; ++r) v[r] = sX[le * NV + i + n * (r + m * c)];
+                for (int r = 0; r < m; ++r) v[r] = sX[le * NVS + i + PN * (r + m * c)];
 #pragma unroll
                 for (int j = 0; j < n; ++j) {
                     double s = 0.0;
@@ -419,41 +434,42 @@ __global__ void __launch_bounds__(256, 2) k_dg_grad2(const Geom g, DivGradParams
             if (act && ln < n * m) {
                 const int i = ln % n, c = ln / n;
 #pragma unroll
-                for (int j = 0; j < n; ++j) sX[le * NV + i + n * (j + n * c)] = o[j];
+                for (int j = 0; j < n; ++j) sX[le * NVS + i + PN * (j + n * c)] = o[j];
             }
             __syncthreads();
             if (act) {  // z lines (i, j) of (n, n, m) -> psi_h (n, n, n)
 #pragma unroll
-                for (int r = 0; r < m; ++r) v[r] = sX[le * NV + ln + n * n * r];
+                for (int r = 0; r < m; ++r) v[r] = sX[le * NVS + ln % n + PN * (ln / n + n * r)];
 #pragma unroll
                 for (int k = 0; k < n; ++k) {
                     double s = 0.0;
 #pragma unroll
                     for (int r = 0; r < m; ++r) s = fma(S.E[k][r], v[r], s);
-                    sH[le * NV + ln + n * n * k] = s;
+                    sH[le * NVS + ln % n + PN * (ln / n + n * k)] = s;
                 }
             }
         } else {
             if (act) {  // y lines (i) of (n, m) -> (n, n)
 #pragma unroll
-                for (int r = 0; r < m; ++r) v[r] = sX[le * NV + ln + n * r];
+                for (int r = 0; r < m; ++r) v[r] = sX[le * NVS + ln + PN * r];
 #pragma unroll
                 for (int j = 0; j < n; ++j) {
                     double s = 0.0;
 #pragma unroll
                     for (int r = 0; r < m; ++r) s = fma(S.E[j][r], v[r], s);
-                    sH[le * NV + ln + n * j] = s;
+                    sH[le * NVS + ln + PN * j] = s;
                 }
             }
         }
         __syncthreads();
         // per direction d: line along d through transverse node (t1, t2) = ln
+#pragma unroll
         for (int d = 0; d < DIM; ++d) {
             const int o1 = d == 0 ? 1 : 0, o2 = d == 2 ? 1 : 2;
             const int t1 = ln % n, t2 = DIM == 3 ? ln / n : 0;
-            const int GS = gstride(d, n, n);
+            const int GS = pstride(d, n, n);
             if (act) {
-                const int base = le * NV + t1 * gstride(o1, n, n) + (DIM == 3 ? t2 * gstride(o2, n, n) : 0);
+                const int base = le * NVS + t1 * pstride(o1, n, n) + (DIM == 3 ? t2 * pstride(o2, n, n) : 0);
                 double Wt = S.w[t1] * g.wfac[d];  // transverse weight W^F
                 if (DIM == 3) Wt *= S.w[t2];
 #pragma unroll
@@ -492,7 +508,7 @@ __global__ void __launch_bounds__(256, 2) k_dg_grad2(const Geom g, DivGradParams
                 for (int k = 0; k < n; ++k) sX[base + k * GS] = o[k];
             }
             __syncthreads();
-            for (int t = threadIdx.x; t < ne * NV; t += NT) a.gout[d][e0 * NV + t] = sX[t];
+            for (int t = threadIdx.x; t < ne * NV; t += NT) a.gout[d][e0 * NV + t] = sX[(t / NV) * NVS + pidx<n>(t % NV)];
             __syncthreads();
         }
     }
@@ -504,20 +520,21 @@ __global__ void __launch_bounds__(256, 2) k_dg_div2(const Geom g, DivGradParams 
 {
     using C = DG2<DIM, P>;
     constexpr int n = C::n, m = C::m, NV = C::NV, NPp = C::NPp, NL = C::NL, FV = C::FV, NT = C::NT, EPC = C::EPC;
+    constexpr int NVS = C::NVS, NPS = C::NPS;
     const StTab &S = c_stab[P];
     extern __shared__ double dsm[];
-    double *sV = dsm;                        // [EPC][NV] one velocity component
-    double *sX = sV + EPC * NV;              // [EPC][NV] work
-    double *sY = sX + EPC * NV;              // [EPC][NV] work
-    double *sO = sY + EPC * NV;              // [EPC][NPp] accumulated divergence
-    double *sF = sO + EPC * NPp;             // [EPC][2][FV] neighbour velocity face layers
+    double *sV = dsm;                        // [EPC][NVS] one velocity component
+    double *sX = sV + EPC * NVS;             // [EPC][NVS] work
+    double *sY = sX + EPC * NVS;             // [EPC][NVS] work
+    double *sO = sY + EPC * NVS;             // [EPC][NPS] accumulated divergence
+    double *sF = sO + EPC * NPS;             // [EPC][2][FV] neighbour velocity face layers
     __shared__ long long sNe[EPC * DIM * 2];  // face-neighbour element indices of the tile (-1 - i: halo layer i)
     const int le = threadIdx.x / NL, ln = threadIdx.x % NL;
     for (long long e0 = (long long)blockIdx.x * EPC; e0 < g.nel; e0 += (long long)gridDim.x * EPC) {
         const int ne = g.nel - e0 < EPC ? (int)(g.nel - e0) : EPC;
         const bool act = le < ne;
         __syncthreads();
-        for (int t = threadIdx.x; t < ne * NPp; t += NT) sO[t] = 0.0;
+        for (int t = threadIdx.x; t < ne * NPS; t += NT) sO[t] = 0.0;
         // the tile's face-neighbour elements, once per (element, direction, side): the local
         // element index, or for a slab-boundary layer of a halo mesh the halo's in-layer index
         // encoded as -1 - li (elem_ptr's convention, resolved per component below)
@@ -534,10 +551,11 @@ __global__ void __launch_bounds__(256, 2) k_dg_div2(const Geom g, DivGradParams 
             const long long off = lo ? p0 - a.vlo[0] : (hi ? p0 - a.vhi[0] : p0 - a.v[0]);
             sNe[t] = 2 * off + (lo || hi ? 1 : 0) + (hi ? 0x4000000000000000LL : 0);
         }
-        for (int c = 0; c < DIM; ++c) {
+#pragma unroll
+        for (int c = 0; c < DIM; ++c) {  // unrolled: the extents ex / ey below stay in registers
             const int o1 = c == 0 ? 1 : 0, o2 = c == 2 ? 1 : 2;
             __syncthreads();
-            for (int t = threadIdx.x; t < ne * NV; t += NT) sV[t] = a.v[c][e0 * NV + t];
+            for (int t = threadIdx.x; t < ne * NV; t += NT) sV[(t / NV) * NVS + pidx<n>(t % NV)] = a.v[c][e0 * NV + t];
             for (int t = threadIdx.x; t < ne * 2 * FV; t += NT) {
                 const int f = t % FV, s = (t / FV) % 2, el = t / (2 * FV);
                 const long long code = sNe[(el * DIM + c) * 2 + s];
@@ -552,12 +570,12 @@ __global__ void __launch_bounds__(256, 2) k_dg_div2(const Geom g, DivGradParams 
             const int t1 = ln % n, t2 = DIM == 3 ? ln / n : 0;
             double v[n], o[n];
             if (act) {
-                const int GS = gstride(c, n, n);
-                const int tb = t1 * gstride(o1, n, n) + (DIM == 3 ? t2 * gstride(o2, n, n) : 0);
+                const int GS = pstride(c, n, n);
+                const int tb = t1 * pstride(o1, n, n) + (DIM == 3 ? t2 * pstride(o2, n, n) : 0);
                 double Wt = S.w[t1] * g.wfac[c];
                 if (DIM == 3) Wt *= S.w[t2];
 #pragma unroll
-                for (int r = 0; r < n; ++r) v[r] = sV[le * NV + tb + r * GS];
+                for (int r = 0; r < n; ++r) v[r] = sV[le * NVS + tb + r * GS];
                 const double sdc = g.sd[c] * g.h[c] * 0.5;
 #pragma unroll
                 for (int q = 0; q < m; ++q) {
@@ -572,9 +590,9 @@ __global__ void __launch_bounds__(256, 2) k_dg_div2(const Geom g, DivGradParams 
                 // result (q along c; transverse n x n) -> sX with the c extent m
                 int ex[3] = {n, n, n};
                 ex[c] = m;
-                const int ob = t1 * gstride(o1, ex[0], ex[1]) + (DIM == 3 ? t2 * gstride(o2, ex[0], ex[1]) : 0);
+                const int ob = t1 * pstride(o1, ex[0], ex[1]) + (DIM == 3 ? t2 * pstride(o2, ex[0], ex[1]) : 0);
 #pragma unroll
-                for (int q = 0; q < m; ++q) sX[le * NV + ob + q * gstride(c, ex[0], ex[1])] = o[q];
+                for (int q = 0; q < m; ++q) sX[le * NVS + ob + q * pstride(c, ex[0], ex[1])] = o[q];
             }
             __syncthreads();
             // transverse projections with E^T along o1 (then o2): n -> m
@@ -587,17 +605,17 @@ __global__ void __launch_bounds__(256, 2) k_dg_div2(const Geom g, DivGradParams 
                     const int u0 = ln % ex[c], u1 = DIM == 3 ? ln / ex[c] : 0;
                     int ey[3] = {ex[0], ex[1], ex[2]};
                     ey[o1] = m;
-                    const int bi = u0 * gstride(c, ex[0], ex[1]) + (DIM == 3 ? u1 * gstride(o2, ex[0], ex[1]) : 0);
-                    const int bo = u0 * gstride(c, ey[0], ey[1]) + (DIM == 3 ? u1 * gstride(o2, ey[0], ey[1]) : 0);
+                    const int bi = u0 * pstride(c, ex[0], ex[1]) + (DIM == 3 ? u1 * pstride(o2, ex[0], ex[1]) : 0);
+                    const int bo = u0 * pstride(c, ey[0], ey[1]) + (DIM == 3 ? u1 * pstride(o2, ey[0], ey[1]) : 0);
 #pragma unroll
-                    for (int r = 0; r < n; ++r) v[r] = sX[le * NV + bi + r * gstride(o1, ex[0], ex[1])];
+                    for (int r = 0; r < n; ++r) v[r] = sX[le * NVS + bi + r * pstride(o1, ex[0], ex[1])];
 #pragma unroll
                     for (int q = 0; q < m; ++q) {
                         double s = 0.0;
 #pragma unroll
                         for (int r = 0; r < n; ++r) s = fma(S.E[r][q], v[r], s);
-                        if (DIM == 3) sY[le * NV + bo + q * gstride(o1, ey[0], ey[1])] = s;
-                        else sO[le * NPp + bo + q * gstride(o1, ey[0], ey[1])] += s;
+                        if (DIM == 3) sY[le * NVS + bo + q * pstride(o1, ey[0], ey[1])] = s;
+                        else sO[le * NPS + bo + q * pstride(o1, ey[0], ey[1])] += s;
                     }
                 }
                 if (DIM == 3) {
@@ -606,23 +624,23 @@ __global__ void __launch_bounds__(256, 2) k_dg_div2(const Geom g, DivGradParams 
                     const int nl2 = ex[c] * ex[o1];
                     if (act && ln < nl2) {
                         const int u0 = ln % ex[c], u1 = ln / ex[c];
-                        const int bi = u0 * gstride(c, ex[0], ex[1]) + u1 * gstride(o1, ex[0], ex[1]);
-                        const int bo = u0 * gstride(c, m, m) + u1 * gstride(o1, m, m);
+                        const int bi = u0 * pstride(c, ex[0], ex[1]) + u1 * pstride(o1, ex[0], ex[1]);
+                        const int bo = u0 * pstride(c, m, m) + u1 * pstride(o1, m, m);
 #pragma unroll
-                        for (int r = 0; r < n; ++r) v[r] = sY[le * NV + bi + r * gstride(o2, ex[0], ex[1])];
+                        for (int r = 0; r < n; ++r) v[r] = sY[le * NVS + bi + r * pstride(o2, ex[0], ex[1])];
 #pragma unroll
                         for (int q = 0; q < m; ++q) {
                             double s = 0.0;
 #pragma unroll
                             for (int r = 0; r < n; ++r) s = fma(S.E[r][q], v[r], s);
-                            sO[le * NPp + bo + q * gstride(o2, m, m)] += s;
+                            sO[le * NPS + bo + q * pstride(o2, m, m)] += s;
                         }
                     }
                 }
             }
         }
         __syncthreads();
-        for (int t = threadIdx.x; t < ne * NPp; t += NT) a.out[e0 * NPp + t] = sO[t];
+        for (int t = threadIdx.x; t < ne * NPp; t += NT) a.out[e0 * NPp + t] = sO[(t / NPp) * NPS + pidx<m>(t % NPp)];
     }
 }
 
@@ -630,8 +648,8 @@ template <int DIM, bool DIV, int P>
 cudaError_t dg2_launch(const Geom &g, const DivGradParams &a, cudaStream_t st)
 {
     using C = DG2<DIM, P>;
-    const int smem = DIV ? (int)sizeof(double) * (3 * C::EPC * C::NV + C::EPC * C::NPp + C::EPC * 2 * C::FV)
-                         : (int)sizeof(double) * (C::EPC * C::NPp + 2 * C::EPC * C::NV + C::EPC * DIM * 2 * C::FP);
+    const int smem = DIV ? (int)sizeof(double) * (3 * C::EPC * C::NVS + C::EPC * C::NPS + C::EPC * 2 * C::FV)
+                         : (int)sizeof(double) * (C::EPC * C::NPS + 2 * C::EPC * C::NVS + C::EPC * DIM * 2 * C::FP);
     if (smem > 227 * 1024) return cudaErrorNotSupported;
     static int resident = 0;  // persistent tiles: one full wave of CTAs
     if (!resident) {
