@@ -363,7 +363,7 @@ __device__ __forceinline__ int pidx(int t) { return t % E0 + (E0 % 2 ? E0 : E0 +
 
 // weak gradient (velocity layout) of the pressure psi, see k_dg_grad
 template <int DIM, int P>
-__global__ void __launch_bounds__(256, 2) k_dg_grad2(const Geom g, DivGradParams a)
+__global__ void __launch_bounds__(256, 3) k_dg_grad2(const Geom g, DivGradParams a)
 {
     using C = DG2<DIM, P>;
     constexpr int n = C::n, m = C::m, NV = C::NV, NPp = C::NPp, NL = C::NL, FP = C::FP, NT = C::NT, EPC = C::EPC;
@@ -516,7 +516,7 @@ __global__ void __launch_bounds__(256, 2) k_dg_grad2(const Geom g, DivGradParams
 
 // weak divergence (pressure layout) of the velocity v, see k_dg_div
 template <int DIM, int P>
-__global__ void __launch_bounds__(256, 2) k_dg_div2(const Geom g, DivGradParams a)
+__global__ void __launch_bounds__(256, 3) k_dg_div2(const Geom g, DivGradParams a)
 {
     using C = DG2<DIM, P>;
     constexpr int n = C::n, m = C::m, NV = C::NV, NPp = C::NPp, NL = C::NL, FV = C::FV, NT = C::NT, EPC = C::EPC;
