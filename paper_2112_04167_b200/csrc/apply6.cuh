@@ -83,7 +83,18 @@ struct KC6 {
     // element slot (doubles); n = 6: SE = 228 == NN (mod 16) keeps the z-pass lines (stride NN,
     // consecutive lanes crossing slot boundaries) and the x-line LDS.128 loads conflict-free
     static constexpr int SE = ROWTMA ? NPE : (n == 6 && DG_V6_SE228) ? 228 : ((NPE + 1) / 2) * 2 + 4;
-    static constexpr int SY0 = ROWTMA ? 4 * SE : 4 * SE + 4;
+#ifndef DG_V6_PITCH
+#define DG_V6_PITCH 0  // development: measured 0.913 vs 0.444 ms on c5 (192 bulk copies of 288 bytes per brick)
+#endif
+    // n = 6: the slot's 12 padding doubles are spread over its z planes (plane pitch 38, SE = 6 * 38)
+    // and the brick rows sit 8 (mod 16) doubles apart: a y-pass request (4 rows x 8 consecutive
+    // lines, line offsets == L mod 16) then touches every bank pair exactly twice -- with the
+    // dense planes (pitch 36 == 4 mod 16, rows 4 mod 16 apart) it needed 3 wavefronts instead of
+    // 2 (ncu: 4.7 M of 60 M shared-memory wavefronts on c5).  The x-pass LDS.128 quarter-warps and
+    // the z-pass 16-lane runs stay conflict-free; the TMA warp copies plane by plane (288 bytes).
+    static constexpr bool PITCH = n == 6 && !ROWTMA && DG_V6_SE228 && DG_V6_PITCH;
+    static constexpr int NNS = PITCH ? 38 : NN;                  // z-plane pitch inside a slot
+    static constexpr int SY0 = ROWTMA ? 4 * SE : (PITCH ? 4 * SE + 8 : 4 * SE + 4);
     static constexpr int SY = ROWTMA ? SY0 + ((4 - SY0 % 16) + 16) % 16 : SY0;  // row stride (== 4 mod 16)
     static constexpr int NCL = BE * NN;                          // consumer lines per pass
     // consumer warps, warpgroup-aligned (18 of 20 busy at P = 5; measured: 18 consumer + 6 producer
@@ -143,7 +154,7 @@ template <class K, int D, bool FIRST>
 __device__ __forceinline__ void cpass_xy(const ApplyParams &a, const DevTab &T, const double *su, double *snu,
                                          double *sacc, const double *tr, int t, const double *sw)
 {
-    constexpr int P = K::P, n = K::n, NN = K::NN, LR = K::template lr<D>(), NV = K::NV, SE = K::SE;
+    constexpr int P = K::P, n = K::n, NN = K::NN, NNS = K::NNS, LR = K::template lr<D>(), NV = K::NV, SE = K::SE;
     constexpr int SSD = D == 0 ? 1 : n;
     constexpr int BD = D == 0 ? K::BX : K::BY;  // elements along D in a brick row (adjacent lanes)
     if ((t & ~31) >= K::NCL) return;  // fully idle warp (warp-uniform: no shuffle partners lost)
@@ -153,7 +164,7 @@ __device__ __forceinline__ void cpass_xy(const ApplyParams &a, const DevTab &T, 
     const int ce = L / NN, tn = L - ce * NN;
     const int ta = tn % n, tb = tn / n;
     const int lx = D == 0 ? l : ce, ly = D == 0 ? ce : l;
-    const int base = lx * SE + ly * K::SY + (D == 0 ? ta * n + tb * NN : ta + tb * NN);
+    const int base = lx * SE + ly * K::SY + (D == 0 ? ta * n + tb * NNS : ta + tb * NNS);
     const Geom &g = a.g;
     const double sd = g.sd[D];
 
@@ -301,7 +312,7 @@ __device__ __forceinline__ void cpass_z(const ApplyParams &a, const DevTab &T, c
                                         const double *sacc, double *zo, long long eb, int t, ZC6 &zc, double &epi0,
                                         double &epi1, const double *sw)
 {
-    constexpr int P = K::P, n = K::n, NN = K::NN, NPE = K::NPE, NCL = K::NCL, SE = K::SE;
+    constexpr int P = K::P, n = K::n, NN = K::NN, NNS = K::NNS, NPE = K::NPE, NCL = K::NCL, SE = K::SE;
     if (t >= NCL) return;
     const Geom &g = a.g;
     const int slot = t / NN, tn = t - slot * NN;
@@ -312,8 +323,8 @@ __device__ __forceinline__ void cpass_z(const ApplyParams &a, const DevTab &T, c
     double v[n], nv[n];
 #pragma unroll
     for (int i = 0; i < n; ++i) {
-        v[i] = su[base + i * NN];
-        nv[i] = K::VARNU ? snu[base + i * NN] : a.nu_const;
+        v[i] = su[base + i * NNS];
+        nv[i] = K::VARNU ? snu[base + i * NNS] : a.nu_const;
     }
     // bottom face: the carry of the brick below (or of the segment's bottom halo brick)
     const double uL = zc.u, nuL = K::VARNU ? zc.nu : a.nu_const, sL = zc.s;
@@ -355,7 +366,7 @@ __device__ __forceinline__ void cpass_z(const ApplyParams &a, const DevTab &T, c
     const double *pa = sacc + base;
 #pragma unroll
     for (int i = 0; i < n; ++i) {
-        const double o = fma(lw * T.w[i], v[i], K::VARNU ? r[i] + pa[i * NN] : fma(W, r[i], pa[i * NN]));
+        const double o = fma(lw * T.w[i], v[i], K::VARNU ? r[i] + pa[i * NNS] : fma(W, r[i], pa[i * NNS]));
         zo[i * NCL + t] = o;
         if (K::MODE >= 1) {
             epi0 = fma(v[i], o, epi0);
@@ -380,7 +391,7 @@ __device__ __forceinline__ void czhalo(const ApplyParams &a, const DevTab &T, co
                                        const double *zo, const int (&e0)[3], int cz, int t, ZC6 &zc, double &epi0,
                                        double &epi1, const double *sw)
 {
-    constexpr int P = K::P, n = K::n, NN = K::NN, NCL = K::NCL, SE = K::SE;
+    constexpr int P = K::P, n = K::n, NN = K::NN, NNS = K::NNS, NCL = K::NCL, SE = K::SE;
     if (t >= NCL) return;
     const Geom &g = a.g;
     const int slot = t / NN, tn = t - slot * NN;
@@ -393,10 +404,10 @@ __device__ __forceinline__ void czhalo(const ApplyParams &a, const DevTab &T, co
         const int base = (slot & 3) * SE + (slot >> 2) * K::SY + ta + tb * n;
         double v[n];
 #pragma unroll
-        for (int i = 0; i < n; ++i) v[i] = su[base + i * NN];
+        for (int i = 0; i < n; ++i) v[i] = su[base + i * NNS];
         gf = rdot<P>(T, fi, v);
         uf = v[fi];
-        nuf = K::VARNU ? snu[base + fi * NN] * (sw[ta] * sw[tb] * T.w[fi]) : a.nu_const;
+        nuf = K::VARNU ? snu[base + fi * NNS] * (sw[ta] * sw[tb] * T.w[fi]) : a.nu_const;
         sf = K::VARNU ? nuf * gf : a.nu_const * sd * gf;
     } else {
         const double *trh = halo_trace(g, a.halo, cz);
@@ -621,8 +632,19 @@ __global__ void __launch_bounds__((KC6<P, VARNU, MODE>::NT)) __maxnreg__((KC6<P,
                         const int el = lane & 15;
                         const long long ge = eb + (el & 3) + s1 * (el >> 2);
                         const int so = (el & 3) * SE + (el >> 2) * K::SY;
-                        if (lane < (int)BE) tma_load(su + so, a.u + ge * NPE, EB, &full_uv[buf]);
-                        if (lane >= 16 && el < (int)BE && VARNU) tma_load(snu + so, a.nu + ge * NPE, EB, &full_uv[buf]);
+                        if (K::PITCH) {  // plane by plane into the pitched slot
+                            const bool isu = lane < (int)BE, isnu = lane >= 16 && el < (int)BE && VARNU;
+                            if (isu || isnu) {
+                                double *dst = (isu ? su : snu) + so;
+                                const double *src = (isu ? a.u : a.nu) + ge * NPE;
+#pragma unroll
+                                for (int k = 0; k < K::n; ++k)
+                                    tma_load(dst + k * K::NNS, src + k * K::NN, K::NN * 8u, &full_uv[buf]);
+                            }
+                        } else {
+                            if (lane < (int)BE) tma_load(su + so, a.u + ge * NPE, EB, &full_uv[buf]);
+                            if (lane >= 16 && el < (int)BE && VARNU) tma_load(snu + so, a.nu + ge * NPE, EB, &full_uv[buf]);
+                        }
                     }
                 }
                 if (j >= 0 && j + 1 < seglen) {
