@@ -63,6 +63,15 @@ using v5::tma_load;
 // brick rows along y (the host's divisibility check uses the same function)
 __host__ __device__ constexpr int v6_by(int P) { return P == 7 ? 2 : (P == 6 ? DG_V6_BY6 : 4); }
 
+// y-pass line order at n = 7 (dense row-TMA slots): a y-pass lane (l_y, line (ta, tb)) hits bank pair
+// 4 l_y + ta + tb + const (mod 16), so a warp is conflict-free when its 8 lines hold two of every
+// class of (ta + tb) mod 4 -- the lines taken round-robin over the four classes (any 8 consecutive
+// entries qualify).  Consecutive lines gave 490 wavefronts per field pass of a brick, this order 364
+// (ideal 343).
+static __constant__ unsigned char c_yperm7[49] = {0,  1,  2,  3,  4,  5,  6,  9,  10, 7,  8,  13, 16, 11, 12, 15, 20,
+                                           17, 14, 19, 22, 23, 18, 21, 26, 27, 24, 25, 28, 29, 30, 31, 32, 33,
+                                           34, 37, 38, 35, 36, 41, 44, 39, 40, 43, 48, 45, 42, 47, 46};
+
 template <int P_, bool VARNU_, int MODE_>
 struct KC6 {
     static constexpr int P = P_;
@@ -135,7 +144,8 @@ struct KC6 {
     static constexpr int OFF_RED = OFF_ZO + n * NCL;
     static constexpr int OFF_BAR = OFF_RED + 64;
     static constexpr int OFF_W = OFF_BAR + 10;         // full_uv[2] empty_uv[2] full_tr[3] empty_tr[3]
-    static constexpr int SMEM_DOUBLES = OFF_W + n;     // GLL weights (per-lane indexed reads)
+    static constexpr int OFF_PERM = OFF_W + n;         // n = 7: the y-pass line order (49 bytes)
+    static constexpr int SMEM_DOUBLES = OFF_PERM + (ROWTMA ? 8 : 0);  // GLL weights (per-lane indexed reads)
     static constexpr int SMEM_BYTES = SMEM_DOUBLES * 8;
     static constexpr int REG_C = 65536 / NT / 8 * 8 > DG_V6_REGCAP ? DG_V6_REGCAP : 65536 / NT / 8 * 8;  // launch registers
 };
@@ -160,8 +170,27 @@ __device__ __forceinline__ void cpass_xy(const ApplyParams &a, const DevTab &T, 
     if ((t & ~31) >= K::NCL) return;  // fully idle warp (warp-uniform: no shuffle partners lost)
     const bool act = t < K::NCL;
     const int tt = act ? t : 0;
-    const int l = tt % BD, L = tt / BD;  // position along D in the brick row, row index
-    const int ce = L / NN, tn = L - ce * NN;
+    const int l = tt % BD;               // position along D in the brick row
+    int L = tt / BD;                     // row index
+    const int ce = L / NN;
+    int tn = L - ce * NN;
+#ifndef DG_V6_XPERM
+#define DG_V6_XPERM 1
+#endif
+    if (DG_V6_XPERM && D == 0 && K::ROWTMA && n == 7) {
+        // dense row-TMA slots (slot stride n^3 == 7, line stride 7): lane (l_x, line t) of the x pass
+        // hits bank pair 7 (l_x + t) mod 16, so 4 elements x 8 consecutive lines need 4 wavefronts
+        // where 2 suffice.  Lines taken in class-major order of t mod 4 (0, 4, .., 48, 1, 5, ..) put
+        // lines 4 apart on a warp: l_x + 4 j covers every residue mod 16 twice (ncu: 13.1 M
+        // shared-memory wavefronts against 7.6 M ideal on the config-4 pressure apply before)
+        const int c = tn < 13 ? 0 : (tn - 13) / 12 + 1;
+        tn = 4 * (tn - (c ? 13 + 12 * (c - 1) : 0)) + c;
+        L = ce * NN + tn;
+    }
+    if (DG_V6_XPERM && D == 1 && K::ROWTMA && n == 7) {  // y pass: round-robin class order (c_yperm7)
+        tn = reinterpret_cast<const unsigned char *>(sw + n)[tn];
+        L = ce * NN + tn;
+    }
     const int ta = tn % n, tb = tn / n;
     const int lx = D == 0 ? l : ce, ly = D == 0 ? ce : l;
     const int base = lx * SE + ly * K::SY + (D == 0 ? ta * n + tb * NNS : ta + tb * NNS);
@@ -547,6 +576,7 @@ __global__ void __launch_bounds__((KC6<P, VARNU, MODE>::NT)) __maxnreg__((KC6<P,
     double *sw = sm + K::OFF_W;
     const int tid = threadIdx.x;
     if (tid < K::n) sw[tid] = T.w[tid];
+    if (K::ROWTMA && K::n == 7 && tid < K::NN) reinterpret_cast<unsigned char *>(sw + K::n)[tid] = c_yperm7[tid];
     if (MODE >= 1 && *a.pro.done) return;  // PCG converged: nothing to do
     if (tid == 0) {
         for (int b = 0; b < 2; ++b) {
