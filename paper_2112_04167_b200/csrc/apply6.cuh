@@ -89,9 +89,15 @@ struct KC6 {
 #ifndef DG_V6_SE228
 #define DG_V6_SE228 1
 #endif
+#ifndef DG_V6_SE514
+#define DG_V6_SE514 1
+#endif
     // element slot (doubles); n = 6: SE = 228 == NN (mod 16) keeps the z-pass lines (stride NN,
     // consecutive lanes crossing slot boundaries) and the x-line LDS.128 loads conflict-free
-    static constexpr int SE = ROWTMA ? NPE : (n == 6 && DG_V6_SE228) ? 228 : ((NPE + 1) / 2) * 2 + 4;
+    // n = 8: SE = 514 (== 2 mod 4) with rows 4 SE apart keeps all three passes conflict-free (bank
+    // model validated against ncu on c5); SE = 516 with rows 4 mod 16 apart cost 2 wavefronts per
+    // quarter-warp LDS.128 in the x pass and 4 instead of 2 per request in the y pass
+    static constexpr int SE = ROWTMA ? NPE : (n == 6 && DG_V6_SE228) ? 228 : (n == 8 && DG_V6_SE514) ? 514 : ((NPE + 1) / 2) * 2 + 4;
 #ifndef DG_V6_PITCH
 #define DG_V6_PITCH 0  // development: measured 0.913 vs 0.444 ms on c5 (192 bulk copies of 288 bytes per brick)
 #endif
@@ -103,7 +109,7 @@ struct KC6 {
     // the z-pass 16-lane runs stay conflict-free; the TMA warp copies plane by plane (288 bytes).
     static constexpr bool PITCH = n == 6 && !ROWTMA && DG_V6_SE228 && DG_V6_PITCH;
     static constexpr int NNS = PITCH ? 38 : NN;                  // z-plane pitch inside a slot
-    static constexpr int SY0 = ROWTMA ? 4 * SE : (PITCH ? 4 * SE + 8 : 4 * SE + 4);
+    static constexpr int SY0 = ROWTMA ? 4 * SE : (PITCH ? 4 * SE + 8 : (n == 8 && DG_V6_SE514) ? 4 * SE : 4 * SE + 4);
     static constexpr int SY = ROWTMA ? SY0 + ((4 - SY0 % 16) + 16) % 16 : SY0;  // row stride (== 4 mod 16)
     static constexpr int NCL = BE * NN;                          // consumer lines per pass
     // consumer warps, warpgroup-aligned (18 of 20 busy at P = 5; measured: 18 consumer + 6 producer
@@ -307,6 +313,11 @@ __device__ __forceinline__ void cpass_xy(const ApplyParams &a, const DevTab &T, 
     if (!act) return;
     const double W = sw[ta] * sw[tb] * g.wfac[D];
     double *pa = sacc + base;
+    if (D == 0 && FIRST && (n % 2) == 0) {  // contiguous x line: 16-byte stores (a quarter-warp per wavefront)
+#pragma unroll
+        for (int i = 0; i < n; i += 2) *reinterpret_cast<double2 *>(pa + i) = make_double2(W * r[i], W * r[i + 1]);
+        return;
+    }
 #pragma unroll
     for (int i = 0; i < n; ++i) pa[i * SSD] = FIRST ? W * r[i] : fma(W, r[i], pa[i * SSD]);
 }
